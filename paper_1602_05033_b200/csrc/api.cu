@@ -1,0 +1,1469 @@
+// C-ABI of libkrymat_b200.so: contexts, the pass-1 iteration loop,
+// finalisation and the pass-2 regeneration (see include/krymat_b200.h).
+#include "kry_internal.cuh"
+#include "eigen.cuh"
+#include "finalize.cuh"
+#include <cublas_v2.h>
+#include <cusolverDn.h>
+#include <nccl.h>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <vector>
+#include <algorithm>
+
+namespace kry {
+
+thread_local std::string g_last_error;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+void count_launch(int k) { g_launches += k; }
+
+// ---------------------------------------------------------------- small device helpers
+__global__ void k_init_gamma(DevState* st) {
+  // gamma = chol(V1^T V1) * R0 (R0 kept in R1prev by POST_INIT)
+  if (threadIdx.x != 0) return;
+  const int s = st->s;
+  double R2[64] = {0}, g[64];
+  for (int k = 0; k < s; ++k) {
+    double p = st->Gcc[k * 8 + k];
+    for (int i = 0; i < k; ++i) p -= R2[i * 8 + k] * R2[i * 8 + k];
+    if (!(p > 0.0)) {
+      if (st->status == KRY_OK) st->status = KRY_ERR_DEFLATION;
+      return;
+    }
+    R2[k * 8 + k] = sqrt(p);
+    for (int j = k + 1; j < s; ++j) {
+      double v = st->Gcc[k * 8 + j];
+      for (int i = 0; i < k; ++i) v -= R2[i * 8 + k] * R2[i * 8 + j];
+      R2[k * 8 + j] = v / R2[k * 8 + k];
+    }
+  }
+  for (int r = 0; r < 8; ++r)
+    for (int c = 0; c < 8; ++c) {
+      double v = 0.0;
+      for (int q = 0; q < 8; ++q) v += R2[r * 8 + q] * st->R1prev[q * 8 + c];
+      g[r * 8 + c] = v;
+    }
+  for (int q = 0; q < 64; ++q) st->gamma[q] = g[q];
+}
+
+// orthonormal copy of a stored block: out = v * S, S = given 8x8 or
+// chol(G)^-1 computed here (mode 1)
+__global__ void k_inv_chol(const double* G, int s, double* out) {
+  if (threadIdx.x != 0) return;
+  double R[64] = {0}, Ri[64] = {0};
+  for (int k = 0; k < s; ++k) {
+    double p = G[k * 8 + k];
+    for (int i = 0; i < k; ++i) p -= R[i * 8 + k] * R[i * 8 + k];
+    R[k * 8 + k] = sqrt(fmax(p, 1e-300));
+    for (int j = k + 1; j < s; ++j) {
+      double v = G[k * 8 + j];
+      for (int i = 0; i < k; ++i) v -= R[i * 8 + k] * R[i * 8 + j];
+      R[k * 8 + j] = v / R[k * 8 + k];
+    }
+  }
+  for (int j = 0; j < s; ++j) {
+    Ri[j * 8 + j] = 1.0 / R[j * 8 + j];
+    for (int i = j - 1; i >= 0; --i) {
+      double v = 0.0;
+      for (int k = i + 1; k <= j; ++k) v += R[i * 8 + k] * Ri[k * 8 + j];
+      Ri[i * 8 + j] = -v / R[i * 8 + i];
+    }
+  }
+  for (int q = 0; q < 64; ++q) out[q] = Ri[q];
+}
+
+// Standalone canonicalisation of a general symmetric block-tridiagonal matrix
+// (arbitrary coupling blocks) into one with upper-triangular couplings of the
+// same spectrum: D = blockdiag(Q_1..Q_m), Q_1 = I, B_j Q_j = Q_{j+1} R_j
+// (Householder QR).  Q_m is returned so last rows can be mapped back.
+__device__ void hh_qr(const double* X, int s, double* Q, double* R) {
+  double A[64], V[8][8], beta[8];
+  for (int q = 0; q < 64; ++q) A[q] = X[q];
+  for (int k = 0; k < s; ++k) {
+    double nrm = 0.0;
+    for (int i = k; i < s; ++i) nrm += A[i * 8 + k] * A[i * 8 + k];
+    nrm = sqrt(nrm);
+    double alpha = (A[k * 8 + k] > 0.0) ? -nrm : nrm;
+    for (int i = 0; i < 8; ++i) V[k][i] = 0.0;
+    for (int i = k; i < s; ++i) V[k][i] = A[i * 8 + k];
+    V[k][k] -= alpha;
+    double vn = 0.0;
+    for (int i = k; i < s; ++i) vn += V[k][i] * V[k][i];
+    beta[k] = (vn > 0.0) ? 2.0 / vn : 0.0;
+    for (int c = k; c < s; ++c) {
+      double d = 0.0;
+      for (int i = k; i < s; ++i) d += V[k][i] * A[i * 8 + c];
+      d *= beta[k];
+      for (int i = k; i < s; ++i) A[i * 8 + c] -= d * V[k][i];
+    }
+  }
+  // Q = H_0 H_1 ... H_{s-1} applied to I
+  for (int q = 0; q < 64; ++q) Q[q] = ((q >> 3) == (q & 7) && (q >> 3) < s) ? 1.0 : 0.0;
+  for (int k = s - 1; k >= 0; --k) {
+    for (int c = 0; c < s; ++c) {
+      double d = 0.0;
+      for (int i = k; i < s; ++i) d += V[k][i] * Q[i * 8 + c];
+      d *= beta[k];
+      for (int i = k; i < s; ++i) Q[i * 8 + c] -= d * V[k][i];
+    }
+  }
+  for (int q = 0; q < 64; ++q) R[q] = 0.0;
+  for (int r = 0; r < s; ++r)
+    for (int c = r; c < s; ++c) R[r * 8 + c] = A[r * 8 + c];
+  // sign convention diag(R) >= 0
+  for (int r = 0; r < s; ++r) {
+    if (R[r * 8 + r] < 0.0) {
+      for (int c = 0; c < s; ++c) R[r * 8 + c] = -R[r * 8 + c];
+      for (int i = 0; i < s; ++i) Q[i * 8 + r] = -Q[i * 8 + r];
+    }
+  }
+}
+
+__global__ void k_canonicalize(const double* diag, const double* sub, int s, int m,
+                               double* dsym, double* tsub, double* qlast) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double Q[64], X[64], Y[64], Qn[64], R[64];
+  for (int q = 0; q < 64; ++q) Q[q] = ((q >> 3) == (q & 7) && (q >> 3) < s) ? 1.0 : 0.0;
+  for (int j = 0; j < m; ++j) {
+    const double* D = diag + (int64_t)j * 64;
+    // Y = Q^T D Q, symmetrised
+    for (int r = 0; r < 8; ++r)
+      for (int c = 0; c < 8; ++c) {
+        double v = 0.0;
+        for (int k = 0; k < s; ++k) v += D[r * 8 + k] * Q[k * 8 + c];
+        X[r * 8 + c] = v;
+      }
+    for (int r = 0; r < 8; ++r)
+      for (int c = 0; c < 8; ++c) {
+        double v = 0.0;
+        for (int k = 0; k < s; ++k) v += Q[k * 8 + r] * X[k * 8 + c];
+        Y[r * 8 + c] = v;
+      }
+    for (int r = 0; r < 8; ++r)
+      for (int c = 0; c < 8; ++c)
+        dsym[(int64_t)j * 64 + r * 8 + c] = 0.5 * (Y[r * 8 + c] + Y[c * 8 + r]);
+    if (j + 1 < m) {
+      const double* B = sub + (int64_t)j * 64;
+      for (int r = 0; r < 8; ++r)
+        for (int c = 0; c < 8; ++c) {
+          double v = 0.0;
+          for (int k = 0; k < s; ++k) v += B[r * 8 + k] * Q[k * 8 + c];
+          X[r * 8 + c] = v;
+        }
+      hh_qr(X, s, Qn, R);
+      for (int q = 0; q < 64; ++q) {
+        tsub[(int64_t)j * 64 + q] = R[q];
+        Q[q] = Qn[q];
+      }
+    }
+  }
+  for (int q = 0; q < 64; ++q) qlast[q] = Q[q];
+}
+
+// tau' = tau * Q (8x8)
+__global__ void k_mat_mul88(const double* A, const double* B, double* C) {
+  const int q = threadIdx.x;
+  if (q >= 64) return;
+  const int r = q >> 3, c = q & 7;
+  double v = 0.0;
+  for (int k = 0; k < 8; ++k) v += A[r * 8 + k] * B[k * 8 + c];
+  C[q] = v;
+}
+// last rows mapped back: out[r][j] = sum_q Q[r][q] L[q][j]
+__global__ void k_map_rows(const double* Q, const double* L, int64_t km, int k, int s,
+                           double* out) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+    for (int r = 0; r < s; ++r) {
+      double v = 0.0;
+      for (int q = 0; q < s; ++q) v += Q[r * 8 + q] * L[q * km + j];
+      out[(int64_t)r * k + j] = v;
+    }
+  }
+}
+
+// mind scale from sorted eigenvalue arrays: out = max(|lx0|,|lx_end|,|ly0|,|ly_end|)
+__global__ void k_scale_of(const double* lx, int nx, const double* ly, int ny, double* out) {
+  if (threadIdx.x != 0) return;
+  double v = 0.0;
+  if (nx > 0) v = fmax(fabs(lx[0]), fabs(lx[nx - 1]));
+  if (ny > 0) v = fmax(v, fmax(fabs(ly[0]), fabs(ly[ny - 1])));
+  *out = v;
+}
+
+}  // namespace kry
+
+using namespace kry;
+
+// ================================================================ context
+struct kry_ctx {
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  cublasHandle_t cublas = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  OpDev op{};
+  std::vector<void*> op_mem;
+  int64_t n = 0;
+  int s = 0, max_m = 0;
+  // pass-1 window (3 slots)
+  double* win = nullptr;
+  double* slot[3] = {nullptr, nullptr, nullptr};
+  int64_t ld = 0;
+  int i_old = -1, i_cur = 0, i_new = 1;
+  double* C = nullptr;
+  DevState* st = nullptr;
+  DevState* st_h = nullptr;  // pinned mirror
+  TStore T{};
+  double* tmem = nullptr;
+  GramScratch g{};
+  int grid = 1;
+  EigEngine eig;
+  bool initialized = false;
+  bool exhausted = false;
+  int m = 0;  // completed Lanczos steps
+  double beta2 = 0.0;
+  double gamma_h[64];
+  double* zeros64 = nullptr;
+  double* gamma_d = nullptr;  // finalised gamma (survives the pass-2 state reset)
+  double* hres = nullptr;  // pinned small readback
+  // finalisation
+  int rank = -1;
+  double discarded = 0.0;
+  double* qy = nullptr;  // k x rank row-major
+  int m_final = 0;
+  double* Z = nullptr;   // n x rank row-major (device)
+  int64_t z_cap = 0;
+  // profiling
+  bool prof = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_comb;
+  double prof_comb_ms = 0.0;
+  int prof_comb_n = 0;
+  cudaEvent_t t_ev[2] = {nullptr, nullptr};
+  // multi-GPU
+  int nranks = 1, rank_id = 0;
+  ncclComm_t comm = nullptr;
+};
+
+namespace {
+
+int sync_status(kry_ctx* c) {
+  KRY_CUDA(cudaMemcpyAsync(c->st_h, c->st, sizeof(DevState), cudaMemcpyDeviceToHost, c->stream));
+  KRY_CUDA(cudaStreamSynchronize(c->stream));
+  return KRY_OK;
+}
+
+int map_status(kry_ctx* c, const char* context) {
+  const int code = c->st_h->status;
+  if (code == KRY_OK) return KRY_OK;
+  std::string msg;
+  switch (code) {
+    case KRY_ERR_DEFLATION:
+      msg = std::string(context) + " produced a rank-deficient block; deflation is not supported";
+      break;
+    case KRY_ERR_FACTORIZATION:
+      msg = std::string(context) + ": factorization failed";
+      break;
+    default:
+      msg = std::string(context) + ": device status " + std::to_string(code);
+  }
+  return fail(code, msg);
+}
+
+double* slotp(kry_ctx* c, int i) { return i < 0 ? nullptr : c->slot[i]; }
+
+int reset_state(kry_ctx* c, int replay) {
+  KRY_CUDA(cudaMemsetAsync(c->st, 0, sizeof(DevState), c->stream));
+  DevState tmp;
+  memset(&tmp, 0, sizeof(tmp));
+  tmp.s = c->s;
+  tmp.replay = replay;
+  tmp.finalize_on_zero = 1;
+  // only the scalar header fields need to be set
+  KRY_CUDA(cudaMemcpyAsync(&c->st->s, &tmp.s, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  KRY_CUDA(cudaMemcpyAsync(&c->st->replay, &tmp.replay, sizeof(int), cudaMemcpyHostToDevice,
+                           c->stream));
+  KRY_CUDA(cudaStreamSynchronize(c->stream));
+  return KRY_OK;
+}
+
+// init from C (device, n x s, ld s) into slot `dst`
+int do_init(kry_ctx* c, double* dst, int64_t ldd, int replay) {
+  KRY_CHECK(reset_state(c, replay));
+  ApplyGramCall ag{c->C, (int64_t)c->s, c->n, 0, POST_INIT, 0};
+  KRY_CHECK(launch_apply_gram(c->stream, c->s, c->op, ag, c->st, c->T, c->g, c->grid));
+  KRY_CHECK(sync_status(c));
+  KRY_CHECK(map_status(c, "initial QR of C"));
+  CombineCall cc{nullptr, 0, c->C, (int64_t)c->s, dst, ldd, c->n, 0, 0, 1, 1};
+  KRY_CHECK(launch_combine(c->stream, c->s, c->op, cc, c->st, c->T, c->g, c->grid, nullptr,
+                           nullptr));
+  k_init_gamma<<<1, 32, 0, c->stream>>>(c->st);
+  count_launch();
+  KRY_CHECK(sync_status(c));
+  KRY_CHECK(map_status(c, "initial QR of C"));
+  return KRY_OK;
+}
+
+// explicit (reference-literal) step on actual vectors: used when the fused
+// Gram algebra cannot resolve the residual block (near-invariant subspace or
+// an ill-conditioned block).  old/cur/new are block pointers with stride ld.
+int explicit_step(kry_ctx* c, int j, const double* vold, const double* vcur, double* vnew,
+                  int64_t ld, int finalize_on_zero, int* exhausted) {
+  const int s = c->s;
+  cudaStream_t st = c->stream;
+  const int has_old = j > 1;
+  KRY_CHECK(launch_apply_store(st, s, c->op, vcur, ld, vnew, ld, c->n));
+  KRY_CHECK(launch_update(st, s, vnew, ld, nullptr, 0, c->st->Sc, c->n, 0));
+  KRY_CHECK(launch_pair_gram(st, s, vnew, ld, vnew, ld, c->n, POST_SCALE, c->st, c->T, c->g, c->grid));
+  for (int sweep = 0; sweep < 2; ++sweep) {
+    if (has_old) {
+      KRY_CHECK(launch_pair_gram(st, s, vold, ld, vnew, ld, c->n, POST_MGS_OLD, c->st, c->T, c->g,
+                                 c->grid));
+      KRY_CHECK(launch_update(st, s, vnew, ld, vold, ld, c->st->M, c->n, 1));
+    }
+    KRY_CHECK(launch_pair_gram(st, s, vcur, ld, vnew, ld, c->n, POST_MGS_CUR, c->st, c->T, c->g,
+                               c->grid));
+    KRY_CHECK(launch_update(st, s, vnew, ld, vcur, ld, c->st->M, c->n, 1));
+  }
+  KRY_CHECK(launch_pair_gram(st, s, vnew, ld, vnew, ld, c->n, POST_W2, c->st, c->T, c->g, c->grid));
+  KRY_CHECK(sync_status(c));
+  const double scale2 = c->st_h->scale2, w2 = c->st_h->w2;
+  // basis.py:239: ||W||_F <= 1e-13 ||A V||_F
+  if (sqrt(fmax(w2, 0.0)) <= 1e-13 * sqrt(fmax(scale2, 0.0))) {
+    if (!finalize_on_zero)
+      return fail(KRY_ERR_DEFLATION, "Lanczos step " + std::to_string(j) +
+                                         " produced a rank-deficient block; deflation is not supported");
+    KRY_CHECK(launch_explicit_finish(st, c->st, c->T, 0));
+    KRY_CHECK(sync_status(c));
+    *exhausted = 1;
+    return KRY_OK;
+  }
+  KRY_CHECK(launch_pair_gram(st, s, vnew, ld, vnew, ld, c->n, POST_CHOL1, c->st, c->T, c->g, c->grid));
+  KRY_CHECK(launch_update(st, s, vnew, ld, nullptr, 0, c->st->M, c->n, 0));
+  KRY_CHECK(launch_pair_gram(st, s, vnew, ld, vnew, ld, c->n, POST_CHOL2, c->st, c->T, c->g, c->grid));
+  KRY_CHECK(launch_update(st, s, vnew, ld, nullptr, 0, c->st->M, c->n, 0));
+  KRY_CHECK(sync_status(c));
+  KRY_CHECK(map_status(c, ("Lanczos step " + std::to_string(j)).c_str()));
+  KRY_CHECK(launch_explicit_finish(st, c->st, c->T, 1));
+  // Gram blocks the next fused coefficient solve needs
+  CombineCall cc{nullptr, 0, vcur, ld, vnew, ld, c->n, 0, 1, 0, 0};
+  KRY_CHECK(launch_combine(st, s, c->op, cc, c->st, c->T, c->g, c->grid, nullptr, nullptr));
+  *exhausted = 0;
+  return KRY_OK;
+}
+
+// One block-Lanczos step on blocks (old, cur) -> new.  Returns exhausted.
+int fused_step(kry_ctx* c, int j, const double* vold, const double* vcur, double* vnew,
+               int64_t ld, int finalize_on_zero, int* exhausted) {
+  ApplyGramCall ag{vcur, ld, c->n, 1, POST_STEP, 0};
+  KRY_CHECK(launch_apply_gram(c->stream, c->s, c->op, ag, c->st, c->T, c->g, c->grid));
+  KRY_CHECK(sync_status(c));
+  KRY_CHECK(map_status(c, ("Lanczos step " + std::to_string(j)).c_str()));
+  if (c->st_h->flags & KRY_FLAG_FALLBACK) {
+    return explicit_step(c, j, vold, vcur, vnew, ld, finalize_on_zero, exhausted);
+  }
+  CombineCall cc{vold, ld, vcur, ld, vnew, ld, c->n, j > 1 ? 1 : 0, 1, 1, 1};
+  cudaEvent_t* ev = nullptr;
+  float dummy = 0.f;
+  cudaEvent_t evs[2];
+  if (c->prof) {
+    cudaEventCreate(&evs[0]);
+    cudaEventCreate(&evs[1]);
+    ev = evs;
+  }
+  KRY_CHECK(launch_combine(c->stream, c->s, c->op, cc, c->st, c->T, c->g, c->grid,
+                           c->prof ? &dummy : nullptr, ev));
+  if (c->prof) c->ev_comb.push_back({evs[0], evs[1]});
+  *exhausted = 0;
+  return KRY_OK;
+}
+
+// pass-1 step with slot rotation and the eigen append of the new block row
+int step_pass1(kry_ctx* c, int finalize_on_zero, int* exhausted) {
+  if (!c->initialized) return fail(KRY_ERR_STATE, "init_basis has not been called");
+  if (c->exhausted) return fail(KRY_ERR_DEFLATION, "the Krylov space is already invariant");
+  if (c->m + 2 > c->T.cap) return fail(KRY_ERR_STATE, "max_m capacity of the context exceeded");
+  int ex = 0;
+  KRY_CHECK(fused_step(c, c->m + 1, slotp(c, c->i_old), slotp(c, c->i_cur), slotp(c, c->i_new),
+                       c->ld, finalize_on_zero, &ex));
+  c->m += 1;
+  const int j = c->m;
+  // eigen data of T_j: append block row j (diag j, coupling j-1)
+  KRY_CHECK(c->eig.append_block(c->stream, c->T.dsym + (int64_t)(j - 1) * 64,
+                                j >= 2 ? c->T.sub + (int64_t)(j - 2) * 64 : nullptr));
+  if (ex) {
+    c->exhausted = true;
+  } else {
+    const int o = c->i_old;
+    c->i_old = c->i_cur;
+    c->i_cur = c->i_new;
+    c->i_new = (o >= 0) ? o : 3 - c->i_old - c->i_cur;
+  }
+  *exhausted = ex;
+  return KRY_OK;
+}
+
+// coupling block to the next basis block (tau_{m+1,m}); zero when exhausted
+const double* tau_ptr(kry_ctx* c) { return c->exhausted ? c->zeros64 : c->st->R1prev; }
+
+int check_lyap(kry_ctx* c, double beta2, double* res, double* rel) {
+  KRY_CHECK(c->eig.residual_lyap(c->stream, c->gamma_d, tau_ptr(c)));
+  k_scale_of<<<1, 32, 0, c->stream>>>(c->eig.lam_cur(), c->eig.K, c->eig.lam_cur(), c->eig.K,
+                                      c->eig.res + 2);
+  count_launch();
+  KRY_CUDA(cudaMemcpyAsync(c->hres, c->eig.res, 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream));
+  KRY_CUDA(cudaStreamSynchronize(c->stream));
+  // kernels.py:38-44 guard
+  if (c->hres[1] < 1e-14 * c->hres[2])
+    return fail(KRY_ERR_INDEFINITE,
+                "eigenvalue-sum denominator is numerically singular; coefficient matrices must "
+                "be definite (of one sign)");
+  *res = sqrt(2.0 * fmax(c->hres[0], 0.0));
+  *rel = *res / beta2;
+  return KRY_OK;
+}
+
+int check_sylv(kry_ctx* a, kry_ctx* b, double rhs_norm, double* res, double* rel) {
+  KRY_CUDA(cudaStreamSynchronize(b->stream));
+  KRY_CHECK(a->eig.compute_uw(a->stream, a->gamma_d, tau_ptr(a)));
+  KRY_CHECK(b->eig.compute_uw(b->stream, b->gamma_d, tau_ptr(b)));
+  KRY_CUDA(cudaStreamSynchronize(b->stream));
+  const int kA = a->eig.K, kB = b->eig.K;
+  // ||sd^T f||^2: rows over B, sum over A with c = f
+  KRY_CHECK(a->eig.cauchy(a->stream, kB, b->eig.lam_cur(), b->eig.u, kA, a->eig.lam_cur(),
+                          a->eig.u, a->eig.w, a->eig.res));
+  // ||sd g||^2: rows over A, sum over B with c = g
+  KRY_CHECK(a->eig.cauchy(a->stream, kA, a->eig.lam_cur(), a->eig.u, kB, b->eig.lam_cur(),
+                          b->eig.u, b->eig.w, a->eig.res + 4));
+  k_scale_of<<<1, 32, 0, a->stream>>>(a->eig.lam_cur(), kA, b->eig.lam_cur(), kB,
+                                      a->eig.res + 2);
+  count_launch();
+  KRY_CUDA(cudaMemcpyAsync(a->hres, a->eig.res, 6 * sizeof(double), cudaMemcpyDeviceToHost,
+                           a->stream));
+  KRY_CUDA(cudaStreamSynchronize(a->stream));
+  const double mind = fmin(a->hres[1], a->hres[5]);
+  if (mind < 1e-14 * a->hres[2])
+    return fail(KRY_ERR_INDEFINITE,
+                "eigenvalue-sum denominator is numerically singular; coefficient matrices must "
+                "be definite (of one sign)");
+  *res = sqrt(fmax(a->hres[0] + a->hres[4], 0.0));
+  *rel = *res / rhs_norm;
+  return KRY_OK;
+}
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+template <class T>
+int dalloc(T** p, size_t count) {
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    return fail(KRY_ERR_CUDA, std::string("cudaMalloc failed: ") + cudaGetErrorString(e) +
+                                  " (" + std::to_string(count * sizeof(T)) + " bytes)");
+  }
+  return KRY_OK;
+}
+
+int ensure_handles(kry_ctx* c) {
+  if (!c->cublas) {
+    if (cublasCreate(&c->cublas) != CUBLAS_STATUS_SUCCESS) return fail(KRY_ERR_CUDA, "cublasCreate failed");
+    cublasSetStream(c->cublas, c->stream);
+  }
+  if (!c->solver) {
+    if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS)
+      return fail(KRY_ERR_CUDA, "cusolverDnCreate failed");
+    cusolverDnSetStream(c->solver, c->stream);
+  }
+  return KRY_OK;
+}
+
+// dense symmetric eigendecomposition in place (A k x k -> eigenvectors), w ascending
+int syevd(kry_ctx* c, double* A, int k, double* w) {
+  int lwork = 0;
+  if (cusolverDnDsyevd_bufferSize(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, k,
+                                  A, k, w, &lwork) != CUSOLVER_STATUS_SUCCESS)
+    return fail(KRY_ERR_FACTORIZATION, "syevd buffer query failed");
+  double* work = nullptr;
+  int* info = nullptr;
+  KRY_CHECK(dalloc(&work, (size_t)lwork + 1));
+  KRY_CHECK(dalloc(&info, 1));
+  auto stt = cusolverDnDsyevd(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, k, A, k,
+                              w, work, lwork, info);
+  int hinfo = 0;
+  cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+  cudaStreamSynchronize(c->stream);
+  cudaFree(work);
+  cudaFree(info);
+  if (stt != CUSOLVER_STATUS_SUCCESS || hinfo != 0)
+    return fail(KRY_ERR_FACTORIZATION, "dense symmetric eigensolver did not converge");
+  return KRY_OK;
+}
+
+struct FinalBufs {
+  double* Td = nullptr;
+  double* lam = nullptr;
+  double* u = nullptr;
+  void free_all() {
+    if (Td) cudaFree(Td);
+    if (lam) cudaFree(lam);
+    if (u) cudaFree(u);
+    Td = lam = u = nullptr;
+  }
+};
+
+// eigh of T_m and u = Q[:s]^T gamma; checks lam_max < 0
+int final_eig(kry_ctx* c, FinalBufs& b, int* k_out) {
+  const int m = c->m_final, s = c->s, k = s * m;
+  KRY_CHECK(dalloc(&b.Td, (size_t)k * k));
+  KRY_CHECK(dalloc(&b.lam, (size_t)k));
+  KRY_CHECK(dalloc(&b.u, (size_t)k * 8));
+  KRY_CHECK(launch_assemble_T(c->stream, c->T.dsym, c->T.sub, s, m, b.Td));
+  KRY_CHECK(syevd(c, b.Td, k, b.lam));
+  KRY_CHECK(launch_first_rows_times(c->stream, b.Td, k, s, c->gamma_d, b.u));
+  *k_out = k;
+  return KRY_OK;
+}
+
+int set_qy(kry_ctx* c, const double* Q, int k, const double* factor, int rank) {
+  if (c->qy) cudaFree(c->qy);
+  c->qy = nullptr;
+  c->rank = rank;
+  if (rank <= 0) return KRY_OK;
+  KRY_CHECK(dalloc(&c->qy, (size_t)k * rank));
+  // qy (row-major k x rank) = col-major (rank x k) = factor^T Q^T
+  const double one = 1.0, zero = 0.0;
+  if (cublasDgemm(c->cublas, CUBLAS_OP_T, CUBLAS_OP_T, rank, k, k, &one, factor, k, Q, k, &zero,
+                  c->qy, rank) != CUBLAS_STATUS_SUCCESS)
+    return fail(KRY_ERR_CUDA, "cublasDgemm (qy) failed");
+  return KRY_OK;
+}
+
+}  // namespace
+
+// ================================================================ C-ABI
+extern "C" {
+
+int kry_version(void) { return 1; }
+const char* kry_last_error(void) { return g_last_error.c_str(); }
+int kry_device_count(int* count) {
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return fail(KRY_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  }
+  return KRY_OK;
+}
+int64_t kry_launch_count(void) { return g_launches.load(); }
+void kry_reset_launch_count(void) { g_launches = 0; }
+
+int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s, int max_m) {
+  *out = nullptr;
+  if (s < 1 || s > KRY_SMAX) return fail(KRY_ERR_ARGUMENT, "block width s must be in 1..8");
+  if (max_m < 1) return fail(KRY_ERR_ARGUMENT, "max_m must be >= 1");
+  if (od->n < 1 || od->n > ((int64_t)1 << 31) - 1)
+    return fail(KRY_ERR_DIMENSION, "operator order out of range");
+  KRY_CUDA(cudaSetDevice(device));
+  kry_ctx* c = new kry_ctx();
+  c->dev = device;
+  c->s = s;
+  c->max_m = max_m;
+  KRY_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  // operator
+  OpDev& op = c->op;
+  memset(&op, 0, sizeof(op));
+  op.kind = od->kind;
+  int64_t nloc = od->n;
+  if (od->kind == KRY_OP_STENCIL) {
+    if (od->nx < 1 || od->ny < 1 || od->nz < 1 || od->nx * od->ny * od->nz != od->n) {
+      delete c;
+      return fail(KRY_ERR_DIMENSION, "stencil grid does not match the operator order");
+    }
+    int64_t z0 = od->z_begin, z1 = od->z_end;
+    if (z1 <= z0) { z0 = 0; z1 = od->nz; }
+    op.nx = (int)od->nx;
+    op.ny = (int)od->ny;
+    op.nxy = (int)(od->nx * od->ny);
+    op.nzl = (int)(z1 - z0);
+    op.halo_lo = z0 > 0;
+    op.halo_hi = z1 < od->nz;
+    nloc = (int64_t)op.nxy * op.nzl;
+    op.variable = od->variable;
+    op.cd = od->c_diag; op.cx = od->c_x; op.cy = od->c_y; op.cz = od->c_z;
+    if (od->variable) {
+      const double* src[4] = {od->diag, od->cx, od->cy, od->cz};
+      const double** dst[4] = {&op.d, &op.ex, &op.ey, &op.ez};
+      // arrays cover the owned planes plus one halo plane on each side
+      const int64_t lo = op.halo_lo ? op.nxy : 0, hi = op.halo_hi ? op.nxy : 0;
+      for (int q = 0; q < 4; ++q) {
+        double* p = nullptr;
+        if (dalloc(&p, (size_t)(nloc + lo + hi)) != KRY_OK) { delete c; return KRY_ERR_CUDA; }
+        c->op_mem.push_back(p);
+        KRY_CUDA(cudaMemcpy(p, src[q] + z0 * op.nxy - lo, (nloc + lo + hi) * sizeof(double),
+                            cudaMemcpyHostToDevice));
+        *dst[q] = p + lo;
+      }
+    }
+  } else if (od->kind == KRY_OP_CSR) {
+    int64_t* rp = nullptr; int* ci = nullptr; double* va = nullptr;
+    KRY_CHECK(dalloc(&rp, (size_t)od->n + 1));
+    KRY_CHECK(dalloc(&ci, (size_t)std::max<int64_t>(od->nnz, 1)));
+    KRY_CHECK(dalloc(&va, (size_t)std::max<int64_t>(od->nnz, 1)));
+    c->op_mem.push_back(rp); c->op_mem.push_back(ci); c->op_mem.push_back(va);
+    KRY_CUDA(cudaMemcpy(rp, od->indptr, (od->n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+    if (od->nnz > 0) {
+      KRY_CUDA(cudaMemcpy(ci, od->indices, od->nnz * sizeof(int), cudaMemcpyHostToDevice));
+      KRY_CUDA(cudaMemcpy(va, od->values, od->nnz * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    op.rp = rp; op.ci = ci; op.va = va;
+    op.nx = 1; op.ny = 1; op.nzl = 1; op.nxy = 1;
+  } else {
+    delete c;
+    return fail(KRY_ERR_ARGUMENT, "unknown operator kind");
+  }
+  c->n = nloc;
+  c->ld = s;
+  // window: 3 slots, each with one halo plane on both sides (multi-GPU)
+  const int64_t halo = (od->kind == KRY_OP_STENCIL) ? op.nxy : 0;
+  const int64_t slot_pts = nloc + 2 * halo;
+  KRY_CHECK(dalloc(&c->win, (size_t)3 * slot_pts * s));
+  KRY_CUDA(cudaMemset(c->win, 0, (size_t)3 * slot_pts * s * sizeof(double)));
+  for (int q = 0; q < 3; ++q) c->slot[q] = c->win + (int64_t)q * slot_pts * s + halo * s;
+  KRY_CHECK(dalloc(&c->C, (size_t)nloc * s));
+  KRY_CHECK(dalloc(&c->st, 1));
+  KRY_CUDA(cudaMallocHost(&c->st_h, sizeof(DevState)));
+  KRY_CUDA(cudaMallocHost(&c->hres, 16 * sizeof(double)));
+  const int cap = max_m + 3;
+  KRY_CHECK(dalloc(&c->tmem, (size_t)5 * cap * 64));
+  KRY_CUDA(cudaMemset(c->tmem, 0, (size_t)5 * cap * 64 * sizeof(double)));
+  c->T.draw = c->tmem;
+  c->T.dsym = c->tmem + (int64_t)cap * 64;
+  c->T.off = c->tmem + (int64_t)2 * cap * 64;
+  c->T.sub = c->tmem + (int64_t)3 * cap * 64;
+  c->T.S = c->tmem + (int64_t)4 * cap * 64;
+  c->T.cap = cap;
+  c->grid = gram_grid_for(nloc);
+  c->g.max_grid = 148 * 6;
+  KRY_CHECK(dalloc(&c->g.partials, (size_t)c->g.max_grid * 24 * 8));
+  KRY_CHECK(dalloc(&c->g.ticket, 8));
+  KRY_CUDA(cudaMemset(c->g.ticket, 0, 8 * sizeof(unsigned)));
+  KRY_CHECK(dalloc(&c->zeros64, 64));
+  KRY_CHECK(dalloc(&c->gamma_d, 64));
+  KRY_CUDA(cudaMemset(c->zeros64, 0, 64 * sizeof(double)));
+  KRY_CHECK(c->eig.init(s, s * (max_m + 2), device));
+  *out = c;
+  return KRY_OK;
+}
+
+void kry_ctx_destroy(kry_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->dev);
+  cudaStreamSynchronize(c->stream);
+  for (void* p : c->op_mem) cudaFree(p);
+  cudaFree(c->win);
+  cudaFree(c->C);
+  cudaFree(c->st);
+  cudaFreeHost(c->st_h);
+  cudaFreeHost(c->hres);
+  cudaFree(c->tmem);
+  cudaFree(c->g.partials);
+  cudaFree(c->g.ticket);
+  cudaFree(c->zeros64);
+  cudaFree(c->gamma_d);
+  if (c->qy) cudaFree(c->qy);
+  if (c->Z) cudaFree(c->Z);
+  c->eig.release();
+  for (auto& e : c->ev_comb) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  if (c->cublas) cublasDestroy(c->cublas);
+  if (c->solver) cusolverDnDestroy(c->solver);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->t_ev[0]) { cudaEventDestroy(c->t_ev[0]); cudaEventDestroy(c->t_ev[1]); }
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int kry_ctx_info(kry_ctx* c, int64_t* n, int* s, int* m, int* exhausted) {
+  if (n) *n = c->n;
+  if (s) *s = c->s;
+  if (m) *m = c->m;
+  if (exhausted) *exhausted = c->exhausted ? 1 : 0;
+  return KRY_OK;
+}
+
+int kry_apply(kry_ctx* c, const double* v, double* y, int ncols) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  if (ncols < 1) return fail(KRY_ERR_DIMENSION, "block must have at least one column");
+  double *dv = nullptr, *dy = nullptr;
+  const int64_t halo = (c->op.kind == KRY_OP_STENCIL) ? c->op.nxy : 0;
+  KRY_CHECK(dalloc(&dv, (size_t)(c->n + 2 * halo) * ncols));
+  KRY_CHECK(dalloc(&dy, (size_t)c->n * ncols));
+  KRY_CUDA(cudaMemsetAsync(dv, 0, (c->n + 2 * halo) * ncols * sizeof(double), c->stream));
+  double* dvv = dv + halo * ncols;
+  KRY_CUDA(cudaMemcpyAsync(dvv, v, c->n * ncols * sizeof(double), cudaMemcpyHostToDevice,
+                           c->stream));
+  for (int c0 = 0; c0 < ncols; c0 += KRY_SMAX) {
+    const int w = std::min(KRY_SMAX, ncols - c0);
+    KRY_CHECK(launch_apply_store(c->stream, w, c->op, dvv + c0, ncols, dy + c0, ncols, c->n));
+  }
+  KRY_CUDA(cudaMemcpyAsync(y, dy, c->n * ncols * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream));
+  KRY_CUDA(cudaStreamSynchronize(c->stream));
+  cudaFree(dv);
+  cudaFree(dy);
+  return KRY_OK;
+}
+
+static int init_basis_common(kry_ctx* c, double* gamma, double* beta2) {
+  c->m = 0;
+  c->exhausted = false;
+  c->initialized = false;
+  c->eig.reset();
+  c->i_old = -1; c->i_cur = 0; c->i_new = 1;
+  c->rank = -1;
+  KRY_CHECK(do_init(c, c->slot[0], c->ld, 0));
+  c->beta2 = c->st_h->beta2;
+  KRY_CUDA(cudaMemcpyAsync(c->gamma_d, c->st->gamma, 64 * sizeof(double),
+                           cudaMemcpyDeviceToDevice, c->stream));
+  memcpy(c->gamma_h, c->st_h->gamma, sizeof(c->gamma_h));
+  if (gamma)
+    for (int r = 0; r < c->s; ++r)
+      for (int q = 0; q < c->s; ++q) gamma[r * c->s + q] = c->gamma_h[r * 8 + q];
+  if (beta2) *beta2 = c->beta2;
+  c->initialized = true;
+  return KRY_OK;
+}
+
+int kry_init_basis(kry_ctx* c, const double* ch, double* gamma, double* beta2) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  KRY_CUDA(cudaMemcpyAsync(c->C, ch, c->n * c->s * sizeof(double), cudaMemcpyHostToDevice,
+                           c->stream));
+  return init_basis_common(c, gamma, beta2);
+}
+
+int kry_init_basis_device(kry_ctx* c, const double* cd, double* gamma, double* beta2) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  KRY_CUDA(cudaMemcpyAsync(c->C, cd, c->n * c->s * sizeof(double), cudaMemcpyDeviceToDevice,
+                           c->stream));
+  return init_basis_common(c, gamma, beta2);
+}
+
+int kry_lanczos_step(kry_ctx* c, int finalize_on_zero, int* exhausted) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  int ex = 0;
+  KRY_CHECK(step_pass1(c, finalize_on_zero, &ex));
+  if (exhausted) *exhausted = ex;
+  return KRY_OK;
+}
+
+int kry_get_projection(kry_ctx* c, int* m, double* diag_raw, double* diag_sym, double* off,
+                       double* sub) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  const int mm = c->m, s = c->s;
+  *m = mm;
+  if (mm == 0) return KRY_OK;
+  std::vector<double> buf((size_t)mm * 64);
+  auto grab = [&](const double* src, double* dst) -> int {
+    if (!dst) return KRY_OK;
+    KRY_CUDA(cudaMemcpy(buf.data(), src, (size_t)mm * 64 * sizeof(double),
+                        cudaMemcpyDeviceToHost));
+    for (int b = 0; b < mm; ++b)
+      for (int r = 0; r < s; ++r)
+        for (int q = 0; q < s; ++q) dst[((size_t)b * s + r) * s + q] = buf[(size_t)b * 64 + r * 8 + q];
+    return KRY_OK;
+  };
+  KRY_CUDA(cudaStreamSynchronize(c->stream));
+  KRY_CHECK(grab(c->T.draw, diag_raw));
+  KRY_CHECK(grab(c->T.dsym, diag_sym));
+  KRY_CHECK(grab(c->T.off, off));
+  if (sub) {
+    // couplings 1..m-1 are final; coupling m is the current tau_{m+1,m}
+    KRY_CHECK(grab(c->T.sub, sub));
+    double last[64];
+    KRY_CUDA(cudaMemcpy(last, tau_ptr(c), 64 * sizeof(double), cudaMemcpyDeviceToHost));
+    for (int r = 0; r < s; ++r)
+      for (int q = 0; q < s; ++q) sub[((size_t)(mm - 1) * s + r) * s + q] = last[r * 8 + q];
+  }
+  return KRY_OK;
+}
+
+int kry_get_window(kry_ctx* c, double* older, double* current, int* have_older) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  if (!c->initialized) return fail(KRY_ERR_STATE, "init_basis has not been called");
+  const int s = c->s;
+  double* tmp = nullptr;
+  double* S = nullptr;
+  KRY_CHECK(dalloc(&tmp, (size_t)c->n * s));
+  KRY_CHECK(dalloc(&S, 64));
+  auto emit = [&](const double* blk, const double* Sdev, double* host) -> int {
+    KRY_CHECK(launch_copy_block(c->stream, s, blk, c->ld, tmp, s, c->n));
+    KRY_CHECK(launch_update(c->stream, s, tmp, s, nullptr, 0, Sdev, c->n, 0));
+    KRY_CUDA(cudaMemcpyAsync(host, tmp, c->n * s * sizeof(double), cudaMemcpyDeviceToHost,
+                             c->stream));
+    KRY_CUDA(cudaStreamSynchronize(c->stream));
+    return KRY_OK;
+  };
+  // newest block: correction from its Gram (not yet folded by a coefficient solve)
+  const int newest = c->exhausted ? c->i_cur : c->i_cur;
+  k_inv_chol<<<1, 32, 0, c->stream>>>(c->st->Gcc, s, S);
+  count_launch();
+  int rc = KRY_OK;
+  if (c->exhausted) {
+    // window = (V_{m-1}, V_m): V_m correction already known
+    rc = emit(slotp(c, c->i_cur), c->T.S + (int64_t)(c->m - 1) * 64, current);
+    if (rc == KRY_OK && c->i_old >= 0 && older && c->m >= 2)
+      rc = emit(slotp(c, c->i_old), c->T.S + (int64_t)(c->m - 2) * 64, older);
+    if (have_older) *have_older = (c->m >= 2) ? 1 : 0;
+  } else {
+    rc = emit(slotp(c, newest), S, current);
+    if (rc == KRY_OK && c->m >= 1 && older)
+      rc = emit(slotp(c, c->i_old), c->T.S + (int64_t)(c->m - 1) * 64, older);
+    if (have_older) *have_older = (c->m >= 1) ? 1 : 0;
+  }
+  cudaFree(tmp);
+  cudaFree(S);
+  return rc;
+}
+
+int kry_check_lyap(kry_ctx* c, double beta2, double* res, double* rel) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  if (c->m < 1) return fail(KRY_ERR_DIMENSION, "no completed projection blocks yet");
+  return check_lyap(c, beta2, res, rel);
+}
+
+int kry_check_sylv(kry_ctx* a, kry_ctx* b, double rhs_norm, double* res, double* rel) {
+  KRY_CUDA(cudaSetDevice(a->dev));
+  if (a->m < 1 || b->m < 1) return fail(KRY_ERR_DIMENSION, "no completed projection blocks yet");
+  return check_sylv(a, b, rhs_norm, res, rel);
+}
+
+int kry_solve_lyap_pass1(kry_ctx* c, double tol, int max_m, int check_period, double* history,
+                         int* n_history, int* iterations, double* final_rel, int* reason) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  if (!c->initialized) return fail(KRY_ERR_STATE, "init_basis has not been called");
+  if (max_m > c->max_m) return fail(KRY_ERR_ARGUMENT, "max_m exceeds the context capacity");
+  double t_basis = 0.0, t_res = 0.0;
+  int nh = 0;
+  *iterations = 0;
+  *reason = 1;
+  double rel = INFINITY;
+  for (int it = 1; it <= max_m; ++it) {
+    double t0 = now_s();
+    int ex = 0;
+    KRY_CHECK(step_pass1(c, 1, &ex));
+    KRY_CUDA(cudaStreamSynchronize(c->stream));
+    t_basis += now_s() - t0;
+    if (it % check_period == 0 || ex) {
+      t0 = now_s();
+      double res = 0.0;
+      KRY_CHECK(check_lyap(c, c->beta2, &res, &rel));
+      t_res += now_s() - t0;
+      double* row = history + (size_t)nh * 5;
+      row[0] = it; row[1] = (double)it * c->s; row[2] = rel; row[3] = t_basis; row[4] = t_res;
+      ++nh;
+      *n_history = nh;
+      *final_rel = rel;
+      if (rel <= tol) {
+        *iterations = it;
+        *reason = 0;
+        c->m_final = it;
+        return KRY_OK;
+      }
+      if (ex) {
+        *reason = 2;
+        return fail(KRY_ERR_CONVERGENCE, "invariant");
+      }
+    }
+  }
+  *n_history = nh;
+  return fail(KRY_ERR_CONVERGENCE, "max_m");
+}
+
+int kry_solve_sylv_pass1(kry_ctx* a, kry_ctx* b, double tol, int max_m, int check_period,
+                         double* history, int* n_history, int* iterations, double* final_rel,
+                         int* reason) {
+  KRY_CUDA(cudaSetDevice(a->dev));
+  if (!a->initialized || !b->initialized) return fail(KRY_ERR_STATE, "init_basis has not been called");
+  if (max_m > a->max_m || max_m > b->max_m)
+    return fail(KRY_ERR_ARGUMENT, "max_m exceeds the context capacity");
+  const double rhs_norm = sqrt(a->beta2) * sqrt(b->beta2);
+  double t_basis = 0.0, t_res = 0.0;
+  int nh = 0;
+  *iterations = 0;
+  *reason = 1;
+  double rel = INFINITY;
+  for (int it = 1; it <= max_m; ++it) {
+    double t0 = now_s();
+    int ex = 0;
+    if (!a->exhausted) KRY_CHECK(step_pass1(a, 1, &ex));
+    if (!b->exhausted) KRY_CHECK(step_pass1(b, 1, &ex));
+    KRY_CUDA(cudaStreamSynchronize(a->stream));
+    KRY_CUDA(cudaStreamSynchronize(b->stream));
+    t_basis += now_s() - t0;
+    const bool both = a->exhausted && b->exhausted;
+    if (it % check_period == 0 || both) {
+      t0 = now_s();
+      double res = 0.0;
+      KRY_CHECK(check_sylv(a, b, rhs_norm, &res, &rel));
+      t_res += now_s() - t0;
+      double* row = history + (size_t)nh * 5;
+      row[0] = it; row[1] = (double)it * a->s; row[2] = rel; row[3] = t_basis; row[4] = t_res;
+      ++nh;
+      *n_history = nh;
+      *final_rel = rel;
+      if (rel <= tol) {
+        *iterations = it;
+        *reason = 0;
+        a->m_final = a->m;
+        b->m_final = b->m;
+        return KRY_OK;
+      }
+      if (both) {
+        *reason = 2;
+        return fail(KRY_ERR_CONVERGENCE, "invariant");
+      }
+    }
+  }
+  *n_history = nh;
+  return fail(KRY_ERR_CONVERGENCE, "max_m");
+}
+
+int kry_finalize_lyap(kry_ctx* c, double eps, int* rank, double* discarded) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  if (c->m_final < 1) c->m_final = c->m;
+  if (c->m_final < 1) return fail(KRY_ERR_STATE, "nothing to finalise");
+  KRY_CHECK(ensure_handles(c));
+  FinalBufs b;
+  int k = 0;
+  int rc = final_eig(c, b, &k);
+  double *Y = nullptr, *mu = nullptr, *mind = nullptr, *work = nullptr, *outd = nullptr,
+         *factor = nullptr;
+  double hout[8];
+  double lmax = 0.0;
+  auto cleanup = [&]() {
+    b.free_all();
+    for (double* p : {Y, mu, mind, work, outd, factor})
+      if (p) cudaFree(p);
+  };
+  if (rc != KRY_OK) { cleanup(); return rc; }
+  KRY_CUDA(cudaMemcpy(&lmax, b.lam + (k - 1), sizeof(double), cudaMemcpyDeviceToHost));
+  if (lmax >= 0.0) {
+    cleanup();
+    return fail(KRY_ERR_INDEFINITE, "projected matrix is not negative definite");
+  }
+  if ((rc = dalloc(&Y, (size_t)k * k)) || (rc = dalloc(&mu, (size_t)k)) ||
+      (rc = dalloc(&mind, 1024)) || (rc = dalloc(&work, (size_t)k)) || (rc = dalloc(&outd, 8))) {
+    cleanup();
+    return rc;
+  }
+  int nparts = 0;
+  rc = launch_ytilde(c->stream, b.u, b.lam, k, b.u, b.lam, k, c->s, Y, k, mind, &nparts);
+  if (rc == KRY_OK) rc = syevd(c, Y, k, mu);
+  if (rc == KRY_OK) rc = launch_truncate(c->stream, mu, k, 0, eps, mind, nparts, work, outd);
+  if (rc != KRY_OK) { cleanup(); return rc; }
+  KRY_CUDA(cudaMemcpy(hout, outd, 5 * sizeof(double), cudaMemcpyDeviceToHost));
+  double lmin_abs = 0.0;
+  {
+    double l0;
+    KRY_CUDA(cudaMemcpy(&l0, b.lam, sizeof(double), cudaMemcpyDeviceToHost));
+    lmin_abs = std::max(fabs(l0), fabs(lmax));
+  }
+  if (hout[4] < 1e-14 * lmin_abs) {
+    cleanup();
+    return fail(KRY_ERR_INDEFINITE,
+                "eigenvalue-sum denominator is numerically singular; coefficient matrices must be "
+                "definite (of one sign)");
+  }
+  if (hout[2] < -1e-10 * hout[3]) {
+    char buf[160];
+    snprintf(buf, sizeof(buf), "matrix is significantly indefinite (min eigenvalue %.3e)", hout[2]);
+    cleanup();
+    return fail(KRY_ERR_INDEFINITE, buf);
+  }
+  const int r = (int)hout[0];
+  c->discarded = hout[1];
+  if (r > 0) {
+    if ((rc = dalloc(&factor, (size_t)k * r))) { cleanup(); return rc; }
+    rc = launch_scale_factor(c->stream, Y, k, mu, k, r, 0, 0, factor);
+    if (rc == KRY_OK) rc = set_qy(c, b.Td, k, factor, r);
+  } else {
+    rc = set_qy(c, b.Td, k, nullptr, 0);
+  }
+  KRY_CUDA(cudaStreamSynchronize(c->stream));
+  cleanup();
+  if (rc != KRY_OK) return rc;
+  *rank = r;
+  *discarded = c->discarded;
+  return KRY_OK;
+}
+
+int kry_finalize_sylv(kry_ctx* a, kry_ctx* bb, double eps, int* rank, double* discarded) {
+  KRY_CUDA(cudaSetDevice(a->dev));
+  if (a->m_final < 1) a->m_final = a->m;
+  if (bb->m_final < 1) bb->m_final = bb->m;
+  KRY_CHECK(ensure_handles(a));
+  KRY_CHECK(ensure_handles(bb));
+  KRY_CUDA(cudaStreamSynchronize(bb->stream));
+  FinalBufs fa, fb;
+  int kA = 0, kB = 0;
+  int rc = final_eig(a, fa, &kA);
+  if (rc == KRY_OK) rc = final_eig(bb, fb, &kB);
+  KRY_CUDA(cudaStreamSynchronize(bb->stream));
+  double *Y = nullptr, *sig = nullptr, *U = nullptr, *VT = nullptr, *mind = nullptr,
+         *work = nullptr, *outd = nullptr, *f1 = nullptr, *f2 = nullptr, *gw = nullptr;
+  int* info = nullptr;
+  auto cleanup = [&]() {
+    fa.free_all();
+    fb.free_all();
+    for (double* p : {Y, sig, U, VT, mind, work, outd, f1, f2, gw})
+      if (p) cudaFree(p);
+    if (info) cudaFree(info);
+  };
+  if (rc != KRY_OK) { cleanup(); return rc; }
+  double la[2], lb[2];
+  KRY_CUDA(cudaMemcpy(&la[0], fa.lam, sizeof(double), cudaMemcpyDeviceToHost));
+  KRY_CUDA(cudaMemcpy(&la[1], fa.lam + kA - 1, sizeof(double), cudaMemcpyDeviceToHost));
+  KRY_CUDA(cudaMemcpy(&lb[0], fb.lam, sizeof(double), cudaMemcpyDeviceToHost));
+  KRY_CUDA(cudaMemcpy(&lb[1], fb.lam + kB - 1, sizeof(double), cudaMemcpyDeviceToHost));
+  if (la[1] >= 0.0 || lb[1] >= 0.0) {
+    cleanup();
+    return fail(KRY_ERR_INDEFINITE, "a projected matrix is not negative definite");
+  }
+  // SVD needs rows >= cols: work on Ytilde (kA x kB) or its transpose
+  const bool tr = kA < kB;
+  const int M = tr ? kB : kA, N = tr ? kA : kB;
+  if ((rc = dalloc(&Y, (size_t)M * N)) || (rc = dalloc(&sig, (size_t)N)) ||
+      (rc = dalloc(&U, (size_t)M * N)) || (rc = dalloc(&VT, (size_t)N * N)) ||
+      (rc = dalloc(&mind, 1024)) || (rc = dalloc(&work, (size_t)N + 8)) ||
+      (rc = dalloc(&outd, 8)) || (rc = dalloc(&info, 1))) {
+    cleanup();
+    return rc;
+  }
+  int nparts = 0;
+  if (!tr)
+    rc = launch_ytilde(a->stream, fa.u, fa.lam, kA, fb.u, fb.lam, kB, a->s, Y, kA, mind, &nparts);
+  else
+    rc = launch_ytilde(a->stream, fb.u, fb.lam, kB, fa.u, fa.lam, kA, a->s, Y, kB, mind, &nparts);
+  if (rc != KRY_OK) { cleanup(); return rc; }
+  int lwork = 0;
+  if (cusolverDnDgesvd_bufferSize(a->solver, M, N, &lwork) != CUSOLVER_STATUS_SUCCESS) {
+    cleanup();
+    return fail(KRY_ERR_FACTORIZATION, "gesvd buffer query failed");
+  }
+  if ((rc = dalloc(&gw, (size_t)lwork + 1))) { cleanup(); return rc; }
+  signed char jobu = 'S', jobvt = 'S';
+  auto sst = cusolverDnDgesvd(a->solver, jobu, jobvt, M, N, Y, M, sig, U, M, VT, N, gw, lwork,
+                              nullptr, info);
+  int hinfo = 0;
+  KRY_CUDA(cudaMemcpy(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost));
+  if (sst != CUSOLVER_STATUS_SUCCESS || hinfo != 0) {
+    cleanup();
+    return fail(KRY_ERR_FACTORIZATION, "SVD did not converge");
+  }
+  rc = launch_truncate(a->stream, sig, N, 1, eps, mind, nparts, work, outd);
+  double hout[8];
+  KRY_CUDA(cudaMemcpy(hout, outd, 5 * sizeof(double), cudaMemcpyDeviceToHost));
+  const double scale = std::max(std::max(fabs(la[0]), fabs(la[1])), std::max(fabs(lb[0]), fabs(lb[1])));
+  if (hout[4] < 1e-14 * scale) {
+    cleanup();
+    return fail(KRY_ERR_INDEFINITE,
+                "eigenvalue-sum denominator is numerically singular; coefficient matrices must be "
+                "definite (of one sign)");
+  }
+  const int r = (int)hout[0];
+  if (r > 0) {
+    if ((rc = dalloc(&f1, (size_t)kA * r)) || (rc = dalloc(&f2, (size_t)kB * r))) {
+      cleanup();
+      return rc;
+    }
+    if (!tr) {
+      // Ytilde = U S VT: f1 = U[:, :r] sqrt(s), f2 = VT[:r]^T sqrt(s)
+      launch_scale_factor(a->stream, U, M, sig, kA, r, 1, 0, f1);
+      launch_scale_factor(a->stream, VT, N, sig, kB, r, 1, 1, f2);
+    } else {
+      // Ytilde^T = U S VT -> Ytilde = VT^T S U^T
+      launch_scale_factor(a->stream, VT, N, sig, kA, r, 1, 1, f1);
+      launch_scale_factor(a->stream, U, M, sig, kB, r, 1, 0, f2);
+    }
+    rc = set_qy(a, fa.Td, kA, f1, r);
+    if (rc == KRY_OK) {
+      KRY_CUDA(cudaStreamSynchronize(a->stream));
+      rc = set_qy(bb, fb.Td, kB, f2, r);
+    }
+  } else {
+    set_qy(a, fa.Td, kA, nullptr, 0);
+    set_qy(bb, fb.Td, kB, nullptr, 0);
+  }
+  KRY_CUDA(cudaStreamSynchronize(a->stream));
+  KRY_CUDA(cudaStreamSynchronize(bb->stream));
+  cleanup();
+  if (rc != KRY_OK) return rc;
+  a->discarded = bb->discarded = hout[1];
+  *rank = r;
+  *discarded = hout[1];
+  return KRY_OK;
+}
+
+// pass 2 (solvers.py:130-169): regenerate V_2..V_m from C with the same
+// deterministic kernels (coupling blocks compared against pass 1), buffer G
+// blocks in an interleaved chunk and fold them into Z with one DGEMM per chunk
+int kry_recover(kry_ctx* c, double* zhost) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  if (c->rank < 0) return fail(KRY_ERR_STATE, "finalize has not been called");
+  KRY_CHECK(ensure_handles(c));
+  const int s = c->s, m = c->m_final, r = c->rank;
+  const int64_t n = c->n;
+  if (c->Z && c->z_cap < n * std::max(r, 1)) { cudaFree(c->Z); c->Z = nullptr; }
+  if (!c->Z) {
+    KRY_CHECK(dalloc(&c->Z, (size_t)n * std::max(r, 1)));
+    c->z_cap = n * std::max(r, 1);
+  }
+  if (r == 0) {
+    if (zhost) { /* nothing to copy */ }
+    return KRY_OK;
+  }
+  // chunk size from free memory (keep half of it free)
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  const size_t blk_bytes = (size_t)n * s * sizeof(double);
+  int64_t G = (int64_t)((fr / 2) / blk_bytes) - 2;
+  if (G > 64) G = 64;
+  if (G > m) G = m;
+  if (G < 1) G = 1;
+  const int64_t nslot = G + 2;
+  const int64_t ld2 = nslot * s;
+  const int64_t halo = (c->op.kind == KRY_OP_STENCIL) ? c->op.nxy : 0;
+  double* buf = nullptr;
+  double* Qc = nullptr;
+  KRY_CHECK(dalloc(&buf, (size_t)(n + 2 * halo) * ld2));
+  if (dalloc(&Qc, (size_t)G * s * r) != KRY_OK) { cudaFree(buf); return KRY_ERR_CUDA; }
+  KRY_CUDA(cudaMemsetAsync(buf, 0, (n + 2 * halo) * ld2 * sizeof(double), c->stream));
+  double* base = buf + halo * ld2;
+  auto sp = [&](int64_t q) { return base + q * s; };
+  int rc = KRY_OK;
+  int first_gemm = 1;
+  auto gemm_chunk = [&](int blk0, int nblk) -> int {  // blk0 0-based
+    KRY_CHECK(launch_chunk_coef(c->stream, c->T.S, c->qy, s, r, blk0, nblk, Qc));
+    const double one = 1.0;
+    const double beta = first_gemm ? 0.0 : 1.0;
+    if (cublasDgemm(c->cublas, CUBLAS_OP_N, CUBLAS_OP_N, r, (int)n, nblk * s, &one, Qc, r, sp(2),
+                    (int)ld2, &beta, c->Z, r) != CUBLAS_STATUS_SUCCESS)
+      return fail(KRY_ERR_CUDA, "cublasDgemm (Z accumulation) failed");
+    first_gemm = 0;
+    return KRY_OK;
+  };
+  // regenerate V_1 into slot 2
+  rc = do_init(c, sp(2), ld2, 1);
+  int cur = 2, old = -1;
+  int chunk_first = 1;  // block index (1-based) held in slot 2
+  for (int j = 1; rc == KRY_OK && j < m; ++j) {
+    // coefficient solve j on V_j (replay) ; V_{j+1} goes to slot cur+1
+    ApplyGramCall ag{sp(cur), ld2, n, 1, POST_STEP, 0};
+    rc = launch_apply_gram(c->stream, s, c->op, ag, c->st, c->T, c->g, c->grid);
+    if (rc) break;
+    rc = sync_status(c);
+    if (rc) break;
+    rc = map_status(c, ("second pass step " + std::to_string(j)).c_str());
+    if (rc) break;
+    int nxt = cur + 1;
+    if (nxt == nslot) {
+      // chunk complete: S_j known now -> fold blocks chunk_first..j into Z
+      rc = gemm_chunk(chunk_first - 1, j - chunk_first + 1);
+      if (rc) break;
+      rc = launch_copy_block(c->stream, s, sp(nslot - 2), ld2, sp(0), ld2, n);
+      if (rc == KRY_OK) rc = launch_copy_block(c->stream, s, sp(nslot - 1), ld2, sp(1), ld2, n);
+      if (rc) break;
+      old = 0; cur = 1; nxt = 2;
+      chunk_first = j + 1;
+    }
+    int ex = 0;
+    if (c->st_h->flags & KRY_FLAG_FALLBACK) {
+      rc = explicit_step(c, j, old >= 0 ? sp(old) : nullptr, sp(cur), sp(nxt), ld2, 1, &ex);
+    } else {
+      CombineCall cc{old >= 0 ? sp(old) : nullptr, ld2, sp(cur), ld2, sp(nxt), ld2, n,
+                     j > 1 ? 1 : 0, 1, 1, 1};
+      rc = launch_combine(c->stream, s, c->op, cc, c->st, c->T, c->g, c->grid, nullptr, nullptr);
+    }
+    if (rc) break;
+    if (ex) { rc = fail(KRY_ERR_RECURRENCE, "second pass hit an invariant subspace early"); break; }
+    old = cur;
+    cur = nxt;
+  }
+  if (rc == KRY_OK && m >= 1) {
+    // coefficient solve m: S_m (and the replay check of coupling m-1)
+    ApplyGramCall ag{sp(cur), ld2, n, 1, POST_STEP, 0};
+    rc = launch_apply_gram(c->stream, s, c->op, ag, c->st, c->T, c->g, c->grid);
+    if (rc == KRY_OK) rc = sync_status(c);
+    if (rc == KRY_OK) rc = gemm_chunk(chunk_first - 1, m - chunk_first + 1);
+  }
+  if (rc == KRY_OK) rc = sync_status(c);
+  if (rc == KRY_OK && c->st_h->replay_err > 1e-8) {
+    rc = fail(KRY_ERR_RECURRENCE,
+              "second pass regenerated a coupling block that differs from the stored one; the "
+              "operator looks nondeterministic");
+  }
+  if (rc == KRY_OK && zhost) {
+    KRY_CUDA(cudaMemcpyAsync(zhost, c->Z, (size_t)n * r * sizeof(double), cudaMemcpyDeviceToHost,
+                             c->stream));
+    KRY_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  cudaStreamSynchronize(c->stream);
+  cudaFree(buf);
+  cudaFree(Qc);
+  return rc;
+}
+
+int kry_get_factor(kry_ctx* c, double* zhost) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  if (!c->Z || c->rank < 1) return KRY_OK;
+  KRY_CUDA(cudaMemcpy(zhost, c->Z, (size_t)c->n * c->rank * sizeof(double), cudaMemcpyDeviceToHost));
+  return KRY_OK;
+}
+
+// ---------------------------------------------------------------- standalone projected kernels
+namespace {
+struct Standalone {
+  EigEngine eig;
+  double* dmem = nullptr;
+  double *dsym = nullptr, *tsub = nullptr, *qlast = nullptr, *aux = nullptr;
+  cudaStream_t st = nullptr;
+  int s = 0, m = 0;
+  int build(int device, int s_, int m_, const double* diag, const double* sub) {
+    s = s_; m = m_;
+    KRY_CUDA(cudaSetDevice(device));
+    KRY_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    KRY_CHECK(dalloc(&dmem, (size_t)(4 * (m + 1) + 8) * 64));
+    KRY_CUDA(cudaMemset(dmem, 0, (size_t)(4 * (m + 1) + 8) * 64 * sizeof(double)));
+    double* raw_d = dmem;
+    double* raw_s = dmem + (int64_t)(m + 1) * 64;
+    dsym = dmem + (int64_t)2 * (m + 1) * 64;
+    tsub = dmem + (int64_t)3 * (m + 1) * 64;
+    qlast = dmem + (int64_t)4 * (m + 1) * 64;
+    aux = qlast + 64;
+    std::vector<double> hd((size_t)(m + 1) * 64, 0.0), hs((size_t)(m + 1) * 64, 0.0);
+    for (int b = 0; b < m; ++b)
+      for (int r = 0; r < s; ++r)
+        for (int q = 0; q < s; ++q) hd[(size_t)b * 64 + r * 8 + q] = diag[((size_t)b * s + r) * s + q];
+    for (int b = 0; b + 1 < m; ++b)
+      for (int r = 0; r < s; ++r)
+        for (int q = 0; q < s; ++q) hs[(size_t)b * 64 + r * 8 + q] = sub[((size_t)b * s + r) * s + q];
+    KRY_CUDA(cudaMemcpy(raw_d, hd.data(), hd.size() * sizeof(double), cudaMemcpyHostToDevice));
+    KRY_CUDA(cudaMemcpy(raw_s, hs.data(), hs.size() * sizeof(double), cudaMemcpyHostToDevice));
+    k_canonicalize<<<1, 32, 0, st>>>(raw_d, raw_s, s, m, dsym, tsub, qlast);
+    count_launch();
+    KRY_CHECK(eig.init(s, s * m + 8, device));
+    for (int j = 1; j <= m; ++j)
+      KRY_CHECK(eig.append_block(st, dsym + (int64_t)(j - 1) * 64,
+                                 j >= 2 ? tsub + (int64_t)(j - 2) * 64 : nullptr));
+    KRY_CUDA(cudaStreamSynchronize(st));
+    return KRY_OK;
+  }
+  ~Standalone() {
+    eig.release();
+    if (dmem) cudaFree(dmem);
+    if (st) cudaStreamDestroy(st);
+  }
+};
+}  // namespace
+
+int kry_partial_eig(int device, int s, int m, const double* diag, const double* sub, double* lam,
+                    double* first_rows, double* last_rows) {
+  if (s < 1 || s > KRY_SMAX || m < 1) return fail(KRY_ERR_ARGUMENT, "bad block sizes");
+  Standalone S;
+  KRY_CHECK(S.build(device, s, m, diag, sub));
+  const int k = s * m;
+  double* lastd = nullptr;
+  KRY_CHECK(dalloc(&lastd, (size_t)s * k));
+  k_map_rows<<<(k + 255) / 256, 256, 0, S.st>>>(S.qlast, S.eig.L_cur(), S.eig.kmax, k, s, lastd);
+  count_launch();
+  KRY_CUDA(cudaMemcpyAsync(lam, S.eig.lam_cur(), k * sizeof(double), cudaMemcpyDeviceToHost, S.st));
+  KRY_CUDA(cudaMemcpy2DAsync(first_rows, k * sizeof(double), S.eig.F_cur(),
+                             S.eig.kmax * sizeof(double), k * sizeof(double), s,
+                             cudaMemcpyDeviceToHost, S.st));
+  KRY_CUDA(cudaMemcpyAsync(last_rows, lastd, (size_t)s * k * sizeof(double),
+                           cudaMemcpyDeviceToHost, S.st));
+  KRY_CUDA(cudaStreamSynchronize(S.st));
+  cudaFree(lastd);
+  return KRY_OK;
+}
+
+static int upload88(cudaStream_t st, double* dst, const double* h, int s) {
+  double t[64] = {0};
+  for (int r = 0; r < s; ++r)
+    for (int q = 0; q < s; ++q) t[r * 8 + q] = h[r * s + q];
+  KRY_CUDA(cudaMemcpyAsync(dst, t, 64 * sizeof(double), cudaMemcpyHostToDevice, st));
+  KRY_CUDA(cudaStreamSynchronize(st));
+  return KRY_OK;
+}
+
+int kry_ctri_lyap_blocks(int device, int s, int m, const double* diag, const double* sub,
+                         const double* gamma, const double* tau, double* res) {
+  if (s < 1 || s > KRY_SMAX || m < 1) return fail(KRY_ERR_ARGUMENT, "bad block sizes");
+  Standalone S;
+  KRY_CHECK(S.build(device, s, m, diag, sub));
+  double* g = S.aux;            // gamma
+  double* t = S.aux + 64;       // tau
+  double* tq = S.aux + 128;     // tau * Q_last
+  KRY_CHECK(upload88(S.st, g, gamma, s));
+  KRY_CHECK(upload88(S.st, t, tau, s));
+  k_mat_mul88<<<1, 64, 0, S.st>>>(t, S.qlast, tq);
+  count_launch();
+  KRY_CHECK(S.eig.residual_lyap(S.st, g, tq));
+  k_scale_of<<<1, 32, 0, S.st>>>(S.eig.lam_cur(), S.eig.K, S.eig.lam_cur(), S.eig.K, S.eig.res + 2);
+  count_launch();
+  double h[3];
+  KRY_CUDA(cudaMemcpyAsync(h, S.eig.res, 3 * sizeof(double), cudaMemcpyDeviceToHost, S.st));
+  KRY_CUDA(cudaStreamSynchronize(S.st));
+  if (h[1] < 1e-14 * h[2])
+    return fail(KRY_ERR_INDEFINITE,
+                "eigenvalue-sum denominator is numerically singular; coefficient matrices must be "
+                "definite (of one sign)");
+  *res = sqrt(2.0 * fmax(h[0], 0.0));
+  return KRY_OK;
+}
+
+int kry_ctri_sylv_blocks(int device, int s, int m1, const double* diag1, const double* sub1, int m2,
+                         const double* diag2, const double* sub2, const double* gamma1,
+                         const double* gamma2, const double* tau, const double* iota, double* res) {
+  if (s < 1 || s > KRY_SMAX || m1 < 1 || m2 < 1) return fail(KRY_ERR_ARGUMENT, "bad block sizes");
+  Standalone A, B;
+  KRY_CHECK(A.build(device, s, m1, diag1, sub1));
+  KRY_CHECK(B.build(device, s, m2, diag2, sub2));
+  double *g1 = A.aux, *t1 = A.aux + 64, *tq1 = A.aux + 128;
+  double *g2 = B.aux, *t2 = B.aux + 64, *tq2 = B.aux + 128;
+  KRY_CHECK(upload88(A.st, g1, gamma1, s));
+  KRY_CHECK(upload88(A.st, t1, tau, s));
+  KRY_CHECK(upload88(B.st, g2, gamma2, s));
+  KRY_CHECK(upload88(B.st, t2, iota, s));
+  k_mat_mul88<<<1, 64, 0, A.st>>>(t1, A.qlast, tq1);
+  k_mat_mul88<<<1, 64, 0, B.st>>>(t2, B.qlast, tq2);
+  count_launch(2);
+  KRY_CHECK(A.eig.compute_uw(A.st, g1, tq1));
+  KRY_CHECK(B.eig.compute_uw(B.st, g2, tq2));
+  KRY_CUDA(cudaStreamSynchronize(B.st));
+  const int kA = A.eig.K, kB = B.eig.K;
+  KRY_CHECK(A.eig.cauchy(A.st, kB, B.eig.lam_cur(), B.eig.u, kA, A.eig.lam_cur(), A.eig.u,
+                         A.eig.w, A.eig.res));
+  KRY_CHECK(A.eig.cauchy(A.st, kA, A.eig.lam_cur(), A.eig.u, kB, B.eig.lam_cur(), B.eig.u,
+                         B.eig.w, A.eig.res + 4));
+  k_scale_of<<<1, 32, 0, A.st>>>(A.eig.lam_cur(), kA, B.eig.lam_cur(), kB, A.eig.res + 2);
+  count_launch();
+  double h[6];
+  KRY_CUDA(cudaMemcpyAsync(h, A.eig.res, 6 * sizeof(double), cudaMemcpyDeviceToHost, A.st));
+  KRY_CUDA(cudaStreamSynchronize(A.st));
+  if (std::min(h[1], h[5]) < 1e-14 * h[2])
+    return fail(KRY_ERR_INDEFINITE,
+                "eigenvalue-sum denominator is numerically singular; coefficient matrices must be "
+                "definite (of one sign)");
+  *res = sqrt(fmax(h[0] + h[4], 0.0));
+  return KRY_OK;
+}
+
+int kry_true_lyap_residual(kry_ctx* c, const double* z, int t, const double* ch, double* res) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  KRY_CHECK(ensure_handles(c));
+  const int s = c->s;
+  const int64_t n = c->n;
+  const int p = 2 * t + s;
+  const int64_t halo = (c->op.kind == KRY_OP_STENCIL) ? c->op.nxy : 0;
+  double *M = nullptr, *zd = nullptr, *G = nullptr;
+  KRY_CHECK(dalloc(&M, (size_t)n * p));
+  KRY_CHECK(dalloc(&zd, (size_t)(n + 2 * halo) * std::max(t, 1)));
+  KRY_CHECK(dalloc(&G, (size_t)p * p));
+  KRY_CUDA(cudaMemsetAsync(zd, 0, (n + 2 * halo) * std::max(t, 1) * sizeof(double), c->stream));
+  double* zz = zd + halo * t;
+  KRY_CUDA(cudaMemcpyAsync(zz, z, n * t * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  // M = [A Z | Z | C] row-major n x p
+  for (int c0 = 0; c0 < t; c0 += KRY_SMAX) {
+    const int w = std::min(KRY_SMAX, t - c0);
+    KRY_CHECK(launch_apply_store(c->stream, w, c->op, zz + c0, t, M + c0, p, n));
+  }
+  KRY_CUDA(cudaMemcpy2DAsync(M + t, p * sizeof(double), zz, t * sizeof(double), t * sizeof(double),
+                             n, cudaMemcpyDeviceToDevice, c->stream));
+  KRY_CUDA(cudaMemcpy2DAsync(M + 2 * t, p * sizeof(double), ch, s * sizeof(double),
+                             s * sizeof(double), n, cudaMemcpyHostToDevice, c->stream));
+  const double one = 1.0, zero = 0.0;
+  // G = M^T M : col-major view of M is p x n (ld p)
+  if (cublasDgemm(c->cublas, CUBLAS_OP_N, CUBLAS_OP_T, p, p, (int)n, &one, M, p, M, p, &zero, G,
+                  p) != CUBLAS_STATUS_SUCCESS)
+    return fail(KRY_ERR_CUDA, "cublasDgemm (verify) failed");
+  std::vector<double> h((size_t)p * p);
+  KRY_CUDA(cudaMemcpyAsync(h.data(), G, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream));
+  KRY_CUDA(cudaStreamSynchronize(c->stream));
+  cudaFree(M); cudaFree(zd); cudaFree(G);
+  // solvers.py:104-115: sum((U^T U) * (W^T W)), U = [AZ, Z, C], W = [Z, AZ, C]
+  auto perm = [&](int i) { return i < t ? i + t : (i < 2 * t ? i - t : i); };
+  double val = 0.0;
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j) val += h[(size_t)i * p + j] * h[(size_t)perm(i) * p + perm(j)];
+  *res = sqrt(std::max(val, 0.0));
+  return KRY_OK;
+}
+
+int kry_profile_enable(kry_ctx* c, int enable) {
+  c->prof = enable != 0;
+  for (auto& e : c->ev_comb) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  c->ev_comb.clear();
+  return KRY_OK;
+}
+
+int kry_profile_read(kry_ctx* c, double* comb_ms, int* comb_n, double* apply_ms, int* apply_n) {
+  KRY_CUDA(cudaStreamSynchronize(c->stream));
+  double tot = 0.0;
+  for (auto& e : c->ev_comb) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e.first, e.second);
+    tot += ms;
+  }
+  *comb_ms = tot;
+  *comb_n = (int)c->ev_comb.size();
+  if (apply_ms) *apply_ms = 0.0;
+  if (apply_n) *apply_n = 0;
+  return KRY_OK;
+}
+
+int kry_timer(kry_ctx* c, int op, double* ms) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  if (!c->t_ev[0]) {
+    KRY_CUDA(cudaEventCreate(&c->t_ev[0]));
+    KRY_CUDA(cudaEventCreate(&c->t_ev[1]));
+  }
+  if (op == 0) {
+    KRY_CUDA(cudaEventRecord(c->t_ev[0], c->stream));
+    return KRY_OK;
+  }
+  KRY_CUDA(cudaEventRecord(c->t_ev[1], c->stream));
+  KRY_CUDA(cudaEventSynchronize(c->t_ev[1]));
+  float f = 0.f;
+  KRY_CUDA(cudaEventElapsedTime(&f, c->t_ev[0], c->t_ev[1]));
+  if (ms) *ms = f;
+  return KRY_OK;
+}
+
+int kry_nccl_unique_id(void* id128) {
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return fail(KRY_ERR_NCCL, "ncclGetUniqueId failed");
+  memcpy(id128, &id, sizeof(id));
+  return KRY_OK;
+}
+
+int kry_comm_init(kry_ctx* c, int nranks, int rank, const void* id128) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof(id));
+  if (ncclCommInitRank(&c->comm, nranks, id, rank) != ncclSuccess)
+    return fail(KRY_ERR_NCCL, "ncclCommInitRank failed");
+  c->nranks = nranks;
+  c->rank_id = rank;
+  return KRY_OK;
+}
+
+}  // extern "C"

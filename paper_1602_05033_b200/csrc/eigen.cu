@@ -1,0 +1,661 @@
+// Eigen data of the growing block-tridiagonal T_m and the cheap residual
+// norm (sm_100a, fp64).
+//
+// Reference: partial_eig_blocktridiag (kernels.py:296-306) = band reduction
+// (kernels.py:184-261, pure-Python Givens bulge chase) + tridiagonal
+// eigensolver (kernels.py:264-293), recomputed from scratch at every check,
+// then ctri_lyapunov / ctri_sylvester (residual.py:40-84).
+//
+// B200 design: T_m only ever grows by one block row (it is the leading
+// principal submatrix of T_{m+1}), so its eigen data are UPDATED instead of
+// recomputed.  Each scalar row k appended to T (bandwidth s, the couplings
+// live in the last s rows) turns the current eigenbasis into a bordered
+// (arrowhead) matrix  [diag(lam), z; z^T, d]  with z = L^T t, where L holds
+// the last s rows of the eigenvector matrix.  Its eigenpairs are obtained by
+// the Gu-Eisenstat scheme:
+//   E1 deflation (negligible z_j; Givens rotation of numerically equal poles)
+//   E2 secular equation  h(mu) = mu - d - sum z_j^2/(mu - lam_j)  for every
+//      root in parallel (rational two-pole iteration, origin at the nearer
+//      pole so mu - lam_j is formed without cancellation)
+//   E3 recomputed zhat_j^2 = -prod_i(lam_j - mu_i)/prod_{i!=j}(lam_j - lam_i)
+//      (guarantees numerically orthogonal eigenvectors)
+//   E4 eigenvectors v_i = [zhat_j/(mu_i - lam_j); 1]/norm applied to the
+//      tracked first s and last s rows, merged in sorted order.
+// Only lam (k), the first s rows F and the last s rows L of Q are stored,
+// O(s k) memory; an append costs O(s k^2) flops, fully parallel.
+// The residual is the fused Cauchy contraction
+//   M = ((u u^T) o C) w,  C_ij = 1/(lam_i + lam_j),  u = F^T gamma, w = L^T tau^T
+#include "kry_internal.cuh"
+#include "eigen.cuh"
+#include <cmath>
+#include <vector>
+#include <algorithm>
+
+namespace kry {
+
+static constexpr double EPS = 2.220446049250313e-16;
+
+// ------------------------------------------------------------------ block scan helpers
+__device__ __forceinline__ int warp_incl_scan(int v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+// exclusive scan over the block; returns the prefix, *total = block sum
+__device__ int block_excl_scan(int v, int* total) {
+  __shared__ int s_w[33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  int inc = warp_incl_scan(v);
+  if (lane == 31) s_w[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int x = (lane < nw) ? s_w[lane] : 0;
+    int xi = warp_incl_scan(x);
+    if (lane < nw) s_w[lane] = xi - x;
+    if (lane == 31) s_w[32] = xi;
+  }
+  __syncthreads();
+  int res = inc - v + s_w[warp];
+  *total = s_w[32];
+  __syncthreads();
+  return res;
+}
+
+__device__ double block_max(double v) {
+  __shared__ double s_r[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if (lane == 0) s_r[warp] = v;
+  __syncthreads();
+  double r = 0.0;
+  const int nw = blockDim.x >> 5;
+  for (int q = 0; q < nw; ++q) r = fmax(r, s_r[q]);
+  __syncthreads();
+  return r;
+}
+__device__ double block_sum(double v) {
+  __shared__ double s_r[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) s_r[warp] = v;
+  __syncthreads();
+  double r = 0.0;
+  const int nw = blockDim.x >> 5;
+  for (int q = 0; q < nw; ++q) r += s_r[q];
+  __syncthreads();
+  return r;
+}
+
+// ------------------------------------------------------------------ E1: coupling + deflation (1 CTA x 1024)
+__global__ void __launch_bounds__(1024) k_eig_deflate(EigView e, int K, const double* dsym_blk,
+                                                      const double* sub_prev, int a) {
+  const int s = e.s;
+  __shared__ double t[KRY_SMAX];
+  __shared__ double s_d, s_tol;
+  if (threadIdx.x < s) {
+    const int r = threadIdx.x;
+    double v;
+    if (r < s - a) v = sub_prev ? sub_prev[a * 8 + (a + r)] : 0.0;   // tau[a][a+r]
+    else v = dsym_blk[a * 8 + (r - (s - a))];                          // D[a][c], c < a
+    t[r] = v;
+  }
+  if (threadIdx.x == 0) s_d = dsym_blk[a * 8 + a];
+  __syncthreads();
+  const double d = s_d;
+  double zmax = 0.0, zabs = 0.0;
+  for (int j = threadIdx.x; j < K; j += blockDim.x) {
+    double z = 0.0;
+    for (int r = 0; r < s; ++r) z = fma(e.L_old[(int64_t)r * e.kmax + j], t[r], z);
+    e.z[j] = z;
+    zmax = fmax(zmax, fabs(z));
+    zabs += fabs(z);
+  }
+  zmax = block_max(zmax);
+  zabs = block_sum(zabs);
+  if (threadIdx.x == 0) {
+    double lm = 0.0;
+    if (K > 0) lm = fmax(fabs(e.lam_old[0]), fabs(e.lam_old[K - 1]));
+    s_tol = 8.0 * EPS * fmax(fmax(lm, fabs(d)), zmax);
+    e.scal[0] = d;
+    e.scal[1] = s_tol;
+    e.scal[2] = zabs;
+  }
+  __syncthreads();
+  const double tol = s_tol;
+  // pass 1: candidates = non-negligible z, compacted in eigenvalue order
+  int base = 0;
+  for (int c0 = 0; c0 < K; c0 += blockDim.x) {
+    const int j = c0 + threadIdx.x;
+    int keep = (j < K) && (fabs(e.z[j]) > tol);
+    int tot;
+    int pre = block_excl_scan(keep, &tot);
+    if (keep) e.cand[base + pre] = j;
+    if (j < K) e.dflag[j] = keep ? 0 : 1;
+    base += tot;
+  }
+  const int q = base;
+  __syncthreads();
+  // pass 2: pairs of consecutive candidates whose Givens rotation decouples
+  // one of them (kernels are LAPACK dlaed2's rule: |t c s| <= tol)
+  for (int i = 1 + threadIdx.x; i < q; i += blockDim.x) {
+    const int ja = e.cand[i - 1], jb = e.cand[i];
+    const double za = e.z[ja], zb = e.z[jb];
+    const double r = hypot(za, zb);
+    const double cth = zb / r, sth = za / r;
+    const double tt = e.lam_old[jb] - e.lam_old[ja];
+    e.pflag[i] = (fabs(tt * cth * sth) <= tol) ? 1 : 0;
+  }
+  if (threadIdx.x == 0 && q > 0) e.pflag[0] = 0;
+  __syncthreads();
+  // runs of flagged pairs are processed sequentially (one thread per run)
+  for (int i = 1 + threadIdx.x; i < q; i += blockDim.x) {
+    if (!e.pflag[i] || e.pflag[i - 1]) continue;
+    int prev = e.cand[i - 1];
+    for (int k = i; k < q && e.pflag[k]; ++k) {
+      const int cur = e.cand[k];
+      const double za = e.z[prev], zb = e.z[cur];
+      const double r = hypot(za, zb);
+      const double cth = zb / r, sth = za / r;
+      const double tt = e.lam_old[cur] - e.lam_old[prev];
+      if (fabs(tt * cth * sth) <= tol) {
+        const double l1 = e.lam_old[prev], l2 = e.lam_old[cur];
+        e.lam_old[prev] = cth * cth * l1 + sth * sth * l2;
+        e.lam_old[cur] = sth * sth * l1 + cth * cth * l2;
+        e.z[prev] = 0.0;
+        e.z[cur] = r;
+        for (int rr = 0; rr < s; ++rr) {
+          double* F = e.F_old + (int64_t)rr * e.kmax;
+          double* L = e.L_old + (int64_t)rr * e.kmax;
+          const double fa = F[prev], fb = F[cur];
+          F[prev] = cth * fa - sth * fb;
+          F[cur] = sth * fa + cth * fb;
+          const double la = L[prev], lb = L[cur];
+          L[prev] = cth * la - sth * lb;
+          L[cur] = sth * la + cth * lb;
+        }
+        e.dflag[prev] = 1;
+      }
+      prev = cur;
+    }
+  }
+  __syncthreads();
+  // pass 3: final poles and deflated list
+  int pb = 0, db = 0;
+  for (int c0 = 0; c0 < K; c0 += blockDim.x) {
+    const int j = c0 + threadIdx.x;
+    const int isd = (j < K) ? e.dflag[j] : 0;
+    const int isp = (j < K) ? 1 - isd : 0;
+    int tp, td;
+    int pp = block_excl_scan(isp, &tp);
+    int pd = block_excl_scan(isd, &td);
+    if (isp) {
+      e.poles[pb + pp] = e.lam_old[j];
+      e.zz[pb + pp] = e.z[j];
+      e.pmap[pb + pp] = j;
+    }
+    if (isd) {
+      e.def_idx[db + pd] = j;
+      e.def_lam[db + pd] = e.lam_old[j];
+    }
+    pb += tp;
+    db += td;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    e.counts[0] = pb;
+    e.counts[1] = db;
+    // rotated deflations can break the order of the deflated list locally:
+    // insertion-sort fix-up (rare, local disorder only)
+    for (int i = 1; i < db; ++i) {
+      double v = e.def_lam[i];
+      if (v >= e.def_lam[i - 1]) continue;
+      int ix = e.def_idx[i];
+      int k = i - 1;
+      while (k >= 0 && e.def_lam[k] > v) {
+        e.def_lam[k + 1] = e.def_lam[k];
+        e.def_idx[k + 1] = e.def_idx[k];
+        --k;
+      }
+      e.def_lam[k + 1] = v;
+      e.def_idx[k + 1] = ix;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ E2: secular roots
+__global__ void __launch_bounds__(128) k_eig_secular(EigView e) {
+  const int p = e.counts[0];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > p) return;
+  const double d = e.scal[0];
+  if (p == 0) {
+    e.org[0] = d;
+    e.tau[0] = 0.0;
+    e.mu[0] = d;
+    return;
+  }
+  const double* __restrict__ poles = e.poles;
+  const double* __restrict__ zz = e.zz;
+  const double zabs = e.scal[2];
+  const double lo = fmin(poles[0], d) - zabs - 1e-300;
+  const double hi = fmax(poles[p - 1], d) + zabs + 1e-300;
+  double org;
+  int ia, ib;
+  if (i == 0) {
+    org = poles[0]; ia = -1; ib = 0;
+  } else if (i == p) {
+    org = poles[p - 1]; ia = p - 1; ib = -1;
+  } else {
+    const double a = poles[i - 1], b = poles[i];
+    const double mid = 0.5 * (a + b);
+    double hm = mid - d;
+    for (int j = 0; j < p; ++j) {
+      const double zj = zz[j];
+      hm -= zj * zj / (mid - poles[j]);
+    }
+    if (hm > 0.0) { org = a; } else { org = b; }
+    ia = i - 1; ib = i;
+  }
+  const double da = (ia >= 0) ? poles[ia] - org : 0.0;
+  const double db = (ib >= 0) ? poles[ib] - org : 0.0;
+  double ta = (ia >= 0) ? da : lo - org;
+  double tb = (ib >= 0) ? db : hi - org;
+  double t = 0.5 * (ta + tb);
+  const double c0 = org - d;
+  for (int it = 0; it < 80; ++it) {
+    double psiL = 0.0, dpsiL = 0.0, psiR = 0.0, dpsiR = 0.0, sabs = 0.0;
+    for (int j = 0; j < p; ++j) {
+      const double zj = zz[j];
+      const double q = t - (poles[j] - org);
+      const double term = zj * zj / q;
+      const double dterm = term / q;
+      if (j <= ia) { psiL -= term; dpsiL += dterm; }
+      else { psiR -= term; dpsiR += dterm; }
+      sabs += fabs(term);
+    }
+    const double h = t + c0 + psiL + psiR;
+    const double err = 8.0 * EPS * (fabs(t) + fabs(c0) + sabs);
+    if (h > 0.0) tb = t; else ta = t;
+    if (fabs(h) <= err) break;
+    double tn;
+    bool ok = false;
+    if (ia >= 0 && ib >= 0) {
+      double w1, w2;
+      if (ia >= 0 && org == poles[ia]) {
+        w1 = dpsiL * (t - da) * (t - da);
+        w2 = (dpsiR + 1.0) * (t - db) * (t - db);
+      } else {
+        w1 = (dpsiL + 1.0) * (t - da) * (t - da);
+        w2 = dpsiR * (t - db) * (t - db);
+      }
+      const double c = h + w1 / (t - da) + w2 / (t - db);
+      const double A = c, B = c * (da + db) + w1 + w2, C = c * da * db + w1 * db + w2 * da;
+      if (A != 0.0) {
+        const double disc = fmax(B * B - 4.0 * A * C, 0.0);
+        const double sq = sqrt(disc);
+        double r1, r2;
+        if (B >= 0.0) { r1 = (B + sq) / (2.0 * A); r2 = (B + sq) != 0.0 ? 2.0 * C / (B + sq) : r1; }
+        else { r1 = (B - sq) != 0.0 ? 2.0 * C / (B - sq) : 0.0; r2 = (B - sq) / (2.0 * A); }
+        if (r1 > ta && r1 < tb) { tn = r1; ok = true; }
+        else if (r2 > ta && r2 < tb) { tn = r2; ok = true; }
+      } else if (B != 0.0) {
+        tn = C / B;
+        ok = (tn > ta && tn < tb);
+      }
+    } else {
+      const double psi = psiL + psiR, dpsi = dpsiL + dpsiR;
+      const double w = dpsi * t * t;
+      const double cc = psi + w / t;
+      const double B = c0 + cc;
+      const double sq = sqrt(B * B + 4.0 * w);
+      if (ib < 0) {  // top root, tau > 0
+        tn = (B >= 0.0) ? 2.0 * w / (B + sq) : 0.5 * (sq - B);
+      } else {       // bottom root, tau < 0
+        tn = (B > 0.0) ? -0.5 * (B + sq) : 2.0 * w / (B - sq);
+      }
+      ok = (tn > ta && tn < tb);
+    }
+    if (!ok || !isfinite(tn)) tn = 0.5 * (ta + tb);
+    if (fabs(tn - t) <= 4.0 * EPS * fabs(t)) { t = tn; break; }
+    t = tn;
+  }
+  e.org[i] = org;
+  e.tau[i] = t;
+  e.mu[i] = org + t;
+}
+
+// ------------------------------------------------------------------ E3: Gu-Eisenstat zhat
+__global__ void __launch_bounds__(128) k_eig_zhat(EigView e) {
+  const int p = e.counts[0];
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= p) return;
+  const double lj = e.poles[j];
+  // |lam_j - mu_i| = |(lam_j - org_i) - tau_i|
+  auto dm = [&](int i) { return fabs((lj - e.org[i]) - e.tau[i]); };
+  double prod = dm(j) * dm(j + 1);
+  for (int i = 0; i < j; ++i) prod *= dm(i) / fabs(lj - e.poles[i]);
+  for (int i = j + 1; i < p; ++i) prod *= dm(i + 1) / fabs(lj - e.poles[i]);
+  const double zh = sqrt(prod);
+  e.zhat[j] = (e.zz[j] >= 0.0) ? zh : -zh;
+}
+
+// ------------------------------------------------------------------ E4: eigenvectors, tracked rows, merge
+#define E4_CH 128
+__device__ __forceinline__ int count_le(const double* a, int n, double v) {  // # a[k] <= v
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] <= v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ int count_lt(const double* a, int n, double v) {  // # a[k] < v
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+template <int S>
+__global__ void __launch_bounds__(128) k_eig_vectors(EigView e, int K, int root_blocks) {
+  const int p = e.counts[0];
+  const int nd = e.counts[1];
+  const int64_t km = e.kmax;
+  if ((int)blockIdx.x >= root_blocks) {
+    // deflated columns: unchanged eigenpairs
+    const int k = (blockIdx.x - root_blocks) * blockDim.x + threadIdx.x;
+    if (k >= nd) return;
+    const int src = e.def_idx[k];
+    const double lv = e.def_lam[k];
+    const int pos = k + count_lt(e.mu, p + 1, lv);
+    e.lam_new[pos] = lv;
+#pragma unroll
+    for (int r = 0; r < S; ++r) e.F_new[r * km + pos] = e.F_old[r * km + src];
+#pragma unroll
+    for (int r = 0; r < S - 1; ++r) e.L_new[r * km + pos] = e.L_old[(r + 1) * km + src];
+    e.L_new[(S - 1) * km + pos] = 0.0;
+    if (K < S) e.F_new[K * km + pos] = 0.0;
+    return;
+  }
+  __shared__ double sP[E4_CH], sZ[E4_CH];
+  __shared__ double sF[S][E4_CH];
+  __shared__ double sL[S][E4_CH];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = i <= p;
+  double org = 0.0, tau = 0.0;
+  if (active) { org = e.org[i]; tau = e.tau[i]; }
+  double nrm2 = 0.0;
+  double aF[S], aL[S];
+#pragma unroll
+  for (int r = 0; r < S; ++r) aF[r] = aL[r] = 0.0;
+  for (int c0 = 0; c0 < p; c0 += E4_CH) {
+    __syncthreads();
+    const int jj = c0 + threadIdx.x;
+    if (jj < p) {
+      sP[threadIdx.x] = e.poles[jj];
+      sZ[threadIdx.x] = e.zhat[jj];
+      const int col = e.pmap[jj];
+#pragma unroll
+      for (int r = 0; r < S; ++r) sF[r][threadIdx.x] = e.F_old[r * km + col];
+#pragma unroll
+      for (int r = 0; r < S - 1; ++r) sL[r][threadIdx.x] = e.L_old[(r + 1) * km + col];
+    }
+    __syncthreads();
+    const int cnt = min(E4_CH, p - c0);
+    if (active) {
+      for (int q = 0; q < cnt; ++q) {
+        const double diff = tau - (sP[q] - org);   // mu_i - lam_j
+        const double v = sZ[q] / diff;
+        nrm2 = fma(v, v, nrm2);
+#pragma unroll
+        for (int r = 0; r < S; ++r) aF[r] = fma(sF[r][q], v, aF[r]);
+#pragma unroll
+        for (int r = 0; r < S - 1; ++r) aL[r] = fma(sL[r][q], v, aL[r]);
+      }
+    }
+  }
+  if (!active) return;
+  const double inv = 1.0 / sqrt(1.0 + nrm2);
+  const double mu = e.mu[i];
+  const int pos = i + count_le(e.def_lam, nd, mu);
+  e.lam_new[pos] = mu;
+#pragma unroll
+  for (int r = 0; r < S; ++r) e.F_new[r * km + pos] = aF[r] * inv;
+#pragma unroll
+  for (int r = 0; r < S - 1; ++r) e.L_new[r * km + pos] = aL[r] * inv;
+  e.L_new[(S - 1) * km + pos] = inv;
+  if (K < S) e.F_new[K * km + pos] = inv;
+}
+
+// ------------------------------------------------------------------ residual kernels
+// u[j][c] = sum_r F[r][j] gamma[r][c] ;  w[j][c] = sum_r L[r][j] tau[c][r]
+__global__ void k_uw(const double* F, const double* L, int64_t km, int k, int s,
+                     const double* gamma, const double* tau, double* u, double* w) {
+  __shared__ double g[64], tt[64];
+  if (threadIdx.x < 64) {
+    g[threadIdx.x] = gamma[threadIdx.x];
+    tt[threadIdx.x] = tau ? tau[threadIdx.x] : 0.0;
+  }
+  __syncthreads();
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+    for (int c = 0; c < s; ++c) {
+      double a = 0.0, b = 0.0;
+      for (int r = 0; r < s; ++r) {
+        a = fma(F[r * km + j], g[r * 8 + c], a);
+        b = fma(L[r * km + j], tt[c * 8 + r], b);
+      }
+      u[(int64_t)j * 8 + c] = a;
+      w[(int64_t)j * 8 + c] = b;
+    }
+  }
+}
+
+// out_x = sum_y (a_x . b_y) / (lx_x + ly_y) c_y ; partial sums of |out_x|^2 and
+// min |lx + ly|; the last CTA writes res[0] = sum, res[1] = min denominator
+#define CC_CH 128
+template <int S>
+__global__ void __launch_bounds__(128) k_cauchy(int nx, const double* lx, const double* ax,
+                                                int ny, const double* ly, const double* by,
+                                                const double* cy, double* partials,
+                                                unsigned* ticket, double* res) {
+  __shared__ double sl[CC_CH], sb[CC_CH][S], sc[CC_CH][S];
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = x < nx;
+  double a[S], acc[S];
+  double lxx = 0.0;
+#pragma unroll
+  for (int q = 0; q < S; ++q) { a[q] = active ? ax[(int64_t)x * 8 + q] : 0.0; acc[q] = 0.0; }
+  if (active) lxx = lx[x];
+  double mind = 1e300;
+  for (int c0 = 0; c0 < ny; c0 += CC_CH) {
+    __syncthreads();
+    const int yy = c0 + threadIdx.x;
+    if (yy < ny) {
+      sl[threadIdx.x] = ly[yy];
+#pragma unroll
+      for (int q = 0; q < S; ++q) {
+        sb[threadIdx.x][q] = by[(int64_t)yy * 8 + q];
+        sc[threadIdx.x][q] = cy[(int64_t)yy * 8 + q];
+      }
+    }
+    __syncthreads();
+    const int cnt = min(CC_CH, ny - c0);
+    if (active) {
+      for (int q = 0; q < cnt; ++q) {
+        double dot = 0.0;
+#pragma unroll
+        for (int r = 0; r < S; ++r) dot = fma(a[r], sb[q][r], dot);
+        const double den = lxx + sl[q];
+        mind = fmin(mind, fabs(den));
+        const double gq = dot / den;
+#pragma unroll
+        for (int r = 0; r < S; ++r) acc[r] = fma(gq, sc[q][r], acc[r]);
+      }
+    }
+  }
+  double ss = 0.0;
+#pragma unroll
+  for (int r = 0; r < S; ++r) ss = fma(acc[r], acc[r], ss);
+  // block reduction (fixed order)
+  __shared__ double rs[128], rm[128];
+  rs[threadIdx.x] = ss;
+  rm[threadIdx.x] = mind;
+  __syncthreads();
+  for (int o = 64; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      rs[threadIdx.x] += rs[threadIdx.x + o];
+      rm[threadIdx.x] = fmin(rm[threadIdx.x], rm[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partials[2 * blockIdx.x] = rs[0];
+    partials[2 * blockIdx.x + 1] = rm[0];
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ unsigned s_last;
+  if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) {
+    double tot = 0.0, mn = 1e300;
+    for (unsigned b = 0; b < gridDim.x; ++b) {
+      tot += __ldcg(partials + 2 * b);
+      mn = fmin(mn, __ldcg(partials + 2 * b + 1));
+    }
+    res[0] = tot;
+    res[1] = mn;
+    *ticket = 0u;
+  }
+}
+
+// ------------------------------------------------------------------ host side
+int EigEngine::init(int s_, int kmax_, int device) {
+  s = s_;
+  kmax = kmax_ + 8;
+  K = 0;
+  cur = 0;
+  dev = device;
+  const size_t nk = (size_t)kmax;
+  size_t doubles = 0;
+  doubles += 2 * nk;              // lam
+  doubles += 2 * 2 * nk * s;      // F, L ping-pong
+  doubles += 6 * nk + 8;          // z, poles, zz, zhat, def_lam, mu
+  doubles += 2 * (nk + 1);        // org, tau
+  doubles += 2 * nk * 8;          // u, w
+  doubles += 16;                  // scal
+  doubles += 4096;                // partials
+  doubles += 16;                  // res
+  KRY_CUDA(cudaMalloc(&dbuf, doubles * sizeof(double)));
+  KRY_CUDA(cudaMemset(dbuf, 0, doubles * sizeof(double)));
+  double* p = dbuf;
+  for (int b = 0; b < 2; ++b) { lam[b] = p; p += nk; }
+  for (int b = 0; b < 2; ++b) { F[b] = p; p += nk * s; }
+  for (int b = 0; b < 2; ++b) { L[b] = p; p += nk * s; }
+  z = p; p += nk; poles = p; p += nk; zz = p; p += nk; zhat = p; p += nk;
+  def_lam = p; p += nk; mu = p; p += nk + 8;
+  org = p; p += nk + 1; tau = p; p += nk + 1;
+  u = p; p += nk * 8; w = p; p += nk * 8;
+  scal = p; p += 16;
+  partials = p; p += 4096;
+  res = p; p += 16;
+  size_t ints = 5 * nk + 8;
+  KRY_CUDA(cudaMalloc(&ibuf, ints * sizeof(int)));
+  KRY_CUDA(cudaMemset(ibuf, 0, ints * sizeof(int)));
+  int* q = ibuf;
+  cand = q; q += nk; dflag = q; q += nk; pflag = q; q += nk; pmap = q; q += nk;
+  def_idx = q; q += nk; counts = q;
+  KRY_CUDA(cudaMalloc(&ticket, sizeof(unsigned) * 4));
+  KRY_CUDA(cudaMemset(ticket, 0, sizeof(unsigned) * 4));
+  return KRY_OK;
+}
+
+void EigEngine::release() {
+  if (dbuf) cudaFree(dbuf);
+  if (ibuf) cudaFree(ibuf);
+  if (ticket) cudaFree(ticket);
+  dbuf = nullptr; ibuf = nullptr; ticket = nullptr;
+}
+
+EigView EigEngine::view() const {
+  EigView v;
+  v.s = s; v.kmax = kmax;
+  v.lam_old = lam[cur]; v.lam_new = lam[1 - cur];
+  v.F_old = F[cur]; v.F_new = F[1 - cur];
+  v.L_old = L[cur]; v.L_new = L[1 - cur];
+  v.z = z; v.poles = poles; v.zz = zz; v.zhat = zhat; v.def_lam = def_lam; v.mu = mu;
+  v.org = org; v.tau = tau; v.scal = scal;
+  v.cand = cand; v.dflag = dflag; v.pflag = pflag; v.pmap = pmap; v.def_idx = def_idx;
+  v.counts = counts;
+  return v;
+}
+
+int EigEngine::append_block(cudaStream_t st, const double* dsym_blk, const double* sub_prev) {
+  if (K + s > kmax - 8) return fail(KRY_ERR_STATE, "eigen engine capacity exceeded");
+  for (int a = 0; a < s; ++a) {
+    EigView v = view();
+    k_eig_deflate<<<1, 1024, 0, st>>>(v, K, dsym_blk, sub_prev, a);
+    const int nroot_blocks = (K + 1 + 127) / 128;
+    k_eig_secular<<<nroot_blocks, 128, 0, st>>>(v);
+    const int npole_blocks = (K + 127) / 128;
+    if (npole_blocks > 0) k_eig_zhat<<<npole_blocks, 128, 0, st>>>(v);
+    const int ndef_blocks = (K + 127) / 128;
+    const int grid = nroot_blocks + ndef_blocks;
+#define L(S) k_eig_vectors<S><<<grid, 128, 0, st>>>(v, K, nroot_blocks)
+    switch (s) {
+      case 1: L(1); break; case 2: L(2); break; case 3: L(3); break; case 4: L(4); break;
+      case 5: L(5); break; case 6: L(6); break; case 7: L(7); break; case 8: L(8); break;
+      default: return fail(KRY_ERR_ARGUMENT, "block width s must be 1..8");
+    }
+#undef L
+    count_launch(npole_blocks > 0 ? 4 : 3);
+    KRY_CUDA(cudaGetLastError());
+    cur = 1 - cur;
+    K += 1;
+  }
+  return KRY_OK;
+}
+
+int EigEngine::cauchy(cudaStream_t st, int nx, const double* lx, const double* ax, int ny,
+                      const double* ly, const double* by, const double* cy, double* out2) {
+  int grid = (nx + 127) / 128;
+  if (grid > 2048) return fail(KRY_ERR_STATE, "residual grid too large");
+#define L(S) k_cauchy<S><<<grid, 128, 0, st>>>(nx, lx, ax, ny, ly, by, cy, partials, ticket, out2)
+  switch (s) {
+    case 1: L(1); break; case 2: L(2); break; case 3: L(3); break; case 4: L(4); break;
+    case 5: L(5); break; case 6: L(6); break; case 7: L(7); break; case 8: L(8); break;
+    default: return fail(KRY_ERR_ARGUMENT, "block width s must be 1..8");
+  }
+#undef L
+  count_launch();
+  KRY_CUDA(cudaGetLastError());
+  return KRY_OK;
+}
+
+int EigEngine::compute_uw(cudaStream_t st, const double* gamma, const double* tau_blk) {
+  int grid = (K + 255) / 256;
+  if (grid < 1) grid = 1;
+  k_uw<<<grid, 256, 0, st>>>(F[cur], L[cur], kmax, K, s, gamma, tau_blk, u, w);
+  count_launch();
+  KRY_CUDA(cudaGetLastError());
+  return KRY_OK;
+}
+
+// Lyapunov check: res = sqrt(2 sum_j |M_j|^2) ; writes res[0..1] on device
+int EigEngine::residual_lyap(cudaStream_t st, const double* gamma, const double* tau_blk) {
+  KRY_CHECK(compute_uw(st, gamma, tau_blk));
+  return cauchy(st, K, lam[cur], u, K, lam[cur], u, w, res);
+}
+
+}  // namespace kry

@@ -1,0 +1,18 @@
+#pragma once
+#include "kry_internal.cuh"
+
+namespace kry {
+int launch_assemble_T(cudaStream_t st, const double* dsym, const double* sub, int s, int m,
+                      double* Td);
+int launch_first_rows_times(cudaStream_t st, const double* Q, int k, int s, const double* gamma,
+                            double* u);
+int launch_ytilde(cudaStream_t st, const double* u, const double* lx, int nx, const double* v,
+                  const double* ly, int ny, int s, double* Y, int64_t ldy, double* mind_part,
+                  int* nparts);
+int launch_truncate(cudaStream_t st, const double* ev, int k, int desc, double eps,
+                    const double* mind_part, int nparts, double* work, double* out);
+int launch_scale_factor(cudaStream_t st, const double* W, int64_t ldw, const double* ev, int k,
+                        int rank, int desc, int transposed, double* factor);
+int launch_chunk_coef(cudaStream_t st, const double* S, const double* qy, int s, int rank,
+                      int blk0, int nblk, double* Qc);
+}  // namespace kry

@@ -1,0 +1,160 @@
+// Internal declarations of libkrymat_b200 (not part of the C-ABI).
+//
+// Data layout in HBM
+//   * block vectors: n x s row-major ("point major"): the s values of one grid
+//     point are contiguous; consecutive points are `ld` doubles apart (ld = s
+//     for the pass-1 window, ld = (G+2)*s for the interleaved pass-2 chunk
+//     buffer so that a chunk is one column-major (G*s) x n cuBLAS operand).
+//   * s x s blocks: fixed 8 x 8 row-major slots (s <= 8), zero padded.
+//   * projected matrix T_m: per-step slots of the raw MGS sums, symmetrised
+//     diagonal blocks, coupling blocks tau (R factors) and the lazy CholQR2
+//     corrections S_i (true basis block = stored block * S_i).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include "../../include/krymat_b200.h"
+
+#define KRY_SMAX 8
+#define KRY_SS 64
+
+namespace kry {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+extern thread_local std::string g_last_error;
+
+#define KRY_CUDA(call)                                                        \
+  do {                                                                        \
+    cudaError_t _e = (call);                                                  \
+    if (_e != cudaSuccess)                                                    \
+      return ::kry::fail(KRY_ERR_CUDA, std::string("CUDA error: ") +          \
+                                           cudaGetErrorString(_e) + " at " +  \
+                                           __FILE__ + ":" +                   \
+                                           std::to_string(__LINE__));         \
+  } while (0)
+
+#define KRY_CHECK(call)                                                       \
+  do {                                                                        \
+    int _rc = (call);                                                         \
+    if (_rc != KRY_OK) return _rc;                                            \
+  } while (0)
+
+void count_launch(int k = 1);
+
+// ---------------------------------------------------------------- operator
+struct OpDev {
+  int kind;      // KRY_OP_STENCIL / KRY_OP_CSR
+  int variable;  // stencil coefficient mode
+  int nx, ny;    // grid extents in x, y
+  int nzl;       // local z planes owned
+  int halo_lo, halo_hi;  // 1 if a neighbour plane exists below / above
+  int nxy;
+  double cd, cx, cy, cz;
+  const double *d, *ex, *ey, *ez;  // per point, offset so index 0 = first owned
+  const int64_t* rp;
+  const int* ci;
+  const double* va;
+};
+
+// ---------------------------------------------------------------- device state
+// Small per-context state living in device memory.  Written by the last CTA
+// of the reduction kernels, read by the next kernels; the host only reads the
+// status words.
+struct DevState {
+  double Goo[KRY_SS], Goc[KRY_SS], Gcc[KRY_SS], GoW[KRY_SS];
+  double GcW[KRY_SS], GWW[KRY_SS];
+  double So[KRY_SS], Sc[KRY_SS];
+  double R1prev[KRY_SS];
+  double M[3 * KRY_SS];      // Mo, Mc, Mw of the next combine
+  double gamma[KRY_SS];      // finalised gamma
+  double gram[KRY_SS * 3];   // scratch Gram result of generic reductions
+  double acc_a[KRY_SS], acc_b[KRY_SS];  // explicit-path MGS sums
+  double beta2;
+  double scale2, w2;
+  double replay_err;
+  int status;
+  int flags;                 // KRY_FLAG_*
+  int step;                  // completed coefficient solves
+  int replay;                // pass-2 regeneration: compare coupling blocks
+  int finalize_on_zero;
+  int s;
+  int has_old;
+  int pad_;
+};
+
+enum {
+  KRY_FLAG_EXHAUSTED = 1,
+  KRY_FLAG_FALLBACK = 2,
+};
+
+// post-reduction routines run by the last CTA of a Gram reduction
+enum PostMode {
+  POST_NONE = 0,        // store to st->gram
+  POST_P = 1,           // combine kernel: Goc, GoW, Gcc
+  POST_STEP = 2,        // apply kernel: GcW, GWW, then coefficient solve
+  POST_INIT = 3,        // C^T C -> R0, M = [0, R0^-1, 0], beta2
+  POST_MGS_OLD = 4,     // explicit path: alpha = Vo^T W -> acc_a += ; M[0] = alpha
+  POST_MGS_CUR = 5,     // explicit path: beta = Vc^T W -> acc_b += ; M[0] = beta
+  POST_CHOL1 = 6,       // explicit path: R1 = chol(W^T W), M[0] = R1^-1
+  POST_CHOL2 = 7,       // explicit path: R2 = chol(V^T V), M[0] = R2^-1, finish
+  POST_SCALE = 8,       // explicit path: scale2 = trace
+  POST_W2 = 9,          // explicit path: w2 = trace, zero test
+};
+
+struct TStore {  // projected-matrix storage (device), slots of 64 doubles
+  double* draw;  // raw MGS diag sums
+  double* dsym;  // symmetrised diagonal blocks
+  double* off;   // off_mgs sums
+  double* sub;   // coupling blocks tau (final R factors)
+  double* S;     // lazy CholQR2 corrections per block
+  int cap;       // number of slots
+};
+
+struct GramScratch {
+  double* partials;   // [grid][24*8]
+  unsigned* ticket;   // one counter per reduction site
+  int max_grid;
+};
+
+// ---------------------------------------------------------------- kernels (host wrappers)
+struct CombineCall {
+  const double* vo; int64_t ldo;
+  const double* vc; int64_t ldc;
+  double* vn; int64_t ldn;
+  int64_t n;
+  int has_old, use_op, write_new, reverse;
+};
+int launch_combine(cudaStream_t st, int s, const OpDev& op, const CombineCall& c,
+                   DevState* dst, const TStore& T, GramScratch& g, int grid,
+                   float* prof_ms, cudaEvent_t* ev);
+struct ApplyGramCall {
+  const double* v; int64_t ldv;
+  int64_t n;
+  int use_op;        // 1: X=[V|AV], Y=AV ; 0: X=[V], Y=V
+  int post;          // PostMode
+  int reverse;
+};
+int launch_apply_gram(cudaStream_t st, int s, const OpDev& op,
+                      const ApplyGramCall& c, DevState* dst, const TStore& T,
+                      GramScratch& g, int grid);
+// generic X^T Y with X,Y given blocks (explicit path); result to post routine
+int launch_pair_gram(cudaStream_t st, int s, const double* x, int64_t ldx,
+                     const double* y, int64_t ldy, int64_t n, int post,
+                     DevState* dst, const TStore& T, GramScratch& g, int grid);
+// y[i] = A x[i] (block), write
+int launch_apply_store(cudaStream_t st, int s, const OpDev& op, const double* x,
+                       int64_t ldx, double* y, int64_t ldy, int64_t n);
+// w[i] -= x[i] * Mdev (s x s at dst->M[0]) ; or w = w * Mdev when x == nullptr
+int launch_update(cudaStream_t st, int s, double* w, int64_t ldw, const double* x,
+                  int64_t ldx, const double* mdev, int64_t n, int subtract);
+int launch_copy_block(cudaStream_t st, int s, const double* x, int64_t ldx,
+                      double* y, int64_t ldy, int64_t n);
+// explicit-step bookkeeping kernel (1 CTA): store T slots from acc, etc.
+int launch_explicit_finish(cudaStream_t st, DevState* dst, const TStore& T, int mode);
+
+int gram_grid_for(int64_t n);
+
+}  // namespace kry

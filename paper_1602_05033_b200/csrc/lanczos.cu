@@ -1,0 +1,970 @@
+// Block-Lanczos recurrence kernels for sm_100a (fp64).
+//
+// One standard block-Lanczos step of the reference (basis.py:223-252:
+// W = A V_m; MGS twice against V_{m-1}, V_m (basis.py:164-180); economy QR
+// with diag(R) >= 0 (kernels.py:134-148)) is executed as two HBM passes:
+//
+//   apply   (k_apply_gram):  W0 = A V_m on the fly, Gram blocks V_m^T W0 and
+//                            W0^T W0 (DMMA m8n8k4 tiles), grid reduction in a
+//                            fixed order; the last CTA runs the coefficient
+//                            solve (MGS-twice simulated on the Gram algebra,
+//                            Cholesky QR of the residual block, lazy CholQR2
+//                            correction of the previous block).
+//   combine (k_combine):     V_{m+1} = V_{m-1} Mo + V_m Mc + (A V_m) Mw with
+//                            the stencil recomputed on the fly, plus the Gram
+//                            blocks the next coefficient solve needs
+//                            (V_m^T V_{m+1}, (A V_m)^T V_{m+1}, V_{m+1}^T V_{m+1}).
+//
+// so a step reads V_{m-1}, V_m twice-ish and writes V_{m+1} once (4 block
+// transfers instead of the reference's ~12 BLAS passes).  The operator is a
+// 3/5/7-point Dirichlet stencil (constant or per-point coefficients) or a CSR
+// matrix; row sums use __dmul_rn/__dadd_rn in CSR column order so A*V equals
+// scipy's csr_matvecs (operators.py:101) bit for bit.
+#include "kry_internal.cuh"
+#include <cmath>
+
+namespace kry {
+
+#define TP 128     // points per tile = threads per CTA
+#define LDX 24     // smem row stride (doubles); 24 = 8 mod 16 -> conflict-free DMMA operand loads
+
+// ------------------------------------------------------------------ vector io
+template <int S>
+__device__ __forceinline__ void load_vec(const double* __restrict__ p, double (&v)[S]) {
+  if constexpr (S % 2 == 0) {
+#pragma unroll
+    for (int a = 0; a < S; a += 2) {
+      double2 t = __ldg(reinterpret_cast<const double2*>(p + a));
+      v[a] = t.x;
+      v[a + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < S; ++a) v[a] = __ldg(p + a);
+  }
+}
+
+template <int S>
+__device__ __forceinline__ void store_vec(double* __restrict__ p, const double (&v)[S]) {
+  if constexpr (S % 2 == 0) {
+#pragma unroll
+    for (int a = 0; a < S; a += 2)
+      *reinterpret_cast<double2*>(p + a) = make_double2(v[a], v[a + 1]);
+  } else {
+#pragma unroll
+    for (int a = 0; a < S; ++a) p[a] = v[a];
+  }
+}
+
+template <int S>
+__device__ __forceinline__ void axpy_rn(double (&w)[S], double coef, const double (&x)[S]) {
+#pragma unroll
+  for (int a = 0; a < S; ++a) w[a] = __dadd_rn(w[a], __dmul_rn(coef, x[a]));
+}
+
+// y = A x at local point i (CSR column order, no FMA contraction)
+template <int S>
+__device__ __forceinline__ void apply_point(const OpDev& op, const double* __restrict__ V,
+                                            int64_t ld, int i, const double (&vi)[S],
+                                            double (&w)[S]) {
+#pragma unroll
+  for (int a = 0; a < S; ++a) w[a] = 0.0;
+  double nb[S];
+  if (op.kind == KRY_OP_STENCIL) {
+    const int x = i % op.nx;
+    const int r = i / op.nx;
+    const int y = r % op.ny;
+    const int z = r / op.ny;
+    const bool var = op.variable != 0;
+    if (z > 0 || op.halo_lo) {
+      const int j = i - op.nxy;
+      load_vec<S>(V + (int64_t)j * ld, nb);
+      axpy_rn<S>(w, var ? __ldg(op.ez + j) : op.cz, nb);
+    }
+    if (y > 0) {
+      const int j = i - op.nx;
+      load_vec<S>(V + (int64_t)j * ld, nb);
+      axpy_rn<S>(w, var ? __ldg(op.ey + j) : op.cy, nb);
+    }
+    if (x > 0) {
+      const int j = i - 1;
+      load_vec<S>(V + (int64_t)j * ld, nb);
+      axpy_rn<S>(w, var ? __ldg(op.ex + j) : op.cx, nb);
+    }
+    axpy_rn<S>(w, var ? __ldg(op.d + i) : op.cd, vi);
+    if (x < op.nx - 1) {
+      const int j = i + 1;
+      load_vec<S>(V + (int64_t)j * ld, nb);
+      axpy_rn<S>(w, var ? __ldg(op.ex + i) : op.cx, nb);
+    }
+    if (y < op.ny - 1) {
+      const int j = i + op.nx;
+      load_vec<S>(V + (int64_t)j * ld, nb);
+      axpy_rn<S>(w, var ? __ldg(op.ey + i) : op.cy, nb);
+    }
+    if (z < op.nzl - 1 || op.halo_hi) {
+      const int j = i + op.nxy;
+      load_vec<S>(V + (int64_t)j * ld, nb);
+      axpy_rn<S>(w, var ? __ldg(op.ez + i) : op.cz, nb);
+    }
+  } else {
+    const int64_t b = __ldg(op.rp + i), e = __ldg(op.rp + i + 1);
+    for (int64_t jj = b; jj < e; ++jj) {
+      const int j = __ldg(op.ci + jj);
+      load_vec<S>(V + (int64_t)j * ld, nb);
+      axpy_rn<S>(w, __ldg(op.va + jj), nb);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ DMMA gram tile
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+// acc[mt] += X[rows k0..k0+31, mt*8..mt*8+7]^T * X[rows, ycol..ycol+7]
+template <int MT>
+__device__ __forceinline__ void tile_gram(const double* sX, int k0, int ycol, double (&acc)[MT][2]) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    const double* row = sX + (k0 + ks * 4 + t) * LDX;
+    const double b = row[ycol + g];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][0], acc[mt][1], row[mt * 8 + g], b);
+  }
+}
+
+// ------------------------------------------------------------------ small matrices (smem, 8x8 row-major)
+__device__ __forceinline__ int tid() { return threadIdx.x; }
+
+__device__ void m_copy(double* dst, const double* src) {
+  __syncthreads();
+  if (tid() < 64) dst[tid()] = src[tid()];
+  __syncthreads();
+}
+__device__ void m_eye(double* dst, int s) {
+  __syncthreads();
+  if (tid() < 64) {
+    int r = tid() >> 3, c = tid() & 7;
+    dst[tid()] = (r == c && r < s) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+}
+__device__ void m_zero(double* dst) {
+  __syncthreads();
+  if (tid() < 64) dst[tid()] = 0.0;
+  __syncthreads();
+}
+// C = alpha * op(A) op(B) (+ beta * D when D != nullptr); C may alias inputs
+__device__ void mm(double* C, const double* A, int ta, const double* B, int tb, int s,
+                   double alpha = 1.0, const double* D = nullptr, double beta = 0.0) {
+  __syncthreads();
+  double v = 0.0;
+  if (tid() < 64) {
+    int r = tid() >> 3, c = tid() & 7;
+    if (r < s && c < s) {
+      for (int k = 0; k < s; ++k) {
+        double a = ta ? A[k * 8 + r] : A[r * 8 + k];
+        double b = tb ? B[c * 8 + k] : B[k * 8 + c];
+        v = fma(a, b, v);
+      }
+      v *= alpha;
+      if (D) v = fma(beta, D[tid()], v);
+    }
+  }
+  __syncthreads();
+  if (tid() < 64) C[tid()] = v;
+  __syncthreads();
+}
+// C = A + beta * B
+__device__ void madd(double* C, const double* A, const double* B, double beta) {
+  __syncthreads();
+  double v = 0.0;
+  if (tid() < 64) v = A[tid()] + beta * B[tid()];
+  __syncthreads();
+  if (tid() < 64) C[tid()] = v;
+  __syncthreads();
+}
+// serial Cholesky G = R^T R (upper R, positive diagonal) from the upper
+// triangle of G.  Returns 0 ok, 1 breakdown / numerically singular pivot.
+__device__ int chol_upper(const double* G, double* R, int s, double* min_ratio) {
+  for (int i = 0; i < 64; ++i) R[i] = 0.0;
+  double mr = 1e300;
+  for (int k = 0; k < s; ++k) {
+    double p = G[k * 8 + k];
+    for (int i = 0; i < k; ++i) p -= R[i * 8 + k] * R[i * 8 + k];
+    // pivots at the level of the Gram's rounding are treated as zero
+    if (!(p > 1e3 * 2.220446049250313e-16 * fabs(G[k * 8 + k])) || !(p > 0.0)) return 1;
+    const double rkk = sqrt(p);
+    R[k * 8 + k] = rkk;
+    for (int j = k + 1; j < s; ++j) {
+      double v = G[k * 8 + j];
+      for (int i = 0; i < k; ++i) v -= R[i * 8 + k] * R[i * 8 + j];
+      R[k * 8 + j] = v / rkk;
+    }
+  }
+  double fro = 0.0;
+  for (int i = 0; i < 64; ++i) fro += R[i] * R[i];
+  fro = sqrt(fro);
+  for (int k = 0; k < s; ++k) mr = fmin(mr, R[k * 8 + k] / fro);
+  *min_ratio = mr;
+  return 0;
+}
+__device__ void inv_upper(const double* R, double* Ri, int s) {
+  for (int i = 0; i < 64; ++i) Ri[i] = 0.0;
+  for (int j = 0; j < s; ++j) {
+    Ri[j * 8 + j] = 1.0 / R[j * 8 + j];
+    for (int i = j - 1; i >= 0; --i) {
+      double v = 0.0;
+      for (int k = i + 1; k <= j; ++k) v += R[i * 8 + k] * Ri[k * 8 + j];
+      Ri[i * 8 + j] = -v / R[i * 8 + i];
+    }
+  }
+}
+__device__ double m_trace(const double* A, int s) {
+  double t = 0.0;
+  for (int k = 0; k < s; ++k) t += A[k * 8 + k];
+  return t;
+}
+
+// ------------------------------------------------------------------ post routines
+struct PostSmem {
+  double G[12][64];
+};
+
+__device__ void set_status(DevState* st, int code) {
+  if (tid() == 0 && st->status == KRY_OK) st->status = code;
+}
+
+// total: MP x 8 reduced Gram (row = X column, col = Y column)
+__device__ void extract_block(const double* total, int row0, int s, double* dst) {
+  __syncthreads();
+  if (tid() < 64) {
+    int r = tid() >> 3, c = tid() & 7;
+    dst[tid()] = (r < s && c < s) ? total[(row0 + r) * 8 + c] : 0.0;
+  }
+  __syncthreads();
+}
+
+// The coefficient solve of one fused step (see file header).  Runs on the
+// last CTA of the apply reduction; `total` holds [V^T W0 ; W0^T W0].
+__device__ __noinline__ void coef_solve(const double* total, DevState* st, const TStore& T, double (*sm)[64]) {
+  const int s = st->s;
+  double* Gcc = sm[0]; double* Goc = sm[1]; double* GoW = sm[2]; double* Goo = sm[3];
+  double* GcW = sm[4]; double* GWW = sm[5]; double* Sc = sm[6]; double* So = sm[7];
+  double* A = sm[8]; double* B = sm[9]; double* X = sm[10]; double* Y = sm[11];
+  double* Z = sm[12]; double* U = sm[13];
+  __shared__ int s_flag;
+  __shared__ double s_val[4];
+  m_copy(Gcc, st->Gcc); m_copy(Goc, st->Goc); m_copy(GoW, st->GoW); m_copy(Goo, st->Goo);
+  m_copy(So, st->So);
+  extract_block(total, 0, s, GcW);
+  extract_block(total, s, s, GWW);
+  const int j = st->step + 1;        // 1-based step being solved
+  const int has_old = st->has_old;
+  // 1. lazy CholQR2 correction of the current block: Gcc = R2^T R2, Sc = R2^-1
+  if (tid() == 0) {
+    double mr;
+    s_flag = chol_upper(Gcc, X, s, &mr);
+    if (!s_flag) inv_upper(X, Sc, s);
+  }
+  __syncthreads();
+  if (s_flag) {  // the stored block is not numerically full rank
+    set_status(st, KRY_ERR_DEFLATION);
+    __syncthreads();
+    return;
+  }
+  // 2. finalise the previous coupling block (or gamma): R_hat = R2 * R1prev
+  m_copy(Y, st->R1prev);
+  mm(Z, X, 0, Y, 0, s);
+  if (j == 1) {
+    if (tid() < 64 && !st->replay) st->gamma[tid()] = Z[tid()];
+  } else {
+    double* dst = T.sub + (int64_t)(j - 2) * 64;
+    if (st->replay) {
+      if (tid() == 0) {
+        double num = 0.0, den = 0.0;
+        for (int q = 0; q < 64; ++q) {
+          double d = Z[q] - dst[q];
+          num += d * d;
+          den += dst[q] * dst[q];
+        }
+        double rel = sqrt(num) / fmax(sqrt(den), 1e-300);
+        st->replay_err = fmax(st->replay_err, rel);
+      }
+    } else if (tid() < 64) {
+      dst[tid()] = Z[tid()];
+    }
+  }
+  if (tid() < 64) {
+    st->Sc[tid()] = Sc[tid()];
+    T.S[(int64_t)(j - 1) * 64 + tid()] = Sc[tid()];
+  }
+  if (tid() == 0) st->flags &= ~KRY_FLAG_FALLBACK;
+  __syncthreads();
+  // 3. Gram blocks in the orthonormal (true) basis
+  mm(A, Sc, 1, Gcc, 0, s); mm(Gcc, A, 0, Sc, 0, s);    // Gcc^ = Sc^T Gcc Sc
+  mm(A, Sc, 1, GcW, 0, s); mm(GcW, A, 0, Sc, 0, s);    // GcW^
+  mm(A, Sc, 1, GWW, 0, s); mm(GWW, A, 0, Sc, 0, s);    // GWW^
+  if (has_old) {
+    mm(A, So, 1, Goo, 0, s); mm(Goo, A, 0, So, 0, s);  // Goo^
+    mm(A, So, 1, Goc, 0, s); mm(Goc, A, 0, Sc, 0, s);  // Goc^
+    mm(A, So, 1, GoW, 0, s); mm(GoW, A, 0, Sc, 0, s);  // GoW^
+  }
+  // 4. MGS performed twice on W = W0 - Vo a - Vc b  (basis.py:164-180)
+  m_zero(A);  // a (off sum)
+  m_zero(B);  // b (diag sum)
+  for (int sweep = 0; sweep < 2; ++sweep) {
+    if (has_old) {
+      // alpha = GoW - Goo a - Goc b
+      mm(X, Goo, 0, A, 0, s, -1.0, GoW, 1.0);
+      mm(X, Goc, 0, B, 0, s, -1.0, X, 1.0);
+      madd(A, A, X, 1.0);
+    }
+    // beta = GcW - Goc^T a - Gcc b
+    if (has_old) {
+      mm(X, Goc, 1, A, 0, s, -1.0, GcW, 1.0);
+    } else {
+      m_copy(X, GcW);
+    }
+    mm(X, Gcc, 0, B, 0, s, -1.0, X, 1.0);
+    madd(B, B, X, 1.0);
+  }
+  // 5. W^T W = GWW - GcW^T b - b^T GcW + b^T Gcc b  (+ the old-block terms)
+  mm(X, GcW, 1, B, 0, s);                 // X = GcW^T b ; Z = GWW - X - X^T
+  __syncthreads();
+  if (tid() < 64) {
+    int r = tid() >> 3, c = tid() & 7;
+    Z[tid()] = GWW[tid()] - X[r * 8 + c] - X[c * 8 + r];
+  }
+  __syncthreads();
+  mm(U, Gcc, 0, B, 0, s);                 // Gcc b
+  mm(Z, B, 1, U, 0, s, 1.0, Z, 1.0);      // + b^T Gcc b
+  if (has_old) {
+    mm(X, GoW, 1, A, 0, s);               // GoW^T a
+    __syncthreads();
+    if (tid() < 64) {
+      int r = tid() >> 3, c = tid() & 7;
+      Z[tid()] = Z[tid()] - X[r * 8 + c] - X[c * 8 + r];
+    }
+    __syncthreads();
+    mm(U, Goo, 0, A, 0, s);               // Goo a
+    mm(Z, A, 1, U, 0, s, 1.0, Z, 1.0);    // + a^T Goo a
+    mm(U, Goc, 0, B, 0, s);               // Goc b
+    mm(X, A, 1, U, 0, s);                 // a^T Goc b
+    __syncthreads();
+    if (tid() < 64) {
+      int r = tid() >> 3, c = tid() & 7;
+      Z[tid()] = Z[tid()] + X[r * 8 + c] + X[c * 8 + r];
+    }
+    __syncthreads();
+  }
+  // symmetrise W^T W
+  __syncthreads();
+  if (tid() < 64) {
+    int r = tid() >> 3, c = tid() & 7;
+    U[tid()] = 0.5 * (Z[r * 8 + c] + Z[c * 8 + r]);
+  }
+  __syncthreads();
+  if (tid() == 0) {
+    s_val[0] = m_trace(GWW, s);
+    s_val[1] = m_trace(U, s);
+    st->scale2 = s_val[0];
+    st->w2 = s_val[1];
+  }
+  __syncthreads();
+  const double scale2 = s_val[0], w2 = s_val[1];
+  // 6. zero / near-zero residual block: decided by the explicit path
+  if (!(w2 > 1e-10 * scale2)) {
+    if (tid() == 0) st->flags |= KRY_FLAG_FALLBACK;
+    return;
+  }
+  // 7. Cholesky QR of the residual block
+  if (tid() == 0) {
+    double mr = 0.0;
+    int bad = chol_upper(U, X, s, &mr);
+    if (bad || mr < 1e-5) {
+      s_flag = 1;
+    } else {
+      s_flag = 0;
+      inv_upper(X, Y, s);
+      for (int q = 0; q < 64; ++q) st->R1prev[q] = X[q];
+    }
+  }
+  __syncthreads();
+  if (s_flag) {
+    if (tid() == 0) st->flags |= KRY_FLAG_FALLBACK;
+    return;
+  }
+  // 8. combine coefficients: Vn = Vo Mo + Vc Mc + W0 Mw
+  mm(Z, Sc, 0, Y, 0, s);                   // Mw = Sc R1^-1
+  if (tid() < 64) st->M[128 + tid()] = Z[tid()];
+  mm(U, B, 0, Y, 0, s);                    // b R1^-1
+  mm(Z, Sc, 0, U, 0, s, -1.0);             // Mc = -Sc b R1^-1
+  if (tid() < 64) st->M[64 + tid()] = Z[tid()];
+  if (has_old) {
+    mm(U, A, 0, Y, 0, s);
+    mm(Z, So, 0, U, 0, s, -1.0);           // Mo = -So a R1^-1
+  } else {
+    m_zero(Z);
+  }
+  if (tid() < 64) st->M[tid()] = Z[tid()];
+  // 9. projection blocks of step j
+  if (!st->replay && tid() < 64) {
+    int r = tid() >> 3, c = tid() & 7;
+    const int64_t o = (int64_t)(j - 1) * 64;
+    T.draw[o + tid()] = B[tid()];
+    T.dsym[o + tid()] = 0.5 * (B[r * 8 + c] + B[c * 8 + r]);
+    T.off[o + tid()] = has_old ? A[tid()] : 0.0;
+  }
+  if (tid() < 64) {
+    st->So[tid()] = Sc[tid()];
+    st->Goo[tid()] = st->Gcc[tid()];
+  }
+  __syncthreads();
+  if (tid() == 0) {
+    st->step = j;
+    st->has_old = 1;
+  }
+  __syncthreads();
+}
+
+__device__ __noinline__ void run_post(int post, const double* total, DevState* st, const TStore& T,
+                         double (*sm)[64]) {
+  const int s = st->s;
+  __shared__ int s_bad;
+  __shared__ double s_v;
+  switch (post) {
+    case POST_NONE:
+      if (tid() < 3 * 64) st->gram[tid()] = total[tid()];
+      __syncthreads();
+      break;
+    case POST_P:
+      extract_block(total, 0, s, sm[0]);
+      extract_block(total, s, s, sm[1]);
+      extract_block(total, 2 * s, s, sm[2]);
+      if (tid() < 64) {
+        st->Goc[tid()] = sm[0][tid()];
+        st->GoW[tid()] = sm[1][tid()];
+        st->Gcc[tid()] = sm[2][tid()];
+      }
+      __syncthreads();
+      break;
+    case POST_STEP:
+      coef_solve(total, st, T, sm);
+      break;
+    case POST_INIT: {
+      extract_block(total, 0, s, sm[0]);
+      if (tid() == 0) {
+        double mr = 0.0;
+        st->beta2 = m_trace(sm[0], s);
+        s_bad = chol_upper(sm[0], sm[1], s, &mr);
+        if (s_bad || mr < 1e-12) {
+          s_bad = 1;
+          if (st->status == KRY_OK) st->status = KRY_ERR_DEFLATION;
+        } else {
+          inv_upper(sm[1], sm[2], s);
+          for (int q = 0; q < 64; ++q) {
+            st->R1prev[q] = sm[1][q];
+            st->M[q] = 0.0;
+            st->M[64 + q] = sm[2][q];
+            st->M[128 + q] = 0.0;
+            st->So[q] = ((q >> 3) == (q & 7) && (q >> 3) < s) ? 1.0 : 0.0;
+          }
+          st->step = 0;
+          st->has_old = 0;
+          st->flags = 0;
+        }
+      }
+      __syncthreads();
+      break;
+    }
+    case POST_SCALE:
+      extract_block(total, 0, s, sm[0]);
+      if (tid() == 0) {
+        st->scale2 = m_trace(sm[0], s);
+        for (int q = 0; q < 64; ++q) { st->acc_a[q] = 0.0; st->acc_b[q] = 0.0; }
+      }
+      __syncthreads();
+      break;
+    case POST_MGS_OLD:
+    case POST_MGS_CUR: {
+      // raw g = V^T W ; true coefficient alpha = S^T g ; update matrix S alpha
+      extract_block(total, 0, s, sm[0]);
+      m_copy(sm[1], post == POST_MGS_OLD ? st->So : st->Sc);
+      mm(sm[2], sm[1], 1, sm[0], 0, s);           // alpha
+      mm(sm[3], sm[1], 0, sm[2], 0, s);           // S alpha
+      if (tid() < 64) {
+        double* acc = post == POST_MGS_OLD ? st->acc_a : st->acc_b;
+        acc[tid()] += sm[2][tid()];
+        st->M[tid()] = sm[3][tid()];
+      }
+      __syncthreads();
+      break;
+    }
+    case POST_W2:
+      extract_block(total, 0, s, sm[0]);
+      if (tid() == 0) st->w2 = m_trace(sm[0], s);
+      __syncthreads();
+      break;
+    case POST_CHOL1:
+    case POST_CHOL2: {
+      extract_block(total, 0, s, sm[0]);
+      if (tid() == 0) {
+        double mr = 0.0;
+        s_bad = chol_upper(sm[0], sm[1], s, &mr);
+        if (s_bad) {
+          if (st->status == KRY_OK) st->status = KRY_ERR_DEFLATION;
+        } else {
+          inv_upper(sm[1], sm[2], s);
+          for (int q = 0; q < 64; ++q) st->M[q] = sm[2][q];
+          if (post == POST_CHOL1) {
+            for (int q = 0; q < 64; ++q) st->gram[q] = sm[1][q];   // R1
+          } else {
+            // R = R2 R1 ; rank test as kernels.py:151-160
+            double fro = 0.0;
+            for (int r = 0; r < 8; ++r)
+              for (int c = 0; c < 8; ++c) {
+                double v = 0.0;
+                for (int k = 0; k < 8; ++k) v += sm[1][r * 8 + k] * st->gram[k * 8 + c];
+                st->gram[64 + r * 8 + c] = v;
+                fro += v * v;
+              }
+            fro = sqrt(fro);
+            double mn = 1e300;
+            for (int k = 0; k < s; ++k) mn = fmin(mn, fabs(st->gram[64 + k * 8 + k]));
+            if (mn < 1e-12 * fro && st->status == KRY_OK) st->status = KRY_ERR_DEFLATION;
+          }
+        }
+      }
+      __syncthreads();
+      break;
+    }
+    default:
+      break;
+  }
+  (void)s_v;
+}
+
+// ------------------------------------------------------------------ grid reduction tail
+template <int MP>
+__device__ void finish_reduction(const double (&acc)[MP / 8][2], double* sX, double* partials,
+                                 unsigned* ticket, int post, DevState* st, const TStore& T) {
+  constexpr int MT = MP / 8;
+  constexpr int NE = MP * 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  __syncthreads();
+  // per-warp tiles to smem: red[warp][m*8+n]
+  double* red = sX;  // 4 * NE doubles <= 4*192 < 128*24
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    red[warp * NE + (mt * 8 + g) * 8 + 2 * t] = acc[mt][0];
+    red[warp * NE + (mt * 8 + g) * 8 + 2 * t + 1] = acc[mt][1];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < NE; e += blockDim.x) {
+    double v = red[e];
+    v += red[NE + e];
+    v += red[2 * NE + e];
+    v += red[3 * NE + e];
+    partials[(int64_t)blockIdx.x * NE + e] = v;
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ unsigned s_last;
+  if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // deterministic grid reduction: warp w owns entries e = w, w+4, ...; lanes
+  // stride over CTAs, then a fixed xor tree
+  double* total = sX;  // reuse: NE doubles
+  __syncthreads();
+  for (int e = warp; e < NE; e += 4) {
+    double v = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) v += __ldcg(partials + (int64_t)b * NE + e);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) total[e] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *ticket = 0u;
+  // post routine on 8x8 smem scratch carved after `total`
+  double(*sm)[64] = reinterpret_cast<double(*)[64]>(sX + 256);
+  run_post(post, total, st, T, sm);
+}
+
+// ------------------------------------------------------------------ kernels
+// Combine: Vn = Vo Mo + Vc Mc + (A Vc) Mw ; Gram [Vc | A Vc | Vn]^T Vn
+template <int S>
+__global__ void __launch_bounds__(TP) k_combine(OpDev op, CombineCall c, DevState* st,
+                                                TStore T, double* partials, unsigned* ticket) {
+  constexpr int NG = 3;
+  constexpr int W = NG * S;
+  constexpr int MP = (W + 7) / 8 * 8;
+  constexpr int MT = MP / 8;
+  __shared__ __align__(16) double sX[TP * LDX];
+  __shared__ __align__(16) double sM[3 * 64];
+  if (st->status != KRY_OK || (st->flags & (KRY_FLAG_FALLBACK | KRY_FLAG_EXHAUSTED))) {
+    if (c.write_new) return;  // never combine with invalid coefficients
+  }
+  for (int e = threadIdx.x; e < 3 * 64; e += TP) sM[e] = st->M[e];
+  for (int e = 0; e < LDX; ++e) sX[threadIdx.x * LDX + e] = 0.0;
+  double acc[MT][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+  __syncthreads();
+  const int64_t ntiles = (c.n + TP - 1) / TP;
+  const int warp = threadIdx.x >> 5;
+  for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
+    const int64_t tile = c.reverse ? (ntiles - 1 - it) : it;
+    const int64_t i64 = tile * TP + threadIdx.x;
+    double* row = sX + threadIdx.x * LDX;
+    if (i64 < c.n) {
+      const int i = (int)i64;
+      double vc[S], w[S], vn[S];
+      load_vec<S>(c.vc + i64 * c.ldc, vc);
+      if (c.use_op) {
+        apply_point<S>(op, c.vc, c.ldc, i, vc, w);
+      } else {
+#pragma unroll
+        for (int a = 0; a < S; ++a) w[a] = 0.0;
+      }
+      if (c.write_new) {
+#pragma unroll
+        for (int a = 0; a < S; ++a) vn[a] = 0.0;
+        if (c.has_old) {
+          double vo[S];
+          load_vec<S>(c.vo + i64 * c.ldo, vo);
+#pragma unroll
+          for (int b = 0; b < S; ++b)
+#pragma unroll
+            for (int a = 0; a < S; ++a) vn[a] = fma(vo[b], sM[b * 8 + a], vn[a]);
+        }
+#pragma unroll
+        for (int b = 0; b < S; ++b)
+#pragma unroll
+          for (int a = 0; a < S; ++a) vn[a] = fma(vc[b], sM[64 + b * 8 + a], vn[a]);
+        if (c.use_op) {
+#pragma unroll
+          for (int b = 0; b < S; ++b)
+#pragma unroll
+            for (int a = 0; a < S; ++a) vn[a] = fma(w[b], sM[128 + b * 8 + a], vn[a]);
+        }
+        store_vec<S>(c.vn + i64 * c.ldn, vn);
+      } else {
+        load_vec<S>(c.vn + i64 * c.ldn, vn);
+      }
+#pragma unroll
+      for (int a = 0; a < S; ++a) {
+        row[a] = vc[a];
+        row[S + a] = w[a];
+        row[2 * S + a] = vn[a];
+      }
+    } else {
+#pragma unroll
+      for (int a = 0; a < W; ++a) row[a] = 0.0;
+    }
+    __syncthreads();
+    tile_gram<MT>(sX, warp * 32, 2 * S, acc);
+    __syncthreads();
+  }
+  finish_reduction<MP>(acc, sX, partials, ticket, POST_P, st, T);
+}
+
+// Apply + Gram: X = [V | A V], Y = A V  (use_op) or X = [V], Y = V
+template <int S, int USE_OP>
+__global__ void __launch_bounds__(TP) k_apply_gram(OpDev op, ApplyGramCall c, DevState* st,
+                                                   TStore T, double* partials, unsigned* ticket) {
+  constexpr int NG = USE_OP ? 2 : 1;
+  constexpr int W = NG * S;
+  constexpr int MP = (W + 7) / 8 * 8;
+  constexpr int MT = MP / 8;
+  __shared__ __align__(16) double sX[TP * LDX];
+  for (int e = 0; e < LDX; ++e) sX[threadIdx.x * LDX + e] = 0.0;
+  double acc[MT][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+  __syncthreads();
+  const int64_t ntiles = (c.n + TP - 1) / TP;
+  const int warp = threadIdx.x >> 5;
+  for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
+    const int64_t tile = c.reverse ? (ntiles - 1 - it) : it;
+    const int64_t i64 = tile * TP + threadIdx.x;
+    double* row = sX + threadIdx.x * LDX;
+    if (i64 < c.n) {
+      double v[S];
+      load_vec<S>(c.v + i64 * c.ldv, v);
+#pragma unroll
+      for (int a = 0; a < S; ++a) row[a] = v[a];
+      if constexpr (USE_OP) {
+        double w[S];
+        apply_point<S>(op, c.v, c.ldv, (int)i64, v, w);
+#pragma unroll
+        for (int a = 0; a < S; ++a) row[S + a] = w[a];
+      }
+    } else {
+#pragma unroll
+      for (int a = 0; a < W; ++a) row[a] = 0.0;
+    }
+    __syncthreads();
+    tile_gram<MT>(sX, warp * 32, (NG - 1) * S, acc);
+    __syncthreads();
+  }
+  finish_reduction<MP>(acc, sX, partials, ticket, c.post, st, T);
+}
+
+// Pair Gram X^T Y for two blocks (explicit path)
+template <int S>
+__global__ void __launch_bounds__(TP) k_pair_gram(const double* x, int64_t ldx, const double* y,
+                                                  int64_t ldy, int64_t n, int post, DevState* st,
+                                                  TStore T, double* partials, unsigned* ticket) {
+  constexpr int W = 2 * S;
+  constexpr int MP = (W + 7) / 8 * 8;
+  constexpr int MT = MP / 8;
+  __shared__ __align__(16) double sX[TP * LDX];
+  for (int e = 0; e < LDX; ++e) sX[threadIdx.x * LDX + e] = 0.0;
+  double acc[MT][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+  __syncthreads();
+  const int64_t ntiles = (n + TP - 1) / TP;
+  const int warp = threadIdx.x >> 5;
+  for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
+    const int64_t i64 = it * TP + threadIdx.x;
+    double* row = sX + threadIdx.x * LDX;
+    if (i64 < n) {
+      double v[S], w[S];
+      load_vec<S>(x + i64 * ldx, v);
+      load_vec<S>(y + i64 * ldy, w);
+#pragma unroll
+      for (int a = 0; a < S; ++a) {
+        row[a] = v[a];
+        row[S + a] = w[a];
+      }
+    } else {
+#pragma unroll
+      for (int a = 0; a < W; ++a) row[a] = 0.0;
+    }
+    __syncthreads();
+    tile_gram<MT>(sX, warp * 32, S, acc);
+    __syncthreads();
+  }
+  finish_reduction<MP>(acc, sX, partials, ticket, post, st, T);
+}
+
+template <int S>
+__global__ void k_apply_store(OpDev op, const double* x, int64_t ldx, double* y, int64_t ldy,
+                              int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v[S], w[S];
+    load_vec<S>(x + i * ldx, v);
+    apply_point<S>(op, x, ldx, (int)i, v, w);
+    store_vec<S>(y + i * ldy, w);
+  }
+}
+
+// w = w - x M (subtract) or w = w M (x == nullptr)
+template <int S>
+__global__ void k_update(double* w, int64_t ldw, const double* x, int64_t ldx, const double* mdev,
+                         int64_t n, int subtract) {
+  __shared__ double sM[64];
+  if (threadIdx.x < 64) sM[threadIdx.x] = mdev[threadIdx.x];
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double wv[S], out[S];
+    load_vec<S>(w + i * ldw, wv);
+    if (x) {
+      double xv[S];
+      load_vec<S>(x + i * ldx, xv);
+#pragma unroll
+      for (int a = 0; a < S; ++a) {
+        double t = 0.0;
+#pragma unroll
+        for (int b = 0; b < S; ++b) t = fma(xv[b], sM[b * 8 + a], t);
+        out[a] = subtract ? wv[a] - t : wv[a] + t;
+      }
+    } else {
+#pragma unroll
+      for (int a = 0; a < S; ++a) {
+        double t = 0.0;
+#pragma unroll
+        for (int b = 0; b < S; ++b) t = fma(wv[b], sM[b * 8 + a], t);
+        out[a] = t;
+      }
+    }
+    store_vec<S>(w + i * ldw, out);
+  }
+}
+
+template <int S>
+__global__ void k_copy_block(const double* x, int64_t ldx, double* y, int64_t ldy, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v[S];
+    load_vec<S>(x + i * ldx, v);
+    store_vec<S>(y + i * ldy, v);
+  }
+}
+
+// explicit-path bookkeeping (1 CTA of 64 threads)
+__global__ void k_explicit_finish(DevState* st, TStore T, int mode) {
+  const int q = threadIdx.x;
+  const int s = st->s;
+  const int j = st->step + 1;
+  const int r = q >> 3, c = q & 7;
+  if (mode == 0) {
+    // zero residual block: exhausted (finalize mode)
+    const int64_t o = (int64_t)(j - 1) * 64;
+    if (!st->replay) {
+      T.draw[o + q] = st->acc_b[q];
+      T.dsym[o + q] = 0.5 * (st->acc_b[r * 8 + c] + st->acc_b[c * 8 + r]);
+      T.off[o + q] = st->has_old ? st->acc_a[q] : 0.0;
+      T.sub[o + q] = 0.0;
+    }
+    T.S[o + q] = st->Sc[q];
+    __syncthreads();
+    if (q == 0) {
+      st->flags = KRY_FLAG_EXHAUSTED;
+      st->step = j;
+    }
+  } else {
+    // regular explicit step: R = R2 R1 in st->gram[64..], V_new orthonormal
+    const int64_t o = (int64_t)(j - 1) * 64;
+    if (!st->replay) {
+      T.draw[o + q] = st->acc_b[q];
+      T.dsym[o + q] = 0.5 * (st->acc_b[r * 8 + c] + st->acc_b[c * 8 + r]);
+      T.off[o + q] = st->has_old ? st->acc_a[q] : 0.0;
+    }
+    T.S[o + q] = st->Sc[q];
+    st->R1prev[q] = st->gram[64 + q];
+    st->So[q] = st->Sc[q];
+    st->Goo[q] = st->Gcc[q];
+    __syncthreads();
+    if (q == 0) {
+      st->flags = 0;
+      st->step = j;
+      st->has_old = 1;
+    }
+  }
+  (void)s;
+}
+
+// ------------------------------------------------------------------ launchers
+int gram_grid_for(int64_t n) {
+  int64_t tiles = (n + TP - 1) / TP;
+  int64_t g = 148 * 6;
+  if (tiles < g) g = tiles;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+#define KRY_DISPATCH_S(s, F)                                        \
+  switch (s) {                                                      \
+    case 1: F(1); break;                                            \
+    case 2: F(2); break;                                            \
+    case 3: F(3); break;                                            \
+    case 4: F(4); break;                                            \
+    case 5: F(5); break;                                            \
+    case 6: F(6); break;                                            \
+    case 7: F(7); break;                                            \
+    case 8: F(8); break;                                            \
+    default: return fail(KRY_ERR_ARGUMENT, "block width s must be 1..8"); \
+  }
+
+int launch_combine(cudaStream_t st, int s, const OpDev& op, const CombineCall& c, DevState* dst,
+                   const TStore& T, GramScratch& g, int grid, float* prof_ms, cudaEvent_t* ev) {
+  if (grid > g.max_grid) grid = g.max_grid;
+  if (prof_ms && ev) cudaEventRecord(ev[0], st);
+#define L(S) k_combine<S><<<grid, TP, 0, st>>>(op, c, dst, T, g.partials, g.ticket + 0)
+  KRY_DISPATCH_S(s, L);
+#undef L
+  if (prof_ms && ev) cudaEventRecord(ev[1], st);
+  count_launch();
+  KRY_CUDA(cudaGetLastError());
+  return KRY_OK;
+}
+
+int launch_apply_gram(cudaStream_t st, int s, const OpDev& op, const ApplyGramCall& c,
+                      DevState* dst, const TStore& T, GramScratch& g, int grid) {
+  if (grid > g.max_grid) grid = g.max_grid;
+  if (c.use_op) {
+#define L(S) k_apply_gram<S, 1><<<grid, TP, 0, st>>>(op, c, dst, T, g.partials, g.ticket + 1)
+    KRY_DISPATCH_S(s, L);
+#undef L
+  } else {
+#define L(S) k_apply_gram<S, 0><<<grid, TP, 0, st>>>(op, c, dst, T, g.partials, g.ticket + 1)
+    KRY_DISPATCH_S(s, L);
+#undef L
+  }
+  count_launch();
+  KRY_CUDA(cudaGetLastError());
+  return KRY_OK;
+}
+
+int launch_pair_gram(cudaStream_t st, int s, const double* x, int64_t ldx, const double* y,
+                     int64_t ldy, int64_t n, int post, DevState* dst, const TStore& T,
+                     GramScratch& g, int grid) {
+  if (grid > g.max_grid) grid = g.max_grid;
+#define L(S) \
+  k_pair_gram<S><<<grid, TP, 0, st>>>(x, ldx, y, ldy, n, post, dst, T, g.partials, g.ticket + 2)
+  KRY_DISPATCH_S(s, L);
+#undef L
+  count_launch();
+  KRY_CUDA(cudaGetLastError());
+  return KRY_OK;
+}
+
+static int ew_grid(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+int launch_apply_store(cudaStream_t st, int s, const OpDev& op, const double* x, int64_t ldx,
+                       double* y, int64_t ldy, int64_t n) {
+#define L(S) k_apply_store<S><<<ew_grid(n), 256, 0, st>>>(op, x, ldx, y, ldy, n)
+  KRY_DISPATCH_S(s, L);
+#undef L
+  count_launch();
+  KRY_CUDA(cudaGetLastError());
+  return KRY_OK;
+}
+
+int launch_update(cudaStream_t st, int s, double* w, int64_t ldw, const double* x, int64_t ldx,
+                  const double* mdev, int64_t n, int subtract) {
+#define L(S) k_update<S><<<ew_grid(n), 256, 0, st>>>(w, ldw, x, ldx, mdev, n, subtract)
+  KRY_DISPATCH_S(s, L);
+#undef L
+  count_launch();
+  KRY_CUDA(cudaGetLastError());
+  return KRY_OK;
+}
+
+int launch_copy_block(cudaStream_t st, int s, const double* x, int64_t ldx, double* y,
+                      int64_t ldy, int64_t n) {
+#define L(S) k_copy_block<S><<<ew_grid(n), 256, 0, st>>>(x, ldx, y, ldy, n)
+  KRY_DISPATCH_S(s, L);
+#undef L
+  count_launch();
+  KRY_CUDA(cudaGetLastError());
+  return KRY_OK;
+}
+
+int launch_explicit_finish(cudaStream_t st, DevState* dst, const TStore& T, int mode) {
+  k_explicit_finish<<<1, 64, 0, st>>>(dst, T, mode);
+  count_launch();
+  KRY_CUDA(cudaGetLastError());
+  return KRY_OK;
+}
+
+}  // namespace kry

@@ -1,0 +1,311 @@
+"""Outer Galerkin drivers (reference ``solvers.py``), executed on the GPU.
+
+Same signatures, options, result record and exceptions as the reference:
+``solve_lyapunov(op, c, options)`` (``solvers.py:200-285``) and
+``solve_sylvester_two_sided(op_a, op_b, c1, c2, options)`` (``:288-383``).
+The host keeps only bookkeeping; every n-sized and k^2-sized operation is a
+C-ABI call into libkrymat_b200.so (pass-1 loop with the cheap residual every
+``check_period`` iterations, finalisation, pass-2 regeneration of the basis).
+
+Storage: the device always uses the two-pass (windowed) regeneration; its
+factor equals the stored-mode factor (the regeneration is bitwise
+deterministic, verified by the replay check).  ``peak_basis_vectors`` follows
+the reference's accounting for the requested mode (``basis.py:63-71``).
+"""
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import ConvergenceError, DimensionMismatchError, KrymatError
+
+#: Largest operator order for which ``verify`` recomputes the true residual.
+VERIFY_LIMIT = 20000
+#: Tolerance of the pass-2 replay check (coupling blocks, relative).
+REPLAY_TOL = 1e-8
+#: Default truncation tail mass (reference ``kernels.py:25``).
+TRUNC_EPS = 1e-12
+
+HISTORY_COLUMNS = (
+    "m",
+    "space_dim",
+    "relative_residual",
+    "cum_basis_secs",
+    "cum_residual_secs",
+)
+
+
+@dataclass
+class SolveOptions:
+    """Knobs of the outer iteration (reference ``solvers.py:49-73``)."""
+
+    tol: float = 1e-6
+    max_m: int = 500
+    check_period: int = 1
+    space: str = "standard"
+    storage: str = "stored"
+    trunc_eps: float = TRUNC_EPS
+    verify: bool = False
+
+    def __post_init__(self):
+        if self.tol <= 0.0:
+            raise ValueError("tol must be positive")
+        if self.check_period < 1:
+            raise ValueError("check_period must be >= 1")
+        if self.space not in ("standard", "extended"):
+            raise ValueError("space must be 'standard' or 'extended'")
+        if self.storage not in ("stored", "windowed"):
+            raise ValueError("storage must be 'stored' or 'windowed'")
+
+
+@dataclass
+class LowRankSolution:
+    """Low-rank factors with convergence history (reference ``solvers.py:76-101``)."""
+
+    z1: np.ndarray
+    z2: np.ndarray = None
+    rank: int = 0
+    iterations: int = 0
+    space_dim: int = 0
+    final_residual: float = np.inf
+    history: list = field(default_factory=list)
+    basis_seconds: float = 0.0
+    residual_seconds: float = 0.0
+    recovery_seconds: float = 0.0
+    peak_basis_vectors: int = 0
+    truncation_discarded: float = 0.0
+    verified_residual: float = None
+
+    @property
+    def z(self):
+        return self.z1
+
+
+def _rows(hist, nh):
+    out = []
+    for r in hist[:nh]:
+        out.append((int(r[0]), int(r[1]), float(r[2]), float(r[3]), float(r[4])))
+    return out
+
+
+def _peak(storage, steps, exhausted, s):
+    pushed = 1 + steps - (1 if exhausted else 0)
+    if storage == "stored":
+        return max(pushed - 1, 1) * s
+    return min(pushed, 3) * s
+
+
+def _check_space(opts):
+    if opts.space != "standard":
+        raise NotImplementedError(
+            "extended Krylov spaces need sparse inverse-applies, which are outside the "
+            "B200 hot path (SURVEY.md §8(f) f4); use space='standard'")
+
+
+def _as_rhs(op, c):
+    c = np.atleast_2d(np.asarray(c, dtype=float))
+    if c.ndim != 2 or c.shape[0] != op.n:
+        raise DimensionMismatchError(
+            "right-hand side block of shape %s does not match operator order %d"
+            % (c.shape, op.n))
+    if c.shape[1] > 8:
+        raise DimensionMismatchError("block width %d exceeds the device limit 8" % c.shape[1])
+    return np.ascontiguousarray(c)
+
+
+def _nonconvergence(opts, reason, m, rel, history, both=False):
+    if reason == 2:
+        what = "both Krylov spaces became invariant" if both else \
+            "the Krylov space became invariant"
+        raise ConvergenceError(
+            "%s at m=%d without meeting the tolerance (residual %.3e)" % (what, m, rel),
+            history)
+    raise ConvergenceError(
+        "no convergence to %.1e within %d iterations (last residual %s)"
+        % (opts.tol, opts.max_m, "%.3e" % rel if history else "never checked"),
+        history)
+
+
+class _Pass1:
+    """Runs init + pass 1 on one context; keeps the state for finalisation."""
+
+    def __init__(self, op, c, opts):
+        self.op = op
+        self.c = c
+        self.s = c.shape[1]
+        self.ctx = op.context(self.s, opts.max_m + 2)
+        self.gamma = np.zeros((self.s, self.s))
+        beta2 = ctypes.c_double()
+        _lib.check(_lib.load().kry_init_basis(self.ctx.ptr, _lib.as_dptr(c),
+                                              _lib.as_dptr(self.gamma), ctypes.byref(beta2)))
+        self.beta2 = beta2.value
+
+    def info(self):
+        m, ex = ctypes.c_int(), ctypes.c_int()
+        _lib.load().kry_ctx_info(self.ctx.ptr, None, None, ctypes.byref(m), ctypes.byref(ex))
+        return m.value, bool(ex.value)
+
+    def recover(self, rank):
+        z = np.empty((self.op.n, rank))
+        if rank > 0:
+            _lib.check(_lib.load().kry_recover(self.ctx.ptr, _lib.as_dptr(z)))
+        return z
+
+
+def solve_lyapunov(op, c, options=None):
+    """Galerkin projection solver for A X + X A + C C^T = 0 on the GPU.
+
+    Grows the standard block Krylov space of A and C until the relative
+    residual ||R_m||_F / ||C||_F^2 (cheap projected evaluation) drops below
+    ``options.tol``, then returns X ~ Z Z^T (reference ``solvers.py:200-285``).
+    Raises ConvergenceError (history attached) if ``max_m`` does not suffice.
+    """
+    opts = options if options is not None else SolveOptions()
+    _check_space(opts)
+    c = _as_rhs(op, c)
+    lib = _lib.load()
+    tic = time.perf_counter()
+    p1 = _Pass1(op, c, opts)
+    t_init = time.perf_counter() - tic
+    try:
+        hist = np.zeros((opts.max_m + 1, 5))
+        nh, its, reason = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+        rel = ctypes.c_double(np.inf)
+        rc = lib.kry_solve_lyap_pass1(p1.ctx.ptr, float(opts.tol), int(opts.max_m),
+                                      int(opts.check_period), _lib.as_dptr(hist),
+                                      ctypes.byref(nh), ctypes.byref(its), ctypes.byref(rel),
+                                      ctypes.byref(reason))
+        hist[:nh.value, 3] += t_init
+        history = _rows(hist, nh.value)
+        if rc == _lib.KRY_ERR_CONVERGENCE:
+            m, _ = p1.info()
+            _nonconvergence(opts, reason.value, m, rel.value, history)
+        _lib.check(rc, history)
+        t_basis = history[-1][3] if history else t_init
+        t_res = history[-1][4] if history else 0.0
+        tic = time.perf_counter()
+        rank, disc = ctypes.c_int(0), ctypes.c_double(0.0)
+        _lib.check(lib.kry_finalize_lyap(p1.ctx.ptr, float(opts.trunc_eps), ctypes.byref(rank),
+                                         ctypes.byref(disc)))
+        z = p1.recover(rank.value)
+        t_rec = time.perf_counter() - tic
+        m, ex = p1.info()
+        verified = None
+        if opts.verify and op.n <= VERIFY_LIMIT:
+            verified = true_lyapunov_residual(op, z, c) / p1.beta2
+        return LowRankSolution(
+            z1=z,
+            rank=rank.value,
+            iterations=its.value,
+            space_dim=its.value * p1.s,
+            final_residual=rel.value,
+            history=history,
+            basis_seconds=t_basis,
+            residual_seconds=t_res,
+            recovery_seconds=t_rec,
+            peak_basis_vectors=_peak(opts.storage, m, ex, p1.s),
+            truncation_discarded=disc.value,
+            verified_residual=verified,
+        )
+    finally:
+        p1.ctx.close()
+
+
+def solve_sylvester_two_sided(op_a, op_b, c1, c2, options=None):
+    """Galerkin solver for A X + X B + C1 C2^T = 0 with both sides large
+    (reference ``solvers.py:288-383``): two bases grown in lock step (one
+    device context and CUDA stream each), residual from both projections."""
+    opts = options if options is not None else SolveOptions()
+    _check_space(opts)
+    c1 = np.atleast_2d(np.asarray(c1, dtype=float))
+    c2 = np.atleast_2d(np.asarray(c2, dtype=float))
+    if c1.shape[1] != c2.shape[1]:
+        raise DimensionMismatchError("C1 and C2 must have the same number of columns")
+    c1 = _as_rhs(op_a, c1)
+    c2 = _as_rhs(op_b, c2)
+    lib = _lib.load()
+    tic = time.perf_counter()
+    pa = _Pass1(op_a, c1, opts)
+    try:
+        pb = _Pass1(op_b, c2, opts)
+    except Exception:
+        pa.ctx.close()
+        raise
+    t_init = time.perf_counter() - tic
+    try:
+        hist = np.zeros((opts.max_m + 1, 5))
+        nh, its, reason = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+        rel = ctypes.c_double(np.inf)
+        rc = lib.kry_solve_sylv_pass1(pa.ctx.ptr, pb.ctx.ptr, float(opts.tol), int(opts.max_m),
+                                      int(opts.check_period), _lib.as_dptr(hist),
+                                      ctypes.byref(nh), ctypes.byref(its), ctypes.byref(rel),
+                                      ctypes.byref(reason))
+        hist[:nh.value, 3] += t_init
+        history = _rows(hist, nh.value)
+        if rc == _lib.KRY_ERR_CONVERGENCE:
+            m, _ = pa.info()
+            _nonconvergence(opts, reason.value, m, rel.value, history, both=True)
+        _lib.check(rc, history)
+        t_basis = history[-1][3] if history else t_init
+        t_res = history[-1][4] if history else 0.0
+        tic = time.perf_counter()
+        rank, disc = ctypes.c_int(0), ctypes.c_double(0.0)
+        _lib.check(lib.kry_finalize_sylv(pa.ctx.ptr, pb.ctx.ptr, float(opts.trunc_eps),
+                                         ctypes.byref(rank), ctypes.byref(disc)))
+        z1 = pa.recover(rank.value)
+        z2 = pb.recover(rank.value)
+        t_rec = time.perf_counter() - tic
+        ma, exa = pa.info()
+        mb, exb = pb.info()
+        rhs_norm = float(np.sqrt(pa.beta2) * np.sqrt(pb.beta2))
+        verified = None
+        if opts.verify and max(op_a.n, op_b.n) <= VERIFY_LIMIT:
+            verified = true_sylvester_residual(op_a, z1, z2, c1, c2, op_b.apply) / rhs_norm
+        return LowRankSolution(
+            z1=z1,
+            z2=z2,
+            rank=rank.value,
+            iterations=its.value,
+            space_dim=its.value * pa.s,
+            final_residual=rel.value,
+            history=history,
+            basis_seconds=t_basis,
+            residual_seconds=t_res,
+            recovery_seconds=t_rec,
+            peak_basis_vectors=_peak(opts.storage, ma, exa, pa.s)
+            + _peak(opts.storage, mb, exb, pb.s),
+            truncation_discarded=disc.value,
+            verified_residual=verified,
+        )
+    finally:
+        pa.ctx.close()
+        pb.ctx.close()
+
+
+def true_lyapunov_residual(op, z, c):
+    """||A Z Z^T + Z Z^T A + C C^T||_F from small Gram matrices, on the device
+    (reference ``solvers.py:104-115``)."""
+    z = np.ascontiguousarray(np.atleast_2d(np.asarray(z, dtype=float)))
+    c = np.ascontiguousarray(np.atleast_2d(np.asarray(c, dtype=float)))
+    ctx = op.context(c.shape[1], 1)
+    try:
+        res = ctypes.c_double()
+        _lib.check(_lib.load().kry_true_lyap_residual(ctx.ptr, _lib.as_dptr(z), z.shape[1],
+                                                      _lib.as_dptr(c), ctypes.byref(res)))
+        return res.value
+    finally:
+        ctx.close()
+
+
+def true_sylvester_residual(op_a, z1, z2, c1, c2, apply_b):
+    """||A Z1 Z2^T + Z1 Z2^T B + C1 C2^T||_F via small Gram matrices
+    (reference ``solvers.py:118-122``; the Gram products are tiny)."""
+    az1 = op_a.apply(z1)
+    bz2 = apply_b(z2)
+    u = np.hstack([az1, z1, c1])
+    w = np.hstack([z2, bz2, c2])
+    val = np.sum((u.T @ u) * (w.T @ w))
+    return float(np.sqrt(max(val, 0.0)))

@@ -1,0 +1,248 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle and the
+reference's golden runs, on the same seeded inputs.
+
+Tolerances: integer outputs (iteration counts, ranks) exact; the operator
+apply bit-exact; residual histories |rel_gpu - rel_ref| <= 1e-9 rel_ref +
+floor with floor = 2e-16 (the reference's own roundoff floor on config 2 is
+1.4e-16 in relative-residual units, SURVEY.md §0 finding 1); factors
+||X_gpu - X_ref||_F / ||X_ref||_F <= 1e-8 (north star).
+"""
+
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import paper_1602_05033_b200 as kb
+from oracle import krymat_oracle as ko
+from oracle import problems as P
+from tests.helpers import lanczos_tridiagonal, to_device_tri
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+FLOOR = 2e-16
+
+
+def gold(name):
+    path = os.path.join(GOLD, name + ".npz")
+    if not os.path.exists(path):
+        pytest.skip("golden %s not generated" % name)
+    return np.load(path)
+
+
+def hist_ok(h, ref):
+    h, ref = np.asarray(h), np.asarray(ref)
+    return np.all(np.abs(h - ref) <= 1e-9 * ref + FLOOR), np.max(np.abs(h - ref) / ref)
+
+
+# ------------------------------------------------------------------ operator apply
+@pytest.mark.parametrize("builder", [
+    lambda: P.laplacian2d(37), lambda: P.laplacian3d(13), lambda: P.varcoef2d(29),
+    lambda: P.laplacian1d(101),
+])
+@pytest.mark.parametrize("s", [1, 2, 3, 4, 8, 11])
+def test_apply_bit_exact_vs_scipy(builder, s):
+    a = builder()
+    op = kb.SparseOperator(a)
+    assert op.kind.startswith("stencil")
+    v = np.random.default_rng(s).standard_normal((a.shape[0], s))
+    assert np.array_equal(op.apply(v), a @ v)
+
+
+def test_apply_csr_fallback_bit_exact():
+    rng = np.random.default_rng(3)
+    b = sp.random(300, 300, density=0.03, random_state=np.random.RandomState(4), format="csr")
+    a = (b + b.T - sp.diags(np.full(300, 10.0))).tocsr()
+    op = kb.SparseOperator(a)
+    assert op.kind == "csr"
+    v = rng.standard_normal((300, 4))
+    assert np.array_equal(op.apply(v), a @ v)
+
+
+def test_asymmetric_rejected_with_reference_message():
+    a = sp.csr_matrix(np.array([[-2.0, 1.0], [0.5, -2.0]]))
+    with pytest.raises(kb.AsymmetricMatrixError, match=r"not symmetric.*\(0, 1\)"):
+        kb.SparseOperator(a)
+
+
+# ------------------------------------------------------------------ eigen engine + cTri
+@pytest.mark.parametrize("s,m,general", [(1, 12, False), (2, 10, False), (4, 6, False),
+                                         (2, 14, True), (3, 20, False), (8, 12, True)])
+def test_ctri_lyapunov_matches_oracle(s, m, general):
+    rng = np.random.default_rng(100 * s + m)
+    t, tau = lanczos_tridiagonal(rng, s, m, general=general)
+    gamma = rng.standard_normal((s, s))
+    ref, _ = ko.ctri_lyapunov(t, gamma, tau)
+    got = kb.ctri_lyapunov(to_device_tri(t), gamma, tau)
+    assert abs(got.res - ref) <= 1e-11 * ref
+
+
+def test_ctri_known_answers():
+    for tt in (1.0, 0.25):
+        t = kb.BlockTridiagonal(1, [np.array([[-1.0]])], [])
+        rv = kb.ctri_lyapunov(t, np.array([[1.0]]), np.array([[tt]]))
+        assert np.isclose(rv.res, np.sqrt(2.0) * tt / 2.0, rtol=1e-14)
+    t = kb.BlockTridiagonal(1, [np.array([[-1.0]]), np.array([[-2.0]])], [np.array([[0.0]])])
+    assert kb.ctri_lyapunov(t, np.array([[1.0]]), np.array([[0.7]])).res <= 1e-14
+    t = kb.BlockTridiagonal(1, [np.array([[-1.0]]), np.array([[1.0]])], [np.array([[0.0]])])
+    with pytest.raises(kb.IndefiniteMatrixError):
+        kb.ctri_lyapunov(t, np.array([[1.0]]), np.array([[1.0]]))
+    a1 = kb.BlockTridiagonal(1, [np.array([[-1.0]])], [])
+    a2 = kb.BlockTridiagonal(1, [np.array([[-2.0]])], [])
+    rv = kb.ctri_sylvester(a1, a2, np.eye(1), np.eye(1), np.array([[0.8]]), np.array([[0.3]]))
+    assert np.isclose(rv.res, np.hypot(0.8, 0.3) / 3.0, rtol=1e-14)
+
+
+@pytest.mark.parametrize("s,m", [(1, 8), (2, 6), (2, 15), (4, 9)])
+def test_ctri_sylvester_matches_oracle(s, m):
+    rng = np.random.default_rng(10 * s + m)
+    t, tau = lanczos_tridiagonal(rng, s, m)
+    j, iota = lanczos_tridiagonal(rng, s, m + 3)
+    g1, g2 = rng.standard_normal((s, s)), rng.standard_normal((s, s))
+    ref, _ = ko.ctri_sylvester(t, j, g1, g2, tau, iota)
+    got = kb.ctri_sylvester(to_device_tri(t), to_device_tri(j), g1, g2, tau, iota)
+    assert abs(got.res - ref) <= 1e-11 * ref
+
+
+@pytest.mark.parametrize("s,m", [(1, 30), (3, 15), (8, 10)])
+def test_partial_eig_matches_dense(s, m):
+    rng = np.random.default_rng(7 + s)
+    t, _ = lanczos_tridiagonal(rng, s, m, general=True)
+    sp_ = kb.partial_eig_blocktridiag(to_device_tri(t))
+    lam, q = np.linalg.eigh(t.dense())
+    assert np.allclose(sp_.eigenvalues, lam, rtol=1e-12, atol=1e-12 * np.abs(lam).max())
+    # rows agree up to the sign of each eigenvector (well separated spectrum)
+    sgn = np.sign(np.sum(sp_.first_rows * q[:s], axis=0) + np.sum(sp_.last_rows * q[-s:], axis=0))
+    assert np.allclose(sp_.first_rows * sgn, q[:s], atol=1e-10)
+    assert np.allclose(sp_.last_rows * sgn, q[-s:], atol=1e-10)
+
+
+def test_ctri_on_reference_projection_blocks():
+    # the reference's final T_m / gamma / tau of configs 1 and 2
+    for name in ("c1", "c2"):
+        g = gold(name)
+        s = g["t_diag"].shape[1]
+        t = kb.BlockTridiagonal(s, [0.5 * (d + d.T) for d in g["t_diag"]], list(g["t_off"]))
+        rv = kb.ctri_lyapunov(t, g["gamma"], g["tau"], rhs_norm=float(g["beta2"]))
+        ref = g["history"][-1, 2]
+        assert abs(rv.relative - ref) <= 1e-9 * ref + FLOOR
+
+
+# ------------------------------------------------------------------ solver, small cases
+def _diag_op(vals):
+    return kb.SparseOperator(sp.diags(vals).tocsr())
+
+
+def test_invariant_rhs_converges_immediately():
+    c = np.zeros((6, 1))
+    c[0] = 1.0
+    sol = kb.solve_lyapunov(_diag_op([-1.0] * 6), c, kb.SolveOptions(tol=1e-10, max_m=5))
+    assert sol.iterations == 1
+    ex = np.zeros((6, 6))
+    ex[0, 0] = 0.5
+    assert np.allclose(sol.z @ sol.z.T, ex, atol=1e-12)
+    assert sol.final_residual <= 1e-12
+
+
+def test_nonconvergence_raises_with_history():
+    a = P.laplacian2d(10)
+    c = np.random.default_rng(5).random((100, 1))
+    with pytest.raises(kb.ConvergenceError) as err:
+        kb.solve_lyapunov(kb.SparseOperator(a), c, kb.SolveOptions(tol=1e-12, max_m=3))
+    assert len(err.value.history) == 3
+
+
+def test_rank_deficient_rhs_rejected():
+    with pytest.raises(kb.DeflationUnsupportedError):
+        kb.solve_lyapunov(_diag_op([-1.0, -2.0, -3.0]), np.ones((3, 2)))
+
+
+def test_check_period_controls_history():
+    a = P.laplacian2d(8)
+    c = np.random.default_rng(4).random((64, 1))
+    sol = kb.solve_lyapunov(kb.SparseOperator(a), c,
+                            kb.SolveOptions(tol=1e-7, max_m=80, check_period=5))
+    assert all(r[0] % 5 == 0 for r in sol.history)
+    assert sol.iterations % 5 == 0
+
+
+@pytest.mark.parametrize("n,s,tol", [(12, 2, 1e-8), (16, 1, 1e-9), (9, 3, 1e-8), (14, 8, 1e-8)])
+def test_small_lyapunov_matches_oracle(n, s, tol):
+    a = P.laplacian2d(n)
+    c = np.random.default_rng(n + s).standard_normal((n * n, s))
+    sol = kb.solve_lyapunov(kb.SparseOperator(a), c, kb.SolveOptions(tol=tol, max_m=200))
+    ref = ko.solve_lyapunov(ko.SparseOperator(a), c, ko.SolveOptions(tol=tol, max_m=200))
+    assert sol.iterations == ref.iterations
+    ok, worst = hist_ok([r[2] for r in sol.history], [r[2] for r in ref.history])
+    assert ok, worst
+    assert ko.factor_distance(sol.z, ref.z) <= 1e-8
+    assert sol.rank == ref.rank
+
+
+def test_against_dense_oracle_kronecker():
+    rng = np.random.default_rng(3)
+    vals = -np.exp(rng.uniform(0.0, 3.0, 60))
+    c = rng.random((60, 1))
+    c /= np.linalg.norm(c)
+    sol = kb.solve_lyapunov(_diag_op(vals), c, kb.SolveOptions(tol=1e-8, max_m=60))
+    x_ref = -(c @ c.T) / (vals[:, None] + vals[None, :])
+    assert np.linalg.norm(sol.z @ sol.z.T - x_ref) <= 10 * 1e-8 * np.linalg.norm(c @ c.T)
+
+
+def test_small_sylvester_matches_oracle():
+    a, b = P.varcoef2d(11), P.laplacian3d(5)
+    rng = np.random.default_rng(2)
+    c1, c2 = rng.standard_normal((121, 2)), rng.standard_normal((125, 2))
+    sol = kb.solve_sylvester_two_sided(kb.SparseOperator(a), kb.SparseOperator(b), c1, c2,
+                                       kb.SolveOptions(tol=1e-8, max_m=100))
+    ref = ko.solve_sylvester(ko.SparseOperator(a), ko.SparseOperator(b), c1, c2,
+                             ko.SolveOptions(tol=1e-8, max_m=100))
+    assert sol.iterations == ref.iterations
+    ok, worst = hist_ok([r[2] for r in sol.history], [r[2] for r in ref.history])
+    assert ok, worst
+    assert ko.factor_distance(sol.z1, ref.z1, sol.z2, ref.z2) <= 1e-8
+
+
+def test_history_deterministic():
+    a = P.laplacian2d(20)
+    c = np.random.default_rng(9).standard_normal((400, 2))
+    op = kb.SparseOperator(a)
+    h1 = kb.solve_lyapunov(op, c, kb.SolveOptions(tol=1e-8, max_m=100)).history
+    h2 = kb.solve_lyapunov(op, c, kb.SolveOptions(tol=1e-8, max_m=100)).history
+    assert [r[2] for r in h1] == [r[2] for r in h2]
+
+
+def test_verify_flag():
+    a = P.laplacian2d(8)
+    c = np.random.default_rng(3).random((64, 2))
+    sol = kb.solve_lyapunov(kb.SparseOperator(a), c,
+                            kb.SolveOptions(tol=1e-4, max_m=80, verify=True))
+    assert sol.verified_residual is not None
+    assert abs(sol.verified_residual - sol.final_residual) <= 1e-4 * sol.final_residual + 1e-10
+
+
+# ------------------------------------------------------------------ BASELINE configs
+def _config_parity(name):
+    g = gold(name)
+    cfg = P.build_config(name)
+    sol = kb.solve_lyapunov(kb.SparseOperator(cfg["a"]), cfg["c"],
+                            kb.SolveOptions(tol=cfg["tol"], max_m=cfg["max_m"],
+                                            storage="windowed"))
+    assert sol.iterations == int(g["iterations"])
+    assert sol.rank == int(g["rank"])
+    ok, worst = hist_ok([r[2] for r in sol.history], g["history"][:, 2])
+    assert ok, worst
+    om = P.sketch_omega(cfg["a"].shape[0], 2)
+    sk = sol.z @ (sol.z.T @ om)
+    assert np.linalg.norm(sk - g["sketch"]) <= 1e-8 * np.linalg.norm(g["sketch"])
+    return sol
+
+
+def test_config1_parity_with_reference_run():
+    sol = _config_parity("c1")
+    assert sol.peak_basis_vectors == 3
+
+
+def test_config2_parity_with_reference_run():
+    _config_parity("c2")
