@@ -1,4 +1,6 @@
 // C-ABI of libkrymat_b200.so: contexts, the pass-1 iteration loop,
+// (streams are created blocking so synchronous cudaMemcpy readbacks on the
+// legacy default stream are ordered after the context's kernels)
 // finalisation and the pass-2 regeneration (see include/krymat_b200.h).
 #include "kry_internal.cuh"
 #include "eigen.cuh"
@@ -576,7 +578,7 @@ int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s
   c->dev = device;
   c->s = s;
   c->max_m = max_m;
-  KRY_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  KRY_CUDA(cudaStreamCreate(&c->stream));
   // operator
   OpDev& op = c->op;
   memset(&op, 0, sizeof(op));
@@ -701,20 +703,22 @@ int kry_ctx_info(kry_ctx* c, int64_t* n, int* s, int* m, int* exhausted) {
 int kry_apply(kry_ctx* c, const double* v, double* y, int ncols) {
   KRY_CUDA(cudaSetDevice(c->dev));
   if (ncols < 1) return fail(KRY_ERR_DIMENSION, "block must have at least one column");
+  // device row stride padded to even so 16-byte vector loads stay aligned
+  const int ld = ncols + (ncols & 1);
   double *dv = nullptr, *dy = nullptr;
   const int64_t halo = (c->op.kind == KRY_OP_STENCIL) ? c->op.nxy : 0;
-  KRY_CHECK(dalloc(&dv, (size_t)(c->n + 2 * halo) * ncols));
-  KRY_CHECK(dalloc(&dy, (size_t)c->n * ncols));
-  KRY_CUDA(cudaMemsetAsync(dv, 0, (c->n + 2 * halo) * ncols * sizeof(double), c->stream));
-  double* dvv = dv + halo * ncols;
-  KRY_CUDA(cudaMemcpyAsync(dvv, v, c->n * ncols * sizeof(double), cudaMemcpyHostToDevice,
-                           c->stream));
+  KRY_CHECK(dalloc(&dv, (size_t)(c->n + 2 * halo) * ld));
+  KRY_CHECK(dalloc(&dy, (size_t)c->n * ld));
+  KRY_CUDA(cudaMemsetAsync(dv, 0, (c->n + 2 * halo) * ld * sizeof(double), c->stream));
+  double* dvv = dv + halo * ld;
+  KRY_CUDA(cudaMemcpy2DAsync(dvv, ld * sizeof(double), v, ncols * sizeof(double),
+                             ncols * sizeof(double), c->n, cudaMemcpyHostToDevice, c->stream));
   for (int c0 = 0; c0 < ncols; c0 += KRY_SMAX) {
     const int w = std::min(KRY_SMAX, ncols - c0);
-    KRY_CHECK(launch_apply_store(c->stream, w, c->op, dvv + c0, ncols, dy + c0, ncols, c->n));
+    KRY_CHECK(launch_apply_store(c->stream, w, c->op, dvv + c0, ld, dy + c0, ld, c->n));
   }
-  KRY_CUDA(cudaMemcpyAsync(y, dy, c->n * ncols * sizeof(double), cudaMemcpyDeviceToHost,
-                           c->stream));
+  KRY_CUDA(cudaMemcpy2DAsync(y, ncols * sizeof(double), dy, ld * sizeof(double),
+                             ncols * sizeof(double), c->n, cudaMemcpyDeviceToHost, c->stream));
   KRY_CUDA(cudaStreamSynchronize(c->stream));
   cudaFree(dv);
   cudaFree(dy);
@@ -1238,7 +1242,7 @@ struct Standalone {
   int build(int device, int s_, int m_, const double* diag, const double* sub) {
     s = s_; m = m_;
     KRY_CUDA(cudaSetDevice(device));
-    KRY_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    KRY_CUDA(cudaStreamCreate(&st));
     KRY_CHECK(dalloc(&dmem, (size_t)(4 * (m + 1) + 8) * 64));
     KRY_CUDA(cudaMemset(dmem, 0, (size_t)(4 * (m + 1) + 8) * 64 * sizeof(double)));
     double* raw_d = dmem;
@@ -1372,27 +1376,30 @@ int kry_true_lyap_residual(kry_ctx* c, const double* z, int t, const double* ch,
   const int s = c->s;
   const int64_t n = c->n;
   const int p = 2 * t + s;
+  const int ldm = p + (p & 1), ldz = t + (t & 1);   // even strides: aligned vector access
   const int64_t halo = (c->op.kind == KRY_OP_STENCIL) ? c->op.nxy : 0;
   double *M = nullptr, *zd = nullptr, *G = nullptr;
-  KRY_CHECK(dalloc(&M, (size_t)n * p));
-  KRY_CHECK(dalloc(&zd, (size_t)(n + 2 * halo) * std::max(t, 1)));
+  KRY_CHECK(dalloc(&M, (size_t)n * ldm));
+  KRY_CHECK(dalloc(&zd, (size_t)(n + 2 * halo) * std::max(ldz, 2)));
   KRY_CHECK(dalloc(&G, (size_t)p * p));
-  KRY_CUDA(cudaMemsetAsync(zd, 0, (n + 2 * halo) * std::max(t, 1) * sizeof(double), c->stream));
-  double* zz = zd + halo * t;
-  KRY_CUDA(cudaMemcpyAsync(zz, z, n * t * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-  // M = [A Z | Z | C] row-major n x p
+  KRY_CUDA(cudaMemsetAsync(zd, 0, (n + 2 * halo) * std::max(ldz, 2) * sizeof(double), c->stream));
+  KRY_CUDA(cudaMemsetAsync(M, 0, n * ldm * sizeof(double), c->stream));
+  double* zz = zd + halo * ldz;
+  KRY_CUDA(cudaMemcpy2DAsync(zz, ldz * sizeof(double), z, t * sizeof(double), t * sizeof(double),
+                             n, cudaMemcpyHostToDevice, c->stream));
+  // M = [A Z | Z | C] row-major n x p (stride ldm)
   for (int c0 = 0; c0 < t; c0 += KRY_SMAX) {
     const int w = std::min(KRY_SMAX, t - c0);
-    KRY_CHECK(launch_apply_store(c->stream, w, c->op, zz + c0, t, M + c0, p, n));
+    KRY_CHECK(launch_apply_store(c->stream, w, c->op, zz + c0, ldz, M + c0, ldm, n));
   }
-  KRY_CUDA(cudaMemcpy2DAsync(M + t, p * sizeof(double), zz, t * sizeof(double), t * sizeof(double),
-                             n, cudaMemcpyDeviceToDevice, c->stream));
-  KRY_CUDA(cudaMemcpy2DAsync(M + 2 * t, p * sizeof(double), ch, s * sizeof(double),
+  KRY_CUDA(cudaMemcpy2DAsync(M + t, ldm * sizeof(double), zz, ldz * sizeof(double),
+                             t * sizeof(double), n, cudaMemcpyDeviceToDevice, c->stream));
+  KRY_CUDA(cudaMemcpy2DAsync(M + 2 * t, ldm * sizeof(double), ch, s * sizeof(double),
                              s * sizeof(double), n, cudaMemcpyHostToDevice, c->stream));
   const double one = 1.0, zero = 0.0;
-  // G = M^T M : col-major view of M is p x n (ld p)
-  if (cublasDgemm(c->cublas, CUBLAS_OP_N, CUBLAS_OP_T, p, p, (int)n, &one, M, p, M, p, &zero, G,
-                  p) != CUBLAS_STATUS_SUCCESS)
+  // G = M^T M : col-major view of M is p x n (ld ldm)
+  if (cublasDgemm(c->cublas, CUBLAS_OP_N, CUBLAS_OP_T, p, p, (int)n, &one, M, ldm, M, ldm, &zero,
+                  G, p) != CUBLAS_STATUS_SUCCESS)
     return fail(KRY_ERR_CUDA, "cublasDgemm (verify) failed");
   std::vector<double> h((size_t)p * p);
   KRY_CUDA(cudaMemcpyAsync(h.data(), G, h.size() * sizeof(double), cudaMemcpyDeviceToHost,

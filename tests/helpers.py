@@ -42,3 +42,27 @@ def to_device_tri(t):
     import paper_1602_05033_b200 as kb
     return kb.BlockTridiagonal(t.ell, [np.array(d) for d in t.diag],
                                [np.array(b) for b in t.off])
+
+
+class ReorderedOperator:
+    """Oracle operator with a different (exact-arithmetic-equal) summation
+    order: (U v + D v) + L v.  Running the oracle with it measures the
+    reference algorithm's own roundoff floor (SURVEY.md §8(c) protocol)."""
+
+    def __init__(self, a):
+        import scipy.sparse as sp
+        a = sp.csr_matrix(a)
+        self.n = a.shape[0]
+        self.lo = sp.tril(a, -1).tocsr()
+        self.up = sp.triu(a, 1).tocsr()
+        self.d = sp.diags(a.diagonal()).tocsr()
+
+    def apply(self, v):
+        return (self.up @ v + self.d @ v) + self.lo @ v
+
+
+def noise_floor(h_ref, h_perturbed):
+    """max |delta| over the common prefix of two residual histories."""
+    k = min(len(h_ref), len(h_perturbed))
+    a, b = np.asarray(h_ref[:k]), np.asarray(h_perturbed[:k])
+    return float(np.max(np.abs(a - b))) if k else 0.0
