@@ -653,7 +653,7 @@ int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s
   c->T.S = c->tmem + (int64_t)4 * cap * 64;
   c->T.cap = cap;
   c->grid = gram_grid_for(nloc);
-  c->g.max_grid = 148 * 6;
+  c->g.max_grid = KRY_MAX_GRID;
   KRY_CHECK(dalloc(&c->g.partials, (size_t)c->g.max_grid * 24 * 8));
   KRY_CHECK(dalloc(&c->g.ticket, 8));
   KRY_CUDA(cudaMemset(c->g.ticket, 0, 8 * sizeof(unsigned)));

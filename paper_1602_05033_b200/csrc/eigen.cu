@@ -229,16 +229,38 @@ __global__ void __launch_bounds__(1024) k_eig_deflate(EigView e, int K, const do
   }
 }
 
-// ------------------------------------------------------------------ E2: secular roots
-__global__ void __launch_bounds__(128) k_eig_secular(EigView e) {
+// ------------------------------------------------------------------ fast reciprocal
+// rcp.approx (MUFU, ~23 bits) + two Newton steps: ~1 ulp, no division
+// slow path.  Used where a relative error of a few ulp per term is far below
+// the rounding level of the surrounding sums.
+__device__ __forceinline__ double frcp(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  double e = fma(-q, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-q, r, 1.0);
+  return fma(r, e, r);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ------------------------------------------------------------------ E2: secular roots (warp per root)
+// h(mu) = mu - d - sum_j z_j^2 / (mu - lam_j); root i lies in (lam_{i-1}, lam_i)
+// (i = 0 / p: below / above all poles).  tau = mu - origin with the origin at
+// the nearer pole; rational two-pole model step (LAPACK dlaed4 style) with a
+// bisection safeguard.  Lanes split the poles; all lanes iterate in lockstep.
+__global__ void __launch_bounds__(256) k_eig_secular(EigView e) {
   const int p = e.counts[0];
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i > p) return;
   const double d = e.scal[0];
   if (p == 0) {
-    e.org[0] = d;
-    e.tau[0] = 0.0;
-    e.mu[0] = d;
+    if (lane == 0) { e.org[0] = d; e.tau[0] = 0.0; e.mu[0] = d; }
     return;
   }
   const double* __restrict__ poles = e.poles;
@@ -255,12 +277,13 @@ __global__ void __launch_bounds__(128) k_eig_secular(EigView e) {
   } else {
     const double a = poles[i - 1], b = poles[i];
     const double mid = 0.5 * (a + b);
-    double hm = mid - d;
-    for (int j = 0; j < p; ++j) {
+    double hm = 0.0;
+    for (int j = lane; j < p; j += 32) {
       const double zj = zz[j];
-      hm -= zj * zj / (mid - poles[j]);
+      hm -= zj * zj * frcp(mid - poles[j]);
     }
-    if (hm > 0.0) { org = a; } else { org = b; }
+    hm = warp_sum(hm) + (mid - d);
+    org = (hm > 0.0) ? a : b;
     ia = i - 1; ib = i;
   }
   const double da = (ia >= 0) ? poles[ia] - org : 0.0;
@@ -269,26 +292,31 @@ __global__ void __launch_bounds__(128) k_eig_secular(EigView e) {
   double tb = (ib >= 0) ? db : hi - org;
   double t = 0.5 * (ta + tb);
   const double c0 = org - d;
+  const bool near_left = (ia >= 0) && (org == poles[ia]);
   for (int it = 0; it < 80; ++it) {
     double psiL = 0.0, dpsiL = 0.0, psiR = 0.0, dpsiR = 0.0, sabs = 0.0;
-    for (int j = 0; j < p; ++j) {
+    for (int j = lane; j < p; j += 32) {
       const double zj = zz[j];
       const double q = t - (poles[j] - org);
-      const double term = zj * zj / q;
-      const double dterm = term / q;
+      const double r = frcp(q);
+      const double term = zj * zj * r;
+      const double dterm = term * r;
       if (j <= ia) { psiL -= term; dpsiL += dterm; }
       else { psiR -= term; dpsiR += dterm; }
       sabs += fabs(term);
     }
+    psiL = warp_sum(psiL); dpsiL = warp_sum(dpsiL);
+    psiR = warp_sum(psiR); dpsiR = warp_sum(dpsiR);
+    sabs = warp_sum(sabs);
     const double h = t + c0 + psiL + psiR;
     const double err = 8.0 * EPS * (fabs(t) + fabs(c0) + sabs);
     if (h > 0.0) tb = t; else ta = t;
     if (fabs(h) <= err) break;
-    double tn;
+    double tn = 0.0;
     bool ok = false;
     if (ia >= 0 && ib >= 0) {
       double w1, w2;
-      if (ia >= 0 && org == poles[ia]) {
+      if (near_left) {
         w1 = dpsiL * (t - da) * (t - da);
         w2 = (dpsiR + 1.0) * (t - db) * (t - db);
       } else {
@@ -298,8 +326,7 @@ __global__ void __launch_bounds__(128) k_eig_secular(EigView e) {
       const double c = h + w1 / (t - da) + w2 / (t - db);
       const double A = c, B = c * (da + db) + w1 + w2, C = c * da * db + w1 * db + w2 * da;
       if (A != 0.0) {
-        const double disc = fmax(B * B - 4.0 * A * C, 0.0);
-        const double sq = sqrt(disc);
+        const double sq = sqrt(fmax(B * B - 4.0 * A * C, 0.0));
         double r1, r2;
         if (B >= 0.0) { r1 = (B + sq) / (2.0 * A); r2 = (B + sq) != 0.0 ? 2.0 * C / (B + sq) : r1; }
         else { r1 = (B - sq) != 0.0 ? 2.0 * C / (B - sq) : 0.0; r2 = (B - sq) / (2.0 * A); }
@@ -312,42 +339,57 @@ __global__ void __launch_bounds__(128) k_eig_secular(EigView e) {
     } else {
       const double psi = psiL + psiR, dpsi = dpsiL + dpsiR;
       const double w = dpsi * t * t;
-      const double cc = psi + w / t;
-      const double B = c0 + cc;
+      const double B = c0 + psi + w / t;
       const double sq = sqrt(B * B + 4.0 * w);
-      if (ib < 0) {  // top root, tau > 0
-        tn = (B >= 0.0) ? 2.0 * w / (B + sq) : 0.5 * (sq - B);
-      } else {       // bottom root, tau < 0
-        tn = (B > 0.0) ? -0.5 * (B + sq) : 2.0 * w / (B - sq);
-      }
+      if (ib < 0) tn = (B >= 0.0) ? 2.0 * w / (B + sq) : 0.5 * (sq - B);   // top root
+      else tn = (B > 0.0) ? -0.5 * (B + sq) : 2.0 * w / (B - sq);          // bottom root
       ok = (tn > ta && tn < tb);
     }
     if (!ok || !isfinite(tn)) tn = 0.5 * (ta + tb);
     if (fabs(tn - t) <= 4.0 * EPS * fabs(t)) { t = tn; break; }
     t = tn;
   }
-  e.org[i] = org;
-  e.tau[i] = t;
-  e.mu[i] = org + t;
+  if (lane == 0) {
+    e.org[i] = org;
+    e.tau[i] = t;
+    e.mu[i] = org + t;
+  }
 }
 
-// ------------------------------------------------------------------ E3: Gu-Eisenstat zhat
-__global__ void __launch_bounds__(128) k_eig_zhat(EigView e) {
+// ------------------------------------------------------------------ E3: Gu-Eisenstat zhat (warp per pole)
+// zhat_j^2 = |lam_j - mu_j| |lam_j - mu_{j+1}| prod_{i<j} |lam_j - mu_i|/|lam_j - lam_i|
+//            prod_{i>j} |lam_j - mu_{i+1}|/|lam_j - lam_i|   (all ratios > 1)
+__global__ void __launch_bounds__(256) k_eig_zhat(EigView e) {
   const int p = e.counts[0];
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (j >= p) return;
   const double lj = e.poles[j];
-  // |lam_j - mu_i| = |(lam_j - org_i) - tau_i|
-  auto dm = [&](int i) { return fabs((lj - e.org[i]) - e.tau[i]); };
-  double prod = dm(j) * dm(j + 1);
-  for (int i = 0; i < j; ++i) prod *= dm(i) / fabs(lj - e.poles[i]);
-  for (int i = j + 1; i < p; ++i) prod *= dm(i + 1) / fabs(lj - e.poles[i]);
-  const double zh = sqrt(prod);
-  e.zhat[j] = (e.zz[j] >= 0.0) ? zh : -zh;
+  double prod = 1.0;
+  for (int i = lane; i < p; i += 32) {
+    if (i == j) continue;
+    const int ir = (i < j) ? i : i + 1;
+    const double num = fabs((lj - e.org[ir]) - e.tau[ir]);
+    prod *= num * frcp(fabs(lj - e.poles[i]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) prod *= __shfl_xor_sync(0xffffffffu, prod, o);
+  if (lane == 0) {
+    const double a = fabs((lj - e.org[j]) - e.tau[j]);
+    const double b = fabs((lj - e.org[j + 1]) - e.tau[j + 1]);
+    const double zh = sqrt(prod * a * b);
+    e.zhat[j] = (e.zz[j] >= 0.0) ? zh : -zh;
+  }
 }
 
 // ------------------------------------------------------------------ E4: eigenvectors, tracked rows, merge
-#define E4_CH 128
+// Stage 1 (k_eig_vec_partial): CTA (root tile x pole chunk) -> partial sums of
+//   nrm2 = sum_j v_ij^2, F[r] = sum_j F_old[r][j] v_ij, L[r] = sum_j L_old[r+1][j] v_ij,
+//   v_ij = zhat_j / (mu_i - lam_j), written to part[chunk][root][2S].
+// Stage 2 (k_eig_vec_finish): fixed-order sum over chunks, normalisation,
+//   merge into sorted order; deflated columns copied unchanged.
+#define E4_RT 128   // roots per CTA
+#define E4_CH 128   // poles per chunk
 __device__ __forceinline__ int count_le(const double* a, int n, double v) {  // # a[k] <= v
   int lo = 0, hi = n;
   while (lo < hi) {
@@ -366,7 +408,52 @@ __device__ __forceinline__ int count_lt(const double* a, int n, double v) {  // 
 }
 
 template <int S>
-__global__ void __launch_bounds__(128) k_eig_vectors(EigView e, int K, int root_blocks) {
+__global__ void __launch_bounds__(E4_RT) k_eig_vec_partial(EigView e, double* part, int nroot_cap) {
+  const int p = e.counts[0];
+  const int chunk = blockIdx.y;
+  const int c0 = chunk * E4_CH;
+  if (c0 >= p && !(p == 0 && chunk == 0)) return;
+  const int64_t km = e.kmax;
+  __shared__ double sP[E4_CH], sZ[E4_CH];
+  __shared__ double sF[S][E4_CH];
+  __shared__ double sL[S][E4_CH];
+  const int jj = c0 + threadIdx.x;
+  if (jj < p) {
+    sP[threadIdx.x] = e.poles[jj];
+    sZ[threadIdx.x] = e.zhat[jj];
+    const int col = e.pmap[jj];
+#pragma unroll
+    for (int r = 0; r < S; ++r) sF[r][threadIdx.x] = e.F_old[r * km + col];
+#pragma unroll
+    for (int r = 0; r < S - 1; ++r) sL[r][threadIdx.x] = e.L_old[(r + 1) * km + col];
+  }
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > p) return;
+  const double org = e.org[i], tau = e.tau[i];
+  double nrm2 = 0.0, aF[S], aL[S];
+#pragma unroll
+  for (int r = 0; r < S; ++r) aF[r] = aL[r] = 0.0;
+  const int cnt = min(E4_CH, p - c0);
+  for (int q = 0; q < cnt; ++q) {
+    const double v = sZ[q] * frcp(tau - (sP[q] - org));   // zhat_j / (mu_i - lam_j)
+    nrm2 = fma(v, v, nrm2);
+#pragma unroll
+    for (int r = 0; r < S; ++r) aF[r] = fma(sF[r][q], v, aF[r]);
+#pragma unroll
+    for (int r = 0; r < S - 1; ++r) aL[r] = fma(sL[r][q], v, aL[r]);
+  }
+  double* out = part + ((int64_t)chunk * nroot_cap + i) * (2 * S);
+  out[0] = nrm2;
+#pragma unroll
+  for (int r = 0; r < S; ++r) out[1 + r] = aF[r];
+#pragma unroll
+  for (int r = 0; r < S - 1; ++r) out[1 + S + r] = aL[r];
+}
+
+template <int S>
+__global__ void __launch_bounds__(128) k_eig_vec_finish(EigView e, const double* part,
+                                                        int nroot_cap, int K, int root_blocks) {
   const int p = e.counts[0];
   const int nd = e.counts[1];
   const int64_t km = e.kmax;
@@ -386,52 +473,25 @@ __global__ void __launch_bounds__(128) k_eig_vectors(EigView e, int K, int root_
     if (K < S) e.F_new[K * km + pos] = 0.0;
     return;
   }
-  __shared__ double sP[E4_CH], sZ[E4_CH];
-  __shared__ double sF[S][E4_CH];
-  __shared__ double sL[S][E4_CH];
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = i <= p;
-  double org = 0.0, tau = 0.0;
-  if (active) { org = e.org[i]; tau = e.tau[i]; }
-  double nrm2 = 0.0;
-  double aF[S], aL[S];
+  if (i > p) return;
+  const int nch = (p + E4_CH - 1) / E4_CH;
+  double acc[2 * S];
 #pragma unroll
-  for (int r = 0; r < S; ++r) aF[r] = aL[r] = 0.0;
-  for (int c0 = 0; c0 < p; c0 += E4_CH) {
-    __syncthreads();
-    const int jj = c0 + threadIdx.x;
-    if (jj < p) {
-      sP[threadIdx.x] = e.poles[jj];
-      sZ[threadIdx.x] = e.zhat[jj];
-      const int col = e.pmap[jj];
+  for (int q = 0; q < 2 * S; ++q) acc[q] = 0.0;
+  for (int c = 0; c < nch; ++c) {
+    const double* src = part + ((int64_t)c * nroot_cap + i) * (2 * S);
 #pragma unroll
-      for (int r = 0; r < S; ++r) sF[r][threadIdx.x] = e.F_old[r * km + col];
-#pragma unroll
-      for (int r = 0; r < S - 1; ++r) sL[r][threadIdx.x] = e.L_old[(r + 1) * km + col];
-    }
-    __syncthreads();
-    const int cnt = min(E4_CH, p - c0);
-    if (active) {
-      for (int q = 0; q < cnt; ++q) {
-        const double diff = tau - (sP[q] - org);   // mu_i - lam_j
-        const double v = sZ[q] / diff;
-        nrm2 = fma(v, v, nrm2);
-#pragma unroll
-        for (int r = 0; r < S; ++r) aF[r] = fma(sF[r][q], v, aF[r]);
-#pragma unroll
-        for (int r = 0; r < S - 1; ++r) aL[r] = fma(sL[r][q], v, aL[r]);
-      }
-    }
+    for (int q = 0; q < 2 * S; ++q) acc[q] += src[q];
   }
-  if (!active) return;
-  const double inv = 1.0 / sqrt(1.0 + nrm2);
+  const double inv = 1.0 / sqrt(1.0 + acc[0]);
   const double mu = e.mu[i];
   const int pos = i + count_le(e.def_lam, nd, mu);
   e.lam_new[pos] = mu;
 #pragma unroll
-  for (int r = 0; r < S; ++r) e.F_new[r * km + pos] = aF[r] * inv;
+  for (int r = 0; r < S; ++r) e.F_new[r * km + pos] = acc[1 + r] * inv;
 #pragma unroll
-  for (int r = 0; r < S - 1; ++r) e.L_new[r * km + pos] = aL[r] * inv;
+  for (int r = 0; r < S - 1; ++r) e.L_new[r * km + pos] = acc[1 + S + r] * inv;
   e.L_new[(S - 1) * km + pos] = inv;
   if (K < S) e.F_new[K * km + pos] = inv;
 }
@@ -557,6 +617,9 @@ int EigEngine::init(int s_, int kmax_, int device) {
   doubles += 16;                  // scal
   doubles += 4096;                // partials
   doubles += 16;                  // res
+  const size_t nch_max = (nk + 127) / 128 + 1;
+  const size_t vpart_n = nch_max * (nk + 8) * 16;
+  doubles += vpart_n;             // E4 partial sums
   KRY_CUDA(cudaMalloc(&dbuf, doubles * sizeof(double)));
   KRY_CUDA(cudaMemset(dbuf, 0, doubles * sizeof(double)));
   double* p = dbuf;
@@ -570,6 +633,7 @@ int EigEngine::init(int s_, int kmax_, int device) {
   scal = p; p += 16;
   partials = p; p += 4096;
   res = p; p += 16;
+  vpart = p; p += vpart_n;
   size_t ints = 5 * nk + 8;
   KRY_CUDA(cudaMalloc(&ibuf, ints * sizeof(int)));
   KRY_CUDA(cudaMemset(ibuf, 0, ints * sizeof(int)));
@@ -606,20 +670,31 @@ int EigEngine::append_block(cudaStream_t st, const double* dsym_blk, const doubl
   for (int a = 0; a < s; ++a) {
     EigView v = view();
     k_eig_deflate<<<1, 1024, 0, st>>>(v, K, dsym_blk, sub_prev, a);
-    const int nroot_blocks = (K + 1 + 127) / 128;
-    k_eig_secular<<<nroot_blocks, 128, 0, st>>>(v);
-    const int npole_blocks = (K + 127) / 128;
-    if (npole_blocks > 0) k_eig_zhat<<<npole_blocks, 128, 0, st>>>(v);
+    // K+1 roots at most, one warp each
+    const int warps_per_cta = 8;
+    const int nroot_warp_blocks = (K + 1 + warps_per_cta - 1) / warps_per_cta;
+    k_eig_secular<<<nroot_warp_blocks, 32 * warps_per_cta, 0, st>>>(v);
+    int nl = 2;
+    if (K > 0) {
+      const int npole_warp_blocks = (K + warps_per_cta - 1) / warps_per_cta;
+      k_eig_zhat<<<npole_warp_blocks, 32 * warps_per_cta, 0, st>>>(v);
+      ++nl;
+    }
+    const int root_blocks = (K + 1 + 127) / 128;
+    const int nch = std::max(1, (K + 127) / 128);
+    const int cap = kmax + 8;
+    dim3 g1(root_blocks, nch);
     const int ndef_blocks = (K + 127) / 128;
-    const int grid = nroot_blocks + ndef_blocks;
-#define L(S) k_eig_vectors<S><<<grid, 128, 0, st>>>(v, K, nroot_blocks)
+#define L(S)                                                                               \
+  k_eig_vec_partial<S><<<g1, 128, 0, st>>>(v, vpart, cap);                                \
+  k_eig_vec_finish<S><<<root_blocks + ndef_blocks, 128, 0, st>>>(v, vpart, cap, K, root_blocks)
     switch (s) {
       case 1: L(1); break; case 2: L(2); break; case 3: L(3); break; case 4: L(4); break;
       case 5: L(5); break; case 6: L(6); break; case 7: L(7); break; case 8: L(8); break;
       default: return fail(KRY_ERR_ARGUMENT, "block width s must be 1..8");
     }
 #undef L
-    count_launch(npole_blocks > 0 ? 4 : 3);
+    count_launch(nl + 2);
     KRY_CUDA(cudaGetLastError());
     cur = 1 - cur;
     K += 1;

@@ -24,7 +24,7 @@ struct EigEngine {
   double *z = nullptr, *poles = nullptr, *zz = nullptr, *zhat = nullptr, *def_lam = nullptr,
          *mu = nullptr;
   double *org = nullptr, *tau = nullptr, *u = nullptr, *w = nullptr, *scal = nullptr,
-         *partials = nullptr, *res = nullptr;
+         *partials = nullptr, *res = nullptr, *vpart = nullptr;
   int *cand = nullptr, *dflag = nullptr, *pflag = nullptr, *pmap = nullptr,
       *def_idx = nullptr, *counts = nullptr;
 

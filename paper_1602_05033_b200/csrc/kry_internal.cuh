@@ -18,6 +18,7 @@
 
 #define KRY_SMAX 8
 #define KRY_SS 64
+#define KRY_MAX_GRID (148 * 16)
 
 namespace kry {
 

@@ -21,12 +21,16 @@
 // matrix; row sums use __dmul_rn/__dadd_rn in CSR column order so A*V equals
 // scipy's csr_matvecs (operators.py:101) bit for bit.
 #include "kry_internal.cuh"
+#include <algorithm>
 #include <cmath>
+#include <mutex>
+#include <unordered_map>
 
 namespace kry {
 
 #define TP 128     // points per tile = threads per CTA
-#define LDX 24     // smem row stride (doubles); 24 = 8 mod 16 -> conflict-free DMMA operand loads
+#define XCOLS 24   // tile columns (<= 3 groups of 8)
+#define LDP (TP + 4)  // transposed tile stride: conflict-free row writes and DMMA loads
 
 // ------------------------------------------------------------------ vector io
 template <int S>
@@ -132,10 +136,10 @@ __device__ __forceinline__ void tile_gram(const double* sX, int k0, int ycol, do
   const int g = lane >> 2, t = lane & 3;
 #pragma unroll
   for (int ks = 0; ks < 8; ++ks) {
-    const double* row = sX + (k0 + ks * 4 + t) * LDX;
-    const double b = row[ycol + g];
+    const int k = k0 + ks * 4 + t;   // point index inside the tile
+    const double b = sX[(ycol + g) * LDP + k];
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][0], acc[mt][1], row[mt * 8 + g], b);
+    for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][0], acc[mt][1], sX[(mt * 8 + g) * LDP + k], b);
   }
 }
 
@@ -561,7 +565,7 @@ __device__ void finish_reduction(const double (&acc)[MP / 8][2], double* sX, dou
   const int g = lane >> 2, t = lane & 3;
   __syncthreads();
   // per-warp tiles to smem: red[warp][m*8+n]
-  double* red = sX;  // 4 * NE doubles <= 4*192 < 128*24
+  double* red = sX;  // 4 * NE doubles <= 4*192 < 24*132
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
     red[warp * NE + (mt * 8 + g) * 8 + 2 * t] = acc[mt][0];
@@ -603,19 +607,19 @@ __device__ void finish_reduction(const double (&acc)[MP / 8][2], double* sX, dou
 // ------------------------------------------------------------------ kernels
 // Combine: Vn = Vo Mo + Vc Mc + (A Vc) Mw ; Gram [Vc | A Vc | Vn]^T Vn
 template <int S>
-__global__ void __launch_bounds__(TP) k_combine(OpDev op, CombineCall c, DevState* st,
+__global__ void __launch_bounds__(TP, 5) k_combine(OpDev op, CombineCall c, DevState* st,
                                                 TStore T, double* partials, unsigned* ticket) {
   constexpr int NG = 3;
   constexpr int W = NG * S;
   constexpr int MP = (W + 7) / 8 * 8;
   constexpr int MT = MP / 8;
-  __shared__ __align__(16) double sX[TP * LDX];
+  __shared__ __align__(16) double sX[XCOLS * LDP];
   __shared__ __align__(16) double sM[3 * 64];
   if (st->status != KRY_OK || (st->flags & (KRY_FLAG_FALLBACK | KRY_FLAG_EXHAUSTED))) {
     if (c.write_new) return;  // never combine with invalid coefficients
   }
   for (int e = threadIdx.x; e < 3 * 64; e += TP) sM[e] = st->M[e];
-  for (int e = 0; e < LDX; ++e) sX[threadIdx.x * LDX + e] = 0.0;
+  for (int e = 0; e < XCOLS; ++e) sX[e * LDP + threadIdx.x] = 0.0;
   double acc[MT][2];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
@@ -625,7 +629,7 @@ __global__ void __launch_bounds__(TP) k_combine(OpDev op, CombineCall c, DevStat
   for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
     const int64_t tile = c.reverse ? (ntiles - 1 - it) : it;
     const int64_t i64 = tile * TP + threadIdx.x;
-    double* row = sX + threadIdx.x * LDX;
+    double* row = sX + threadIdx.x;   // column c at row[c * LDP]
     if (i64 < c.n) {
       const int i = (int)i64;
       double vc[S], w[S], vn[S];
@@ -663,13 +667,13 @@ __global__ void __launch_bounds__(TP) k_combine(OpDev op, CombineCall c, DevStat
       }
 #pragma unroll
       for (int a = 0; a < S; ++a) {
-        row[a] = vc[a];
-        row[S + a] = w[a];
-        row[2 * S + a] = vn[a];
+        row[(a) * LDP] = vc[a];
+        row[(S + a) * LDP] = w[a];
+        row[(2 * S + a) * LDP] = vn[a];
       }
     } else {
 #pragma unroll
-      for (int a = 0; a < W; ++a) row[a] = 0.0;
+      for (int a = 0; a < W; ++a) row[(a) * LDP] = 0.0;
     }
     __syncthreads();
     tile_gram<MT>(sX, warp * 32, 2 * S, acc);
@@ -680,14 +684,14 @@ __global__ void __launch_bounds__(TP) k_combine(OpDev op, CombineCall c, DevStat
 
 // Apply + Gram: X = [V | A V], Y = A V  (use_op) or X = [V], Y = V
 template <int S, int USE_OP>
-__global__ void __launch_bounds__(TP) k_apply_gram(OpDev op, ApplyGramCall c, DevState* st,
+__global__ void __launch_bounds__(TP, 5) k_apply_gram(OpDev op, ApplyGramCall c, DevState* st,
                                                    TStore T, double* partials, unsigned* ticket) {
   constexpr int NG = USE_OP ? 2 : 1;
   constexpr int W = NG * S;
   constexpr int MP = (W + 7) / 8 * 8;
   constexpr int MT = MP / 8;
-  __shared__ __align__(16) double sX[TP * LDX];
-  for (int e = 0; e < LDX; ++e) sX[threadIdx.x * LDX + e] = 0.0;
+  __shared__ __align__(16) double sX[XCOLS * LDP];
+  for (int e = 0; e < XCOLS; ++e) sX[e * LDP + threadIdx.x] = 0.0;
   double acc[MT][2];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
@@ -697,21 +701,21 @@ __global__ void __launch_bounds__(TP) k_apply_gram(OpDev op, ApplyGramCall c, De
   for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
     const int64_t tile = c.reverse ? (ntiles - 1 - it) : it;
     const int64_t i64 = tile * TP + threadIdx.x;
-    double* row = sX + threadIdx.x * LDX;
+    double* row = sX + threadIdx.x;   // column c at row[c * LDP]
     if (i64 < c.n) {
       double v[S];
       load_vec<S>(c.v + i64 * c.ldv, v);
 #pragma unroll
-      for (int a = 0; a < S; ++a) row[a] = v[a];
+      for (int a = 0; a < S; ++a) row[(a) * LDP] = v[a];
       if constexpr (USE_OP) {
         double w[S];
         apply_point<S>(op, c.v, c.ldv, (int)i64, v, w);
 #pragma unroll
-        for (int a = 0; a < S; ++a) row[S + a] = w[a];
+        for (int a = 0; a < S; ++a) row[(S + a) * LDP] = w[a];
       }
     } else {
 #pragma unroll
-      for (int a = 0; a < W; ++a) row[a] = 0.0;
+      for (int a = 0; a < W; ++a) row[(a) * LDP] = 0.0;
     }
     __syncthreads();
     tile_gram<MT>(sX, warp * 32, (NG - 1) * S, acc);
@@ -728,8 +732,8 @@ __global__ void __launch_bounds__(TP) k_pair_gram(const double* x, int64_t ldx, 
   constexpr int W = 2 * S;
   constexpr int MP = (W + 7) / 8 * 8;
   constexpr int MT = MP / 8;
-  __shared__ __align__(16) double sX[TP * LDX];
-  for (int e = 0; e < LDX; ++e) sX[threadIdx.x * LDX + e] = 0.0;
+  __shared__ __align__(16) double sX[XCOLS * LDP];
+  for (int e = 0; e < XCOLS; ++e) sX[e * LDP + threadIdx.x] = 0.0;
   double acc[MT][2];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
@@ -738,19 +742,19 @@ __global__ void __launch_bounds__(TP) k_pair_gram(const double* x, int64_t ldx, 
   const int warp = threadIdx.x >> 5;
   for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
     const int64_t i64 = it * TP + threadIdx.x;
-    double* row = sX + threadIdx.x * LDX;
+    double* row = sX + threadIdx.x;   // column c at row[c * LDP]
     if (i64 < n) {
       double v[S], w[S];
       load_vec<S>(x + i64 * ldx, v);
       load_vec<S>(y + i64 * ldy, w);
 #pragma unroll
       for (int a = 0; a < S; ++a) {
-        row[a] = v[a];
-        row[S + a] = w[a];
+        row[(a) * LDP] = v[a];
+        row[(S + a) * LDP] = w[a];
       }
     } else {
 #pragma unroll
-      for (int a = 0; a < W; ++a) row[a] = 0.0;
+      for (int a = 0; a < W; ++a) row[(a) * LDP] = 0.0;
     }
     __syncthreads();
     tile_gram<MT>(sX, warp * 32, S, acc);
@@ -861,10 +865,36 @@ __global__ void k_explicit_finish(DevState* st, TStore T, int mode) {
 // ------------------------------------------------------------------ launchers
 int gram_grid_for(int64_t n) {
   int64_t tiles = (n + TP - 1) / TP;
-  int64_t g = 148 * 6;
+  int64_t g = KRY_MAX_GRID;
   if (tiles < g) g = tiles;
   if (g < 1) g = 1;
   return (int)g;
+}
+
+// persistent grid = resident CTAs (occupancy x SMs), capped by the tile count,
+// so the grid-stride tile loop runs in exactly one wave
+template <class Kern>
+static int resident_grid(Kern kernel, int64_t n) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> cache;
+  int per_sm = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find((const void*)kernel);
+    if (it == cache.end()) {
+      int dev = 0, sms = 148, nb = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, TP, 0);
+      per_sm = std::max(1, nb) * sms;
+      cache[(const void*)kernel] = per_sm;
+    } else {
+      per_sm = it->second;
+    }
+  }
+  int64_t tiles = (n + TP - 1) / TP;
+  int64_t g = std::min<int64_t>(std::min<int64_t>(tiles, per_sm), KRY_MAX_GRID);
+  return (int)std::max<int64_t>(g, 1);
 }
 
 #define KRY_DISPATCH_S(s, F)                                        \
@@ -882,9 +912,11 @@ int gram_grid_for(int64_t n) {
 
 int launch_combine(cudaStream_t st, int s, const OpDev& op, const CombineCall& c, DevState* dst,
                    const TStore& T, GramScratch& g, int grid, float* prof_ms, cudaEvent_t* ev) {
-  if (grid > g.max_grid) grid = g.max_grid;
+  (void)grid;
   if (prof_ms && ev) cudaEventRecord(ev[0], st);
-#define L(S) k_combine<S><<<grid, TP, 0, st>>>(op, c, dst, T, g.partials, g.ticket + 0)
+#define L(S)                                                     \
+  k_combine<S><<<resident_grid(k_combine<S>, c.n), TP, 0, st>>>( \
+      op, c, dst, T, g.partials, g.ticket + 0)
   KRY_DISPATCH_S(s, L);
 #undef L
   if (prof_ms && ev) cudaEventRecord(ev[1], st);
@@ -895,13 +927,17 @@ int launch_combine(cudaStream_t st, int s, const OpDev& op, const CombineCall& c
 
 int launch_apply_gram(cudaStream_t st, int s, const OpDev& op, const ApplyGramCall& c,
                       DevState* dst, const TStore& T, GramScratch& g, int grid) {
-  if (grid > g.max_grid) grid = g.max_grid;
+  (void)grid;
   if (c.use_op) {
-#define L(S) k_apply_gram<S, 1><<<grid, TP, 0, st>>>(op, c, dst, T, g.partials, g.ticket + 1)
+#define L(S)                                                                 \
+  k_apply_gram<S, 1><<<resident_grid(k_apply_gram<S, 1>, c.n), TP, 0, st>>>( \
+      op, c, dst, T, g.partials, g.ticket + 1)
     KRY_DISPATCH_S(s, L);
 #undef L
   } else {
-#define L(S) k_apply_gram<S, 0><<<grid, TP, 0, st>>>(op, c, dst, T, g.partials, g.ticket + 1)
+#define L(S)                                                                 \
+  k_apply_gram<S, 0><<<resident_grid(k_apply_gram<S, 0>, c.n), TP, 0, st>>>( \
+      op, c, dst, T, g.partials, g.ticket + 1)
     KRY_DISPATCH_S(s, L);
 #undef L
   }
@@ -913,9 +949,10 @@ int launch_apply_gram(cudaStream_t st, int s, const OpDev& op, const ApplyGramCa
 int launch_pair_gram(cudaStream_t st, int s, const double* x, int64_t ldx, const double* y,
                      int64_t ldy, int64_t n, int post, DevState* dst, const TStore& T,
                      GramScratch& g, int grid) {
-  if (grid > g.max_grid) grid = g.max_grid;
-#define L(S) \
-  k_pair_gram<S><<<grid, TP, 0, st>>>(x, ldx, y, ldy, n, post, dst, T, g.partials, g.ticket + 2)
+  (void)grid;
+#define L(S)                                                       \
+  k_pair_gram<S><<<resident_grid(k_pair_gram<S>, n), TP, 0, st>>>( \
+      x, ldx, y, ldy, n, post, dst, T, g.partials, g.ticket + 2)
   KRY_DISPATCH_S(s, L);
 #undef L
   count_launch();
