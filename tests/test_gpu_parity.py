@@ -251,3 +251,58 @@ def test_config1_parity_with_reference_run():
 
 def test_config2_parity_with_reference_run():
     _config_parity("c2")
+
+
+def test_config3_sylvester_parity_with_reference_run():
+    g = gold("c3")
+    cfg = P.build_config("c3")
+    sol = kb.solve_sylvester_two_sided(
+        kb.SparseOperator(cfg["a"]), kb.SparseOperator(cfg["b"]), cfg["c1"], cfg["c2"],
+        kb.SolveOptions(tol=cfg["tol"], max_m=cfg["max_m"], storage="windowed"))
+    assert sol.iterations == int(g["iterations"]) == 681
+    assert sol.rank == int(g["rank"])
+    ok, worst = hist_ok([r[2] for r in sol.history], g["history"][:, 2])
+    assert ok, worst
+    om2 = P.sketch_omega(cfg["b"].shape[0], 2)
+    om1 = P.sketch_omega(cfg["a"].shape[0], 2)
+    right = sol.z1 @ (sol.z2.T @ om2)
+    left = sol.z2 @ (sol.z1.T @ om1)
+    assert np.linalg.norm(right - g["sketch_right"]) <= 1e-8 * np.linalg.norm(g["sketch_right"])
+    assert np.linalg.norm(left - g["sketch_left"]) <= 1e-8 * np.linalg.norm(g["sketch_left"])
+
+
+def _c5_operator():
+    import bench
+    cfg, op, _ = bench.build_problem("c5")
+    return cfg, op
+
+
+def test_config5_early_history_matches_oracle():
+    # the reference cannot finish config 5 (~1.4 days on CPU); compare the first
+    # 12 iterations with the oracle on the same input
+    cfg, op = _c5_operator()
+    ref = []
+    bs = ko.Basis(ko.SparseOperator(P.laplacian2d(2000)), cfg["c"])
+    beta2 = float(np.linalg.norm(cfg["c"]) ** 2)
+    for _ in range(12):
+        bs.step()
+        ref.append(ko.ctri_lyapunov(bs.projection(), bs.gamma, bs.coupling(), beta2)[1])
+    with pytest.raises(kb.ConvergenceError) as err:
+        kb.solve_lyapunov(op, cfg["c"], kb.SolveOptions(tol=cfg["tol"], max_m=12))
+    got = [r[2] for r in err.value.history]
+    ok, worst = hist_ok(got, ref)
+    assert ok, worst
+
+
+@pytest.mark.slow
+def test_config5_full_run_raises_with_survey_values():
+    # SURVEY.md §6 (reference lanczos_step + validated surrogate): rel 7.3e-5
+    # at m=175, 4.6e-6 at 700, 2.0e-6 at 975, 1.42e-6 at 1100; no convergence
+    # to 1e-10 within 1500 iterations
+    cfg, op = _c5_operator()
+    with pytest.raises(kb.ConvergenceError) as err:
+        kb.solve_lyapunov(op, cfg["c"], kb.SolveOptions(tol=cfg["tol"], max_m=cfg["max_m"]))
+    h = dict((r[0], r[2]) for r in err.value.history)
+    assert len(err.value.history) == 1500
+    for m, v in ((175, 7.3e-5), (700, 4.6e-6), (975, 2.0e-6), (1100, 1.42e-6)):
+        assert abs(h[m] - v) <= 0.05 * v, (m, h[m], v)
