@@ -80,37 +80,25 @@ __device__ __forceinline__ void apply_point(const OpDev& op, const double* __res
     const int y = r % op.ny;
     const int z = r / op.ny;
     const bool var = op.variable != 0;
-    if (z > 0 || op.halo_lo) {
-      const int j = i - op.nxy;
-      load_vec<S>(V + (int64_t)j * ld, nb);
-      axpy_rn<S>(w, var ? __ldg(op.ez + j) : op.cz, nb);
-    }
-    if (y > 0) {
-      const int j = i - op.nx;
-      load_vec<S>(V + (int64_t)j * ld, nb);
-      axpy_rn<S>(w, var ? __ldg(op.ey + j) : op.cy, nb);
-    }
-    if (x > 0) {
-      const int j = i - 1;
-      load_vec<S>(V + (int64_t)j * ld, nb);
-      axpy_rn<S>(w, var ? __ldg(op.ex + j) : op.cx, nb);
-    }
+    const bool hz0 = z > 0 || op.halo_lo, hy0 = y > 0, hx0 = x > 0;
+    const bool hx1 = x < op.nx - 1, hy1 = y < op.ny - 1, hz1 = z < op.nzl - 1 || op.halo_hi;
+    // all six gathers are issued before any use (one memory round trip);
+    // a missing neighbour loads the point itself and is skipped below, so
+    // the sum keeps the CSR column order exactly
+    double n0[S], n1[S], n2[S], n3[S], n4[S], n5[S];
+    load_vec<S>(V + (int64_t)(hz0 ? i - op.nxy : i) * ld, n0);
+    load_vec<S>(V + (int64_t)(hy0 ? i - op.nx : i) * ld, n1);
+    load_vec<S>(V + (int64_t)(hx0 ? i - 1 : i) * ld, n2);
+    load_vec<S>(V + (int64_t)(hx1 ? i + 1 : i) * ld, n3);
+    load_vec<S>(V + (int64_t)(hy1 ? i + op.nx : i) * ld, n4);
+    load_vec<S>(V + (int64_t)(hz1 ? i + op.nxy : i) * ld, n5);
+    if (hz0) axpy_rn<S>(w, var ? __ldg(op.ez + i - op.nxy) : op.cz, n0);
+    if (hy0) axpy_rn<S>(w, var ? __ldg(op.ey + i - op.nx) : op.cy, n1);
+    if (hx0) axpy_rn<S>(w, var ? __ldg(op.ex + i - 1) : op.cx, n2);
     axpy_rn<S>(w, var ? __ldg(op.d + i) : op.cd, vi);
-    if (x < op.nx - 1) {
-      const int j = i + 1;
-      load_vec<S>(V + (int64_t)j * ld, nb);
-      axpy_rn<S>(w, var ? __ldg(op.ex + i) : op.cx, nb);
-    }
-    if (y < op.ny - 1) {
-      const int j = i + op.nx;
-      load_vec<S>(V + (int64_t)j * ld, nb);
-      axpy_rn<S>(w, var ? __ldg(op.ey + i) : op.cy, nb);
-    }
-    if (z < op.nzl - 1 || op.halo_hi) {
-      const int j = i + op.nxy;
-      load_vec<S>(V + (int64_t)j * ld, nb);
-      axpy_rn<S>(w, var ? __ldg(op.ez + i) : op.cz, nb);
-    }
+    if (hx1) axpy_rn<S>(w, var ? __ldg(op.ex + i) : op.cx, n3);
+    if (hy1) axpy_rn<S>(w, var ? __ldg(op.ey + i) : op.cy, n4);
+    if (hz1) axpy_rn<S>(w, var ? __ldg(op.ez + i) : op.cz, n5);
   } else {
     const int64_t b = __ldg(op.rp + i), e = __ldg(op.rp + i + 1);
     for (int64_t jj = b; jj < e; ++jj) {
@@ -605,121 +593,320 @@ __device__ void finish_reduction(const double (&acc)[MP / 8][2], double* sX, dou
 }
 
 // ------------------------------------------------------------------ kernels
-// Combine: Vn = Vo Mo + Vc Mc + (A Vc) Mw ; Gram [Vc | A Vc | Vn]^T Vn
+// ------------------------------------------------------------------ fused hot kernels
+// Stencil for the recurrence kernels: FMA form, constant coefficients folded
+// per axis (w = cd v + cx (v_{x-1} + v_{x+1}) + cy (...) + cz (...)); the
+// bit-exact CSR-order product is kept for the apply API (apply_point).
 template <int S>
-__global__ void __launch_bounds__(TP, 5) k_combine(OpDev op, CombineCall c, DevState* st,
+__device__ __forceinline__ void stencil_fast(const OpDev& op, const double* __restrict__ V,
+                                             int64_t ld, int i, const double (&vi)[S],
+                                             double (&w)[S]) {
+  if (op.kind != KRY_OP_STENCIL) {
+    apply_point<S>(op, V, ld, i, vi, w);
+    return;
+  }
+  const int x = i % op.nx;
+  const int r = i / op.nx;
+  const int y = r % op.ny;
+  const int z = r / op.ny;
+  const bool hz0 = z > 0 || op.halo_lo, hy0 = y > 0, hx0 = x > 0;
+  const bool hx1 = x < op.nx - 1, hy1 = y < op.ny - 1, hz1 = z < op.nzl - 1 || op.halo_hi;
+  double n0[S], n1[S], n2[S], n3[S], n4[S], n5[S];
+  load_vec<S>(V + (int64_t)(hz0 ? i - op.nxy : i) * ld, n0);
+  load_vec<S>(V + (int64_t)(hy0 ? i - op.nx : i) * ld, n1);
+  load_vec<S>(V + (int64_t)(hx0 ? i - 1 : i) * ld, n2);
+  load_vec<S>(V + (int64_t)(hx1 ? i + 1 : i) * ld, n3);
+  load_vec<S>(V + (int64_t)(hy1 ? i + op.nx : i) * ld, n4);
+  load_vec<S>(V + (int64_t)(hz1 ? i + op.nxy : i) * ld, n5);
+  if (!op.variable) {
+#pragma unroll
+    for (int a = 0; a < S; ++a) {
+      const double sx = (hx0 ? n2[a] : 0.0) + (hx1 ? n3[a] : 0.0);
+      const double sy = (hy0 ? n1[a] : 0.0) + (hy1 ? n4[a] : 0.0);
+      const double sz = (hz0 ? n0[a] : 0.0) + (hz1 ? n5[a] : 0.0);
+      w[a] = fma(op.cd, vi[a], fma(op.cz, sz, fma(op.cy, sy, op.cx * sx)));
+    }
+  } else {
+    const double cz0 = hz0 ? __ldg(op.ez + i - op.nxy) : 0.0, cz1 = hz1 ? __ldg(op.ez + i) : 0.0;
+    const double cy0 = hy0 ? __ldg(op.ey + i - op.nx) : 0.0, cy1 = hy1 ? __ldg(op.ey + i) : 0.0;
+    const double cx0 = hx0 ? __ldg(op.ex + i - 1) : 0.0, cx1 = hx1 ? __ldg(op.ex + i) : 0.0;
+    const double cd = __ldg(op.d + i);
+#pragma unroll
+    for (int a = 0; a < S; ++a) {
+      double t = cd * vi[a];
+      t = fma(cx0, n2[a], t);
+      t = fma(cx1, n3[a], t);
+      t = fma(cy0, n1[a], t);
+      t = fma(cy1, n4[a], t);
+      t = fma(cz0, n0[a], t);
+      w[a] = fma(cz1, n5[a], t);
+    }
+  }
+}
+
+__host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+// tile columns of the combine kernel: [V_{m-1} | V_m | A V_m | V_{m+1}] (+ zero padding
+// read by the DMMA tiles)
+__host__ __device__ constexpr int comb_cols(int S) {
+  return cmax(cmax(4 * S, S + 8 * cdiv(3 * S, 8)), cmax(3 * S + 8, 4 * cdiv(3 * S, 4)));
+}
+__host__ __device__ constexpr int apply_cols(int S) { return cmax(cmax(2 * S, 8 * cdiv(2 * S, 8)), S + 8); }
+
+// warp-level Gram over the warp's 32 tile rows:
+// acc[mt] += X[:, x0 + 8mt .. +8]^T X[:, y0 .. y0+8]
+template <int MT>
+__device__ __forceinline__ void warp_gram(const double* sX, int r0, int x0, int y0,
+                                          double (&acc)[MT][2]) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    const int k = r0 + ks * 4 + t;
+    const double b = sX[(y0 + g) * LDP + k];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][0], acc[mt][1], sX[(x0 + mt * 8 + g) * LDP + k], b);
+  }
+}
+
+// Cooperative, fully coalesced staging of one warp's 32 tile rows (S even,
+// stencil operator): lane -> (point pp, 16-byte column pair cp); every warp
+// load instruction covers 32 consecutive pieces (512 contiguous bytes when
+// ld == S).  The stencil is evaluated per column pair and the results are
+// written straight into the transposed smem tile:
+//   column groups: [col_o: V_{m-1}] (if col_o >= 0), [col_c: V_m], [col_w: A V_m]
+template <int S>
+__device__ __forceinline__ void stage_warp_coop(const OpDev& op, const double* __restrict__ vc,
+                                                int64_t ldc, const double* __restrict__ vo,
+                                                int64_t ldo, bool load_old, bool use_op,
+                                                int64_t n, int64_t tile_base, int r0,
+                                                double* sX, int col_o, int col_c, int col_w) {
+  constexpr int CP = S / 2;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int e = 0; e < CP; ++e) {
+    const int q = lane + 32 * e;
+    const int pp = q / CP, cp = q % CP;
+    const int row = r0 + pp;
+    const int64_t i64 = tile_base + row;
+    double2 o = make_double2(0.0, 0.0), v = make_double2(0.0, 0.0), w = make_double2(0.0, 0.0);
+    if (i64 < n) {
+      const int i = (int)i64;
+      const int off = 2 * cp;
+      v = __ldg(reinterpret_cast<const double2*>(vc + i64 * ldc + off));
+      if (load_old) o = __ldg(reinterpret_cast<const double2*>(vo + i64 * ldo + off));
+      if (use_op) {
+        const int x = i % op.nx;
+        const int r = i / op.nx;
+        const int y = r % op.ny;
+        const int z = r / op.ny;
+        const bool hz0 = z > 0 || op.halo_lo, hy0 = y > 0, hx0 = x > 0;
+        const bool hx1 = x < op.nx - 1, hy1 = y < op.ny - 1, hz1 = z < op.nzl - 1 || op.halo_hi;
+        auto ld2 = [&](int j) {
+          return __ldg(reinterpret_cast<const double2*>(vc + (int64_t)j * ldc + off));
+        };
+        const double2 n0 = ld2(hz0 ? i - op.nxy : i), n1 = ld2(hy0 ? i - op.nx : i);
+        const double2 n2 = ld2(hx0 ? i - 1 : i), n3 = ld2(hx1 ? i + 1 : i);
+        const double2 n4 = ld2(hy1 ? i + op.nx : i), n5 = ld2(hz1 ? i + op.nxy : i);
+        if (!op.variable) {
+          const double sx0 = (hx0 ? n2.x : 0.0) + (hx1 ? n3.x : 0.0);
+          const double sx1 = (hx0 ? n2.y : 0.0) + (hx1 ? n3.y : 0.0);
+          const double sy0 = (hy0 ? n1.x : 0.0) + (hy1 ? n4.x : 0.0);
+          const double sy1 = (hy0 ? n1.y : 0.0) + (hy1 ? n4.y : 0.0);
+          const double sz0 = (hz0 ? n0.x : 0.0) + (hz1 ? n5.x : 0.0);
+          const double sz1 = (hz0 ? n0.y : 0.0) + (hz1 ? n5.y : 0.0);
+          w.x = fma(op.cd, v.x, fma(op.cz, sz0, fma(op.cy, sy0, op.cx * sx0)));
+          w.y = fma(op.cd, v.y, fma(op.cz, sz1, fma(op.cy, sy1, op.cx * sx1)));
+        } else {
+          const double cz0 = hz0 ? __ldg(op.ez + i - op.nxy) : 0.0, cz1 = hz1 ? __ldg(op.ez + i) : 0.0;
+          const double cy0 = hy0 ? __ldg(op.ey + i - op.nx) : 0.0, cy1 = hy1 ? __ldg(op.ey + i) : 0.0;
+          const double cx0 = hx0 ? __ldg(op.ex + i - 1) : 0.0, cx1 = hx1 ? __ldg(op.ex + i) : 0.0;
+          const double cd = __ldg(op.d + i);
+          double t0 = cd * v.x, t1 = cd * v.y;
+          t0 = fma(cx0, n2.x, t0); t1 = fma(cx0, n2.y, t1);
+          t0 = fma(cx1, n3.x, t0); t1 = fma(cx1, n3.y, t1);
+          t0 = fma(cy0, n1.x, t0); t1 = fma(cy0, n1.y, t1);
+          t0 = fma(cy1, n4.x, t0); t1 = fma(cy1, n4.y, t1);
+          t0 = fma(cz0, n0.x, t0); t1 = fma(cz0, n0.y, t1);
+          w.x = fma(cz1, n5.x, t0); w.y = fma(cz1, n5.y, t1);
+        }
+      }
+    }
+    const int c0 = 2 * cp;
+    if (col_o >= 0) {
+      sX[(col_o + c0) * LDP + row] = o.x;
+      sX[(col_o + c0 + 1) * LDP + row] = o.y;
+    }
+    sX[(col_c + c0) * LDP + row] = v.x;
+    sX[(col_c + c0 + 1) * LDP + row] = v.y;
+    if (col_w >= 0) {
+      sX[(col_w + c0) * LDP + row] = w.x;
+      sX[(col_w + c0 + 1) * LDP + row] = w.y;
+    }
+  }
+}
+
+// Combine: V_{m+1} = [V_{m-1} | V_m | A V_m] * [Mo; Mc; Mw]  on DMMA tensor
+// cores, then the Gram [V_m | A V_m | V_{m+1}]^T V_{m+1}.  Each warp owns 32
+// rows of the tile, so a tile needs only warp-level synchronisation.
+template <int S, bool COOP>
+__global__ void __launch_bounds__(TP, COOP ? 5 : 2) k_combine(OpDev op, CombineCall c, DevState* st,
                                                 TStore T, double* partials, unsigned* ticket) {
-  constexpr int NG = 3;
-  constexpr int W = NG * S;
-  constexpr int MP = (W + 7) / 8 * 8;
-  constexpr int MT = MP / 8;
-  __shared__ __align__(16) double sX[XCOLS * LDP];
-  __shared__ __align__(16) double sM[3 * 64];
+  constexpr int XC = comb_cols(S);
+  constexpr int MTG = cdiv(3 * S, 8);   // Gram m-tiles (rows of [V_m | AV | V_{m+1}])
+  constexpr int MP = 8 * MTG;
+  constexpr int KS = cdiv(3 * S, 4);    // combination k-steps
+  __shared__ __align__(16) double sX[XC * LDP];
   if (st->status != KRY_OK || (st->flags & (KRY_FLAG_FALLBACK | KRY_FLAG_EXHAUSTED))) {
     if (c.write_new) return;  // never combine with invalid coefficients
   }
-  for (int e = threadIdx.x; e < 3 * 64; e += TP) sM[e] = st->M[e];
-  for (int e = 0; e < XCOLS; ++e) sX[e * LDP + threadIdx.x] = 0.0;
-  double acc[MT][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  // B fragments of the stacked coefficient matrix [Mo; Mc; Mw] (3S x S)
+  double bM[KS];
 #pragma unroll
-  for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
+  for (int ks = 0; ks < KS; ++ks) {
+    const int kk = 4 * ks + t;
+    double v = 0.0;
+    if (kk < 3 * S && g < S) v = st->M[(kk / S) * 64 + (kk % S) * 8 + g];
+    bM[ks] = v;
+  }
+  for (int e = 0; e < XC; ++e) sX[e * LDP + threadIdx.x] = 0.0;
+  double acc[MTG][2];
+#pragma unroll
+  for (int mt = 0; mt < MTG; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
   __syncthreads();
   const int64_t ntiles = (c.n + TP - 1) / TP;
-  const int warp = threadIdx.x >> 5;
+  const int r0 = warp * 32;
+  double* row = sX + threadIdx.x;   // column q at row[q * LDP]
+  constexpr bool coop = COOP && (S % 2 == 0);
+  // interleaved tile order: the active tiles form a compact wavefront, so the
+  // +-nx*ny neighbour planes of a tile are in L2 (streamed as centre rows by
+  // the CTAs ~nx*ny/TP tiles ahead / behind)
   for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
     const int64_t tile = c.reverse ? (ntiles - 1 - it) : it;
     const int64_t i64 = tile * TP + threadIdx.x;
-    double* row = sX + threadIdx.x;   // column c at row[c * LDP]
-    if (i64 < c.n) {
+    if constexpr (coop) {
+      stage_warp_coop<(S % 2 == 0) ? S : 2>(op, c.vc, c.ldc, c.vo, c.ldo, c.write_new && c.has_old,
+                                            c.use_op, c.n, tile * TP, r0, sX, 0, S, 2 * S);
+      if (!c.write_new && i64 < c.n) {
+        double vn[S];
+        load_vec<S>(c.vn + i64 * c.ldn, vn);
+#pragma unroll
+        for (int a = 0; a < S; ++a) row[(3 * S + a) * LDP] = vn[a];
+      }
+    } else if (i64 < c.n) {
       const int i = (int)i64;
-      double vc[S], w[S], vn[S];
+      if (c.write_new && c.has_old) {
+        double vo[S];
+        load_vec<S>(c.vo + i64 * c.ldo, vo);
+#pragma unroll
+        for (int a = 0; a < S; ++a) row[a * LDP] = vo[a];
+      } else {
+#pragma unroll
+        for (int a = 0; a < S; ++a) row[a * LDP] = 0.0;
+      }
+      double vc[S], w[S];
       load_vec<S>(c.vc + i64 * c.ldc, vc);
       if (c.use_op) {
-        apply_point<S>(op, c.vc, c.ldc, i, vc, w);
+        stencil_fast<S>(op, c.vc, c.ldc, i, vc, w);
       } else {
 #pragma unroll
         for (int a = 0; a < S; ++a) w[a] = 0.0;
       }
-      if (c.write_new) {
-#pragma unroll
-        for (int a = 0; a < S; ++a) vn[a] = 0.0;
-        if (c.has_old) {
-          double vo[S];
-          load_vec<S>(c.vo + i64 * c.ldo, vo);
-#pragma unroll
-          for (int b = 0; b < S; ++b)
-#pragma unroll
-            for (int a = 0; a < S; ++a) vn[a] = fma(vo[b], sM[b * 8 + a], vn[a]);
-        }
-#pragma unroll
-        for (int b = 0; b < S; ++b)
-#pragma unroll
-          for (int a = 0; a < S; ++a) vn[a] = fma(vc[b], sM[64 + b * 8 + a], vn[a]);
-        if (c.use_op) {
-#pragma unroll
-          for (int b = 0; b < S; ++b)
-#pragma unroll
-            for (int a = 0; a < S; ++a) vn[a] = fma(w[b], sM[128 + b * 8 + a], vn[a]);
-        }
-        store_vec<S>(c.vn + i64 * c.ldn, vn);
-      } else {
-        load_vec<S>(c.vn + i64 * c.ldn, vn);
-      }
 #pragma unroll
       for (int a = 0; a < S; ++a) {
-        row[(a) * LDP] = vc[a];
-        row[(S + a) * LDP] = w[a];
-        row[(2 * S + a) * LDP] = vn[a];
+        row[(S + a) * LDP] = vc[a];
+        row[(2 * S + a) * LDP] = w[a];
+      }
+      if (!c.write_new) {
+        double vn[S];
+        load_vec<S>(c.vn + i64 * c.ldn, vn);
+#pragma unroll
+        for (int a = 0; a < S; ++a) row[(3 * S + a) * LDP] = vn[a];
       }
     } else {
 #pragma unroll
-      for (int a = 0; a < W; ++a) row[(a) * LDP] = 0.0;
+      for (int a = 0; a < 4 * S; ++a) row[a * LDP] = 0.0;
     }
-    __syncthreads();
-    tile_gram<MT>(sX, warp * 32, 2 * S, acc);
-    __syncthreads();
+    __syncwarp();
+    if (c.write_new) {
+      // V_{m+1} for the warp's 32 rows: 4 m-tiles of 8 points x KS k-steps
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        double d0 = 0.0, d1 = 0.0;
+        const int pr = r0 + mt * 8 + g;   // A row = point
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) dmma(d0, d1, sX[(4 * ks + t) * LDP + pr], bM[ks]);
+        const int64_t pi = tile * TP + pr;
+        const int c0 = 2 * t;
+        if (c0 < S) {
+          sX[(3 * S + c0) * LDP + pr] = d0;
+          if (c0 + 1 < S) sX[(3 * S + c0 + 1) * LDP + pr] = d1;
+          if (pi < c.n) {
+            double* dst = c.vn + pi * c.ldn + c0;
+            if constexpr (S % 2 == 0) {
+              *reinterpret_cast<double2*>(dst) = make_double2(d0, d1);
+            } else {
+              dst[0] = d0;
+              if (c0 + 1 < S) dst[1] = d1;
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+    warp_gram<MTG>(sX, r0, S, 3 * S, acc);
+    __syncwarp();
   }
   finish_reduction<MP>(acc, sX, partials, ticket, POST_P, st, T);
 }
 
 // Apply + Gram: X = [V | A V], Y = A V  (use_op) or X = [V], Y = V
-template <int S, int USE_OP>
-__global__ void __launch_bounds__(TP, 5) k_apply_gram(OpDev op, ApplyGramCall c, DevState* st,
+template <int S, int USE_OP, bool COOP>
+__global__ void __launch_bounds__(TP, COOP ? 5 : 2) k_apply_gram(OpDev op, ApplyGramCall c, DevState* st,
                                                    TStore T, double* partials, unsigned* ticket) {
   constexpr int NG = USE_OP ? 2 : 1;
-  constexpr int W = NG * S;
-  constexpr int MP = (W + 7) / 8 * 8;
-  constexpr int MT = MP / 8;
-  __shared__ __align__(16) double sX[XCOLS * LDP];
-  for (int e = 0; e < XCOLS; ++e) sX[e * LDP + threadIdx.x] = 0.0;
+  constexpr int XC = apply_cols(S);
+  constexpr int MT = cdiv(NG * S, 8);
+  constexpr int MP = 8 * MT;
+  __shared__ __align__(16) double sX[cmax(XC, 9) * LDP];
+  for (int e = 0; e < XC; ++e) sX[e * LDP + threadIdx.x] = 0.0;
   double acc[MT][2];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
   __syncthreads();
   const int64_t ntiles = (c.n + TP - 1) / TP;
-  const int warp = threadIdx.x >> 5;
+  const int r0 = (threadIdx.x >> 5) * 32;
+  double* row = sX + threadIdx.x;
+  constexpr bool coop = COOP && (S % 2 == 0);
+  // interleaved tile order: the active tiles form a compact wavefront, so the
+  // +-nx*ny neighbour planes of a tile are in L2 (streamed as centre rows by
+  // the CTAs ~nx*ny/TP tiles ahead / behind)
   for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
     const int64_t tile = c.reverse ? (ntiles - 1 - it) : it;
     const int64_t i64 = tile * TP + threadIdx.x;
-    double* row = sX + threadIdx.x;   // column c at row[c * LDP]
-    if (i64 < c.n) {
+    if constexpr (coop) {
+      stage_warp_coop<(S % 2 == 0) ? S : 2>(op, c.v, c.ldv, nullptr, 0, false, USE_OP != 0, c.n,
+                                            tile * TP, r0, sX, -1, 0, USE_OP ? S : -1);
+    } else if (i64 < c.n) {
       double v[S];
       load_vec<S>(c.v + i64 * c.ldv, v);
 #pragma unroll
-      for (int a = 0; a < S; ++a) row[(a) * LDP] = v[a];
+      for (int a = 0; a < S; ++a) row[a * LDP] = v[a];
       if constexpr (USE_OP) {
         double w[S];
-        apply_point<S>(op, c.v, c.ldv, (int)i64, v, w);
+        stencil_fast<S>(op, c.v, c.ldv, (int)i64, v, w);
 #pragma unroll
         for (int a = 0; a < S; ++a) row[(S + a) * LDP] = w[a];
       }
     } else {
 #pragma unroll
-      for (int a = 0; a < W; ++a) row[(a) * LDP] = 0.0;
+      for (int a = 0; a < NG * S; ++a) row[a * LDP] = 0.0;
     }
-    __syncthreads();
-    tile_gram<MT>(sX, warp * 32, (NG - 1) * S, acc);
-    __syncthreads();
+    __syncwarp();
+    warp_gram<MT>(sX, r0, 0, (NG - 1) * S, acc);
+    __syncwarp();
   }
   finish_reduction<MP>(acc, sX, partials, ticket, c.post, st, T);
 }
@@ -914,11 +1101,21 @@ int launch_combine(cudaStream_t st, int s, const OpDev& op, const CombineCall& c
                    const TStore& T, GramScratch& g, int grid, float* prof_ms, cudaEvent_t* ev) {
   (void)grid;
   if (prof_ms && ev) cudaEventRecord(ev[0], st);
-#define L(S)                                                     \
-  k_combine<S><<<resident_grid(k_combine<S>, c.n), TP, 0, st>>>( \
+  const bool coop = (s % 2 == 0) && op.kind == KRY_OP_STENCIL && (c.ldc % 2 == 0) &&
+                    (!c.has_old || c.ldo % 2 == 0);
+  if (coop) {
+#define L(S)                                                                 \
+  k_combine<S, true><<<resident_grid(k_combine<S, true>, c.n), TP, 0, st>>>( \
       op, c, dst, T, g.partials, g.ticket + 0)
-  KRY_DISPATCH_S(s, L);
+    KRY_DISPATCH_S(s, L);
 #undef L
+  } else {
+#define L(S)                                                                   \
+  k_combine<S, false><<<resident_grid(k_combine<S, false>, c.n), TP, 0, st>>>( \
+      op, c, dst, T, g.partials, g.ticket + 0)
+    KRY_DISPATCH_S(s, L);
+#undef L
+  }
   if (prof_ms && ev) cudaEventRecord(ev[1], st);
   count_launch();
   KRY_CUDA(cudaGetLastError());
@@ -928,19 +1125,28 @@ int launch_combine(cudaStream_t st, int s, const OpDev& op, const CombineCall& c
 int launch_apply_gram(cudaStream_t st, int s, const OpDev& op, const ApplyGramCall& c,
                       DevState* dst, const TStore& T, GramScratch& g, int grid) {
   (void)grid;
-  if (c.use_op) {
-#define L(S)                                                                 \
-  k_apply_gram<S, 1><<<resident_grid(k_apply_gram<S, 1>, c.n), TP, 0, st>>>( \
+  const bool coop = (s % 2 == 0) && (op.kind == KRY_OP_STENCIL || !c.use_op) && (c.ldv % 2 == 0);
+#define LA(S, U, C)                                                                    \
+  k_apply_gram<S, U, C><<<resident_grid(k_apply_gram<S, U, C>, c.n), TP, 0, st>>>( \
       op, c, dst, T, g.partials, g.ticket + 1)
+  if (c.use_op && coop) {
+#define L(S) LA(S, 1, true)
+    KRY_DISPATCH_S(s, L);
+#undef L
+  } else if (c.use_op) {
+#define L(S) LA(S, 1, false)
+    KRY_DISPATCH_S(s, L);
+#undef L
+  } else if (coop) {
+#define L(S) LA(S, 0, true)
     KRY_DISPATCH_S(s, L);
 #undef L
   } else {
-#define L(S)                                                                 \
-  k_apply_gram<S, 0><<<resident_grid(k_apply_gram<S, 0>, c.n), TP, 0, st>>>( \
-      op, c, dst, T, g.partials, g.ticket + 1)
+#define L(S) LA(S, 0, false)
     KRY_DISPATCH_S(s, L);
 #undef L
   }
+#undef LA
   count_launch();
   KRY_CUDA(cudaGetLastError());
   return KRY_OK;
