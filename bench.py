@@ -44,6 +44,21 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def captured_traffic(config):
+    """DRAM bytes per k_combine launch from the committed ncu --set full
+    capture of this config (profiles/r1_k_combine_<config>_ncu.json), or None."""
+    path = os.path.join(ROOT, "profiles", "r1_k_combine_%s_ncu.json" % config)
+    try:
+        d = json.load(open(path))
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+        tot = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot += float(d[k]["value"].replace(",", "")) * scale[d[k]["unit"]]
+        return tot
+    except Exception:
+        return None
+
+
 def laplacian_stencil_constants(dims, n):
     """Exactly the doubles of oracle.problems' CSR for the Laplacians:
     1-D: main -2/h^2, off 1/h^2; 3-D diag = ((d + d) + d) (kron sum order);
@@ -56,20 +71,26 @@ def laplacian_stencil_constants(dims, n):
     return -(((c + c) + c) + c), c
 
 
-def build_problem(name):
-    """Operators (device stencil descriptions) + right-hand sides, seeded."""
+def build_problem(name, slab=None, comm=None):
+    """Operators (device stencil descriptions) + right-hand sides, seeded.
+    With ``slab`` (planes [z0, z1) of the slowest axis) the operator and C are
+    this rank's row slab (parallel.py)."""
     import paper_1602_05033_b200 as kb
     from oracle import problems as P
+    from paper_1602_05033_b200.parallel import local_rows
 
     if name in ("c4", "c5"):
         cfg = P.build_config(name, with_matrix=False)
-        g = cfg["grid_a"]
-        if len(g) == 3:
+        g = tuple(cfg["grid_a"]) + (1,) * (3 - len(cfg["grid_a"]))
+        if len(cfg["grid_a"]) == 3:
             cd, co = laplacian_stencil_constants(3, g[0])
-            op = kb.StencilOperator(g, cd, co, co, co)
+            op = kb.StencilOperator(g, cd, co, co, co, slab=slab, comm=comm)
         else:
             cd, co = laplacian_stencil_constants(2, g[0])
-            op = kb.StencilOperator(g, cd, co, co, 0.0)
+            # 2-D grid: the slab axis is y -> present it as (nx, 1, ny)
+            op = kb.StencilOperator((g[0], 1, g[1]), cd, co, 0.0, co, slab=slab, comm=comm)
+        if slab is not None:
+            cfg["c"] = local_rows(cfg["c"], op.grid, slab)
         return cfg, op, None
     cfg = P.build_config(name)
     op = kb.SparseOperator(cfg["a"])
@@ -208,8 +229,6 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     vals = []
     desc = ""
-    for _ in range(args.warmup if args.warmup < 1 else 0):
-        pass
     t_all = 0.0
     for _ in range(max(1, args.steps)):
         v, desc, t = cpu_sample(args.config, threads)
@@ -226,7 +245,7 @@ def run_reference(args):
         "warmup": args.warmup,
         "ms_per_step": 1000.0 / value if value else None,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded, SURVEY.md §8(d))",
@@ -266,7 +285,14 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = _lib.load()
-    cfg, op, opb = build_problem(args.config)
+    slab = comm = None
+    if world > 1:
+        from oracle import problems as P
+        from paper_1602_05033_b200.parallel import Communicator, slab_partition
+        g = P.build_config(args.config, with_matrix=False)["grid_a"]
+        slab = slab_partition(g[-1], world, rank)
+        comm = Communicator()
+    cfg, op, opb = build_problem(args.config, slab=slab, comm=comm)
     if cfg["kind"] != "lyapunov":
         raise SystemExit("bench.py measures the Lyapunov configs (c1, c2, c4, c5)")
     op.device = local
@@ -301,11 +327,7 @@ def main():
         t = torch.tensor([ms_total], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
-        it = torch.tensor([its_total], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(it)
-        its_total_all = float(it.item())
-    else:
-        its_total_all = its_total
+    its_total_all = its_total   # sharded: all ranks advance the same solve
     value = its_total_all / (ms_total / 1000.0)
     ctx.close()
     # roofline of the fused recurrence kernel (k_combine): reads V_{m-1}, V_m,
@@ -329,7 +351,11 @@ def main():
         e2e_s = sum(r[0] for r in e2e_runs)
         e2e_its = sum(r[1] for r in e2e_runs)
         rank_z = e2e_runs[-1][2]
-        e2e = {"value": e2e_its / e2e_s * (world if world > 1 else 1), "unit": "iters/s",
+        if dist:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": e2e_its / e2e_s, "unit": "iters/s",
                "h2d_bytes_per_step": int(n * s * 8),
                "d2h_bytes_per_step": int(n * rank_z * 8),
                "ms_per_solve": 1000.0 * e2e_s / len(e2e_runs)}
@@ -353,14 +379,14 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": ms_total / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded, SURVEY.md §8(d)); inputs larger than L2",
         "config": {"workload": args.config, "desc": CONFIG_DOC[args.config], "n": n, "s": s,
                    "tol": cfg["tol"], "iterations": r0["iterations"], "rank": r0["rank"],
                    "final_rel_residual": r0["rel"],
-                   "parallelism": "replicas" if world > 1 else "single",
+                   "parallelism": "slab-z%d" % world if world > 1 else "single",
                    "l2": "inputs (4 x %d MB blocks) exceed the 126 MB L2" % (n * s * 8 >> 20)},
         "time_to_tol_ms": ms_total / args.steps,
         "phases_s": {"pass1": r0["pass1_s"], "checks_in_pass1": r0["check_s"],
@@ -368,7 +394,8 @@ def main():
         "roofline": {"bound": "hbm", "kernel": "k_combine (fused stencil SpMM + 3-term "
                      "recurrence + Gram)", "achieved": achieved, "peak": hbm,
                      "peak_kind": hbm_kind, "unit": "GB/s",
-                     "frac": achieved / hbm if hbm else None, "traffic": None,
+                     "frac": achieved / hbm if hbm else None,
+                     "traffic": captured_traffic(args.config),
                      "bytes_per_launch": bytes_launch, "avg_launch_ms": comb_avg_ms,
                      "launches": comb_n.value},
         "cpu_baseline": cpu,

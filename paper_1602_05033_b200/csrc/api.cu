@@ -251,6 +251,7 @@ struct kry_ctx {
   // multi-GPU
   int nranks = 1, rank_id = 0;
   ncclComm_t comm = nullptr;
+  double* halo_buf = nullptr;
 };
 
 namespace {
@@ -280,6 +281,105 @@ int map_status(kry_ctx* c, const char* context) {
 
 double* slotp(kry_ctx* c, int i) { return i < 0 ? nullptr : c->slot[i]; }
 
+template <class T>
+int dalloc(T** p, size_t count) {
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    return fail(KRY_ERR_CUDA, std::string("cudaMalloc failed: ") + cudaGetErrorString(e) +
+                                  " (" + std::to_string(count * sizeof(T)) + " bytes)");
+  }
+  return KRY_OK;
+}
+
+// ---------------------------------------------------------------- multi-GPU plumbing
+// Row-slab sharding along the slowest grid axis: every rank owns planes
+// [z_begin, z_end) and one halo plane on each side of every block.  After a
+// block is written its boundary planes are exchanged with the neighbours
+// (NCCL send/recv, packed when the block is strided), and every Gram
+// reduction is summed across ranks (one ncclAllReduce of <= 192 doubles)
+// before the replicated coefficient solve / post routine runs.
+bool dist(kry_ctx* c) { return c->nranks > 1; }
+
+int allreduce_gram(kry_ctx* c) {
+  if (ncclAllReduce(c->st->gram, c->st->gram, 3 * 64, ncclDouble, ncclSum, c->comm, c->stream) !=
+      ncclSuccess)
+    return fail(KRY_ERR_NCCL, "ncclAllReduce (Gram) failed");
+  return KRY_OK;
+}
+
+int run_apply_gram(kry_ctx* c, ApplyGramCall ag) {
+  const int post = ag.post;
+  if (dist(c)) ag.post = POST_NONE;
+  KRY_CHECK(run_apply_gram(c, ag));
+  if (dist(c)) {
+    KRY_CHECK(allreduce_gram(c));
+    KRY_CHECK(launch_post(c->stream, post, c->st, c->T));
+  }
+  return KRY_OK;
+}
+
+int run_combine(kry_ctx* c, CombineCall cc, float* prof, cudaEvent_t* ev) {
+  const int post = cc.post;
+  if (dist(c)) cc.post = POST_NONE;
+  KRY_CHECK(launch_combine(c->stream, c->s, c->op, cc, c->st, c->T, c->g, c->grid, prof, ev));
+  if (dist(c)) {
+    KRY_CHECK(allreduce_gram(c));
+    KRY_CHECK(launch_post(c->stream, post, c->st, c->T));
+  }
+  return KRY_OK;
+}
+
+int run_pair_gram(kry_ctx* c, const double* x, int64_t ldx, const double* y, int64_t ldy,
+                  int post) {
+  KRY_CHECK(launch_pair_gram(c->stream, c->s, x, ldx, y, ldy, c->n, dist(c) ? POST_NONE : post,
+                             c->st, c->T, c->g, c->grid));
+  if (dist(c)) {
+    KRY_CHECK(allreduce_gram(c));
+    KRY_CHECK(launch_post(c->stream, post, c->st, c->T));
+  }
+  return KRY_OK;
+}
+
+// exchange the boundary planes of block `blk` (first owned point, stride ld)
+int halo_exchange(kry_ctx* c, double* blk, int64_t ld, int s) {
+  if (!dist(c) || c->op.kind != KRY_OP_STENCIL) return KRY_OK;
+  const int64_t P = c->op.nxy;
+  const int64_t cnt = P * s;
+  const int lo = c->rank_id - 1, hi = c->rank_id + 1;
+  const bool has_lo = c->op.halo_lo, has_hi = c->op.halo_hi;
+  double* first = blk;
+  double* last = blk + (int64_t)(c->op.nzl - 1) * P * ld;
+  double* hlo = blk - P * ld;
+  double* hhi = blk + (int64_t)c->op.nzl * P * ld;
+  const bool packed = ld != s;
+  if (packed && !c->halo_buf) KRY_CHECK(dalloc(&c->halo_buf, (size_t)4 * P * KRY_SMAX));
+  double *s_lo = first, *s_hi = last, *r_lo = hlo, *r_hi = hhi;
+  if (packed) {
+    s_lo = c->halo_buf;
+    s_hi = c->halo_buf + P * KRY_SMAX;
+    r_lo = c->halo_buf + 2 * P * KRY_SMAX;
+    r_hi = c->halo_buf + 3 * P * KRY_SMAX;
+    if (has_lo) KRY_CHECK(launch_copy_block(c->stream, s, first, ld, s_lo, s, P));
+    if (has_hi) KRY_CHECK(launch_copy_block(c->stream, s, last, ld, s_hi, s, P));
+  }
+  ncclGroupStart();
+  if (has_lo) {
+    ncclSend(s_lo, cnt, ncclDouble, lo, c->comm, c->stream);
+    ncclRecv(r_lo, cnt, ncclDouble, lo, c->comm, c->stream);
+  }
+  if (has_hi) {
+    ncclSend(s_hi, cnt, ncclDouble, hi, c->comm, c->stream);
+    ncclRecv(r_hi, cnt, ncclDouble, hi, c->comm, c->stream);
+  }
+  if (ncclGroupEnd() != ncclSuccess) return fail(KRY_ERR_NCCL, "halo exchange failed");
+  if (packed) {
+    if (has_lo) KRY_CHECK(launch_copy_block(c->stream, s, r_lo, s, hlo, ld, P));
+    if (has_hi) KRY_CHECK(launch_copy_block(c->stream, s, r_hi, s, hhi, ld, P));
+  }
+  return KRY_OK;
+}
+
 int reset_state(kry_ctx* c, int replay) {
   KRY_CUDA(cudaMemsetAsync(c->st, 0, sizeof(DevState), c->stream));
   DevState tmp;
@@ -299,12 +399,12 @@ int reset_state(kry_ctx* c, int replay) {
 int do_init(kry_ctx* c, double* dst, int64_t ldd, int replay) {
   KRY_CHECK(reset_state(c, replay));
   ApplyGramCall ag{c->C, (int64_t)c->s, c->n, 0, POST_INIT, 0};
-  KRY_CHECK(launch_apply_gram(c->stream, c->s, c->op, ag, c->st, c->T, c->g, c->grid));
+  KRY_CHECK(run_apply_gram(c, ag));
   KRY_CHECK(sync_status(c));
   KRY_CHECK(map_status(c, "initial QR of C"));
   CombineCall cc{nullptr, 0, c->C, (int64_t)c->s, dst, ldd, c->n, 0, 0, 1, 1};
-  KRY_CHECK(launch_combine(c->stream, c->s, c->op, cc, c->st, c->T, c->g, c->grid, nullptr,
-                           nullptr));
+  KRY_CHECK(run_combine(c, cc, nullptr, nullptr));
+  KRY_CHECK(halo_exchange(c, dst, ldd, c->s));
   k_init_gamma<<<1, 32, 0, c->stream>>>(c->st);
   count_launch();
   KRY_CHECK(sync_status(c));
@@ -322,18 +422,16 @@ int explicit_step(kry_ctx* c, int j, const double* vold, const double* vcur, dou
   const int has_old = j > 1;
   KRY_CHECK(launch_apply_store(st, s, c->op, vcur, ld, vnew, ld, c->n));
   KRY_CHECK(launch_update(st, s, vnew, ld, nullptr, 0, c->st->Sc, c->n, 0));
-  KRY_CHECK(launch_pair_gram(st, s, vnew, ld, vnew, ld, c->n, POST_SCALE, c->st, c->T, c->g, c->grid));
+  KRY_CHECK(run_pair_gram(c, vnew, ld, vnew, ld, POST_SCALE));
   for (int sweep = 0; sweep < 2; ++sweep) {
     if (has_old) {
-      KRY_CHECK(launch_pair_gram(st, s, vold, ld, vnew, ld, c->n, POST_MGS_OLD, c->st, c->T, c->g,
-                                 c->grid));
+      KRY_CHECK(run_pair_gram(c, vold, ld, vnew, ld, POST_MGS_OLD));
       KRY_CHECK(launch_update(st, s, vnew, ld, vold, ld, c->st->M, c->n, 1));
     }
-    KRY_CHECK(launch_pair_gram(st, s, vcur, ld, vnew, ld, c->n, POST_MGS_CUR, c->st, c->T, c->g,
-                               c->grid));
+    KRY_CHECK(run_pair_gram(c, vcur, ld, vnew, ld, POST_MGS_CUR));
     KRY_CHECK(launch_update(st, s, vnew, ld, vcur, ld, c->st->M, c->n, 1));
   }
-  KRY_CHECK(launch_pair_gram(st, s, vnew, ld, vnew, ld, c->n, POST_W2, c->st, c->T, c->g, c->grid));
+  KRY_CHECK(run_pair_gram(c, vnew, ld, vnew, ld, POST_W2));
   KRY_CHECK(sync_status(c));
   const double scale2 = c->st_h->scale2, w2 = c->st_h->w2;
   // basis.py:239: ||W||_F <= 1e-13 ||A V||_F
@@ -346,16 +444,17 @@ int explicit_step(kry_ctx* c, int j, const double* vold, const double* vcur, dou
     *exhausted = 1;
     return KRY_OK;
   }
-  KRY_CHECK(launch_pair_gram(st, s, vnew, ld, vnew, ld, c->n, POST_CHOL1, c->st, c->T, c->g, c->grid));
+  KRY_CHECK(run_pair_gram(c, vnew, ld, vnew, ld, POST_CHOL1));
   KRY_CHECK(launch_update(st, s, vnew, ld, nullptr, 0, c->st->M, c->n, 0));
-  KRY_CHECK(launch_pair_gram(st, s, vnew, ld, vnew, ld, c->n, POST_CHOL2, c->st, c->T, c->g, c->grid));
+  KRY_CHECK(run_pair_gram(c, vnew, ld, vnew, ld, POST_CHOL2));
   KRY_CHECK(launch_update(st, s, vnew, ld, nullptr, 0, c->st->M, c->n, 0));
   KRY_CHECK(sync_status(c));
   KRY_CHECK(map_status(c, ("Lanczos step " + std::to_string(j)).c_str()));
   KRY_CHECK(launch_explicit_finish(st, c->st, c->T, 1));
+  KRY_CHECK(halo_exchange(c, vnew, ld, s));
   // Gram blocks the next fused coefficient solve needs
   CombineCall cc{nullptr, 0, vcur, ld, vnew, ld, c->n, 0, 1, 0, 0};
-  KRY_CHECK(launch_combine(st, s, c->op, cc, c->st, c->T, c->g, c->grid, nullptr, nullptr));
+  KRY_CHECK(run_combine(c, cc, nullptr, nullptr));
   *exhausted = 0;
   return KRY_OK;
 }
@@ -364,7 +463,7 @@ int explicit_step(kry_ctx* c, int j, const double* vold, const double* vcur, dou
 int fused_step(kry_ctx* c, int j, const double* vold, const double* vcur, double* vnew,
                int64_t ld, int finalize_on_zero, int* exhausted) {
   ApplyGramCall ag{vcur, ld, c->n, 1, POST_STEP, 0};
-  KRY_CHECK(launch_apply_gram(c->stream, c->s, c->op, ag, c->st, c->T, c->g, c->grid));
+  KRY_CHECK(run_apply_gram(c, ag));
   KRY_CHECK(sync_status(c));
   KRY_CHECK(map_status(c, ("Lanczos step " + std::to_string(j)).c_str()));
   if (c->st_h->flags & KRY_FLAG_FALLBACK) {
@@ -379,8 +478,8 @@ int fused_step(kry_ctx* c, int j, const double* vold, const double* vcur, double
     cudaEventCreate(&evs[1]);
     ev = evs;
   }
-  KRY_CHECK(launch_combine(c->stream, c->s, c->op, cc, c->st, c->T, c->g, c->grid,
-                           c->prof ? &dummy : nullptr, ev));
+  KRY_CHECK(run_combine(c, cc, c->prof ? &dummy : nullptr, ev));
+  KRY_CHECK(halo_exchange(c, vnew, ld, c->s));
   if (c->prof) c->ev_comb.push_back({evs[0], evs[1]});
   *exhausted = 0;
   return KRY_OK;
@@ -464,16 +563,6 @@ double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
-template <class T>
-int dalloc(T** p, size_t count) {
-  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
-  if (e != cudaSuccess) {
-    *p = nullptr;
-    return fail(KRY_ERR_CUDA, std::string("cudaMalloc failed: ") + cudaGetErrorString(e) +
-                                  " (" + std::to_string(count * sizeof(T)) + " bytes)");
-  }
-  return KRY_OK;
-}
 
 int ensure_handles(kry_ctx* c) {
   if (!c->cublas) {
@@ -631,6 +720,8 @@ int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s
     delete c;
     return fail(KRY_ERR_ARGUMENT, "unknown operator kind");
   }
+  op.fx = make_fastdiv((unsigned)std::max(op.nx, 1));
+  op.fy = make_fastdiv((unsigned)std::max(op.ny, 1));
   c->n = nloc;
   c->ld = s;
   // window: 3 slots, each with one halo plane on both sides (multi-GPU)
@@ -687,6 +778,7 @@ void kry_ctx_destroy(kry_ctx* c) {
   if (c->cublas) cublasDestroy(c->cublas);
   if (c->solver) cusolverDnDestroy(c->solver);
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->halo_buf) cudaFree(c->halo_buf);
   if (c->t_ev[0]) { cudaEventDestroy(c->t_ev[0]); cudaEventDestroy(c->t_ev[1]); }
   cudaStreamDestroy(c->stream);
   delete c;
@@ -715,6 +807,7 @@ int kry_apply(kry_ctx* c, const double* v, double* y, int ncols) {
                              ncols * sizeof(double), c->n, cudaMemcpyHostToDevice, c->stream));
   for (int c0 = 0; c0 < ncols; c0 += KRY_SMAX) {
     const int w = std::min(KRY_SMAX, ncols - c0);
+    KRY_CHECK(halo_exchange(c, dvv + c0, ld, w));
     KRY_CHECK(launch_apply_store(c->stream, w, c->op, dvv + c0, ld, dy + c0, ld, c->n));
   }
   KRY_CUDA(cudaMemcpy2DAsync(y, ncols * sizeof(double), dy, ld * sizeof(double),
@@ -1170,7 +1263,7 @@ int kry_recover(kry_ctx* c, double* zhost) {
   for (int j = 1; rc == KRY_OK && j < m; ++j) {
     // coefficient solve j on V_j (replay) ; V_{j+1} goes to slot cur+1
     ApplyGramCall ag{sp(cur), ld2, n, 1, POST_STEP, 0};
-    rc = launch_apply_gram(c->stream, s, c->op, ag, c->st, c->T, c->g, c->grid);
+    rc = run_apply_gram(c, ag);
     if (rc) break;
     rc = sync_status(c);
     if (rc) break;
@@ -1181,8 +1274,12 @@ int kry_recover(kry_ctx* c, double* zhost) {
       // chunk complete: S_j known now -> fold blocks chunk_first..j into Z
       rc = gemm_chunk(chunk_first - 1, j - chunk_first + 1);
       if (rc) break;
-      rc = launch_copy_block(c->stream, s, sp(nslot - 2), ld2, sp(0), ld2, n);
-      if (rc == KRY_OK) rc = launch_copy_block(c->stream, s, sp(nslot - 1), ld2, sp(1), ld2, n);
+      // copy the last two blocks (halo planes included) to slots 0, 1
+      rc = launch_copy_block(c->stream, s, sp(nslot - 2) - halo * ld2, ld2, sp(0) - halo * ld2,
+                             ld2, n + 2 * halo);
+      if (rc == KRY_OK)
+        rc = launch_copy_block(c->stream, s, sp(nslot - 1) - halo * ld2, ld2, sp(1) - halo * ld2,
+                               ld2, n + 2 * halo);
       if (rc) break;
       old = 0; cur = 1; nxt = 2;
       chunk_first = j + 1;
@@ -1193,7 +1290,8 @@ int kry_recover(kry_ctx* c, double* zhost) {
     } else {
       CombineCall cc{old >= 0 ? sp(old) : nullptr, ld2, sp(cur), ld2, sp(nxt), ld2, n,
                      j > 1 ? 1 : 0, 1, 1, 1};
-      rc = launch_combine(c->stream, s, c->op, cc, c->st, c->T, c->g, c->grid, nullptr, nullptr);
+      rc = run_combine(c, cc, nullptr, nullptr);
+      if (rc == KRY_OK) rc = halo_exchange(c, sp(nxt), ld2, s);
     }
     if (rc) break;
     if (ex) { rc = fail(KRY_ERR_RECURRENCE, "second pass hit an invariant subspace early"); break; }
@@ -1203,7 +1301,7 @@ int kry_recover(kry_ctx* c, double* zhost) {
   if (rc == KRY_OK && m >= 1) {
     // coefficient solve m: S_m (and the replay check of coupling m-1)
     ApplyGramCall ag{sp(cur), ld2, n, 1, POST_STEP, 0};
-    rc = launch_apply_gram(c->stream, s, c->op, ag, c->st, c->T, c->g, c->grid);
+    rc = run_apply_gram(c, ag);
     if (rc == KRY_OK) rc = sync_status(c);
     if (rc == KRY_OK) rc = gemm_chunk(chunk_first - 1, m - chunk_first + 1);
   }

@@ -46,6 +46,26 @@ extern thread_local std::string g_last_error;
 void count_launch(int k = 1);
 
 // ---------------------------------------------------------------- operator
+// division by an invariant 32-bit divisor: q = (umulhi(n, mul) + n) >> shift
+// (round-up method, valid for n < 2^31)
+struct FastDiv {
+  unsigned d, mul, shift;
+};
+inline FastDiv make_fastdiv(unsigned d) {
+  FastDiv f;
+  f.d = d;
+  unsigned l = 0;
+  while ((1ull << l) < d) ++l;
+  f.shift = l;
+  f.mul = (unsigned)((((1ull << 32) * ((1ull << l) - d)) / d) + 1);
+  return f;
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned fdiv(unsigned n, const FastDiv& f) {
+  return (__umulhi(n, f.mul) + n) >> f.shift;
+}
+#endif
+
 struct OpDev {
   int kind;      // KRY_OP_STENCIL / KRY_OP_CSR
   int variable;  // stencil coefficient mode
@@ -58,6 +78,7 @@ struct OpDev {
   const int64_t* rp;
   const int* ci;
   const double* va;
+  FastDiv fx, fy;   // division by nx and ny
 };
 
 // ---------------------------------------------------------------- device state
@@ -127,6 +148,7 @@ struct CombineCall {
   double* vn; int64_t ldn;
   int64_t n;
   int has_old, use_op, write_new, reverse;
+  int post = POST_P;   // POST_NONE in multi-GPU mode (all-reduce, then k_post)
 };
 int launch_combine(cudaStream_t st, int s, const OpDev& op, const CombineCall& c,
                    DevState* dst, const TStore& T, GramScratch& g, int grid,
@@ -155,6 +177,8 @@ int launch_copy_block(cudaStream_t st, int s, const double* x, int64_t ldx,
                       double* y, int64_t ldy, int64_t n);
 // explicit-step bookkeeping kernel (1 CTA): store T slots from acc, etc.
 int launch_explicit_finish(cudaStream_t st, DevState* dst, const TStore& T, int mode);
+// post routine on st->gram (the all-reduced Gram totals) in one CTA
+int launch_post(cudaStream_t st, int post, DevState* dst, const TStore& T);
 
 int gram_grid_for(int64_t n);
 

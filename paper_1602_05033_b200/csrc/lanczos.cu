@@ -433,7 +433,7 @@ __device__ __noinline__ void run_post(int post, const double* total, DevState* s
   __shared__ double s_v;
   switch (post) {
     case POST_NONE:
-      if (tid() < 3 * 64) st->gram[tid()] = total[tid()];
+      for (int e = tid(); e < 3 * 64; e += blockDim.x) st->gram[e] = total[e];
       __syncthreads();
       break;
     case POST_P:
@@ -585,6 +585,7 @@ __device__ void finish_reduction(const double (&acc)[MP / 8][2], double* sX, dou
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
     if (lane == 0) total[e] = v;
   }
+  for (int e = NE + threadIdx.x; e < 256; e += blockDim.x) total[e] = 0.0;
   __syncthreads();
   if (threadIdx.x == 0) *ticket = 0u;
   // post routine on 8x8 smem scratch carved after `total`
@@ -696,10 +697,11 @@ __device__ __forceinline__ void stage_warp_coop(const OpDev& op, const double* _
       v = __ldg(reinterpret_cast<const double2*>(vc + i64 * ldc + off));
       if (load_old) o = __ldg(reinterpret_cast<const double2*>(vo + i64 * ldo + off));
       if (use_op) {
-        const int x = i % op.nx;
-        const int r = i / op.nx;
-        const int y = r % op.ny;
-        const int z = r / op.ny;
+        const unsigned r = fdiv((unsigned)i, op.fx);
+        const int x = i - (int)r * op.nx;
+        const unsigned zq = fdiv(r, op.fy);
+        const int y = (int)r - (int)zq * op.ny;
+        const int z = (int)zq;
         const bool hz0 = z > 0 || op.halo_lo, hy0 = y > 0, hx0 = x > 0;
         const bool hx1 = x < op.nx - 1, hy1 = y < op.ny - 1, hz1 = z < op.nzl - 1 || op.halo_hi;
         auto ld2 = [&](int j) {
@@ -859,7 +861,7 @@ __global__ void __launch_bounds__(TP, COOP ? 5 : 2) k_combine(OpDev op, CombineC
     warp_gram<MTG>(sX, r0, S, 3 * S, acc);
     __syncwarp();
   }
-  finish_reduction<MP>(acc, sX, partials, ticket, POST_P, st, T);
+  finish_reduction<MP>(acc, sX, partials, ticket, c.post, st, T);
 }
 
 // Apply + Gram: X = [V | A V], Y = A V  (use_op) or X = [V], Y = V
@@ -1198,6 +1200,20 @@ int launch_copy_block(cudaStream_t st, int s, const double* x, int64_t ldx, doub
 #define L(S) k_copy_block<S><<<ew_grid(n), 256, 0, st>>>(x, ldx, y, ldy, n)
   KRY_DISPATCH_S(s, L);
 #undef L
+  count_launch();
+  KRY_CUDA(cudaGetLastError());
+  return KRY_OK;
+}
+
+__global__ void __launch_bounds__(128) k_post(int post, DevState* st, TStore T) {
+  __shared__ double buf[256 + 14 * 64];
+  for (int e = threadIdx.x; e < 256; e += blockDim.x) buf[e] = e < 3 * 64 ? st->gram[e] : 0.0;
+  __syncthreads();
+  run_post(post, buf, st, T, reinterpret_cast<double(*)[64]>(buf + 256));
+}
+
+int launch_post(cudaStream_t st, int post, DevState* dst, const TStore& T) {
+  k_post<<<1, 128, 0, st>>>(post, dst, T);
   count_launch();
   KRY_CUDA(cudaGetLastError());
   return KRY_OK;

@@ -142,7 +142,11 @@ class _DeviceOperator(LinearOperator):
         ctx = ctypes.c_void_p()
         _lib.check(lib.kry_ctx_create(ctypes.byref(ctx), int(self.device), ctypes.byref(desc),
                                       int(s), int(max_m)))
-        return Context(ctx, self, s, max_m)
+        context = Context(ctx, self, s, max_m)
+        comm = getattr(self, "comm", None)
+        if comm is not None and comm.nranks > 1:
+            comm.attach(context)
+        return context
 
     def apply(self, v):
         v = np.asarray(v, dtype=float)
@@ -165,16 +169,21 @@ class StencilOperator(_DeviceOperator):
     """Dirichlet-grid stencil operator (x fastest), constant or per point."""
 
     def __init__(self, grid, c_diag=None, c_x=0.0, c_y=0.0, c_z=0.0, diag=None, cx=None,
-                 cy=None, cz=None, definite=True):
+                 cy=None, cz=None, definite=True, slab=None, comm=None):
         g = tuple(int(v) for v in grid) + (1,) * (3 - len(grid))
         self.grid = g
-        self.n = g[0] * g[1] * g[2]
+        self.n_global = g[0] * g[1] * g[2]
         self.definite = definite
+        # slab sharding (parallel.py): this rank owns planes [z0, z1) of the
+        # slowest axis; n is then the local row count
+        self.comm = comm
+        self.slab = tuple(slab) if slab is not None else (0, g[2])
+        self.n = g[0] * g[1] * (self.slab[1] - self.slab[0])
         self.variable = diag is not None
         if self.variable:
             self._arrays = [np.ascontiguousarray(x, dtype=float) for x in (diag, cx, cy, cz)]
             for arr in self._arrays:
-                if arr.shape != (self.n,):
+                if arr.shape != (self.n_global,):
                     raise DimensionMismatchError("coefficient array has the wrong length")
         else:
             self._arrays = None
@@ -185,12 +194,12 @@ class StencilOperator(_DeviceOperator):
         d = _lib.OperatorDesc()
         d.kind = _lib.KRY_OP_STENCIL
         d.variable = 1 if self.variable else 0
-        d.n = self.n
+        d.n = self.n_global
         d.nx, d.ny, d.nz = self.grid
         d.c_diag, d.c_x, d.c_y, d.c_z = self.c
         if self.variable:
             d.diag, d.cx, d.cy, d.cz = (_lib.as_dptr(x) for x in self._arrays)
-        d.z_begin, d.z_end = 0, self.grid[2]
+        d.z_begin, d.z_end = self.slab
         return d
 
 
