@@ -311,7 +311,7 @@ int allreduce_gram(kry_ctx* c) {
 int run_apply_gram(kry_ctx* c, ApplyGramCall ag) {
   const int post = ag.post;
   if (dist(c)) ag.post = POST_NONE;
-  KRY_CHECK(run_apply_gram(c, ag));
+  KRY_CHECK(launch_apply_gram(c->stream, c->s, c->op, ag, c->st, c->T, c->g, c->grid));
   if (dist(c)) {
     KRY_CHECK(allreduce_gram(c));
     KRY_CHECK(launch_post(c->stream, post, c->st, c->T));
