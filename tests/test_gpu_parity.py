@@ -261,8 +261,17 @@ def test_config3_sylvester_parity_with_reference_run():
         kb.SolveOptions(tol=cfg["tol"], max_m=cfg["max_m"], storage="windowed"))
     assert sol.iterations == int(g["iterations"]) == 681
     assert sol.rank == int(g["rank"])
-    ok, worst = hist_ok([r[2] for r in sol.history], g["history"][:, 2])
-    assert ok, worst
+    # Config 3's history is chaotic once Ritz values converge (m > ~100): the
+    # reference algorithm against ITSELF with a reordered SpMM summation
+    # deviates by up to 2.7% (tests/golden/c3_selfnoise.npz).  Floor-adjusted
+    # criterion: |d| <= 1e-9 rel + 4 x running max of the
+    # reference's self-deviation; early iterations stay at ~1e-14.
+    ref = g["history"][:, 2]
+    selfn = np.abs(gold("c3_selfnoise")["history"][:, 2] - ref)
+    envelope = np.maximum.accumulate(selfn)
+    h = np.array([r[2] for r in sol.history])
+    assert np.all(np.abs(h - ref) <= 1e-9 * ref + 4.0 * envelope + FLOOR)
+    assert np.all(np.abs(h[:60] - ref[:60]) <= 1e-9 * ref[:60] + FLOOR)
     om2 = P.sketch_omega(cfg["b"].shape[0], 2)
     om1 = P.sketch_omega(cfg["a"].shape[0], 2)
     right = sol.z1 @ (sol.z2.T @ om2)
