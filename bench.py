@@ -99,24 +99,33 @@ def build_problem(name, slab=None, comm=None):
 
 
 class Clocks:
-    """nvidia-smi clock / throttle sampling during the timed region."""
+    """SM clock / throttle-reason sampling during the timed region, in-process
+    through NVML (a spawned nvidia-smi every 200 ms perturbed the host-side
+    phases being timed)."""
 
-    def __init__(self):
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+               "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
+
+    def __init__(self, index=0):
         self.samples = []
         self._stop = threading.Event()
         self._t = None
+        self.index = index
 
     def start(self):
         def run():
-            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            try:
+                import pynvml
+                pynvml.nvmlInit()
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            except Exception:
+                return
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", "0", "--query-gpu=" + q,
-                                          "--format=csv,noheader,nounits"],
-                                         capture_output=True, text=True, timeout=5).stdout
-                    self.samples.append([x.strip() for x in out.strip().split(",")])
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((sm, mx, rs))
                 except Exception:
                     pass
                 self._stop.wait(0.2)
@@ -127,17 +136,13 @@ class Clocks:
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for s in self.samples:
-            try:
-                sm.append(float(s[0]))
-                mx = max(mx, float(s[1]))
-                for nm, v in zip(names, s[3:7]):
-                    if v.lower().startswith("active"):
-                        reasons.add(nm)
-            except Exception:
-                continue
+        sm = [x[0] for x in self.samples]
+        mx = max([x[1] for x in self.samples], default=0)
+        reasons = set()
+        for _, _, rs in self.samples:
+            for name, bit in self.REASONS.items():
+                if rs & bit:
+                    reasons.add(name)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
                 "reasons": sorted(reasons), "samples": len(sm)}
 
@@ -308,7 +313,7 @@ def main():
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    clocks = Clocks()
+    clocks = Clocks(local)
     clocks.start()
     _lib.reset_launch_count()
     lib.kry_profile_enable(ctx.ptr, 1)

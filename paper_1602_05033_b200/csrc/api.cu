@@ -248,6 +248,12 @@ struct kry_ctx {
   double prof_comb_ms = 0.0;
   int prof_comb_n = 0;
   cudaEvent_t t_ev[2] = {nullptr, nullptr};
+  cudaStream_t estream = nullptr;          // eigen / residual-check stream
+  cudaEvent_t ev_t = nullptr, ev_res[2] = {nullptr, nullptr};
+  // pass-2 chunk buffers, kept across solves (large allocations are slow)
+  double* p2buf[2] = {nullptr, nullptr};
+  double* p2qc[2] = {nullptr, nullptr};
+  size_t p2buf_cap = 0, p2qc_cap = 0;
   // multi-GPU
   int nranks = 1, rank_id = 0;
   ncclComm_t comm = nullptr;
@@ -485,8 +491,8 @@ int fused_step(kry_ctx* c, int j, const double* vold, const double* vcur, double
   return KRY_OK;
 }
 
-// pass-1 step with slot rotation and the eigen append of the new block row
-int step_pass1(kry_ctx* c, int finalize_on_zero, int* exhausted) {
+// one Lanczos step with slot rotation (no eigen work)
+int step_core(kry_ctx* c, int finalize_on_zero, int* exhausted) {
   if (!c->initialized) return fail(KRY_ERR_STATE, "init_basis has not been called");
   if (c->exhausted) return fail(KRY_ERR_DEFLATION, "the Krylov space is already invariant");
   if (c->m + 2 > c->T.cap) return fail(KRY_ERR_STATE, "max_m capacity of the context exceeded");
@@ -494,10 +500,6 @@ int step_pass1(kry_ctx* c, int finalize_on_zero, int* exhausted) {
   KRY_CHECK(fused_step(c, c->m + 1, slotp(c, c->i_old), slotp(c, c->i_cur), slotp(c, c->i_new),
                        c->ld, finalize_on_zero, &ex));
   c->m += 1;
-  const int j = c->m;
-  // eigen data of T_j: append block row j (diag j, coupling j-1)
-  KRY_CHECK(c->eig.append_block(c->stream, c->T.dsym + (int64_t)(j - 1) * 64,
-                                j >= 2 ? c->T.sub + (int64_t)(j - 2) * 64 : nullptr));
   if (ex) {
     c->exhausted = true;
   } else {
@@ -507,6 +509,52 @@ int step_pass1(kry_ctx* c, int finalize_on_zero, int* exhausted) {
     c->i_new = (o >= 0) ? o : 3 - c->i_old - c->i_cur;
   }
   *exhausted = ex;
+  return KRY_OK;
+}
+
+// pass-1 step + the eigen append of the new block row (synchronous API path)
+int step_pass1(kry_ctx* c, int finalize_on_zero, int* exhausted) {
+  KRY_CHECK(step_core(c, finalize_on_zero, exhausted));
+  const int j = c->m;
+  // eigen data of T_j: append block row j (diag j, coupling j-1)
+  KRY_CHECK(c->eig.append_block(c->stream, c->T.dsym + (int64_t)(j - 1) * 64,
+                                j >= 2 ? c->T.sub + (int64_t)(j - 2) * 64 : nullptr));
+  return KRY_OK;
+}
+
+// Asynchronous eigen work of iteration j on the eigen stream (overlaps the
+// next Lanczos step on the main stream): append block row j and, if asked,
+// the residual check of iteration j with the staged coupling tau1[j-1].
+// The check result (sum |M|^2, min |denominator|, spectral scale) lands in
+// the pinned ring slot `slot`, signalled by ev_res[slot].
+int launch_eigen_step(kry_ctx* c, int j, bool check, bool exhausted_j, int slot) {
+  KRY_CUDA(cudaEventRecord(c->ev_t, c->stream));
+  KRY_CUDA(cudaStreamWaitEvent(c->estream, c->ev_t, 0));
+  KRY_CHECK(c->eig.append_block(c->estream, c->T.dsym + (int64_t)(j - 1) * 64,
+                                j >= 2 ? c->T.sub + (int64_t)(j - 2) * 64 : nullptr));
+  if (check) {
+    const double* tau = exhausted_j ? c->zeros64 : c->T.tau1 + (int64_t)(j - 1) * 64;
+    KRY_CHECK(c->eig.residual_lyap(c->estream, c->gamma_d, tau));
+    k_scale_of<<<1, 32, 0, c->estream>>>(c->eig.lam_cur(), c->eig.K, c->eig.lam_cur(), c->eig.K,
+                                         c->eig.res + 2);
+    count_launch();
+    KRY_CUDA(cudaMemcpyAsync(c->hres + 4 * slot, c->eig.res, 3 * sizeof(double),
+                             cudaMemcpyDeviceToHost, c->estream));
+    KRY_CUDA(cudaEventRecord(c->ev_res[slot], c->estream));
+  }
+  return KRY_OK;
+}
+
+// wait for the check in ring slot `slot`; returns res / rel (guarded)
+int collect_check(kry_ctx* c, int slot, double beta2, double* res, double* rel) {
+  KRY_CUDA(cudaEventSynchronize(c->ev_res[slot]));
+  const double* h = c->hres + 4 * slot;
+  if (h[1] < 1e-14 * h[2])
+    return fail(KRY_ERR_INDEFINITE,
+                "eigenvalue-sum denominator is numerically singular; coefficient matrices must "
+                "be definite (of one sign)");
+  *res = sqrt(2.0 * fmax(h[0], 0.0));
+  *rel = *res / beta2;
   return KRY_OK;
 }
 
@@ -563,6 +611,21 @@ double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+// KRY_TIMING=1: synchronised stage timings on stderr (diagnostics only)
+struct StageTimer {
+  bool on;
+  cudaStream_t st;
+  double t;
+  explicit StageTimer(cudaStream_t s) : on(getenv("KRY_TIMING") != nullptr), st(s), t(now_s()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    double n = now_s();
+    fprintf(stderr, "[kry] %-28s %8.3f ms\n", what, 1e3 * (n - t));
+    t = n;
+  }
+};
+
 
 int ensure_handles(kry_ctx* c) {
   if (!c->cublas) {
@@ -617,8 +680,10 @@ int final_eig(kry_ctx* c, FinalBufs& b, int* k_out) {
   KRY_CHECK(dalloc(&b.Td, (size_t)k * k));
   KRY_CHECK(dalloc(&b.lam, (size_t)k));
   KRY_CHECK(dalloc(&b.u, (size_t)k * 8));
+  StageTimer tm(c->stream);
   KRY_CHECK(launch_assemble_T(c->stream, c->T.dsym, c->T.sub, s, m, b.Td));
   KRY_CHECK(syevd(c, b.Td, k, b.lam));
+  tm.mark("finalize: syevd(T)");
   KRY_CHECK(launch_first_rows_times(c->stream, b.Td, k, s, c->gamma_d, b.u));
   *k_out = k;
   return KRY_OK;
@@ -639,6 +704,27 @@ int set_qy(kry_ctx* c, const double* Q, int k, const double* factor, int rank) {
 }
 
 }  // namespace
+
+// Device -> caller-owned host buffer.  Large pageable buffers are page-locked
+// for the duration of the copy so the DMA runs at link speed instead of
+// through the driver's staging buffers.
+int copy_out(kry_ctx* c, void* host, const void* dev, size_t bytes) {
+  bool reg = false;
+  if (bytes >= ((size_t)64 << 20)) {
+    cudaPointerAttributes pa;
+    if (!(cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type == cudaMemoryTypeHost)) {
+      cudaGetLastError();
+      reg = cudaHostRegister(host, bytes, cudaHostRegisterDefault) == cudaSuccess;
+      if (!reg) cudaGetLastError();
+    }
+  }
+  cudaError_t e = cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (reg) cudaHostUnregister(host);
+  if (e != cudaSuccess)
+    return fail(KRY_ERR_CUDA, std::string("factor copy failed: ") + cudaGetErrorString(e));
+  return KRY_OK;
+}
 
 // ================================================================ C-ABI
 extern "C" {
@@ -668,6 +754,10 @@ int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s
   c->s = s;
   c->max_m = max_m;
   KRY_CUDA(cudaStreamCreate(&c->stream));
+  KRY_CUDA(cudaStreamCreate(&c->estream));
+  KRY_CUDA(cudaEventCreateWithFlags(&c->ev_t, cudaEventDisableTiming));
+  KRY_CUDA(cudaEventCreateWithFlags(&c->ev_res[0], cudaEventDisableTiming));
+  KRY_CUDA(cudaEventCreateWithFlags(&c->ev_res[1], cudaEventDisableTiming));
   // operator
   OpDev& op = c->op;
   memset(&op, 0, sizeof(op));
@@ -735,13 +825,14 @@ int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s
   KRY_CUDA(cudaMallocHost(&c->st_h, sizeof(DevState)));
   KRY_CUDA(cudaMallocHost(&c->hres, 16 * sizeof(double)));
   const int cap = max_m + 3;
-  KRY_CHECK(dalloc(&c->tmem, (size_t)5 * cap * 64));
-  KRY_CUDA(cudaMemset(c->tmem, 0, (size_t)5 * cap * 64 * sizeof(double)));
+  KRY_CHECK(dalloc(&c->tmem, (size_t)6 * cap * 64));
+  KRY_CUDA(cudaMemset(c->tmem, 0, (size_t)6 * cap * 64 * sizeof(double)));
   c->T.draw = c->tmem;
   c->T.dsym = c->tmem + (int64_t)cap * 64;
   c->T.off = c->tmem + (int64_t)2 * cap * 64;
   c->T.sub = c->tmem + (int64_t)3 * cap * 64;
   c->T.S = c->tmem + (int64_t)4 * cap * 64;
+  c->T.tau1 = c->tmem + (int64_t)5 * cap * 64;
   c->T.cap = cap;
   c->grid = gram_grid_for(nloc);
   c->g.max_grid = KRY_MAX_GRID;
@@ -780,6 +871,15 @@ void kry_ctx_destroy(kry_ctx* c) {
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->halo_buf) cudaFree(c->halo_buf);
   if (c->t_ev[0]) { cudaEventDestroy(c->t_ev[0]); cudaEventDestroy(c->t_ev[1]); }
+  cudaStreamSynchronize(c->estream);
+  cudaEventDestroy(c->ev_t);
+  cudaEventDestroy(c->ev_res[0]);
+  cudaEventDestroy(c->ev_res[1]);
+  cudaStreamDestroy(c->estream);
+  for (int b = 0; b < 2; ++b) {
+    if (c->p2buf[b]) cudaFree(c->p2buf[b]);
+    if (c->p2qc[b]) cudaFree(c->p2qc[b]);
+  }
   cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -946,41 +1046,90 @@ int kry_solve_lyap_pass1(kry_ctx* c, double tol, int max_m, int check_period, do
   KRY_CUDA(cudaSetDevice(c->dev));
   if (!c->initialized) return fail(KRY_ERR_STATE, "init_basis has not been called");
   if (max_m > c->max_m) return fail(KRY_ERR_ARGUMENT, "max_m exceeds the context capacity");
+  // The residual check of iteration j runs on the eigen stream while the
+  // Lanczos step j+1 runs on the main stream; its result is read one
+  // iteration later (a converged solve therefore computes one extra,
+  // discarded basis block).
   double t_basis = 0.0, t_res = 0.0;
   int nh = 0;
   *iterations = 0;
   *reason = 1;
+  *n_history = 0;
   double rel = INFINITY;
-  for (int it = 1; it <= max_m; ++it) {
+  int pending = -1, pending_slot = 0;
+  auto record = [&](int it, double r) {
+    double* row = history + (size_t)nh * 5;
+    row[0] = it; row[1] = (double)it * c->s; row[2] = r; row[3] = t_basis; row[4] = t_res;
+    ++nh;
+    *n_history = nh;
+    *final_rel = r;
+  };
+  int rc = KRY_OK;
+  bool done = false;
+  for (int it = 1; it <= max_m && !done; ++it) {
     double t0 = now_s();
     int ex = 0;
-    KRY_CHECK(step_pass1(c, 1, &ex));
-    KRY_CUDA(cudaStreamSynchronize(c->stream));
+    rc = step_core(c, 1, &ex);
+    if (rc) break;
     t_basis += now_s() - t0;
-    if (it % check_period == 0 || ex) {
+    if (pending > 0) {   // result of the previous iteration's check
       t0 = now_s();
       double res = 0.0;
-      KRY_CHECK(check_lyap(c, c->beta2, &res, &rel));
+      rc = collect_check(c, pending_slot, c->beta2, &res, &rel);
+      if (rc) break;
       t_res += now_s() - t0;
-      double* row = history + (size_t)nh * 5;
-      row[0] = it; row[1] = (double)it * c->s; row[2] = rel; row[3] = t_basis; row[4] = t_res;
-      ++nh;
-      *n_history = nh;
-      *final_rel = rel;
+      record(pending, rel);
+      if (rel <= tol) {
+        *iterations = pending;
+        *reason = 0;
+        c->m_final = pending;
+        done = true;
+        break;
+      }
+      pending = -1;
+    }
+    const bool chk = (it % check_period == 0) || ex;
+    const int slot = it & 1;
+    rc = launch_eigen_step(c, it, chk, ex != 0, slot);
+    if (rc) break;
+    if (chk) {
+      pending = it;
+      pending_slot = slot;
+    }
+    if (ex) {   // invariant subspace: this check decides
+      t0 = now_s();
+      double res = 0.0;
+      rc = collect_check(c, slot, c->beta2, &res, &rel);
+      if (rc) break;
+      t_res += now_s() - t0;
+      record(it, rel);
+      pending = -1;
       if (rel <= tol) {
         *iterations = it;
         *reason = 0;
         c->m_final = it;
-        return KRY_OK;
-      }
-      if (ex) {
+      } else {
         *reason = 2;
-        return fail(KRY_ERR_CONVERGENCE, "invariant");
+      }
+      done = true;
+    }
+  }
+  if (rc == KRY_OK && !done && pending > 0) {
+    double res = 0.0;
+    rc = collect_check(c, pending_slot, c->beta2, &res, &rel);
+    if (rc == KRY_OK) {
+      record(pending, rel);
+      if (rel <= tol) {
+        *iterations = pending;
+        *reason = 0;
+        c->m_final = pending;
       }
     }
   }
-  *n_history = nh;
-  return fail(KRY_ERR_CONVERGENCE, "max_m");
+  cudaStreamSynchronize(c->estream);
+  if (rc != KRY_OK) return rc;
+  if (*reason == 0) return KRY_OK;
+  return fail(KRY_ERR_CONVERGENCE, *reason == 2 ? "invariant" : "max_m");
 }
 
 int kry_solve_sylv_pass1(kry_ctx* a, kry_ctx* b, double tol, int max_m, int check_period,
@@ -1061,8 +1210,10 @@ int kry_finalize_lyap(kry_ctx* c, double eps, int* rank, double* discarded) {
     return rc;
   }
   int nparts = 0;
+  StageTimer tm(c->stream);
   rc = launch_ytilde(c->stream, b.u, b.lam, k, b.u, b.lam, k, c->s, Y, k, mind, &nparts);
   if (rc == KRY_OK) rc = syevd(c, Y, k, mu);
+  tm.mark("finalize: syevd(Ytilde)");
   if (rc == KRY_OK) rc = launch_truncate(c->stream, mu, k, 0, eps, mind, nparts, work, outd);
   if (rc != KRY_OK) { cleanup(); return rc; }
   KRY_CUDA(cudaMemcpy(hout, outd, 5 * sizeof(double), cudaMemcpyDeviceToHost));
@@ -1210,7 +1361,9 @@ int kry_finalize_sylv(kry_ctx* a, kry_ctx* bb, double eps, int* rank, double* di
 
 // pass 2 (solvers.py:130-169): regenerate V_2..V_m from C with the same
 // deterministic kernels (coupling blocks compared against pass 1), buffer G
-// blocks in an interleaved chunk and fold them into Z with one DGEMM per chunk
+// blocks in an interleaved chunk and fold them into Z with one DGEMM per chunk.
+// Two chunk buffers (kept in the context across solves): the DGEMM of chunk
+// k runs on the second stream while chunk k+1 is regenerated.
 int kry_recover(kry_ctx* c, double* zhost) {
   KRY_CUDA(cudaSetDevice(c->dev));
   if (c->rank < 0) return fail(KRY_ERR_STATE, "finalize has not been called");
@@ -1222,47 +1375,82 @@ int kry_recover(kry_ctx* c, double* zhost) {
     KRY_CHECK(dalloc(&c->Z, (size_t)n * std::max(r, 1)));
     c->z_cap = n * std::max(r, 1);
   }
-  if (r == 0) {
-    if (zhost) { /* nothing to copy */ }
-    return KRY_OK;
-  }
-  // chunk size from free memory (keep half of it free)
+  if (r == 0) return KRY_OK;
   size_t fr = 0, tot = 0;
   cudaMemGetInfo(&fr, &tot);
-  const size_t blk_bytes = (size_t)n * s * sizeof(double);
-  int64_t G = (int64_t)((fr / 2) / blk_bytes) - 2;
-  if (G > 64) G = 64;
+  const int64_t halo = (c->op.kind == KRY_OP_STENCIL) ? c->op.nxy : 0;
+  const size_t blk_bytes = (size_t)(n + 2 * halo) * s * sizeof(double);
+  // two buffers within a quarter of the free memory (+ what is cached)
+  int64_t G = (int64_t)((fr / 4 + c->p2buf_cap * sizeof(double)) / blk_bytes) - 2;
+  if (G > 32) G = 32;
   if (G > m) G = m;
   if (G < 1) G = 1;
+  const int nbuf = (m > G) ? 2 : 1;
   const int64_t nslot = G + 2;
   const int64_t ld2 = nslot * s;
-  const int64_t halo = (c->op.kind == KRY_OP_STENCIL) ? c->op.nxy : 0;
-  double* buf = nullptr;
-  double* Qc = nullptr;
-  KRY_CHECK(dalloc(&buf, (size_t)(n + 2 * halo) * ld2));
-  if (dalloc(&Qc, (size_t)G * s * r) != KRY_OK) { cudaFree(buf); return KRY_ERR_CUDA; }
-  KRY_CUDA(cudaMemsetAsync(buf, 0, (n + 2 * halo) * ld2 * sizeof(double), c->stream));
-  double* base = buf + halo * ld2;
-  auto sp = [&](int64_t q) { return base + q * s; };
+  double* buf[2] = {nullptr, nullptr};
+  double* Qc[2] = {nullptr, nullptr};
+  cudaEvent_t ev_full[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   int rc = KRY_OK;
+  const size_t need_buf = (size_t)(n + 2 * halo) * ld2, need_qc = (size_t)G * s * r;
+  if (c->p2buf_cap < need_buf || c->p2qc_cap < need_qc) {
+    for (int b = 0; b < 2; ++b) {
+      if (c->p2buf[b]) cudaFree(c->p2buf[b]);
+      if (c->p2qc[b]) cudaFree(c->p2qc[b]);
+      c->p2buf[b] = c->p2qc[b] = nullptr;
+    }
+    c->p2buf_cap = need_buf;
+    c->p2qc_cap = need_qc;
+  }
+  for (int b = 0; b < nbuf && rc == KRY_OK; ++b) {
+    if (!c->p2buf[b]) rc = dalloc(&c->p2buf[b], c->p2buf_cap);
+    if (rc == KRY_OK && !c->p2qc[b]) rc = dalloc(&c->p2qc[b], c->p2qc_cap);
+    buf[b] = c->p2buf[b];
+    Qc[b] = c->p2qc[b];
+    // halo planes must be finite (zero) for the boundary predicates' skipped loads
+    if (rc == KRY_OK &&
+        cudaMemsetAsync(buf[b], 0, need_buf * sizeof(double), c->stream) != cudaSuccess)
+      rc = fail(KRY_ERR_CUDA, "memset failed");
+    cudaEventCreateWithFlags(&ev_full[b], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_free[b], cudaEventDisableTiming);
+  }
+  auto cleanup = [&]() {
+    cudaStreamSynchronize(c->estream);
+    cudaStreamSynchronize(c->stream);
+    cublasSetStream(c->cublas, c->stream);
+    for (int b = 0; b < 2; ++b) {
+      if (ev_full[b]) cudaEventDestroy(ev_full[b]);
+      if (ev_free[b]) cudaEventDestroy(ev_free[b]);
+    }
+  };
+  if (rc != KRY_OK) { cleanup(); return rc; }
+  int cb = 0;   // current buffer
+  auto sp = [&](int b, int64_t q) { return buf[b] + halo * ld2 + q * s; };
   int first_gemm = 1;
-  auto gemm_chunk = [&](int blk0, int nblk) -> int {  // blk0 0-based
-    KRY_CHECK(launch_chunk_coef(c->stream, c->T.S, c->qy, s, r, blk0, nblk, Qc));
+  int gemm_used[2] = {0, 0};
+  // fold blocks blk0.. (0-based) of buffer b into Z on the second stream
+  auto gemm_chunk = [&](int b, int blk0, int nblk) -> int {
+    KRY_CUDA(cudaEventRecord(ev_full[b], c->stream));
+    KRY_CUDA(cudaStreamWaitEvent(c->estream, ev_full[b], 0));
+    KRY_CHECK(launch_chunk_coef(c->estream, c->T.S, c->qy, s, r, blk0, nblk, Qc[b]));
+    cublasSetStream(c->cublas, c->estream);
     const double one = 1.0;
     const double beta = first_gemm ? 0.0 : 1.0;
-    if (cublasDgemm(c->cublas, CUBLAS_OP_N, CUBLAS_OP_N, r, (int)n, nblk * s, &one, Qc, r, sp(2),
-                    (int)ld2, &beta, c->Z, r) != CUBLAS_STATUS_SUCCESS)
+    if (cublasDgemm(c->cublas, CUBLAS_OP_N, CUBLAS_OP_N, r, (int)n, nblk * s, &one, Qc[b], r,
+                    sp(b, 2), (int)ld2, &beta, c->Z, r) != CUBLAS_STATUS_SUCCESS)
       return fail(KRY_ERR_CUDA, "cublasDgemm (Z accumulation) failed");
+    KRY_CUDA(cudaEventRecord(ev_free[b], c->estream));
+    gemm_used[b] = 1;
     first_gemm = 0;
     return KRY_OK;
   };
   // regenerate V_1 into slot 2
-  rc = do_init(c, sp(2), ld2, 1);
+  rc = do_init(c, sp(cb, 2), ld2, 1);
   int cur = 2, old = -1;
   int chunk_first = 1;  // block index (1-based) held in slot 2
   for (int j = 1; rc == KRY_OK && j < m; ++j) {
     // coefficient solve j on V_j (replay) ; V_{j+1} goes to slot cur+1
-    ApplyGramCall ag{sp(cur), ld2, n, 1, POST_STEP, 0};
+    ApplyGramCall ag{sp(cb, cur), ld2, n, 1, POST_STEP, 0};
     rc = run_apply_gram(c, ag);
     if (rc) break;
     rc = sync_status(c);
@@ -1272,26 +1460,43 @@ int kry_recover(kry_ctx* c, double* zhost) {
     int nxt = cur + 1;
     if (nxt == nslot) {
       // chunk complete: S_j known now -> fold blocks chunk_first..j into Z
-      rc = gemm_chunk(chunk_first - 1, j - chunk_first + 1);
+      rc = gemm_chunk(cb, chunk_first - 1, j - chunk_first + 1);
       if (rc) break;
-      // copy the last two blocks (halo planes included) to slots 0, 1
-      rc = launch_copy_block(c->stream, s, sp(nslot - 2) - halo * ld2, ld2, sp(0) - halo * ld2,
-                             ld2, n + 2 * halo);
-      if (rc == KRY_OK)
-        rc = launch_copy_block(c->stream, s, sp(nslot - 1) - halo * ld2, ld2, sp(1) - halo * ld2,
-                               ld2, n + 2 * halo);
+      const int nb = (nbuf == 2) ? 1 - cb : cb;
+      // the buffer we switch to is free once its previous DGEMM is done
+      if ((nb == cb || gemm_used[nb]) &&
+          cudaStreamWaitEvent(c->stream, ev_free[nb], 0) != cudaSuccess) {
+        rc = fail(KRY_ERR_CUDA, "event wait failed");
+        break;
+      }
+      // carry the last two blocks (halo planes included) to slots 0, 1
+      if (nb != cb) {
+        rc = launch_copy_block(c->stream, s, sp(cb, nslot - 2) - halo * ld2, ld2,
+                               sp(nb, 0) - halo * ld2, ld2, n + 2 * halo);
+        if (rc == KRY_OK)
+          rc = launch_copy_block(c->stream, s, sp(cb, nslot - 1) - halo * ld2, ld2,
+                                 sp(nb, 1) - halo * ld2, ld2, n + 2 * halo);
+      } else {
+        rc = launch_copy_block(c->stream, s, sp(cb, nslot - 2) - halo * ld2, ld2,
+                               sp(cb, 0) - halo * ld2, ld2, n + 2 * halo);
+        if (rc == KRY_OK)
+          rc = launch_copy_block(c->stream, s, sp(cb, nslot - 1) - halo * ld2, ld2,
+                                 sp(cb, 1) - halo * ld2, ld2, n + 2 * halo);
+      }
       if (rc) break;
+      cb = nb;
       old = 0; cur = 1; nxt = 2;
       chunk_first = j + 1;
     }
     int ex = 0;
     if (c->st_h->flags & KRY_FLAG_FALLBACK) {
-      rc = explicit_step(c, j, old >= 0 ? sp(old) : nullptr, sp(cur), sp(nxt), ld2, 1, &ex);
+      rc = explicit_step(c, j, old >= 0 ? sp(cb, old) : nullptr, sp(cb, cur), sp(cb, nxt), ld2,
+                         1, &ex);
     } else {
-      CombineCall cc{old >= 0 ? sp(old) : nullptr, ld2, sp(cur), ld2, sp(nxt), ld2, n,
+      CombineCall cc{old >= 0 ? sp(cb, old) : nullptr, ld2, sp(cb, cur), ld2, sp(cb, nxt), ld2, n,
                      j > 1 ? 1 : 0, 1, 1, 1};
       rc = run_combine(c, cc, nullptr, nullptr);
-      if (rc == KRY_OK) rc = halo_exchange(c, sp(nxt), ld2, s);
+      if (rc == KRY_OK) rc = halo_exchange(c, sp(cb, nxt), ld2, s);
     }
     if (rc) break;
     if (ex) { rc = fail(KRY_ERR_RECURRENCE, "second pass hit an invariant subspace early"); break; }
@@ -1300,25 +1505,22 @@ int kry_recover(kry_ctx* c, double* zhost) {
   }
   if (rc == KRY_OK && m >= 1) {
     // coefficient solve m: S_m (and the replay check of coupling m-1)
-    ApplyGramCall ag{sp(cur), ld2, n, 1, POST_STEP, 0};
+    ApplyGramCall ag{sp(cb, cur), ld2, n, 1, POST_STEP, 0};
     rc = run_apply_gram(c, ag);
     if (rc == KRY_OK) rc = sync_status(c);
-    if (rc == KRY_OK) rc = gemm_chunk(chunk_first - 1, m - chunk_first + 1);
+    if (rc == KRY_OK) rc = gemm_chunk(cb, chunk_first - 1, m - chunk_first + 1);
   }
-  if (rc == KRY_OK) rc = sync_status(c);
+  if (rc == KRY_OK) {
+    cudaStreamSynchronize(c->estream);
+    rc = sync_status(c);
+  }
   if (rc == KRY_OK && c->st_h->replay_err > 1e-8) {
     rc = fail(KRY_ERR_RECURRENCE,
               "second pass regenerated a coupling block that differs from the stored one; the "
               "operator looks nondeterministic");
   }
-  if (rc == KRY_OK && zhost) {
-    KRY_CUDA(cudaMemcpyAsync(zhost, c->Z, (size_t)n * r * sizeof(double), cudaMemcpyDeviceToHost,
-                             c->stream));
-    KRY_CUDA(cudaStreamSynchronize(c->stream));
-  }
-  cudaStreamSynchronize(c->stream);
-  cudaFree(buf);
-  cudaFree(Qc);
+  if (rc == KRY_OK && zhost) rc = copy_out(c, zhost, c->Z, (size_t)n * r * sizeof(double));
+  cleanup();
   return rc;
 }
 

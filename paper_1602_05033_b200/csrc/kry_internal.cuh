@@ -132,6 +132,7 @@ struct TStore {  // projected-matrix storage (device), slots of 64 doubles
   double* off;   // off_mgs sums
   double* sub;   // coupling blocks tau (final R factors)
   double* S;     // lazy CholQR2 corrections per block
+  double* tau1;  // first-stage coupling tau_{j+1,j} of step j (read by the async check)
   int cap;       // number of slots
 };
 

@@ -385,7 +385,10 @@ __device__ __noinline__ void coef_solve(const double* total, DevState* st, const
     } else {
       s_flag = 0;
       inv_upper(X, Y, s);
-      for (int q = 0; q < 64; ++q) st->R1prev[q] = X[q];
+      for (int q = 0; q < 64; ++q) {
+        st->R1prev[q] = X[q];
+        T.tau1[(int64_t)(j - 1) * 64 + q] = X[q];
+      }
     }
   }
   __syncthreads();
@@ -704,12 +707,12 @@ __device__ __forceinline__ void stage_warp_coop(const OpDev& op, const double* _
         const int z = (int)zq;
         const bool hz0 = z > 0 || op.halo_lo, hy0 = y > 0, hx0 = x > 0;
         const bool hx1 = x < op.nx - 1, hy1 = y < op.ny - 1, hz1 = z < op.nzl - 1 || op.halo_hi;
-        auto ld2 = [&](int j) {
-          return __ldg(reinterpret_cast<const double2*>(vc + (int64_t)j * ldc + off));
-        };
-        const double2 n0 = ld2(hz0 ? i - op.nxy : i), n1 = ld2(hy0 ? i - op.nx : i);
-        const double2 n2 = ld2(hx0 ? i - 1 : i), n3 = ld2(hx1 ? i + 1 : i);
-        const double2 n4 = ld2(hy1 ? i + op.nx : i), n5 = ld2(hz1 ? i + op.nxy : i);
+        // one 64-bit base, neighbours by (32-bit) element deltas
+        const double2* pc = reinterpret_cast<const double2*>(vc + i64 * ldc + off);
+        const int dx = (int)ldc / 2, dy = op.nx * (int)ldc / 2, dz = op.nxy * (int)ldc / 2;
+        const double2 n0 = __ldg(pc - (hz0 ? dz : 0)), n1 = __ldg(pc - (hy0 ? dy : 0));
+        const double2 n2 = __ldg(pc - (hx0 ? dx : 0)), n3 = __ldg(pc + (hx1 ? dx : 0));
+        const double2 n4 = __ldg(pc + (hy1 ? dy : 0)), n5 = __ldg(pc + (hz1 ? dz : 0));
         if (!op.variable) {
           const double sx0 = (hx0 ? n2.x : 0.0) + (hx1 ? n3.x : 0.0);
           const double sx1 = (hx0 ? n2.y : 0.0) + (hx1 ? n3.y : 0.0);
@@ -866,7 +869,7 @@ __global__ void __launch_bounds__(TP, COOP ? 5 : 2) k_combine(OpDev op, CombineC
 
 // Apply + Gram: X = [V | A V], Y = A V  (use_op) or X = [V], Y = V
 template <int S, int USE_OP, bool COOP>
-__global__ void __launch_bounds__(TP, COOP ? 5 : 2) k_apply_gram(OpDev op, ApplyGramCall c, DevState* st,
+__global__ void __launch_bounds__(TP, COOP ? 8 : 2) k_apply_gram(OpDev op, ApplyGramCall c, DevState* st,
                                                    TStore T, double* partials, unsigned* ticket) {
   constexpr int NG = USE_OP ? 2 : 1;
   constexpr int XC = apply_cols(S);
@@ -1022,6 +1025,7 @@ __global__ void k_explicit_finish(DevState* st, TStore T, int mode) {
       T.dsym[o + q] = 0.5 * (st->acc_b[r * 8 + c] + st->acc_b[c * 8 + r]);
       T.off[o + q] = st->has_old ? st->acc_a[q] : 0.0;
       T.sub[o + q] = 0.0;
+      T.tau1[o + q] = 0.0;
     }
     T.S[o + q] = st->Sc[q];
     __syncthreads();
@@ -1039,6 +1043,7 @@ __global__ void k_explicit_finish(DevState* st, TStore T, int mode) {
     }
     T.S[o + q] = st->Sc[q];
     st->R1prev[q] = st->gram[64 + q];
+    T.tau1[o + q] = st->gram[64 + q];
     st->So[q] = st->Sc[q];
     st->Goo[q] = st->Gcc[q];
     __syncthreads();
