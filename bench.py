@@ -155,8 +155,10 @@ def timed_solve_device(kb, lib, ctx, c_dev_ptr, opts, s, prof=True):
     beta2 = ctypes.c_double()
     ms = ctypes.c_double()
     _lib.check(lib.kry_timer(ctx.ptr, 0, None))
+    ti = time.perf_counter()
     _lib.check(lib.kry_init_basis_device(ctx.ptr, ctypes.c_void_p(c_dev_ptr), _lib.as_dptr(gamma),
                                          ctypes.byref(beta2)))
+    t_init = time.perf_counter() - ti
     hist = np.zeros((opts.max_m + 1, 5))
     nh, its, reason = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
     rel = ctypes.c_double()
@@ -173,7 +175,7 @@ def timed_solve_device(kb, lib, ctx, c_dev_ptr, opts, s, prof=True):
     _lib.check(lib.kry_timer(ctx.ptr, 1, ctypes.byref(ms)))
     t3 = time.perf_counter()
     return dict(ms=ms.value, iterations=its.value, rank=rank.value, rel=rel.value,
-                pass1_s=t1 - t0, finalize_s=t2 - t1, pass2_s=t3 - t2,
+                init_s=t_init, pass1_s=t1 - t0, finalize_s=t2 - t1, pass2_s=t3 - t2,
                 check_s=float(hist[nh.value - 1, 4]) if nh.value else 0.0)
 
 
@@ -394,7 +396,10 @@ def main():
                    "parallelism": "slab-z%d" % world if world > 1 else "single",
                    "l2": "inputs (4 x %d MB blocks) exceed the 126 MB L2" % (n * s * 8 >> 20)},
         "time_to_tol_ms": ms_total / args.steps,
-        "phases_s": {"pass1": r0["pass1_s"], "checks_in_pass1": r0["check_s"],
+        "phases_all_s": [{k: round(r[k], 4) for k in ("pass1_s", "finalize_s", "pass2_s")}
+                         for r in runs],
+        "phases_s": {"init": r0["init_s"], "pass1": r0["pass1_s"],
+                     "checks_in_pass1": r0["check_s"],
                      "finalize": r0["finalize_s"], "pass2": r0["pass2_s"]},
         "roofline": {"bound": "hbm", "kernel": "k_combine (fused stencil SpMM + 3-term "
                      "recurrence + Gram)", "achieved": achieved, "peak": hbm,
