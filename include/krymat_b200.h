@@ -145,6 +145,10 @@ int kry_finalize_lyap(kry_ctx *ctx, double trunc_eps, int *rank,
 int kry_finalize_sylv(kry_ctx *a, kry_ctx *b, double trunc_eps, int *rank,
                       double *discarded);
 
+/* install a caller-provided reduced factor qy (k x t row-major, k = s*m) for
+ * the first m blocks, as two_pass_recover(op, state, qy) does (solvers.py:130) */
+int kry_set_qy(kry_ctx *ctx, int m, int t, const double *qy);
+
 /* pass 2: regenerate the basis and accumulate Z = sum_i V_i qy_i.
  * z: host n x rank row-major (or NULL to keep Z on the device only). */
 int kry_recover(kry_ctx *ctx, double *z);

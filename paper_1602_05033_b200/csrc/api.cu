@@ -1524,6 +1524,22 @@ int kry_recover(kry_ctx* c, double* zhost) {
   return rc;
 }
 
+int kry_set_qy(kry_ctx* c, int m, int t, const double* qy) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  if (m < 1 || m > c->m) return fail(KRY_ERR_DIMENSION, "qy covers more blocks than generated");
+  if (t < 0) return fail(KRY_ERR_DIMENSION, "negative factor rank");
+  KRY_CHECK(ensure_handles(c));
+  if (c->qy) cudaFree(c->qy);
+  c->qy = nullptr;
+  c->m_final = m;
+  c->rank = t;
+  if (t == 0) return KRY_OK;
+  const size_t cnt = (size_t)m * c->s * t;
+  KRY_CHECK(dalloc(&c->qy, cnt));
+  KRY_CUDA(cudaMemcpy(c->qy, qy, cnt * sizeof(double), cudaMemcpyHostToDevice));
+  return KRY_OK;
+}
+
 int kry_get_factor(kry_ctx* c, double* zhost) {
   KRY_CUDA(cudaSetDevice(c->dev));
   if (!c->Z || c->rank < 1) return KRY_OK;
