@@ -836,9 +836,10 @@ int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s
   c->T.cap = cap;
   c->grid = gram_grid_for(nloc);
   c->g.max_grid = KRY_MAX_GRID;
-  KRY_CHECK(dalloc(&c->g.partials, (size_t)c->g.max_grid * 24 * 8));
-  KRY_CHECK(dalloc(&c->g.ticket, 8));
-  KRY_CUDA(cudaMemset(c->g.ticket, 0, 8 * sizeof(unsigned)));
+  // per-CTA partials + per-group totals of the two-level grid reduction
+  KRY_CHECK(dalloc(&c->g.partials, (size_t)(c->g.max_grid + c->g.max_grid / 32 + 1) * 24 * 8));
+  KRY_CHECK(dalloc(&c->g.ticket, 2 + c->g.max_grid / 32));
+  KRY_CUDA(cudaMemset(c->g.ticket, 0, (2 + c->g.max_grid / 32) * sizeof(unsigned)));
   KRY_CHECK(dalloc(&c->zeros64, 64));
   KRY_CHECK(dalloc(&c->gamma_d, 64));
   KRY_CUDA(cudaMemset(c->zeros64, 0, 64 * sizeof(double)));

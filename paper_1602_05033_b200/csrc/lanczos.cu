@@ -31,6 +31,12 @@ namespace kry {
 #define TP 128     // points per tile = threads per CTA
 #define XCOLS 24   // tile columns (<= 3 groups of 8)
 #define LDP (TP + 4)  // transposed tile stride: conflict-free row writes and DMMA loads
+// column k of a transposed tile starts at CB(k): stride LDP plus a 4-row
+// shift on every other group of 4 columns, so a half-warp storing 4 column
+// pairs x 4 points (the cooperative staging order, which keeps each quarter
+// warp's 16-byte global loads inside one 128-byte line) hits 16 distinct bank
+// pairs; the shift is uniform per DMMA fragment load, which stays conflict-free.
+#define CB(k) ((k) * LDP + ((k) & 4))
 
 // ------------------------------------------------------------------ vector io
 template <int S>
@@ -125,9 +131,9 @@ __device__ __forceinline__ void tile_gram(const double* sX, int k0, int ycol, do
 #pragma unroll
   for (int ks = 0; ks < 8; ++ks) {
     const int k = k0 + ks * 4 + t;   // point index inside the tile
-    const double b = sX[(ycol + g) * LDP + k];
+    const double b = sX[CB(ycol + g) + k];
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][0], acc[mt][1], sX[(mt * 8 + g) * LDP + k], b);
+    for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][0], acc[mt][1], sX[CB(mt * 8 + g) + k], b);
   }
 }
 
@@ -218,6 +224,67 @@ __device__ void inv_upper(const double* R, double* Ri, int s) {
     }
   }
 }
+// Warp-parallel Cholesky + triangular inverse for the coefficient tail (all
+// threads of the CTA call it; warp 0 computes).  Same arithmetic order as
+// chol_upper (right-looking form of the same left-to-right subtractions) and
+// inv_upper (one lane per column).  Returns the breakdown flag uniformly;
+// Ri is written only when the factorisation succeeded.
+__device__ int chol_inv_par(const double* G, double* R, double* Ri, int s, double* min_ratio) {
+  __shared__ double s_W[64];
+  __shared__ int s_bad;
+  __shared__ double s_mr;
+  __syncthreads();
+  if (tid() < 32) {
+    const int l = tid();
+    for (int q = l; q < 64; q += 32) {
+      s_W[q] = G[q];
+      R[q] = 0.0;
+    }
+    __syncwarp();
+    int bad = 0;
+    for (int k = 0; k < s; ++k) {
+      const double p = s_W[k * 8 + k];
+      if (!(p > 1e3 * 2.220446049250313e-16 * fabs(G[k * 8 + k])) || !(p > 0.0)) {
+        bad = 1;
+        break;
+      }
+      const double rkk = sqrt(p);
+      if (l >= k && l < s) R[k * 8 + l] = (l == k) ? rkk : s_W[k * 8 + l] / rkk;
+      __syncwarp();
+      for (int q = l; q < 64; q += 32) {
+        const int i = q >> 3, j = q & 7;
+        if (i > k && j >= i && j < s) s_W[q] -= R[k * 8 + i] * R[k * 8 + j];
+      }
+      __syncwarp();
+    }
+    if (!bad) {
+      if (l < s) {
+        const int j = l;
+        for (int i = 0; i < 8; ++i) Ri[i * 8 + j] = 0.0;
+        Ri[j * 8 + j] = 1.0 / R[j * 8 + j];
+        for (int i = j - 1; i >= 0; --i) {
+          double v = 0.0;
+          for (int k = i + 1; k <= j; ++k) v += R[i * 8 + k] * Ri[k * 8 + j];
+          Ri[i * 8 + j] = -v / R[i * 8 + i];
+        }
+      } else if (l < 8) {
+        for (int i = 0; i < 8; ++i) Ri[i * 8 + l] = 0.0;
+      }
+      if (l == 0) {
+        double fro = 0.0;
+        for (int i = 0; i < 64; ++i) fro += R[i] * R[i];
+        fro = sqrt(fro);
+        double mr = 1e300;
+        for (int k = 0; k < s; ++k) mr = fmin(mr, R[k * 8 + k] / fro);
+        s_mr = mr;
+      }
+    }
+    if (l == 0) s_bad = bad;
+  }
+  __syncthreads();
+  *min_ratio = s_mr;
+  return s_bad;
+}
 __device__ double m_trace(const double* A, int s) {
   double t = 0.0;
   for (int k = 0; k < s; ++k) t += A[k * 8 + k];
@@ -253,17 +320,24 @@ __device__ __noinline__ void coef_solve(const double* total, DevState* st, const
   double* Z = sm[12]; double* U = sm[13];
   __shared__ int s_flag;
   __shared__ double s_val[4];
-  m_copy(Gcc, st->Gcc); m_copy(Goc, st->Goc); m_copy(GoW, st->GoW); m_copy(Goo, st->Goo);
-  m_copy(So, st->So);
+  // the five carried 8x8 blocks in one batch of loads (all in flight)
+  __syncthreads();
+  for (int q = tid(); q < 5 * 64; q += blockDim.x) {
+    const int b = q >> 6, e = q & 63;
+    const double* src = b == 0 ? st->Gcc : b == 1 ? st->Goc : b == 2 ? st->GoW : b == 3 ? st->Goo : st->So;
+    double* dst = b == 0 ? Gcc : b == 1 ? Goc : b == 2 ? GoW : b == 3 ? Goo : So;
+    dst[e] = src[e];
+  }
   extract_block(total, 0, s, GcW);
   extract_block(total, s, s, GWW);
   const int j = st->step + 1;        // 1-based step being solved
   const int has_old = st->has_old;
   // 1. lazy CholQR2 correction of the current block: Gcc = R2^T R2, Sc = R2^-1
-  if (tid() == 0) {
+  {
     double mr;
-    s_flag = chol_upper(Gcc, X, s, &mr);
-    if (!s_flag) inv_upper(X, Sc, s);
+    if (tid() == 0) s_flag = 0;
+    const int bad = chol_inv_par(Gcc, X, Sc, s, &mr);
+    if (tid() == 0) s_flag = bad;
   }
   __syncthreads();
   if (s_flag) {  // the stored block is not numerically full rank
@@ -377,19 +451,15 @@ __device__ __noinline__ void coef_solve(const double* total, DevState* st, const
     return;
   }
   // 7. Cholesky QR of the residual block
-  if (tid() == 0) {
+  {
     double mr = 0.0;
-    int bad = chol_upper(U, X, s, &mr);
-    if (bad || mr < 1e-5) {
-      s_flag = 1;
-    } else {
-      s_flag = 0;
-      inv_upper(X, Y, s);
-      for (int q = 0; q < 64; ++q) {
-        st->R1prev[q] = X[q];
-        T.tau1[(int64_t)(j - 1) * 64 + q] = X[q];
-      }
+    const int bad = chol_inv_par(U, X, Y, s, &mr);
+    const int fail = bad || mr < 1e-5;
+    if (!fail && tid() < 64) {
+      st->R1prev[tid()] = X[tid()];
+      T.tau1[(int64_t)(j - 1) * 64 + tid()] = X[tid()];
     }
+    if (tid() == 0) s_flag = fail;
   }
   __syncthreads();
   if (s_flag) {
@@ -572,21 +642,54 @@ __device__ void finish_reduction(const double (&acc)[MP / 8][2], double* sX, dou
   }
   __threadfence();
   __syncthreads();
+  // Two-level deterministic grid reduction: the last CTA to finish in each
+  // group of RG consecutive CTAs sums the group's partials in CTA order; the
+  // last group to finish sums the group totals in group order.  The order of
+  // every addition is fixed by the grid shape, never by arrival order (pass 2
+  // reproduces pass 1 bit for bit), and each tail reads at most RG partials
+  // with all loads in flight (a single-CTA sweep over ~1000 partials cost
+  // 100+ us of one SM while the rest of the GPU idled).
+  constexpr int RG = 32;
   __shared__ unsigned s_last;
-  if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+  const int ngroups = (gridDim.x + RG - 1) / RG;
+  const int grp = blockIdx.x / RG;
+  const int g0 = grp * RG, gn = min(RG, (int)gridDim.x - g0);
+  if (threadIdx.x == 0) {
+    s_last = (atomicAdd(ticket + 1 + grp, 1u) == (unsigned)gn - 1) ? 1u : 0u;
+    if (s_last) ticket[1 + grp] = 0u;
+  }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // deterministic grid reduction: warp w owns entries e = w, w+4, ...; lanes
-  // stride over CTAs, then a fixed xor tree
+  double* gpart = partials + (int64_t)gridDim.x * NE;
+  for (int e = threadIdx.x; e < NE; e += blockDim.x) {
+    const double* src = partials + (int64_t)g0 * NE + e;
+    double v[RG];
+#pragma unroll
+    for (int b = 0; b < RG; ++b) v[b] = b < gn ? __ldcg(src + (int64_t)b * NE) : 0.0;
+    double sum = v[0];
+#pragma unroll
+    for (int b = 1; b < RG; ++b) sum += v[b];
+    gpart[(int64_t)grp * NE + e] = sum;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == (unsigned)ngroups - 1) ? 1u : 0u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
   double* total = sX;  // reuse: NE doubles
   __syncthreads();
-  for (int e = warp; e < NE; e += 4) {
-    double v = 0.0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) v += __ldcg(partials + (int64_t)b * NE + e);
+  for (int e = threadIdx.x; e < NE; e += blockDim.x) {
+    double sum = 0.0;
+    for (int b0 = 0; b0 < ngroups; b0 += 16) {
+      double v[16];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    if (lane == 0) total[e] = v;
+      for (int b = 0; b < 16; ++b) v[b] = b0 + b < ngroups ? __ldcg(gpart + (int64_t)(b0 + b) * NE + e) : 0.0;
+#pragma unroll
+      for (int b = 0; b < 16; ++b) sum += v[b];
+    }
+    total[e] = sum;
   }
   for (int e = NE + threadIdx.x; e < 256; e += blockDim.x) total[e] = 0.0;
   __syncthreads();
@@ -667,9 +770,9 @@ __device__ __forceinline__ void warp_gram(const double* sX, int r0, int x0, int 
 #pragma unroll
   for (int ks = 0; ks < 8; ++ks) {
     const int k = r0 + ks * 4 + t;
-    const double b = sX[(y0 + g) * LDP + k];
+    const double b = sX[CB(y0 + g) + k];
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][0], acc[mt][1], sX[(x0 + mt * 8 + g) * LDP + k], b);
+    for (int mt = 0; mt < MT; ++mt) dmma(acc[mt][0], acc[mt][1], sX[CB(x0 + mt * 8 + g) + k], b);
   }
 }
 
@@ -739,14 +842,14 @@ __device__ __forceinline__ void stage_warp_coop(const OpDev& op, const double* _
     }
     const int c0 = 2 * cp;
     if (col_o >= 0) {
-      sX[(col_o + c0) * LDP + row] = o.x;
-      sX[(col_o + c0 + 1) * LDP + row] = o.y;
+      sX[CB(col_o + c0) + row] = o.x;
+      sX[CB(col_o + c0 + 1) + row] = o.y;
     }
-    sX[(col_c + c0) * LDP + row] = v.x;
-    sX[(col_c + c0 + 1) * LDP + row] = v.y;
+    sX[CB(col_c + c0) + row] = v.x;
+    sX[CB(col_c + c0 + 1) + row] = v.y;
     if (col_w >= 0) {
-      sX[(col_w + c0) * LDP + row] = w.x;
-      sX[(col_w + c0 + 1) * LDP + row] = w.y;
+      sX[CB(col_w + c0) + row] = w.x;
+      sX[CB(col_w + c0 + 1) + row] = w.y;
     }
   }
 }
@@ -776,14 +879,14 @@ __global__ void __launch_bounds__(TP, COOP ? 5 : 2) k_combine(OpDev op, CombineC
     if (kk < 3 * S && g < S) v = st->M[(kk / S) * 64 + (kk % S) * 8 + g];
     bM[ks] = v;
   }
-  for (int e = 0; e < XC; ++e) sX[e * LDP + threadIdx.x] = 0.0;
+  for (int e = 0; e < XC; ++e) sX[CB(e) + threadIdx.x] = 0.0;
   double acc[MTG][2];
 #pragma unroll
   for (int mt = 0; mt < MTG; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
   __syncthreads();
   const int64_t ntiles = (c.n + TP - 1) / TP;
   const int r0 = warp * 32;
-  double* row = sX + threadIdx.x;   // column q at row[q * LDP]
+  double* row = sX + threadIdx.x;   // column q at row[CB(q)]
   constexpr bool coop = COOP && (S % 2 == 0);
   // interleaved tile order: the active tiles form a compact wavefront, so the
   // +-nx*ny neighbour planes of a tile are in L2 (streamed as centre rows by
@@ -798,7 +901,7 @@ __global__ void __launch_bounds__(TP, COOP ? 5 : 2) k_combine(OpDev op, CombineC
         double vn[S];
         load_vec<S>(c.vn + i64 * c.ldn, vn);
 #pragma unroll
-        for (int a = 0; a < S; ++a) row[(3 * S + a) * LDP] = vn[a];
+        for (int a = 0; a < S; ++a) row[CB(3 * S + a)] = vn[a];
       }
     } else if (i64 < c.n) {
       const int i = (int)i64;
@@ -806,10 +909,10 @@ __global__ void __launch_bounds__(TP, COOP ? 5 : 2) k_combine(OpDev op, CombineC
         double vo[S];
         load_vec<S>(c.vo + i64 * c.ldo, vo);
 #pragma unroll
-        for (int a = 0; a < S; ++a) row[a * LDP] = vo[a];
+        for (int a = 0; a < S; ++a) row[CB(a)] = vo[a];
       } else {
 #pragma unroll
-        for (int a = 0; a < S; ++a) row[a * LDP] = 0.0;
+        for (int a = 0; a < S; ++a) row[CB(a)] = 0.0;
       }
       double vc[S], w[S];
       load_vec<S>(c.vc + i64 * c.ldc, vc);
@@ -821,18 +924,18 @@ __global__ void __launch_bounds__(TP, COOP ? 5 : 2) k_combine(OpDev op, CombineC
       }
 #pragma unroll
       for (int a = 0; a < S; ++a) {
-        row[(S + a) * LDP] = vc[a];
-        row[(2 * S + a) * LDP] = w[a];
+        row[CB(S + a)] = vc[a];
+        row[CB(2 * S + a)] = w[a];
       }
       if (!c.write_new) {
         double vn[S];
         load_vec<S>(c.vn + i64 * c.ldn, vn);
 #pragma unroll
-        for (int a = 0; a < S; ++a) row[(3 * S + a) * LDP] = vn[a];
+        for (int a = 0; a < S; ++a) row[CB(3 * S + a)] = vn[a];
       }
     } else {
 #pragma unroll
-      for (int a = 0; a < 4 * S; ++a) row[a * LDP] = 0.0;
+      for (int a = 0; a < 4 * S; ++a) row[CB(a)] = 0.0;
     }
     __syncwarp();
     if (c.write_new) {
@@ -842,12 +945,12 @@ __global__ void __launch_bounds__(TP, COOP ? 5 : 2) k_combine(OpDev op, CombineC
         double d0 = 0.0, d1 = 0.0;
         const int pr = r0 + mt * 8 + g;   // A row = point
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) dmma(d0, d1, sX[(4 * ks + t) * LDP + pr], bM[ks]);
+        for (int ks = 0; ks < KS; ++ks) dmma(d0, d1, sX[CB(4 * ks + t) + pr], bM[ks]);
         const int64_t pi = tile * TP + pr;
         const int c0 = 2 * t;
         if (c0 < S) {
-          sX[(3 * S + c0) * LDP + pr] = d0;
-          if (c0 + 1 < S) sX[(3 * S + c0 + 1) * LDP + pr] = d1;
+          sX[CB(3 * S + c0) + pr] = d0;
+          if (c0 + 1 < S) sX[CB(3 * S + c0 + 1) + pr] = d1;
           if (pi < c.n) {
             double* dst = c.vn + pi * c.ldn + c0;
             if constexpr (S % 2 == 0) {
@@ -876,7 +979,7 @@ __global__ void __launch_bounds__(TP, COOP ? 8 : 2) k_apply_gram(OpDev op, Apply
   constexpr int MT = cdiv(NG * S, 8);
   constexpr int MP = 8 * MT;
   __shared__ __align__(16) double sX[cmax(XC, 9) * LDP];
-  for (int e = 0; e < XC; ++e) sX[e * LDP + threadIdx.x] = 0.0;
+  for (int e = 0; e < XC; ++e) sX[CB(e) + threadIdx.x] = 0.0;
   double acc[MT][2];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
@@ -898,16 +1001,16 @@ __global__ void __launch_bounds__(TP, COOP ? 8 : 2) k_apply_gram(OpDev op, Apply
       double v[S];
       load_vec<S>(c.v + i64 * c.ldv, v);
 #pragma unroll
-      for (int a = 0; a < S; ++a) row[a * LDP] = v[a];
+      for (int a = 0; a < S; ++a) row[CB(a)] = v[a];
       if constexpr (USE_OP) {
         double w[S];
         stencil_fast<S>(op, c.v, c.ldv, (int)i64, v, w);
 #pragma unroll
-        for (int a = 0; a < S; ++a) row[(S + a) * LDP] = w[a];
+        for (int a = 0; a < S; ++a) row[CB(S + a)] = w[a];
       }
     } else {
 #pragma unroll
-      for (int a = 0; a < NG * S; ++a) row[a * LDP] = 0.0;
+      for (int a = 0; a < NG * S; ++a) row[CB(a)] = 0.0;
     }
     __syncwarp();
     warp_gram<MT>(sX, r0, 0, (NG - 1) * S, acc);
@@ -925,7 +1028,7 @@ __global__ void __launch_bounds__(TP) k_pair_gram(const double* x, int64_t ldx, 
   constexpr int MP = (W + 7) / 8 * 8;
   constexpr int MT = MP / 8;
   __shared__ __align__(16) double sX[XCOLS * LDP];
-  for (int e = 0; e < XCOLS; ++e) sX[e * LDP + threadIdx.x] = 0.0;
+  for (int e = 0; e < XCOLS; ++e) sX[CB(e) + threadIdx.x] = 0.0;
   double acc[MT][2];
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) acc[mt][0] = acc[mt][1] = 0.0;
@@ -934,19 +1037,19 @@ __global__ void __launch_bounds__(TP) k_pair_gram(const double* x, int64_t ldx, 
   const int warp = threadIdx.x >> 5;
   for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
     const int64_t i64 = it * TP + threadIdx.x;
-    double* row = sX + threadIdx.x;   // column c at row[c * LDP]
+    double* row = sX + threadIdx.x;   // column c at row[CB(c)]
     if (i64 < n) {
       double v[S], w[S];
       load_vec<S>(x + i64 * ldx, v);
       load_vec<S>(y + i64 * ldy, w);
 #pragma unroll
       for (int a = 0; a < S; ++a) {
-        row[(a) * LDP] = v[a];
-        row[(S + a) * LDP] = w[a];
+        row[CB(a)] = v[a];
+        row[CB(S + a)] = w[a];
       }
     } else {
 #pragma unroll
-      for (int a = 0; a < W; ++a) row[(a) * LDP] = 0.0;
+      for (int a = 0; a < W; ++a) row[CB(a)] = 0.0;
     }
     __syncthreads();
     tile_gram<MT>(sX, warp * 32, S, acc);
