@@ -94,8 +94,19 @@ __device__ double block_sum(double v) {
 }
 
 // ------------------------------------------------------------------ E1: coupling + deflation (1 CTA x 1024)
+// The per-pole work arrays (z, candidate list, flags) live in shared memory
+// when they fit (SM = true): the passes below are chains of dependent
+// accesses, and each global round trip costs ~1 us on this single CTA.
+template <bool SM>
 __global__ void __launch_bounds__(1024) k_eig_deflate(EigView e, int K, const double* dsym_blk,
                                                       const double* sub_prev, int a) {
+  extern __shared__ double dyn_sm[];
+  if (SM) {
+    e.z = dyn_sm;
+    e.cand = reinterpret_cast<int*>(dyn_sm + K);
+    e.dflag = e.cand + K;
+    e.pflag = e.dflag + K;
+  }
   const int s = e.s;
   __shared__ double t[KRY_SMAX];
   __shared__ double s_d, s_tol;
@@ -248,19 +259,48 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// ------------------------------------------------------------------ E2: secular roots (warp per root)
+// ------------------------------------------------------------------ E2: secular roots (CTA per root)
 // h(mu) = mu - d - sum_j z_j^2 / (mu - lam_j); root i lies in (lam_{i-1}, lam_i)
 // (i = 0 / p: below / above all poles).  tau = mu - origin with the origin at
 // the nearer pole; rational two-pole model step (LAPACK dlaed4 style) with a
-// bisection safeguard.  Lanes split the poles; all lanes iterate in lockstep.
-__global__ void __launch_bounds__(256) k_eig_secular(EigView e) {
+// bisection safeguard.  One CTA of NT = 32 W threads per root: the sums over
+// the poles are split NT ways (two independent accumulator sets per thread)
+// and reduced in a fixed order, so every thread holds bit-identical sums and
+// runs the (uniform) iteration logic redundantly.  The first version used
+// one warp per root: ~50 serially dependent terms per lane per iteration,
+// ~10 warps per SM, 48 us per call at K = 1600 (ncu); this is latency-bound
+// work, so it wants short chains and many warps.
+template <int W>
+__device__ __forceinline__ void block_sum5(double (&v)[5], double (*red)[W][5]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < 5; ++q) v[q] = warp_sum(v[q]);
+  if (W == 1) return;
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < 5; ++q) (*red)[warp][q] = v[q];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    double t = (*red)[0][q];
+#pragma unroll
+    for (int w = 1; w < W; ++w) t += (*red)[w][q];
+    v[q] = t;
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(32 * W) k_eig_secular(EigView e) {
+  constexpr int NT = 32 * W;
+  __shared__ double red[2][W][5];   // double-buffered: one barrier per reduction
   const int p = e.counts[0];
-  const int lane = threadIdx.x & 31;
-  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int i = blockIdx.x;
   if (i > p) return;
+  const int tid = threadIdx.x;
   const double d = e.scal[0];
   if (p == 0) {
-    if (lane == 0) { e.org[0] = d; e.tau[0] = 0.0; e.mu[0] = d; }
+    if (tid == 0) { e.org[0] = d; e.tau[0] = 0.0; e.mu[0] = d; }
     return;
   }
   const double* __restrict__ poles = e.poles;
@@ -268,6 +308,7 @@ __global__ void __launch_bounds__(256) k_eig_secular(EigView e) {
   const double zabs = e.scal[2];
   const double lo = fmin(poles[0], d) - zabs - 1e-300;
   const double hi = fmax(poles[p - 1], d) + zabs + 1e-300;
+  int rb = 0;
   double org;
   int ia, ib;
   if (i == 0) {
@@ -277,12 +318,20 @@ __global__ void __launch_bounds__(256) k_eig_secular(EigView e) {
   } else {
     const double a = poles[i - 1], b = poles[i];
     const double mid = 0.5 * (a + b);
-    double hm = 0.0;
-    for (int j = lane; j < p; j += 32) {
+    double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int j = tid; j < p; j += 2 * NT) {
       const double zj = zz[j];
-      hm -= zj * zj * frcp(mid - poles[j]);
+      v[0] -= zj * zj * frcp(mid - poles[j]);
+      if (j + NT < p) {
+        const double zk = zz[j + NT];
+        v[1] -= zk * zk * frcp(mid - poles[j + NT]);
+      }
     }
-    hm = warp_sum(hm) + (mid - d);
+    v[0] += v[1];
+    v[1] = 0.0;
+    block_sum5<W>(v, &red[rb]);
+    rb ^= 1;
+    const double hm = v[0] + (mid - d);
     org = (hm > 0.0) ? a : b;
     ia = i - 1; ib = i;
   }
@@ -294,20 +343,36 @@ __global__ void __launch_bounds__(256) k_eig_secular(EigView e) {
   const double c0 = org - d;
   const bool near_left = (ia >= 0) && (org == poles[ia]);
   for (int it = 0; it < 80; ++it) {
-    double psiL = 0.0, dpsiL = 0.0, psiR = 0.0, dpsiR = 0.0, sabs = 0.0;
-    for (int j = lane; j < p; j += 32) {
-      const double zj = zz[j];
-      const double q = t - (poles[j] - org);
-      const double r = frcp(q);
-      const double term = zj * zj * r;
-      const double dterm = term * r;
-      if (j <= ia) { psiL -= term; dpsiL += dterm; }
-      else { psiR -= term; dpsiR += dterm; }
-      sabs += fabs(term);
+    // v = {psiL, dpsiL, psiR, dpsiR, sabs}; two accumulator sets for ILP
+    double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0}, u[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int j = tid; j < p; j += 2 * NT) {
+      {
+        const double zj = zz[j];
+        const double r = frcp(t - (poles[j] - org));
+        const double term = zj * zj * r;
+        const double dterm = term * r;
+        const bool left = j <= ia;
+        v[0] -= left ? term : 0.0; v[1] += left ? dterm : 0.0;
+        v[2] -= left ? 0.0 : term; v[3] += left ? 0.0 : dterm;
+        v[4] += fabs(term);
+      }
+      const int k = j + NT;
+      if (k < p) {
+        const double zk = zz[k];
+        const double r = frcp(t - (poles[k] - org));
+        const double term = zk * zk * r;
+        const double dterm = term * r;
+        const bool left = k <= ia;
+        u[0] -= left ? term : 0.0; u[1] += left ? dterm : 0.0;
+        u[2] -= left ? 0.0 : term; u[3] += left ? 0.0 : dterm;
+        u[4] += fabs(term);
+      }
     }
-    psiL = warp_sum(psiL); dpsiL = warp_sum(dpsiL);
-    psiR = warp_sum(psiR); dpsiR = warp_sum(dpsiR);
-    sabs = warp_sum(sabs);
+#pragma unroll
+    for (int q = 0; q < 5; ++q) v[q] += u[q];
+    block_sum5<W>(v, &red[rb]);
+    rb ^= 1;
+    const double psiL = v[0], dpsiL = v[1], psiR = v[2], dpsiR = v[3], sabs = v[4];
     const double h = t + c0 + psiL + psiR;
     const double err = 8.0 * EPS * (fabs(t) + fabs(c0) + sabs);
     if (h > 0.0) tb = t; else ta = t;
@@ -349,32 +414,50 @@ __global__ void __launch_bounds__(256) k_eig_secular(EigView e) {
     if (fabs(tn - t) <= 4.0 * EPS * fabs(t)) { t = tn; break; }
     t = tn;
   }
-  if (lane == 0) {
+  if (tid == 0) {
     e.org[i] = org;
     e.tau[i] = t;
     e.mu[i] = org + t;
   }
 }
 
-// ------------------------------------------------------------------ E3: Gu-Eisenstat zhat (warp per pole)
+// ------------------------------------------------------------------ E3: Gu-Eisenstat zhat (CTA per pole)
 // zhat_j^2 = |lam_j - mu_j| |lam_j - mu_{j+1}| prod_{i<j} |lam_j - mu_i|/|lam_j - lam_i|
-//            prod_{i>j} |lam_j - mu_{i+1}|/|lam_j - lam_i|   (all ratios > 1)
-__global__ void __launch_bounds__(256) k_eig_zhat(EigView e) {
+//            prod_{i>j} |lam_j - mu_{i+1}|/|lam_j - lam_i|
+// Each thread multiplies two interleaved partial products; fixed-order
+// combination across lanes and warps.
+template <int W>
+__global__ void __launch_bounds__(32 * W) k_eig_zhat(EigView e) {
+  constexpr int NT = 32 * W;
+  __shared__ double red[W];
   const int p = e.counts[0];
-  const int lane = threadIdx.x & 31;
-  const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int j = blockIdx.x;
   if (j >= p) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double lj = e.poles[j];
-  double prod = 1.0;
-  for (int i = lane; i < p; i += 32) {
-    if (i == j) continue;
-    const int ir = (i < j) ? i : i + 1;
-    const double num = fabs((lj - e.org[ir]) - e.tau[ir]);
-    prod *= num * frcp(fabs(lj - e.poles[i]));
+  double p0 = 1.0, p1 = 1.0;
+  for (int i = tid; i < p; i += 2 * NT) {
+    if (i != j) {
+      const int ir = (i < j) ? i : i + 1;
+      p0 *= fabs((lj - e.org[ir]) - e.tau[ir]) * frcp(fabs(lj - e.poles[i]));
+    }
+    const int k = i + NT;
+    if (k < p && k != j) {
+      const int kr = (k < j) ? k : k + 1;
+      p1 *= fabs((lj - e.org[kr]) - e.tau[kr]) * frcp(fabs(lj - e.poles[k]));
+    }
   }
+  double prod = p0 * p1;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) prod *= __shfl_xor_sync(0xffffffffu, prod, o);
-  if (lane == 0) {
+  if (W > 1) {
+    if (lane == 0) red[warp] = prod;
+    __syncthreads();
+    prod = red[0];
+#pragma unroll
+    for (int w = 1; w < W; ++w) prod *= red[w];
+  }
+  if (tid == 0) {
     const double a = fabs((lj - e.org[j]) - e.tau[j]);
     const double b = fabs((lj - e.org[j + 1]) - e.tau[j + 1]);
     const double zh = sqrt(prod * a * b);
@@ -389,7 +472,7 @@ __global__ void __launch_bounds__(256) k_eig_zhat(EigView e) {
 // Stage 2 (k_eig_vec_finish): fixed-order sum over chunks, normalisation,
 //   merge into sorted order; deflated columns copied unchanged.
 #define E4_RT 128   // roots per CTA
-#define E4_CH 128   // poles per chunk
+#define E4_CH 64    // poles per chunk (more CTAs: this stage is latency-bound)
 __device__ __forceinline__ int count_le(const double* a, int n, double v) {  // # a[k] <= v
   int lo = 0, hi = n;
   while (lo < hi) {
@@ -417,15 +500,16 @@ __global__ void __launch_bounds__(E4_RT) k_eig_vec_partial(EigView e, double* pa
   __shared__ double sP[E4_CH], sZ[E4_CH];
   __shared__ double sF[S][E4_CH];
   __shared__ double sL[S][E4_CH];
-  const int jj = c0 + threadIdx.x;
-  if (jj < p) {
-    sP[threadIdx.x] = e.poles[jj];
-    sZ[threadIdx.x] = e.zhat[jj];
+  for (int q = threadIdx.x; q < E4_CH; q += blockDim.x) {
+    const int jj = c0 + q;
+    if (jj >= p) break;
+    sP[q] = e.poles[jj];
+    sZ[q] = e.zhat[jj];
     const int col = e.pmap[jj];
 #pragma unroll
-    for (int r = 0; r < S; ++r) sF[r][threadIdx.x] = e.F_old[r * km + col];
+    for (int r = 0; r < S; ++r) sF[r][q] = e.F_old[r * km + col];
 #pragma unroll
-    for (int r = 0; r < S - 1; ++r) sL[r][threadIdx.x] = e.L_old[(r + 1) * km + col];
+    for (int r = 0; r < S - 1; ++r) sL[r][q] = e.L_old[(r + 1) * km + col];
   }
   __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -451,9 +535,16 @@ __global__ void __launch_bounds__(E4_RT) k_eig_vec_partial(EigView e, double* pa
   for (int r = 0; r < S - 1; ++r) out[1 + S + r] = aL[r];
 }
 
+// Stage 2: thread per (root, value); the 2S values of a root sit in 2S
+// consecutive lanes, so the chunk sums are coalesced and all chunk loads of
+// a thread are independent (the first version had one thread per root
+// walking 16 values x all chunks: 26 CTAs, 22 us of pure latency at K=1600).
 template <int S>
 __global__ void __launch_bounds__(128) k_eig_vec_finish(EigView e, const double* part,
                                                         int nroot_cap, int K, int root_blocks) {
+  constexpr int NV = 2 * S;
+  constexpr int NVP = NV <= 2 ? 2 : NV <= 4 ? 4 : NV <= 8 ? 8 : 16;   // lanes per root (pow2)
+  constexpr int RPB = 128 / NVP;
   const int p = e.counts[0];
   const int nd = e.counts[1];
   const int64_t km = e.kmax;
@@ -473,27 +564,40 @@ __global__ void __launch_bounds__(128) k_eig_vec_finish(EigView e, const double*
     if (K < S) e.F_new[K * km + pos] = 0.0;
     return;
   }
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i > p) return;
+  const int i = blockIdx.x * RPB + (int)threadIdx.x / NVP;
+  const int q = (int)threadIdx.x % NVP;
+  const bool valid = q < NV && i <= p;
   const int nch = (p + E4_CH - 1) / E4_CH;
-  double acc[2 * S];
-#pragma unroll
-  for (int q = 0; q < 2 * S; ++q) acc[q] = 0.0;
-  for (int c = 0; c < nch; ++c) {
-    const double* src = part + ((int64_t)c * nroot_cap + i) * (2 * S);
-#pragma unroll
-    for (int q = 0; q < 2 * S; ++q) acc[q] += src[q];
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (valid) {
+    const double* src = part + (int64_t)i * NV + q;
+    const int64_t cs = (int64_t)nroot_cap * NV;
+    int c = 0;
+    for (; c + 4 <= nch; c += 4) {
+      a0 += __ldcg(src + c * cs);
+      a1 += __ldcg(src + (c + 1) * cs);
+      a2 += __ldcg(src + (c + 2) * cs);
+      a3 += __ldcg(src + (c + 3) * cs);
+    }
+    for (; c < nch; ++c) a0 += __ldcg(src + c * cs);
   }
-  const double inv = 1.0 / sqrt(1.0 + acc[0]);
+  const double acc = (a0 + a1) + (a2 + a3);
+  // the group's nrm2 (q == 0); groups never straddle a warp (NVP divides 32)
+  const int lane = threadIdx.x & 31;
+  const double nrm = __shfl_sync(0xffffffffu, acc, lane - q);
+  if (!valid) return;
+  const double inv = 1.0 / sqrt(1.0 + nrm);
   const double mu = e.mu[i];
   const int pos = i + count_le(e.def_lam, nd, mu);
-  e.lam_new[pos] = mu;
-#pragma unroll
-  for (int r = 0; r < S; ++r) e.F_new[r * km + pos] = acc[1 + r] * inv;
-#pragma unroll
-  for (int r = 0; r < S - 1; ++r) e.L_new[r * km + pos] = acc[1 + S + r] * inv;
-  e.L_new[(S - 1) * km + pos] = inv;
-  if (K < S) e.F_new[K * km + pos] = inv;
+  if (q == 0) {
+    e.lam_new[pos] = mu;
+    e.L_new[(S - 1) * km + pos] = inv;
+  } else if (q <= S) {
+    // row K of Q is the new unit row while K < S (it is one of the first S rows)
+    e.F_new[(q - 1) * km + pos] = (q - 1 == K) ? inv : acc * inv;
+  } else {
+    e.L_new[(q - 1 - S) * km + pos] = acc * inv;
+  }
 }
 
 // ------------------------------------------------------------------ residual kernels
@@ -519,68 +623,88 @@ __global__ void k_uw(const double* F, const double* L, int64_t km, int k, int s,
   }
 }
 
-// out_x = sum_y (a_x . b_y) / (lx_x + ly_y) c_y ; partial sums of |out_x|^2 and
-// min |lx + ly|; the last CTA writes res[0] = sum, res[1] = min denominator
+// out_x = sum_y (a_x . b_y) / (lx_x + ly_y) c_y, res[0] = sum_x |out_x|^2,
+// res[1] = min |lx + ly|.  Stage 1 splits BOTH x and y over CTAs (grid
+// x-tiles x y-chunks; the first version split only x: 16 CTAs at k = 2056,
+// 119 us per check) and writes partial out_x per y-chunk; stage 2 sums the
+// chunks in a fixed order per x and reduces |out_x|^2 with a last-CTA tail.
 #define CC_CH 128
 template <int S>
-__global__ void __launch_bounds__(128) k_cauchy(int nx, const double* lx, const double* ax,
-                                                int ny, const double* ly, const double* by,
-                                                const double* cy, double* partials,
-                                                unsigned* ticket, double* res) {
+__global__ void __launch_bounds__(128) k_cauchy_part(int nx, const double* lx, const double* ax,
+                                                     int ny, const double* ly, const double* by,
+                                                     const double* cy, double* part, double* pmin) {
   __shared__ double sl[CC_CH], sb[CC_CH][S], sc[CC_CH][S];
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y0 = blockIdx.y * CC_CH;
   const bool active = x < nx;
   double a[S], acc[S];
   double lxx = 0.0;
 #pragma unroll
   for (int q = 0; q < S; ++q) { a[q] = active ? ax[(int64_t)x * 8 + q] : 0.0; acc[q] = 0.0; }
   if (active) lxx = lx[x];
-  double mind = 1e300;
-  for (int c0 = 0; c0 < ny; c0 += CC_CH) {
-    __syncthreads();
-    const int yy = c0 + threadIdx.x;
-    if (yy < ny) {
-      sl[threadIdx.x] = ly[yy];
+  const int yy = y0 + threadIdx.x;
+  if (yy < ny) {
+    sl[threadIdx.x] = ly[yy];
 #pragma unroll
-      for (int q = 0; q < S; ++q) {
-        sb[threadIdx.x][q] = by[(int64_t)yy * 8 + q];
-        sc[threadIdx.x][q] = cy[(int64_t)yy * 8 + q];
-      }
-    }
-    __syncthreads();
-    const int cnt = min(CC_CH, ny - c0);
-    if (active) {
-      for (int q = 0; q < cnt; ++q) {
-        double dot = 0.0;
-#pragma unroll
-        for (int r = 0; r < S; ++r) dot = fma(a[r], sb[q][r], dot);
-        const double den = lxx + sl[q];
-        mind = fmin(mind, fabs(den));
-        const double gq = dot / den;
-#pragma unroll
-        for (int r = 0; r < S; ++r) acc[r] = fma(gq, sc[q][r], acc[r]);
-      }
+    for (int q = 0; q < S; ++q) {
+      sb[threadIdx.x][q] = by[(int64_t)yy * 8 + q];
+      sc[threadIdx.x][q] = cy[(int64_t)yy * 8 + q];
     }
   }
-  double ss = 0.0;
+  __syncthreads();
+  double mind = 1e300;
+  const int cnt = min(CC_CH, ny - y0);
+  if (active) {
+    for (int q = 0; q < cnt; ++q) {
+      double dot = 0.0;
 #pragma unroll
-  for (int r = 0; r < S; ++r) ss = fma(acc[r], acc[r], ss);
-  // block reduction (fixed order)
-  __shared__ double rs[128], rm[128];
+      for (int r = 0; r < S; ++r) dot = fma(a[r], sb[q][r], dot);
+      const double den = lxx + sl[q];
+      mind = fmin(mind, fabs(den));
+      const double gq = dot / den;
+#pragma unroll
+      for (int r = 0; r < S; ++r) acc[r] = fma(gq, sc[q][r], acc[r]);
+    }
+    double* o = part + ((int64_t)blockIdx.y * nx + x) * 8;
+#pragma unroll
+    for (int r = 0; r < S; ++r) o[r] = acc[r];
+  }
+  // per-CTA min denominator
+  __shared__ double rm[4];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mind = fmin(mind, __shfl_xor_sync(0xffffffffu, mind, o));
+  if ((threadIdx.x & 31) == 0) rm[threadIdx.x >> 5] = mind;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    pmin[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = fmin(fmin(rm[0], rm[1]), fmin(rm[2], rm[3]));
+}
+
+template <int S>
+__global__ void __launch_bounds__(128) k_cauchy_sum(int nx, int nyc, int nmin, const double* part,
+                                                    const double* pmin, double* partials,
+                                                    unsigned* ticket, double* res) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  double ss = 0.0;
+  if (x < nx) {
+    double acc[S];
+#pragma unroll
+    for (int r = 0; r < S; ++r) acc[r] = 0.0;
+    for (int c = 0; c < nyc; ++c) {
+      const double* o = part + ((int64_t)c * nx + x) * 8;
+#pragma unroll
+      for (int r = 0; r < S; ++r) acc[r] += __ldcg(o + r);
+    }
+#pragma unroll
+    for (int r = 0; r < S; ++r) ss = fma(acc[r], acc[r], ss);
+  }
+  __shared__ double rs[128];
   rs[threadIdx.x] = ss;
-  rm[threadIdx.x] = mind;
   __syncthreads();
   for (int o = 64; o > 0; o >>= 1) {
-    if (threadIdx.x < o) {
-      rs[threadIdx.x] += rs[threadIdx.x + o];
-      rm[threadIdx.x] = fmin(rm[threadIdx.x], rm[threadIdx.x + o]);
-    }
+    if (threadIdx.x < o) rs[threadIdx.x] += rs[threadIdx.x + o];
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    partials[2 * blockIdx.x] = rs[0];
-    partials[2 * blockIdx.x + 1] = rm[0];
-  }
+  if (threadIdx.x == 0) partials[blockIdx.x] = rs[0];
   __threadfence();
   __syncthreads();
   __shared__ unsigned s_last;
@@ -590,10 +714,8 @@ __global__ void __launch_bounds__(128) k_cauchy(int nx, const double* lx, const 
   __threadfence();
   if (threadIdx.x == 0) {
     double tot = 0.0, mn = 1e300;
-    for (unsigned b = 0; b < gridDim.x; ++b) {
-      tot += __ldcg(partials + 2 * b);
-      mn = fmin(mn, __ldcg(partials + 2 * b + 1));
-    }
+    for (unsigned b = 0; b < gridDim.x; ++b) tot += __ldcg(partials + b);
+    for (int b = 0; b < nmin; ++b) mn = fmin(mn, __ldcg(pmin + b));
     res[0] = tot;
     res[1] = mn;
     *ticket = 0u;
@@ -601,6 +723,9 @@ __global__ void __launch_bounds__(128) k_cauchy(int nx, const double* lx, const 
 }
 
 // ------------------------------------------------------------------ host side
+static constexpr int fin_rpb(int S) {
+  return 128 / (2 * S <= 2 ? 2 : 2 * S <= 4 ? 4 : 2 * S <= 8 ? 8 : 16);
+}
 int EigEngine::init(int s_, int kmax_, int device) {
   s = s_;
   kmax = kmax_ + 8;
@@ -617,9 +742,12 @@ int EigEngine::init(int s_, int kmax_, int device) {
   doubles += 16;                  // scal
   doubles += 4096;                // partials
   doubles += 16;                  // res
-  const size_t nch_max = (nk + 127) / 128 + 1;
+  const size_t nch_max = (nk + E4_CH - 1) / E4_CH + 1;
   const size_t vpart_n = nch_max * (nk + 8) * 16;
   doubles += vpart_n;             // E4 partial sums
+  // Cauchy stage-1 partials: [y-chunk][x][8] for x, y up to 2 kmax, + mins
+  cpart_cap = ((2 * nk + CC_CH - 1) / CC_CH + 1) * (2 * nk);
+  doubles += cpart_cap * 8 + cpart_cap / 64 + 64;
   KRY_CUDA(cudaMalloc(&dbuf, doubles * sizeof(double)));
   KRY_CUDA(cudaMemset(dbuf, 0, doubles * sizeof(double)));
   double* p = dbuf;
@@ -634,6 +762,7 @@ int EigEngine::init(int s_, int kmax_, int device) {
   partials = p; p += 4096;
   res = p; p += 16;
   vpart = p; p += vpart_n;
+  cpart = p; p += cpart_cap * 8 + cpart_cap / 64 + 64;
   size_t ints = 5 * nk + 8;
   KRY_CUDA(cudaMalloc(&ibuf, ints * sizeof(int)));
   KRY_CUDA(cudaMemset(ibuf, 0, ints * sizeof(int)));
@@ -669,25 +798,37 @@ int EigEngine::append_block(cudaStream_t st, const double* dsym_blk, const doubl
   if (K + s > kmax - 8) return fail(KRY_ERR_STATE, "eigen engine capacity exceeded");
   for (int a = 0; a < s; ++a) {
     EigView v = view();
-    k_eig_deflate<<<1, 1024, 0, st>>>(v, K, dsym_blk, sub_prev, a);
-    // K+1 roots at most, one warp each
-    const int warps_per_cta = 8;
-    const int nroot_warp_blocks = (K + 1 + warps_per_cta - 1) / warps_per_cta;
-    k_eig_secular<<<nroot_warp_blocks, 32 * warps_per_cta, 0, st>>>(v);
+    const size_t dsm = (size_t)K * (sizeof(double) + 3 * sizeof(int));
+    if (dsm <= 200 * 1024) {
+      if (!deflate_attr) {
+        KRY_CUDA(cudaFuncSetAttribute(k_eig_deflate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      200 * 1024));
+        deflate_attr = true;
+      }
+      k_eig_deflate<true><<<1, 1024, dsm, st>>>(v, K, dsym_blk, sub_prev, a);
+    } else {
+      k_eig_deflate<false><<<1, 1024, 0, st>>>(v, K, dsym_blk, sub_prev, a);
+    }
+    // K+1 roots at most, one CTA each; threads per root grow with K
+    if (K >= 1024) k_eig_secular<4><<<K + 1, 128, 0, st>>>(v);
+    else if (K >= 256) k_eig_secular<2><<<K + 1, 64, 0, st>>>(v);
+    else k_eig_secular<1><<<K + 1, 32, 0, st>>>(v);
     int nl = 2;
     if (K > 0) {
-      const int npole_warp_blocks = (K + warps_per_cta - 1) / warps_per_cta;
-      k_eig_zhat<<<npole_warp_blocks, 32 * warps_per_cta, 0, st>>>(v);
+      if (K >= 1024) k_eig_zhat<4><<<K, 128, 0, st>>>(v);
+      else if (K >= 256) k_eig_zhat<2><<<K, 64, 0, st>>>(v);
+      else k_eig_zhat<1><<<K, 32, 0, st>>>(v);
       ++nl;
     }
     const int root_blocks = (K + 1 + 127) / 128;
-    const int nch = std::max(1, (K + 127) / 128);
+    const int nch = std::max(1, (K + E4_CH - 1) / E4_CH);
     const int cap = kmax + 8;
     dim3 g1(root_blocks, nch);
     const int ndef_blocks = (K + 127) / 128;
 #define L(S)                                                                               \
   k_eig_vec_partial<S><<<g1, 128, 0, st>>>(v, vpart, cap);                                \
-  k_eig_vec_finish<S><<<root_blocks + ndef_blocks, 128, 0, st>>>(v, vpart, cap, K, root_blocks)
+  k_eig_vec_finish<S><<<(K + 1 + fin_rpb(S) - 1) / fin_rpb(S) + ndef_blocks, 128, 0, st>>>( \
+      v, vpart, cap, K, (K + 1 + fin_rpb(S) - 1) / fin_rpb(S))
     switch (s) {
       case 1: L(1); break; case 2: L(2); break; case 3: L(3); break; case 4: L(4); break;
       case 5: L(5); break; case 6: L(6); break; case 7: L(7); break; case 8: L(8); break;
@@ -704,16 +845,21 @@ int EigEngine::append_block(cudaStream_t st, const double* dsym_blk, const doubl
 
 int EigEngine::cauchy(cudaStream_t st, int nx, const double* lx, const double* ax, int ny,
                       const double* ly, const double* by, const double* cy, double* out2) {
-  int grid = (nx + 127) / 128;
-  if (grid > 2048) return fail(KRY_ERR_STATE, "residual grid too large");
-#define L(S) k_cauchy<S><<<grid, 128, 0, st>>>(nx, lx, ax, ny, ly, by, cy, partials, ticket, out2)
+  const int gx = std::max(1, (nx + 127) / 128);
+  const int nyc = std::max(1, (ny + CC_CH - 1) / CC_CH);
+  if (gx > 4096 || (size_t)nyc * nx > cpart_cap) return fail(KRY_ERR_STATE, "residual grid too large");
+  double* pmin = cpart + cpart_cap * 8;
+  dim3 g1(gx, nyc);
+#define L(S)                                                                                    \
+  k_cauchy_part<S><<<g1, 128, 0, st>>>(nx, lx, ax, ny, ly, by, cy, cpart, pmin);               \
+  k_cauchy_sum<S><<<gx, 128, 0, st>>>(nx, nyc, gx * nyc, cpart, pmin, partials, ticket, out2)
   switch (s) {
     case 1: L(1); break; case 2: L(2); break; case 3: L(3); break; case 4: L(4); break;
     case 5: L(5); break; case 6: L(6); break; case 7: L(7); break; case 8: L(8); break;
     default: return fail(KRY_ERR_ARGUMENT, "block width s must be 1..8");
   }
 #undef L
-  count_launch();
+  count_launch(2);
   KRY_CUDA(cudaGetLastError());
   return KRY_OK;
 }

@@ -17,6 +17,7 @@ struct EigView {
 
 struct EigEngine {
   int s = 0, kmax = 0, K = 0, cur = 0, dev = 0;
+  bool deflate_attr = false;
   double* dbuf = nullptr;
   int* ibuf = nullptr;
   unsigned* ticket = nullptr;
@@ -24,7 +25,8 @@ struct EigEngine {
   double *z = nullptr, *poles = nullptr, *zz = nullptr, *zhat = nullptr, *def_lam = nullptr,
          *mu = nullptr;
   double *org = nullptr, *tau = nullptr, *u = nullptr, *w = nullptr, *scal = nullptr,
-         *partials = nullptr, *res = nullptr, *vpart = nullptr;
+         *partials = nullptr, *res = nullptr, *vpart = nullptr, *cpart = nullptr;
+  size_t cpart_cap = 0;   // x-by-y-chunk entries of cpart
   int *cand = nullptr, *dflag = nullptr, *pflag = nullptr, *pmap = nullptr,
       *def_idx = nullptr, *counts = nullptr;
 
