@@ -12,6 +12,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <mutex>
+#include <thread>
 #include <vector>
 #include <algorithm>
 
@@ -200,6 +202,19 @@ __global__ void k_scale_of(const double* lx, int nx, const double* ly, int ny, d
   *out = v;
 }
 
+void keep_pool_memory(int device) {
+  static std::mutex mu;
+  static bool done[64] = {false};
+  std::lock_guard<std::mutex> lock(mu);
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = true;
+}
+
 }  // namespace kry
 
 using namespace kry;
@@ -286,17 +301,6 @@ int map_status(kry_ctx* c, const char* context) {
 }
 
 double* slotp(kry_ctx* c, int i) { return i < 0 ? nullptr : c->slot[i]; }
-
-template <class T>
-int dalloc(T** p, size_t count) {
-  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
-  if (e != cudaSuccess) {
-    *p = nullptr;
-    return fail(KRY_ERR_CUDA, std::string("cudaMalloc failed: ") + cudaGetErrorString(e) +
-                                  " (" + std::to_string(count * sizeof(T)) + " bytes)");
-  }
-  return KRY_OK;
-}
 
 // ---------------------------------------------------------------- multi-GPU plumbing
 // Row-slab sharding along the slowest grid axis: every rank owns planes
@@ -627,17 +631,53 @@ struct StageTimer {
 };
 
 
+// cuBLAS / cuSOLVER handles are pooled per device: creating them costs
+// ~0.1-0.5 s (it dominated a whole small solve), so a context checks a pair
+// out on first use and returns it on destroy (a handle is never shared by
+// two live contexts, so concurrent solves stay safe).
+struct HandlePair {
+  cublasHandle_t blas;
+  cusolverDnHandle_t solver;
+};
+static std::mutex g_handle_mu;
+static std::vector<HandlePair> g_handle_pool[64];
+
 int ensure_handles(kry_ctx* c) {
-  if (!c->cublas) {
-    if (cublasCreate(&c->cublas) != CUBLAS_STATUS_SUCCESS) return fail(KRY_ERR_CUDA, "cublasCreate failed");
-    cublasSetStream(c->cublas, c->stream);
+  if (c->cublas && c->solver) return KRY_OK;
+  HandlePair h{nullptr, nullptr};
+  {
+    std::lock_guard<std::mutex> lock(g_handle_mu);
+    auto& pool = g_handle_pool[c->dev & 63];
+    if (!pool.empty()) {
+      h = pool.back();
+      pool.pop_back();
+    }
   }
-  if (!c->solver) {
-    if (cusolverDnCreate(&c->solver) != CUSOLVER_STATUS_SUCCESS)
-      return fail(KRY_ERR_CUDA, "cusolverDnCreate failed");
-    cusolverDnSetStream(c->solver, c->stream);
+  if (!h.blas && cublasCreate(&h.blas) != CUBLAS_STATUS_SUCCESS)
+    return fail(KRY_ERR_CUDA, "cublasCreate failed");
+  if (!h.solver && cusolverDnCreate(&h.solver) != CUSOLVER_STATUS_SUCCESS) {
+    cublasDestroy(h.blas);
+    return fail(KRY_ERR_CUDA, "cusolverDnCreate failed");
   }
+  c->cublas = h.blas;
+  c->solver = h.solver;
+  cublasSetStream(c->cublas, c->stream);
+  cusolverDnSetStream(c->solver, c->stream);
   return KRY_OK;
+}
+
+static void release_handles(kry_ctx* c) {
+  if (!c->cublas || !c->solver) {
+    if (c->cublas) cublasDestroy(c->cublas);
+    if (c->solver) cusolverDnDestroy(c->solver);
+  } else {
+    cublasSetStream(c->cublas, 0);
+    cusolverDnSetStream(c->solver, 0);
+    std::lock_guard<std::mutex> lock(g_handle_mu);
+    g_handle_pool[c->dev & 63].push_back(HandlePair{c->cublas, c->solver});
+  }
+  c->cublas = nullptr;
+  c->solver = nullptr;
 }
 
 // dense symmetric eigendecomposition in place (A k x k -> eigenvectors), w ascending
@@ -655,8 +695,8 @@ int syevd(kry_ctx* c, double* A, int k, double* w) {
   int hinfo = 0;
   cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
   cudaStreamSynchronize(c->stream);
-  cudaFree(work);
-  cudaFree(info);
+  dfree(work);
+  dfree(info);
   if (stt != CUSOLVER_STATUS_SUCCESS || hinfo != 0)
     return fail(KRY_ERR_FACTORIZATION, "dense symmetric eigensolver did not converge");
   return KRY_OK;
@@ -667,9 +707,9 @@ struct FinalBufs {
   double* lam = nullptr;
   double* u = nullptr;
   void free_all() {
-    if (Td) cudaFree(Td);
-    if (lam) cudaFree(lam);
-    if (u) cudaFree(u);
+    if (Td) dfree(Td);
+    if (lam) dfree(lam);
+    if (u) dfree(u);
     Td = lam = u = nullptr;
   }
 };
@@ -690,7 +730,7 @@ int final_eig(kry_ctx* c, FinalBufs& b, int* k_out) {
 }
 
 int set_qy(kry_ctx* c, const double* Q, int k, const double* factor, int rank) {
-  if (c->qy) cudaFree(c->qy);
+  if (c->qy) dfree(c->qy);
   c->qy = nullptr;
   c->rank = rank;
   if (rank <= 0) return KRY_OK;
@@ -705,24 +745,97 @@ int set_qy(kry_ctx* c, const double* Q, int k, const double* factor, int rank) {
 
 }  // namespace
 
-// Device -> caller-owned host buffer.  Large pageable buffers are page-locked
-// for the duration of the copy so the DMA runs at link speed instead of
-// through the driver's staging buffers.
-int copy_out(kry_ctx* c, void* host, const void* dev, size_t bytes) {
-  bool reg = false;
-  if (bytes >= ((size_t)64 << 20)) {
+// Device -> caller-owned host buffer.
+//
+// The factor Z is the largest object a solve returns (c4: 8e6 x 231 doubles =
+// 14.8 GB) and lands in a freshly allocated pageable numpy array.  Page-
+// locking such a buffer (cudaHostRegister) first faults in and pins every
+// page on one thread, which cost seconds.  Instead:
+//  * prefault_begin() touches the destination pages on host threads while
+//    pass 2 still runs on the GPU (the host would only wait there);
+//  * copy_out() streams the device buffer through a ring of pinned staging
+//    chunks (cached per device) and copies each landed chunk into place with
+//    the host threads, overlapping the DMA of the next chunks.
+static int host_threads() {
+  unsigned h = std::thread::hardware_concurrency();
+  return (int)std::max(1u, std::min(h ? h : 1u, 16u));
+}
+
+struct Prefault {
+  std::vector<std::thread> th;
+  void begin(void* host, size_t bytes) {
+    if (bytes < ((size_t)256 << 20)) return;
     cudaPointerAttributes pa;
-    if (!(cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type == cudaMemoryTypeHost)) {
-      cudaGetLastError();
-      reg = cudaHostRegister(host, bytes, cudaHostRegisterDefault) == cudaSuccess;
-      if (!reg) cudaGetLastError();
+    if (cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type == cudaMemoryTypeHost) return;
+    cudaGetLastError();
+    const int T = host_threads();
+    const size_t per = (bytes / T + 4095) & ~(size_t)4095;
+    for (int t = 0; t < T; ++t) {
+      char* p0 = (char*)host + std::min(bytes, per * t);
+      char* p1 = (char*)host + std::min(bytes, per * (t + 1));
+      th.emplace_back([p0, p1]() {
+        for (volatile char* q = p0; q < p1; q += 4096) *q = 0;
+      });
     }
   }
-  cudaError_t e = cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, c->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
-  if (reg) cudaHostUnregister(host);
-  if (e != cudaSuccess)
-    return fail(KRY_ERR_CUDA, std::string("factor copy failed: ") + cudaGetErrorString(e));
+  void end() {
+    for (auto& t : th) t.join();
+    th.clear();
+  }
+  ~Prefault() { end(); }
+};
+
+struct StagingRing {
+  static constexpr int NB = 3;
+  static constexpr size_t CH = (size_t)128 << 20;
+  char* buf[NB] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev[NB] = {nullptr, nullptr, nullptr};
+  std::mutex mu;   // one copy at a time per device
+};
+static StagingRing g_staging[64];
+
+int copy_out(kry_ctx* c, void* host, const void* dev, size_t bytes) {
+  cudaPointerAttributes pa;
+  const bool pinned = cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  if (pinned || bytes < ((size_t)64 << 20)) {
+    cudaError_t e = cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess)
+      return fail(KRY_ERR_CUDA, std::string("factor copy failed: ") + cudaGetErrorString(e));
+    return KRY_OK;
+  }
+  StagingRing& R = g_staging[c->dev & 63];
+  std::lock_guard<std::mutex> lock(R.mu);
+  for (int b = 0; b < StagingRing::NB; ++b) {
+    if (!R.buf[b]) KRY_CUDA(cudaHostAlloc((void**)&R.buf[b], StagingRing::CH, cudaHostAllocDefault));
+    if (!R.ev[b]) KRY_CUDA(cudaEventCreateWithFlags(&R.ev[b], cudaEventDisableTiming));
+  }
+  const size_t CH = StagingRing::CH;
+  const size_t nch = (bytes + CH - 1) / CH;
+  auto issue = [&](size_t i) -> cudaError_t {
+    const size_t off = i * CH, len = std::min(CH, bytes - off);
+    const int b = (int)(i % StagingRing::NB);
+    cudaError_t e = cudaMemcpyAsync(R.buf[b], (const char*)dev + off, len, cudaMemcpyDeviceToHost, c->stream);
+    if (e == cudaSuccess) e = cudaEventRecord(R.ev[b], c->stream);
+    return e;
+  };
+  const int T = host_threads();
+  for (size_t i = 0; i < std::min(nch, (size_t)StagingRing::NB); ++i) KRY_CUDA(issue(i));
+  for (size_t i = 0; i < nch; ++i) {
+    const int b = (int)(i % StagingRing::NB);
+    KRY_CUDA(cudaEventSynchronize(R.ev[b]));
+    const size_t off = i * CH, len = std::min(CH, bytes - off);
+    const size_t per = ((len / T) + 63) & ~(size_t)63;
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t) {
+      const size_t a0 = std::min(len, per * t), a1 = std::min(len, per * (t + 1));
+      if (a1 > a0)
+        th.emplace_back([&, a0, a1]() { std::memcpy((char*)host + off + a0, R.buf[b] + a0, a1 - a0); });
+    }
+    for (auto& x : th) x.join();
+    if (i + StagingRing::NB < nch) KRY_CUDA(issue(i + StagingRing::NB));
+  }
   return KRY_OK;
 }
 
@@ -749,6 +862,7 @@ int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s
   if (od->n < 1 || od->n > ((int64_t)1 << 31) - 1)
     return fail(KRY_ERR_DIMENSION, "operator order out of range");
   KRY_CUDA(cudaSetDevice(device));
+  keep_pool_memory(device);
   kry_ctx* c = new kry_ctx();
   c->dev = device;
   c->s = s;
@@ -852,25 +966,25 @@ void kry_ctx_destroy(kry_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->dev);
   cudaStreamSynchronize(c->stream);
-  for (void* p : c->op_mem) cudaFree(p);
-  cudaFree(c->win);
-  cudaFree(c->C);
-  cudaFree(c->st);
+  for (void* p : c->op_mem) dfree(p);
+  dfree(c->win);
+  dfree(c->C);
+  dfree(c->st);
   cudaFreeHost(c->st_h);
   cudaFreeHost(c->hres);
-  cudaFree(c->tmem);
-  cudaFree(c->g.partials);
-  cudaFree(c->g.ticket);
-  cudaFree(c->zeros64);
-  cudaFree(c->gamma_d);
-  if (c->qy) cudaFree(c->qy);
-  if (c->Z) cudaFree(c->Z);
+  dfree(c->tmem);
+  dfree(c->g.partials);
+  dfree(c->g.ticket);
+  dfree(c->zeros64);
+  dfree(c->gamma_d);
+  if (c->qy) dfree(c->qy);
+  if (c->Z) dfree(c->Z);
   c->eig.release();
   for (auto& e : c->ev_comb) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
-  if (c->cublas) cublasDestroy(c->cublas);
-  if (c->solver) cusolverDnDestroy(c->solver);
+  cudaStreamSynchronize(c->stream);
+  release_handles(c);
   if (c->comm) ncclCommDestroy(c->comm);
-  if (c->halo_buf) cudaFree(c->halo_buf);
+  if (c->halo_buf) dfree(c->halo_buf);
   if (c->t_ev[0]) { cudaEventDestroy(c->t_ev[0]); cudaEventDestroy(c->t_ev[1]); }
   cudaStreamSynchronize(c->estream);
   cudaEventDestroy(c->ev_t);
@@ -878,8 +992,8 @@ void kry_ctx_destroy(kry_ctx* c) {
   cudaEventDestroy(c->ev_res[1]);
   cudaStreamDestroy(c->estream);
   for (int b = 0; b < 2; ++b) {
-    if (c->p2buf[b]) cudaFree(c->p2buf[b]);
-    if (c->p2qc[b]) cudaFree(c->p2qc[b]);
+    if (c->p2buf[b]) dfree(c->p2buf[b]);
+    if (c->p2qc[b]) dfree(c->p2qc[b]);
   }
   cudaStreamDestroy(c->stream);
   delete c;
@@ -914,8 +1028,8 @@ int kry_apply(kry_ctx* c, const double* v, double* y, int ncols) {
   KRY_CUDA(cudaMemcpy2DAsync(y, ncols * sizeof(double), dy, ld * sizeof(double),
                              ncols * sizeof(double), c->n, cudaMemcpyDeviceToHost, c->stream));
   KRY_CUDA(cudaStreamSynchronize(c->stream));
-  cudaFree(dv);
-  cudaFree(dy);
+  dfree(dv);
+  dfree(dy);
   return KRY_OK;
 }
 
@@ -1025,8 +1139,8 @@ int kry_get_window(kry_ctx* c, double* older, double* current, int* have_older) 
       rc = emit(slotp(c, c->i_old), c->T.S + (int64_t)(c->m - 1) * 64, older);
     if (have_older) *have_older = (c->m >= 1) ? 1 : 0;
   }
-  cudaFree(tmp);
-  cudaFree(S);
+  dfree(tmp);
+  dfree(S);
   return rc;
 }
 
@@ -1197,7 +1311,7 @@ int kry_finalize_lyap(kry_ctx* c, double eps, int* rank, double* discarded) {
   auto cleanup = [&]() {
     b.free_all();
     for (double* p : {Y, mu, mind, work, outd, factor})
-      if (p) cudaFree(p);
+      if (p) dfree(p);
   };
   if (rc != KRY_OK) { cleanup(); return rc; }
   KRY_CUDA(cudaMemcpy(&lmax, b.lam + (k - 1), sizeof(double), cudaMemcpyDeviceToHost));
@@ -1272,8 +1386,8 @@ int kry_finalize_sylv(kry_ctx* a, kry_ctx* bb, double eps, int* rank, double* di
     fa.free_all();
     fb.free_all();
     for (double* p : {Y, sig, U, VT, mind, work, outd, f1, f2, gw})
-      if (p) cudaFree(p);
-    if (info) cudaFree(info);
+      if (p) dfree(p);
+    if (info) dfree(info);
   };
   if (rc != KRY_OK) { cleanup(); return rc; }
   double la[2], lb[2];
@@ -1371,12 +1485,14 @@ int kry_recover(kry_ctx* c, double* zhost) {
   KRY_CHECK(ensure_handles(c));
   const int s = c->s, m = c->m_final, r = c->rank;
   const int64_t n = c->n;
-  if (c->Z && c->z_cap < n * std::max(r, 1)) { cudaFree(c->Z); c->Z = nullptr; }
+  if (c->Z && c->z_cap < n * std::max(r, 1)) { dfree(c->Z); c->Z = nullptr; }
   if (!c->Z) {
     KRY_CHECK(dalloc(&c->Z, (size_t)n * std::max(r, 1)));
     c->z_cap = n * std::max(r, 1);
   }
   if (r == 0) return KRY_OK;
+  Prefault pf;   // fault in the host factor's pages while pass 2 runs
+  if (zhost) pf.begin(zhost, (size_t)n * r * sizeof(double));
   size_t fr = 0, tot = 0;
   cudaMemGetInfo(&fr, &tot);
   const int64_t halo = (c->op.kind == KRY_OP_STENCIL) ? c->op.nxy : 0;
@@ -1396,8 +1512,8 @@ int kry_recover(kry_ctx* c, double* zhost) {
   const size_t need_buf = (size_t)(n + 2 * halo) * ld2, need_qc = (size_t)G * s * r;
   if (c->p2buf_cap < need_buf || c->p2qc_cap < need_qc) {
     for (int b = 0; b < 2; ++b) {
-      if (c->p2buf[b]) cudaFree(c->p2buf[b]);
-      if (c->p2qc[b]) cudaFree(c->p2qc[b]);
+      if (c->p2buf[b]) dfree(c->p2buf[b]);
+      if (c->p2qc[b]) dfree(c->p2qc[b]);
       c->p2buf[b] = c->p2qc[b] = nullptr;
     }
     c->p2buf_cap = need_buf;
@@ -1520,6 +1636,7 @@ int kry_recover(kry_ctx* c, double* zhost) {
               "second pass regenerated a coupling block that differs from the stored one; the "
               "operator looks nondeterministic");
   }
+  pf.end();
   if (rc == KRY_OK && zhost) rc = copy_out(c, zhost, c->Z, (size_t)n * r * sizeof(double));
   cleanup();
   return rc;
@@ -1530,7 +1647,7 @@ int kry_set_qy(kry_ctx* c, int m, int t, const double* qy) {
   if (m < 1 || m > c->m) return fail(KRY_ERR_DIMENSION, "qy covers more blocks than generated");
   if (t < 0) return fail(KRY_ERR_DIMENSION, "negative factor rank");
   KRY_CHECK(ensure_handles(c));
-  if (c->qy) cudaFree(c->qy);
+  if (c->qy) dfree(c->qy);
   c->qy = nullptr;
   c->m_final = m;
   c->rank = t;
@@ -1588,7 +1705,7 @@ struct Standalone {
   }
   ~Standalone() {
     eig.release();
-    if (dmem) cudaFree(dmem);
+    if (dmem) dfree(dmem);
     if (st) cudaStreamDestroy(st);
   }
 };
@@ -1611,7 +1728,7 @@ int kry_partial_eig(int device, int s, int m, const double* diag, const double* 
   KRY_CUDA(cudaMemcpyAsync(last_rows, lastd, (size_t)s * k * sizeof(double),
                            cudaMemcpyDeviceToHost, S.st));
   KRY_CUDA(cudaStreamSynchronize(S.st));
-  cudaFree(lastd);
+  dfree(lastd);
   return KRY_OK;
 }
 
@@ -1722,7 +1839,7 @@ int kry_true_lyap_residual(kry_ctx* c, const double* z, int t, const double* ch,
   KRY_CUDA(cudaMemcpyAsync(h.data(), G, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
                            c->stream));
   KRY_CUDA(cudaStreamSynchronize(c->stream));
-  cudaFree(M); cudaFree(zd); cudaFree(G);
+  dfree(M); dfree(zd); dfree(G);
   // solvers.py:104-115: sum((U^T U) * (W^T W)), U = [AZ, Z, C], W = [Z, AZ, C]
   auto perm = [&](int i) { return i < t ? i + t : (i < 2 * t ? i - t : i); };
   double val = 0.0;

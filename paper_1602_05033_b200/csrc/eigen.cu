@@ -270,19 +270,19 @@ __device__ __forceinline__ double warp_sum(double v) {
 // one warp per root: ~50 serially dependent terms per lane per iteration,
 // ~10 warps per SM, 48 us per call at K = 1600 (ncu); this is latency-bound
 // work, so it wants short chains and many warps.
-template <int W>
-__device__ __forceinline__ void block_sum5(double (&v)[5], double (*red)[W][5]) {
+template <int W, int NV>
+__device__ __forceinline__ void block_sumv(double (&v)[NV], double (*red)[W][NV]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int q = 0; q < 5; ++q) v[q] = warp_sum(v[q]);
+  for (int q = 0; q < NV; ++q) v[q] = warp_sum(v[q]);
   if (W == 1) return;
   if (lane == 0) {
 #pragma unroll
-    for (int q = 0; q < 5; ++q) (*red)[warp][q] = v[q];
+    for (int q = 0; q < NV; ++q) (*red)[warp][q] = v[q];
   }
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < 5; ++q) {
+  for (int q = 0; q < NV; ++q) {
     double t = (*red)[0][q];
 #pragma unroll
     for (int w = 1; w < W; ++w) t += (*red)[w][q];
@@ -290,10 +290,16 @@ __device__ __forceinline__ void block_sum5(double (&v)[5], double (*red)[W][5]) 
   }
 }
 
-template <int W>
+// a / b for the iteration update only (the iterate's accuracy sets the
+// convergence speed, not the converged root, which is decided by h)
+__device__ __forceinline__ double fdivi(double a, double b) { return a * frcp(b); }
+
+// Per-thread register cache of the shifted poles and z^2 (MT terms per
+// thread, MT * NT >= p); MT = 0: stream them from global memory.
+template <int W, int MT>
 __global__ void __launch_bounds__(32 * W) k_eig_secular(EigView e) {
   constexpr int NT = 32 * W;
-  __shared__ double red[2][W][5];   // double-buffered: one barrier per reduction
+  __shared__ double red[2][W][4];   // double-buffered: one barrier per reduction
   const int p = e.counts[0];
   const int i = blockIdx.x;
   if (i > p) return;
@@ -318,7 +324,7 @@ __global__ void __launch_bounds__(32 * W) k_eig_secular(EigView e) {
   } else {
     const double a = poles[i - 1], b = poles[i];
     const double mid = 0.5 * (a + b);
-    double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
     for (int j = tid; j < p; j += 2 * NT) {
       const double zj = zz[j];
       v[0] -= zj * zj * frcp(mid - poles[j]);
@@ -329,11 +335,23 @@ __global__ void __launch_bounds__(32 * W) k_eig_secular(EigView e) {
     }
     v[0] += v[1];
     v[1] = 0.0;
-    block_sum5<W>(v, &red[rb]);
+    block_sumv<W, 4>(v, &red[rb]);
     rb ^= 1;
     const double hm = v[0] + (mid - d);
     org = (hm > 0.0) ? a : b;
     ia = i - 1; ib = i;
+  }
+  // shifted poles sh_j = lam_j - org and z_j^2, cached once per root
+  double shc[MT > 0 ? MT : 1], z2c[MT > 0 ? MT : 1];
+  if (MT > 0) {
+#pragma unroll
+    for (int q = 0; q < MT; ++q) {
+      const int j = tid + q * NT;
+      const bool in = j < p;
+      const double zj = in ? zz[j] : 0.0;
+      shc[q] = in ? poles[j] - org : 1.0;
+      z2c[q] = zj * zj;
+    }
   }
   const double da = (ia >= 0) ? poles[ia] - org : 0.0;
   const double db = (ib >= 0) ? poles[ib] - org : 0.0;
@@ -343,36 +361,47 @@ __global__ void __launch_bounds__(32 * W) k_eig_secular(EigView e) {
   const double c0 = org - d;
   const bool near_left = (ia >= 0) && (org == poles[ia]);
   for (int it = 0; it < 80; ++it) {
-    // v = {psiL, dpsiL, psiR, dpsiR, sabs}; two accumulator sets for ILP
-    double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0}, u[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int j = tid; j < p; j += 2 * NT) {
-      {
-        const double zj = zz[j];
-        const double r = frcp(t - (poles[j] - org));
-        const double term = zj * zj * r;
+    // v = {psiL, dpsiL, psiR, dpsiR}: poles j <= ia give positive terms,
+    // j > ia negative ones, so sum |term| = psiR - psiL
+    double v[4] = {0.0, 0.0, 0.0, 0.0}, u[4] = {0.0, 0.0, 0.0, 0.0};
+    if (MT > 0) {
+#pragma unroll
+      for (int q = 0; q < MT; ++q) {
+        const int j = tid + q * NT;
+        const double r = frcp(t - shc[q]);
+        const double term = z2c[q] * r;
         const double dterm = term * r;
-        const bool left = j <= ia;
-        v[0] -= left ? term : 0.0; v[1] += left ? dterm : 0.0;
-        v[2] -= left ? 0.0 : term; v[3] += left ? 0.0 : dterm;
-        v[4] += fabs(term);
+        double* acc = (q & 1) ? u : v;
+        if (j <= ia) { acc[0] -= term; acc[1] += dterm; }
+        else { acc[2] -= term; acc[3] += dterm; }   // j >= p: z2c = 0 contributes 0
       }
-      const int k = j + NT;
-      if (k < p) {
-        const double zk = zz[k];
-        const double r = frcp(t - (poles[k] - org));
-        const double term = zk * zk * r;
-        const double dterm = term * r;
-        const bool left = k <= ia;
-        u[0] -= left ? term : 0.0; u[1] += left ? dterm : 0.0;
-        u[2] -= left ? 0.0 : term; u[3] += left ? 0.0 : dterm;
-        u[4] += fabs(term);
+    } else {
+      for (int j = tid; j < p; j += 2 * NT) {
+        {
+          const double zj = zz[j];
+          const double r = frcp(t - (poles[j] - org));
+          const double term = zj * zj * r;
+          const double dterm = term * r;
+          if (j <= ia) { v[0] -= term; v[1] += dterm; }
+          else { v[2] -= term; v[3] += dterm; }
+        }
+        const int k = j + NT;
+        if (k < p) {
+          const double zk = zz[k];
+          const double r = frcp(t - (poles[k] - org));
+          const double term = zk * zk * r;
+          const double dterm = term * r;
+          if (k <= ia) { u[0] -= term; u[1] += dterm; }
+          else { u[2] -= term; u[3] += dterm; }
+        }
       }
     }
 #pragma unroll
-    for (int q = 0; q < 5; ++q) v[q] += u[q];
-    block_sum5<W>(v, &red[rb]);
+    for (int q = 0; q < 4; ++q) v[q] += u[q];
+    block_sumv<W, 4>(v, &red[rb]);
     rb ^= 1;
-    const double psiL = v[0], dpsiL = v[1], psiR = v[2], dpsiR = v[3], sabs = v[4];
+    const double psiL = v[0], dpsiL = v[1], psiR = v[2], dpsiR = v[3];
+    const double sabs = psiR - psiL;
     const double h = t + c0 + psiL + psiR;
     const double err = 8.0 * EPS * (fabs(t) + fabs(c0) + sabs);
     if (h > 0.0) tb = t; else ta = t;
@@ -388,26 +417,26 @@ __global__ void __launch_bounds__(32 * W) k_eig_secular(EigView e) {
         w1 = (dpsiL + 1.0) * (t - da) * (t - da);
         w2 = dpsiR * (t - db) * (t - db);
       }
-      const double c = h + w1 / (t - da) + w2 / (t - db);
+      const double c = h + fdivi(w1, t - da) + fdivi(w2, t - db);
       const double A = c, B = c * (da + db) + w1 + w2, C = c * da * db + w1 * db + w2 * da;
       if (A != 0.0) {
         const double sq = sqrt(fmax(B * B - 4.0 * A * C, 0.0));
         double r1, r2;
-        if (B >= 0.0) { r1 = (B + sq) / (2.0 * A); r2 = (B + sq) != 0.0 ? 2.0 * C / (B + sq) : r1; }
-        else { r1 = (B - sq) != 0.0 ? 2.0 * C / (B - sq) : 0.0; r2 = (B - sq) / (2.0 * A); }
+        if (B >= 0.0) { r1 = fdivi(B + sq, 2.0 * A); r2 = (B + sq) != 0.0 ? fdivi(2.0 * C, B + sq) : r1; }
+        else { r1 = (B - sq) != 0.0 ? fdivi(2.0 * C, B - sq) : 0.0; r2 = fdivi(B - sq, 2.0 * A); }
         if (r1 > ta && r1 < tb) { tn = r1; ok = true; }
         else if (r2 > ta && r2 < tb) { tn = r2; ok = true; }
       } else if (B != 0.0) {
-        tn = C / B;
+        tn = fdivi(C, B);
         ok = (tn > ta && tn < tb);
       }
     } else {
       const double psi = psiL + psiR, dpsi = dpsiL + dpsiR;
       const double w = dpsi * t * t;
-      const double B = c0 + psi + w / t;
+      const double B = c0 + psi + fdivi(w, t);
       const double sq = sqrt(B * B + 4.0 * w);
-      if (ib < 0) tn = (B >= 0.0) ? 2.0 * w / (B + sq) : 0.5 * (sq - B);   // top root
-      else tn = (B > 0.0) ? -0.5 * (B + sq) : 2.0 * w / (B - sq);          // bottom root
+      if (ib < 0) tn = (B >= 0.0) ? fdivi(2.0 * w, B + sq) : 0.5 * (sq - B);   // top root
+      else tn = (B > 0.0) ? -0.5 * (B + sq) : fdivi(2.0 * w, B - sq);          // bottom root
       ok = (tn > ta && tn < tb);
     }
     if (!ok || !isfinite(tn)) tn = 0.5 * (ta + tb);
@@ -748,7 +777,7 @@ int EigEngine::init(int s_, int kmax_, int device) {
   // Cauchy stage-1 partials: [y-chunk][x][8] for x, y up to 2 kmax, + mins
   cpart_cap = ((2 * nk + CC_CH - 1) / CC_CH + 1) * (2 * nk);
   doubles += cpart_cap * 8 + cpart_cap / 64 + 64;
-  KRY_CUDA(cudaMalloc(&dbuf, doubles * sizeof(double)));
+  KRY_CHECK(dalloc(&dbuf, doubles));
   KRY_CUDA(cudaMemset(dbuf, 0, doubles * sizeof(double)));
   double* p = dbuf;
   for (int b = 0; b < 2; ++b) { lam[b] = p; p += nk; }
@@ -764,20 +793,20 @@ int EigEngine::init(int s_, int kmax_, int device) {
   vpart = p; p += vpart_n;
   cpart = p; p += cpart_cap * 8 + cpart_cap / 64 + 64;
   size_t ints = 5 * nk + 8;
-  KRY_CUDA(cudaMalloc(&ibuf, ints * sizeof(int)));
+  KRY_CHECK(dalloc(&ibuf, ints));
   KRY_CUDA(cudaMemset(ibuf, 0, ints * sizeof(int)));
   int* q = ibuf;
   cand = q; q += nk; dflag = q; q += nk; pflag = q; q += nk; pmap = q; q += nk;
   def_idx = q; q += nk; counts = q;
-  KRY_CUDA(cudaMalloc(&ticket, sizeof(unsigned) * 4));
+  KRY_CHECK(dalloc(&ticket, 4));
   KRY_CUDA(cudaMemset(ticket, 0, sizeof(unsigned) * 4));
   return KRY_OK;
 }
 
 void EigEngine::release() {
-  if (dbuf) cudaFree(dbuf);
-  if (ibuf) cudaFree(ibuf);
-  if (ticket) cudaFree(ticket);
+  if (dbuf) dfree(dbuf);
+  if (ibuf) dfree(ibuf);
+  if (ticket) dfree(ticket);
   dbuf = nullptr; ibuf = nullptr; ticket = nullptr;
 }
 
@@ -810,9 +839,16 @@ int EigEngine::append_block(cudaStream_t st, const double* dsym_blk, const doubl
       k_eig_deflate<false><<<1, 1024, 0, st>>>(v, K, dsym_blk, sub_prev, a);
     }
     // K+1 roots at most, one CTA each; threads per root grow with K
-    if (K >= 1024) k_eig_secular<4><<<K + 1, 128, 0, st>>>(v);
-    else if (K >= 256) k_eig_secular<2><<<K + 1, 64, 0, st>>>(v);
-    else k_eig_secular<1><<<K + 1, 32, 0, st>>>(v);
+    if (K >= 1024) {
+      if (K <= 128 * 16) k_eig_secular<4, 16><<<K + 1, 128, 0, st>>>(v);
+      else k_eig_secular<4, 0><<<K + 1, 128, 0, st>>>(v);
+    } else if (K >= 256) {
+      k_eig_secular<2, 16><<<K + 1, 64, 0, st>>>(v);
+    } else if (K >= 64) {
+      k_eig_secular<1, 8><<<K + 1, 32, 0, st>>>(v);
+    } else {
+      k_eig_secular<1, 2><<<K + 1, 32, 0, st>>>(v);
+    }
     int nl = 2;
     if (K > 0) {
       if (K >= 1024) k_eig_zhat<4><<<K, 128, 0, st>>>(v);

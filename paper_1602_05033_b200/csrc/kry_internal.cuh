@@ -25,6 +25,27 @@ namespace kry {
 // ---------------------------------------------------------------- errors
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
+
+// Device allocations go through the stream-ordered pool on the legacy stream
+// (ordered with every blocking stream of a context): repeated solves and
+// finalisations reuse cached memory, and a free never synchronises the
+// device (plain cudaFree did, which made finalisation times erratic).
+template <class T>
+inline int dalloc(T** p, size_t count) {
+  cudaError_t e = cudaMallocAsync((void**)p, count * sizeof(T) + 16, (cudaStream_t)0);
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    return fail(KRY_ERR_CUDA, std::string("cudaMallocAsync failed: ") + cudaGetErrorString(e) +
+                                  " (" + std::to_string(count * sizeof(T)) + " bytes)");
+  }
+  return KRY_OK;
+}
+template <class T>
+inline void dfree(T* p) {
+  if (p) cudaFreeAsync((void*)p, (cudaStream_t)0);
+}
+// keep freed pool memory cached in the process (once per device)
+void keep_pool_memory(int device);
 extern thread_local std::string g_last_error;
 
 #define KRY_CUDA(call)                                                        \
