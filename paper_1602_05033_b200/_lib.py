@@ -136,11 +136,12 @@ def load():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
+    path = os.environ.get("KRY_LIB_PATH", LIB_PATH)   # experiments: alternative build
+    if not os.path.exists(path):
         raise KrymatError(
             "libkrymat_b200.so is not built (expected at %s); run "
             "`python -c 'import __graft_entry__ as g; g.build()'`" % LIB_PATH)
-    lib = ctypes.CDLL(LIB_PATH)
+    lib = ctypes.CDLL(path)
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype = res

@@ -1495,21 +1495,26 @@ int kry_recover(kry_ctx* c, double* zhost) {
   if (zhost) pf.begin(zhost, (size_t)n * r * sizeof(double));
   size_t fr = 0, tot = 0;
   cudaMemGetInfo(&fr, &tot);
-  const int64_t halo = (c->op.kind == KRY_OP_STENCIL) ? c->op.nxy : 0;
-  const size_t blk_bytes = (size_t)(n + 2 * halo) * s * sizeof(double);
+  // Pass 2 regenerates V_j in the contiguous three-block ring (the same
+  // layout and kernels as pass 1) and the combine kernel writes each new block
+  // a second time into a point-interleaved chunk buffer [point][block][s] of G
+  // blocks, which one DGEMM per chunk folds into Z on the second stream while
+  // the next chunk is regenerated into the other buffer.  (The recurrence
+  // itself used to run on the interleaved layout: 64-byte rows at a
+  // G*s*8-byte stride made its kernels 25-45% slower than in pass 1.)
+  const size_t blk_bytes = (size_t)n * s * sizeof(double);
   // two buffers within a quarter of the free memory (+ what is cached)
-  int64_t G = (int64_t)((fr / 4 + c->p2buf_cap * sizeof(double)) / blk_bytes) - 2;
+  int64_t G = (int64_t)((fr / 4 + c->p2buf_cap * sizeof(double)) / blk_bytes) / 2;
   if (G > 32) G = 32;
   if (G > m) G = m;
   if (G < 1) G = 1;
   const int nbuf = (m > G) ? 2 : 1;
-  const int64_t nslot = G + 2;
-  const int64_t ld2 = nslot * s;
+  const int64_t ld2 = G * s;
   double* buf[2] = {nullptr, nullptr};
   double* Qc[2] = {nullptr, nullptr};
   cudaEvent_t ev_full[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   int rc = KRY_OK;
-  const size_t need_buf = (size_t)(n + 2 * halo) * ld2, need_qc = (size_t)G * s * r;
+  const size_t need_buf = (size_t)n * ld2, need_qc = (size_t)G * s * r;
   if (c->p2buf_cap < need_buf || c->p2qc_cap < need_qc) {
     for (int b = 0; b < 2; ++b) {
       if (c->p2buf[b]) dfree(c->p2buf[b]);
@@ -1524,10 +1529,6 @@ int kry_recover(kry_ctx* c, double* zhost) {
     if (rc == KRY_OK && !c->p2qc[b]) rc = dalloc(&c->p2qc[b], c->p2qc_cap);
     buf[b] = c->p2buf[b];
     Qc[b] = c->p2qc[b];
-    // halo planes must be finite (zero) for the boundary predicates' skipped loads
-    if (rc == KRY_OK &&
-        cudaMemsetAsync(buf[b], 0, need_buf * sizeof(double), c->stream) != cudaSuccess)
-      rc = fail(KRY_ERR_CUDA, "memset failed");
     cudaEventCreateWithFlags(&ev_full[b], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ev_free[b], cudaEventDisableTiming);
   }
@@ -1541,8 +1542,10 @@ int kry_recover(kry_ctx* c, double* zhost) {
     }
   };
   if (rc != KRY_OK) { cleanup(); return rc; }
-  int cb = 0;   // current buffer
-  auto sp = [&](int b, int64_t q) { return buf[b] + halo * ld2 + q * s; };
+  int cb = 0;   // current chunk buffer
+  auto sp = [&](int b, int64_t q) { return buf[b] + q * s; };
+  auto ring = [&](int j) { return c->slot[(j - 1) % 3]; };   // V_j, 1-based
+  const int64_t ldr = c->ld;
   int first_gemm = 1;
   int gemm_used[2] = {0, 0};
   // fold blocks blk0.. (0-based) of buffer b into Z on the second stream
@@ -1554,28 +1557,27 @@ int kry_recover(kry_ctx* c, double* zhost) {
     const double one = 1.0;
     const double beta = first_gemm ? 0.0 : 1.0;
     if (cublasDgemm(c->cublas, CUBLAS_OP_N, CUBLAS_OP_N, r, (int)n, nblk * s, &one, Qc[b], r,
-                    sp(b, 2), (int)ld2, &beta, c->Z, r) != CUBLAS_STATUS_SUCCESS)
+                    sp(b, 0), (int)ld2, &beta, c->Z, r) != CUBLAS_STATUS_SUCCESS)
       return fail(KRY_ERR_CUDA, "cublasDgemm (Z accumulation) failed");
     KRY_CUDA(cudaEventRecord(ev_free[b], c->estream));
     gemm_used[b] = 1;
     first_gemm = 0;
     return KRY_OK;
   };
-  // regenerate V_1 into slot 2
-  rc = do_init(c, sp(cb, 2), ld2, 1);
-  int cur = 2, old = -1;
-  int chunk_first = 1;  // block index (1-based) held in slot 2
+  // regenerate V_1 into the ring and the chunk buffer
+  rc = do_init(c, ring(1), ldr, 1);
+  if (rc == KRY_OK) rc = launch_copy_block(c->stream, s, ring(1), ldr, sp(cb, 0), ld2, n);
+  int chunk_first = 1;  // 1-based block index held in chunk slot 0
   for (int j = 1; rc == KRY_OK && j < m; ++j) {
-    // coefficient solve j on V_j (replay) ; V_{j+1} goes to slot cur+1
-    ApplyGramCall ag{sp(cb, cur), ld2, n, 1, POST_STEP, 0};
+    // coefficient solve j on V_j (replay); V_{j+1} goes to the ring and the chunk
+    ApplyGramCall ag{ring(j), ldr, n, 1, POST_STEP, 0};
     rc = run_apply_gram(c, ag);
     if (rc) break;
     rc = sync_status(c);
     if (rc) break;
     rc = map_status(c, ("second pass step " + std::to_string(j)).c_str());
     if (rc) break;
-    int nxt = cur + 1;
-    if (nxt == nslot) {
+    if (j + 1 - chunk_first == G) {
       // chunk complete: S_j known now -> fold blocks chunk_first..j into Z
       rc = gemm_chunk(cb, chunk_first - 1, j - chunk_first + 1);
       if (rc) break;
@@ -1586,43 +1588,28 @@ int kry_recover(kry_ctx* c, double* zhost) {
         rc = fail(KRY_ERR_CUDA, "event wait failed");
         break;
       }
-      // carry the last two blocks (halo planes included) to slots 0, 1
-      if (nb != cb) {
-        rc = launch_copy_block(c->stream, s, sp(cb, nslot - 2) - halo * ld2, ld2,
-                               sp(nb, 0) - halo * ld2, ld2, n + 2 * halo);
-        if (rc == KRY_OK)
-          rc = launch_copy_block(c->stream, s, sp(cb, nslot - 1) - halo * ld2, ld2,
-                                 sp(nb, 1) - halo * ld2, ld2, n + 2 * halo);
-      } else {
-        rc = launch_copy_block(c->stream, s, sp(cb, nslot - 2) - halo * ld2, ld2,
-                               sp(cb, 0) - halo * ld2, ld2, n + 2 * halo);
-        if (rc == KRY_OK)
-          rc = launch_copy_block(c->stream, s, sp(cb, nslot - 1) - halo * ld2, ld2,
-                                 sp(cb, 1) - halo * ld2, ld2, n + 2 * halo);
-      }
-      if (rc) break;
       cb = nb;
-      old = 0; cur = 1; nxt = 2;
       chunk_first = j + 1;
     }
+    double* chunk_dst = sp(cb, j + 1 - chunk_first);
     int ex = 0;
     if (c->st_h->flags & KRY_FLAG_FALLBACK) {
-      rc = explicit_step(c, j, old >= 0 ? sp(cb, old) : nullptr, sp(cb, cur), sp(cb, nxt), ld2,
-                         1, &ex);
+      rc = explicit_step(c, j, j > 1 ? ring(j - 1) : nullptr, ring(j), ring(j + 1), ldr, 1, &ex);
+      if (rc == KRY_OK && !ex) rc = launch_copy_block(c->stream, s, ring(j + 1), ldr, chunk_dst, ld2, n);
     } else {
-      CombineCall cc{old >= 0 ? sp(cb, old) : nullptr, ld2, sp(cb, cur), ld2, sp(cb, nxt), ld2, n,
+      CombineCall cc{j > 1 ? ring(j - 1) : nullptr, ldr, ring(j), ldr, ring(j + 1), ldr, n,
                      j > 1 ? 1 : 0, 1, 1, 1};
+      cc.vn2 = chunk_dst;
+      cc.ldn2 = ld2;
       rc = run_combine(c, cc, nullptr, nullptr);
-      if (rc == KRY_OK) rc = halo_exchange(c, sp(cb, nxt), ld2, s);
+      if (rc == KRY_OK) rc = halo_exchange(c, ring(j + 1), ldr, s);
     }
     if (rc) break;
     if (ex) { rc = fail(KRY_ERR_RECURRENCE, "second pass hit an invariant subspace early"); break; }
-    old = cur;
-    cur = nxt;
   }
   if (rc == KRY_OK && m >= 1) {
     // coefficient solve m: S_m (and the replay check of coupling m-1)
-    ApplyGramCall ag{sp(cb, cur), ld2, n, 1, POST_STEP, 0};
+    ApplyGramCall ag{ring(m), ldr, n, 1, POST_STEP, 0};
     rc = run_apply_gram(c, ag);
     if (rc == KRY_OK) rc = sync_status(c);
     if (rc == KRY_OK) rc = gemm_chunk(cb, chunk_first - 1, m - chunk_first + 1);

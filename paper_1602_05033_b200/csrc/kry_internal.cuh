@@ -171,6 +171,8 @@ struct CombineCall {
   int64_t n;
   int has_old, use_op, write_new, reverse;
   int post = POST_P;   // POST_NONE in multi-GPU mode (all-reduce, then k_post)
+  double* vn2 = nullptr;   // optional second copy of V_{m+1} (pass-2 chunk buffer)
+  int64_t ldn2 = 0;
 };
 int launch_combine(cudaStream_t st, int s, const OpDev& op, const CombineCall& c,
                    DevState* dst, const TStore& T, GramScratch& g, int grid,
