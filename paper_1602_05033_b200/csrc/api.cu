@@ -14,6 +14,7 @@
 #include <cstring>
 #include <mutex>
 #include <thread>
+#include <sys/mman.h>
 #include <vector>
 #include <algorithm>
 
@@ -768,6 +769,12 @@ struct Prefault {
     cudaPointerAttributes pa;
     if (cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type == cudaMemoryTypeHost) return;
     cudaGetLastError();
+    // 2 MB pages where the kernel allows: 512x fewer faults
+    {
+      const uintptr_t a0 = ((uintptr_t)host + ((1u << 21) - 1)) & ~(uintptr_t)((1u << 21) - 1);
+      const uintptr_t a1 = ((uintptr_t)host + bytes) & ~(uintptr_t)((1u << 21) - 1);
+      if (a1 > a0) madvise((void*)a0, a1 - a0, MADV_HUGEPAGE);
+    }
     const int T = host_threads();
     const size_t per = (bytes / T + 4095) & ~(size_t)4095;
     for (int t = 0; t < T; ++t) {
@@ -805,6 +812,8 @@ int copy_out(kry_ctx* c, void* host, const void* dev, size_t bytes) {
       return fail(KRY_ERR_CUDA, std::string("factor copy failed: ") + cudaGetErrorString(e));
     return KRY_OK;
   }
+  // (page-locking the destination instead measured 0.5-1.1 s to register +
+  // 0.24 s to unregister for 14.8 GB, vs 0.40 s for this whole staged copy)
   StagingRing& R = g_staging[c->dev & 63];
   std::lock_guard<std::mutex> lock(R.mu);
   for (int b = 0; b < StagingRing::NB; ++b) {
@@ -1623,8 +1632,12 @@ int kry_recover(kry_ctx* c, double* zhost) {
               "second pass regenerated a coupling block that differs from the stored one; the "
               "operator looks nondeterministic");
   }
+  StageTimer tm(c->stream);
+  tm.mark("recover: pass 2");
   pf.end();
+  tm.mark("recover: prefault wait");
   if (rc == KRY_OK && zhost) rc = copy_out(c, zhost, c->Z, (size_t)n * r * sizeof(double));
+  tm.mark("recover: copy out");
   cleanup();
   return rc;
 }
