@@ -26,13 +26,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CONFIG_DOC = {
-    "c1": "Lyapunov L2D 100^2 (n=10,000), s=1, tol 1e-6",
-    "c2": "Lyapunov L3D 50^3 (n=125,000), s=4 QR'd C, tol 1e-8",
-    "c3": "Sylvester var-coef 2D 300^2 x L3D 40^3, s=2, tol 1e-8",
-    "c4": "Lyapunov L3D 200^3 (n=8,000,000), s=8, tol 1e-8, maxit 600",
-    "c5": "Lyapunov L2D 2000^2 (n=4,000,000), s=4, tol 1e-10, 1500 its",
-}
+from paper_1602_05033_b200.problems import DESCRIPTIONS as CONFIG_DOC  # noqa: E402
 
 
 def peaks():
@@ -59,40 +53,22 @@ def captured_traffic(config):
         return None
 
 
-def laplacian_stencil_constants(dims, n):
-    """Exactly the doubles of oracle.problems' CSR for the Laplacians:
-    1-D: main -2/h^2, off 1/h^2; 3-D diag = ((d + d) + d) (kron sum order);
-    2-D (five-point, face coefficients 1): diag = -(((c + c) + c) + c)."""
-    h = 1.0 / (n + 1)
-    if dims == 3:
-        d = -2.0 / h ** 2
-        return (d + d) + d, 1.0 / h ** 2
-    c = 1.0 / h ** 2
-    return -(((c + c) + c) + c), c
-
-
 def build_problem(name, slab=None, comm=None):
-    """Operators (device stencil descriptions) + right-hand sides, seeded.
-    With ``slab`` (planes [z0, z1) of the slowest axis) the operator and C are
-    this rank's row slab (parallel.py)."""
+    """Operators (device stencil descriptions for c4/c5, CSR otherwise) and
+    the seeded right-hand sides of a BASELINE workload
+    (paper_1602_05033_b200.problems).  With ``slab`` (planes [z0, z1) of the
+    slowest axis) the operator and C are this rank's row slab (parallel.py)."""
     import paper_1602_05033_b200 as kb
-    from oracle import problems as P
+    from paper_1602_05033_b200 import problems as P
     from paper_1602_05033_b200.parallel import local_rows
 
     if name in ("c4", "c5"):
-        cfg = P.build_config(name, with_matrix=False)
-        g = tuple(cfg["grid_a"]) + (1,) * (3 - len(cfg["grid_a"]))
-        if len(cfg["grid_a"]) == 3:
-            cd, co = laplacian_stencil_constants(3, g[0])
-            op = kb.StencilOperator(g, cd, co, co, co, slab=slab, comm=comm)
-        else:
-            cd, co = laplacian_stencil_constants(2, g[0])
-            # 2-D grid: the slab axis is y -> present it as (nx, 1, ny)
-            op = kb.StencilOperator((g[0], 1, g[1]), cd, co, 0.0, co, slab=slab, comm=comm)
+        cfg = P.workload(name, with_matrix=False)
+        op = P.stencil_operator(cfg["grid_a"], slab=slab, comm=comm)
         if slab is not None:
             cfg["c"] = local_rows(cfg["c"], op.grid, slab)
         return cfg, op, None
-    cfg = P.build_config(name)
+    cfg = P.workload(name)
     op = kb.SparseOperator(cfg["a"])
     opb = kb.SparseOperator(cfg["b"]) if cfg["kind"] == "sylvester" else None
     return cfg, op, opb
@@ -294,9 +270,9 @@ def main():
     lib = _lib.load()
     slab = comm = None
     if world > 1:
-        from oracle import problems as P
+        from paper_1602_05033_b200 import problems as P
         from paper_1602_05033_b200.parallel import Communicator, slab_partition
-        g = P.build_config(args.config, with_matrix=False)["grid_a"]
+        g = P.workload(args.config, with_matrix=False)["grid_a"]
         slab = slab_partition(g[-1], world, rank)
         comm = Communicator()
     cfg, op, opb = build_problem(args.config, slab=slab, comm=comm)

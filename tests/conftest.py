@@ -14,11 +14,12 @@ def pytest_configure(config):
 
 
 def _have_gpu():
+    """A CUDA device is visible (decided WITHOUT the library, so a GPU box
+    whose libkrymat_b200.so is missing or broken fails the gpu tests loudly
+    instead of skipping them)."""
     try:
-        from paper_1602_05033_b200 import _lib
-        import ctypes
-        n = ctypes.c_int(0)
-        return _lib.load().kry_device_count(ctypes.byref(n)) == 0 and n.value > 0
+        import torch
+        return torch.cuda.is_available() and torch.cuda.device_count() > 0
     except Exception:
         return False
 

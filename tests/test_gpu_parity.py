@@ -285,6 +285,26 @@ def test_config3_sylvester_parity_with_reference_run():
     assert np.linalg.norm(left - g["sketch_left"]) <= 1e-8 * np.linalg.norm(g["sketch_left"])
 
 
+def test_config4_full_size_parity_with_reference_run():
+    # the bench workload (n = 8e6, s = 8) against the reference's own 2.3 h
+    # run: iterations and rank exact, history 1e-9 rel + floor, factor
+    # sketch X @ Omega on 4096 seeded rows (golden) to 1e-8
+    import bench
+    g = gold("c4")
+    cfg, op, _ = bench.build_problem("c4")
+    sol = kb.solve_lyapunov(op, cfg["c"], kb.SolveOptions(tol=cfg["tol"], max_m=cfg["max_m"],
+                                                          storage="windowed"))
+    assert sol.iterations == int(g["iterations"]) == 257
+    assert sol.rank == int(g["rank"])
+    ok, worst = hist_ok([r[2] for r in sol.history], g["history"][:, 2])
+    assert ok, worst
+    z = sol.z
+    om = P.sketch_omega(z.shape[0], 2)
+    sk = z[g["sketch_rows"]] @ (z.T @ om)
+    assert np.linalg.norm(sk - g["sketch"]) <= 1e-8 * np.linalg.norm(g["sketch"])
+    assert abs(np.linalg.norm(z.T @ z) - float(g["x_norm_fro"])) <= 1e-8 * float(g["x_norm_fro"])
+
+
 def _c5_operator():
     import bench
     cfg, op, _ = bench.build_problem("c5")
