@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <thread>
 #include <sys/mman.h>
@@ -270,6 +271,11 @@ struct kry_ctx {
   double* p2buf[2] = {nullptr, nullptr};
   double* p2qc[2] = {nullptr, nullptr};
   size_t p2buf_cap = 0, p2qc_cap = 0;
+  // fused single-pass step (stencil operators, one GPU)
+  bool use_step = false;
+  bool coef_ready = false;   // st->M holds the coefficients of the next step
+  StepScratch sx{};
+  int step_ch = 0, step_nch = 0, step_lag = 0;
   // multi-GPU
   int nranks = 1, rank_id = 0;
   ncclComm_t comm = nullptr;
@@ -409,6 +415,7 @@ int reset_state(kry_ctx* c, int replay) {
 // init from C (device, n x s, ld s) into slot `dst`
 int do_init(kry_ctx* c, double* dst, int64_t ldd, int replay) {
   KRY_CHECK(reset_state(c, replay));
+  c->coef_ready = false;
   ApplyGramCall ag{c->C, (int64_t)c->s, c->n, 0, POST_INIT, 0};
   KRY_CHECK(run_apply_gram(c, ag));
   KRY_CHECK(sync_status(c));
@@ -470,15 +477,66 @@ int explicit_step(kry_ctx* c, int j, const double* vold, const double* vcur, dou
   return KRY_OK;
 }
 
+// the fused single-pass kernel applies (stencil operator, one GPU, s != 5, 7)
+bool step_on(kry_ctx* c) { return c->use_step && !dist(c); }
+
+// One fused-kernel launch: V_{j+1} from the coefficients of step j (already
+// in st->M) plus the Gram blocks and the (deferred) coefficient solve of
+// step j+1.  `vn2` / `ldn2`: optional second copy (pass-2 chunk buffer).
+int run_step_kernel(kry_ctx* c, int j, const double* vold, const double* vcur, double* vnew,
+                    int64_t ld, double* vn2, int64_t ldn2, bool prof) {
+  StepCall sc;
+  sc.vo = vold ? vold : vcur;   // step 1: Mo == 0
+  sc.vc = vcur;
+  sc.vn = vnew;
+  sc.ld = ld;
+  sc.vn2 = vn2;
+  sc.ldn2 = ldn2;
+  sc.n = c->n;
+  sc.has_old = vold != nullptr;
+  sc.ch = c->step_ch;
+  sc.nch = c->step_nch;
+  sc.lag = c->step_lag;
+  // alternate the chunk order by step (L2 reuse of the previous step's
+  // tail); a function of j only, so pass 2 sums every Gram in pass 1's order
+  sc.reverse = j & 1;
+  cudaEvent_t evs[2];
+  float dummy = 0.f;
+  if (prof) {
+    cudaEventCreate(&evs[0]);
+    cudaEventCreate(&evs[1]);
+  }
+  KRY_CHECK(launch_step(c->stream, c->s, c->op, sc, c->st, c->T, c->sx, prof ? &dummy : nullptr,
+                        prof ? evs : nullptr));
+  if (prof) c->ev_comb.push_back({evs[0], evs[1]});
+  return KRY_OK;
+}
+
 // One block-Lanczos step on blocks (old, cur) -> new.  Returns exhausted.
+// Fused path: when the previous launch already solved this step's
+// coefficients (coef_ready), one k_step launch produces V_{j+1} and solves
+// step j+1; otherwise (first step, after an explicit step, or when the
+// deferred solve asked for the fallback) the two-kernel path runs the
+// coefficient solve of step j first (and the explicit step when needed).
 int fused_step(kry_ctx* c, int j, const double* vold, const double* vcur, double* vnew,
                int64_t ld, int finalize_on_zero, int* exhausted) {
-  ApplyGramCall ag{vcur, ld, c->n, 1, POST_STEP, 0};
-  KRY_CHECK(run_apply_gram(c, ag));
-  KRY_CHECK(sync_status(c));
-  KRY_CHECK(map_status(c, ("Lanczos step " + std::to_string(j)).c_str()));
-  if (c->st_h->flags & KRY_FLAG_FALLBACK) {
-    return explicit_step(c, j, vold, vcur, vnew, ld, finalize_on_zero, exhausted);
+  *exhausted = 0;
+  if (!(step_on(c) && c->coef_ready)) {
+    c->coef_ready = false;
+    ApplyGramCall ag{vcur, ld, c->n, 1, POST_STEP, 0};
+    KRY_CHECK(run_apply_gram(c, ag));
+    KRY_CHECK(sync_status(c));
+    KRY_CHECK(map_status(c, ("Lanczos step " + std::to_string(j)).c_str()));
+    if (c->st_h->flags & KRY_FLAG_FALLBACK) {
+      return explicit_step(c, j, vold, vcur, vnew, ld, finalize_on_zero, exhausted);
+    }
+  }
+  if (step_on(c)) {
+    KRY_CHECK(run_step_kernel(c, j, j > 1 ? vold : nullptr, vcur, vnew, ld, nullptr, 0, c->prof));
+    KRY_CHECK(sync_status(c));
+    KRY_CHECK(map_status(c, ("Lanczos step " + std::to_string(j)).c_str()));
+    c->coef_ready = !(c->st_h->flags & KRY_FLAG_FALLBACK);
+    return KRY_OK;
   }
   CombineCall cc{vold, ld, vcur, ld, vnew, ld, c->n, j > 1 ? 1 : 0, 1, 1, 1};
   cudaEvent_t* ev = nullptr;
@@ -492,7 +550,6 @@ int fused_step(kry_ctx* c, int j, const double* vold, const double* vcur, double
   KRY_CHECK(run_combine(c, cc, c->prof ? &dummy : nullptr, ev));
   KRY_CHECK(halo_exchange(c, vnew, ld, c->s));
   if (c->prof) c->ev_comb.push_back({evs[0], evs[1]});
-  *exhausted = 0;
   return KRY_OK;
 }
 
@@ -905,15 +962,19 @@ int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s
     if (od->variable) {
       const double* src[4] = {od->diag, od->cx, od->cy, od->cz};
       const double** dst[4] = {&op.d, &op.ex, &op.ey, &op.ez};
-      // arrays cover the owned planes plus one halo plane on each side
+      // arrays cover the owned planes plus one plane on each side: the
+      // neighbour's coefficients (sharded) or zeros (the fused step kernel
+      // loads the couplings of boundary points unmasked)
       const int64_t lo = op.halo_lo ? op.nxy : 0, hi = op.halo_hi ? op.nxy : 0;
+      const int64_t pad = op.nxy;
       for (int q = 0; q < 4; ++q) {
         double* p = nullptr;
-        if (dalloc(&p, (size_t)(nloc + lo + hi)) != KRY_OK) { delete c; return KRY_ERR_CUDA; }
+        if (dalloc(&p, (size_t)(nloc + 2 * pad)) != KRY_OK) { delete c; return KRY_ERR_CUDA; }
         c->op_mem.push_back(p);
-        KRY_CUDA(cudaMemcpy(p, src[q] + z0 * op.nxy - lo, (nloc + lo + hi) * sizeof(double),
-                            cudaMemcpyHostToDevice));
-        *dst[q] = p + lo;
+        KRY_CUDA(cudaMemset(p, 0, (nloc + 2 * pad) * sizeof(double)));
+        KRY_CUDA(cudaMemcpy(p + pad - lo, src[q] + z0 * op.nxy - lo,
+                            (nloc + lo + hi) * sizeof(double), cudaMemcpyHostToDevice));
+        *dst[q] = p + pad;
       }
     }
   } else if (od->kind == KRY_OP_CSR) {
@@ -963,6 +1024,21 @@ int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s
   KRY_CHECK(dalloc(&c->g.partials, (size_t)(c->g.max_grid + c->g.max_grid / 32 + 1) * 24 * 8));
   KRY_CHECK(dalloc(&c->g.ticket, 2 + c->g.max_grid / 32));
   KRY_CUDA(cudaMemset(c->g.ticket, 0, (2 + c->g.max_grid / 32) * sizeof(unsigned)));
+  // fused single-pass step scratch (stencil operators on one GPU)
+  {
+    const char* off = getenv("KRY_NO_FUSED_STEP");
+    c->use_step = step_supported(op, s, c->ld) && !(off && off[0] == '1');
+    if (c->use_step) {
+      step_geometry(op, nloc, &c->step_ch, &c->step_nch, &c->step_lag);
+      const int gmax = KRY_MAX_GRID;
+      c->sx.nch_cap = gmax;
+      KRY_CHECK(dalloc(&c->sx.part, (size_t)(gmax + gmax / 32 + 1) * 320));
+      KRY_CHECK(dalloc(&c->sx.gcnt, (size_t)gmax / 32 + 2));
+      KRY_CHECK(dalloc(&c->sx.flags, (size_t)c->step_nch));
+      KRY_CUDA(cudaMemset(c->sx.gcnt, 0, (gmax / 32 + 2) * sizeof(unsigned)));
+      KRY_CUDA(cudaMemset(c->sx.flags, 0, c->step_nch * sizeof(unsigned)));
+    }
+  }
   KRY_CHECK(dalloc(&c->zeros64, 64));
   KRY_CHECK(dalloc(&c->gamma_d, 64));
   KRY_CUDA(cudaMemset(c->zeros64, 0, 64 * sizeof(double)));
@@ -984,6 +1060,9 @@ void kry_ctx_destroy(kry_ctx* c) {
   dfree(c->tmem);
   dfree(c->g.partials);
   dfree(c->g.ticket);
+  dfree(c->sx.part);
+  dfree(c->sx.gcnt);
+  dfree(c->sx.flags);
   dfree(c->zeros64);
   dfree(c->gamma_d);
   if (c->qy) dfree(c->qy);
@@ -1578,14 +1657,19 @@ int kry_recover(kry_ctx* c, double* zhost) {
   if (rc == KRY_OK) rc = launch_copy_block(c->stream, s, ring(1), ldr, sp(cb, 0), ld2, n);
   int chunk_first = 1;  // 1-based block index held in chunk slot 0
   for (int j = 1; rc == KRY_OK && j < m; ++j) {
-    // coefficient solve j on V_j (replay); V_{j+1} goes to the ring and the chunk
-    ApplyGramCall ag{ring(j), ldr, n, 1, POST_STEP, 0};
-    rc = run_apply_gram(c, ag);
-    if (rc) break;
-    rc = sync_status(c);
-    if (rc) break;
-    rc = map_status(c, ("second pass step " + std::to_string(j)).c_str());
-    if (rc) break;
+    // coefficient solve j on V_j (replay) -- already done by the previous
+    // fused launch when coef_ready; V_{j+1} goes to the ring and the chunk
+    const bool fused = step_on(c) && c->coef_ready;
+    if (!fused) {
+      c->coef_ready = false;
+      ApplyGramCall ag{ring(j), ldr, n, 1, POST_STEP, 0};
+      rc = run_apply_gram(c, ag);
+      if (rc) break;
+      rc = sync_status(c);
+      if (rc) break;
+      rc = map_status(c, ("second pass step " + std::to_string(j)).c_str());
+      if (rc) break;
+    }
     if (j + 1 - chunk_first == G) {
       // chunk complete: S_j known now -> fold blocks chunk_first..j into Z
       rc = gemm_chunk(cb, chunk_first - 1, j - chunk_first + 1);
@@ -1602,9 +1686,15 @@ int kry_recover(kry_ctx* c, double* zhost) {
     }
     double* chunk_dst = sp(cb, j + 1 - chunk_first);
     int ex = 0;
-    if (c->st_h->flags & KRY_FLAG_FALLBACK) {
+    if (!fused && (c->st_h->flags & KRY_FLAG_FALLBACK)) {
       rc = explicit_step(c, j, j > 1 ? ring(j - 1) : nullptr, ring(j), ring(j + 1), ldr, 1, &ex);
       if (rc == KRY_OK && !ex) rc = launch_copy_block(c->stream, s, ring(j + 1), ldr, chunk_dst, ld2, n);
+    } else if (step_on(c)) {
+      rc = run_step_kernel(c, j, j > 1 ? ring(j - 1) : nullptr, ring(j), ring(j + 1), ldr,
+                           chunk_dst, ld2, false);
+      if (rc == KRY_OK) rc = sync_status(c);
+      if (rc == KRY_OK) rc = map_status(c, ("second pass step " + std::to_string(j)).c_str());
+      c->coef_ready = !(c->st_h->flags & KRY_FLAG_FALLBACK);
     } else {
       CombineCall cc{j > 1 ? ring(j - 1) : nullptr, ldr, ring(j), ldr, ring(j + 1), ldr, n,
                      j > 1 ? 1 : 0, 1, 1, 1};
@@ -1617,10 +1707,13 @@ int kry_recover(kry_ctx* c, double* zhost) {
     if (ex) { rc = fail(KRY_ERR_RECURRENCE, "second pass hit an invariant subspace early"); break; }
   }
   if (rc == KRY_OK && m >= 1) {
-    // coefficient solve m: S_m (and the replay check of coupling m-1)
-    ApplyGramCall ag{ring(m), ldr, n, 1, POST_STEP, 0};
-    rc = run_apply_gram(c, ag);
-    if (rc == KRY_OK) rc = sync_status(c);
+    // coefficient solve m: S_m (and the replay check of coupling m-1); the
+    // last fused launch has done it already
+    if (!(step_on(c) && c->coef_ready && m > 1)) {
+      ApplyGramCall ag{ring(m), ldr, n, 1, POST_STEP, 0};
+      rc = run_apply_gram(c, ag);
+      if (rc == KRY_OK) rc = sync_status(c);
+    }
     if (rc == KRY_OK) rc = gemm_chunk(cb, chunk_first - 1, m - chunk_first + 1);
   }
   if (rc == KRY_OK) {

@@ -145,6 +145,7 @@ enum PostMode {
   POST_CHOL2 = 7,       // explicit path: R2 = chol(V^T V), M[0] = R2^-1, finish
   POST_SCALE = 8,       // explicit path: scale2 = trace
   POST_W2 = 9,          // explicit path: w2 = trace, zero test
+  POST_FUSED = 10,      // fused step kernel: carried blocks + deferred solve of step j+1
 };
 
 struct TStore {  // projected-matrix storage (device), slots of 64 doubles
@@ -205,5 +206,41 @@ int launch_explicit_finish(cudaStream_t st, DevState* dst, const TStore& T, int 
 int launch_post(cudaStream_t st, int post, DevState* dst, const TStore& T);
 
 int gram_grid_for(int64_t n);
+
+// ---------------------------------------------------------------- fused single-pass step
+// One kernel per block-Lanczos step (stencil operators): produces
+// V_{m+1} = V_{m-1} Mo + V_m Mc + (A V_m) Mw chunk by chunk and, trailing the
+// production front by `lag` chunks inside the same launch, consumes it:
+// W0 = A V_{m+1} from the just-written (L2-resident) rows and the Gram blocks
+// [V_m^T V_{m+1} | V_m^T W0 | V_{m+1}^T V_{m+1} | V_{m+1}^T W0 | W0^T W0] of
+// the next coefficient solve, which the last CTA runs (POST_FUSED).  HBM
+// traffic per step: read V_{m-1}, V_m, write V_{m+1} (the three-term minimum).
+struct StepCall {
+  const double* vo;      // V_{m-1} (nullptr at step 1)
+  const double* vc;      // V_m
+  double* vn;            // V_{m+1}
+  int64_t ld;            // point stride of the three ring blocks (= s)
+  double* vn2 = nullptr; // optional second copy of V_{m+1} (pass-2 chunk buffer)
+  int64_t ldn2 = 0;
+  int64_t n = 0;
+  int has_old = 0;
+  int ch = 0;            // points per chunk (multiple of 32)
+  int nch = 0;           // number of chunks
+  int lag = 0;           // consumption lag (chunks; grid strides in the kernel)
+  int reverse = 0;       // chunk order descending (L2 reuse across steps)
+  unsigned epoch = 0;    // flag value published by this launch
+};
+struct StepScratch {
+  double* part = nullptr;     // [grid + grid/32 + 1][320] per-CTA / per-group partials
+  unsigned* gcnt = nullptr;   // [grid/32 + 2] completion counters (self-resetting)
+  unsigned* flags = nullptr;  // [nch] production epochs
+  int nch_cap = 0;            // max grid
+  unsigned epoch = 0;
+};
+// fused-step geometry for an operator of n local points
+void step_geometry(const OpDev& op, int64_t n, int* ch, int* nch, int* lag);
+bool step_supported(const OpDev& op, int s, int64_t ld);
+int launch_step(cudaStream_t st, int s, const OpDev& op, StepCall c, DevState* dst,
+                const TStore& T, StepScratch& sc, float* prof_ms, cudaEvent_t* ev);
 
 }  // namespace kry

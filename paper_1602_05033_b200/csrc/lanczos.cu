@@ -312,7 +312,13 @@ __device__ void extract_block(const double* total, int row0, int s, double* dst)
 
 // The coefficient solve of one fused step (see file header).  Runs on the
 // last CTA of the apply reduction; `total` holds [V^T W0 ; W0^T W0].
-__device__ __noinline__ void coef_solve(const double* total, DevState* st, const TStore& T, double (*sm)[64]) {
+// `row_cw` / `row_ww`: first rows of V_c^T W0 and W0^T W0 in `total`.  With
+// `deferred` (the fused step kernel solves step j+1 ahead of time) a failure
+// only raises KRY_FLAG_FALLBACK: the host then redoes step j+1 on the
+// two-kernel path, which repeats this (idempotent up to the failure point)
+// solve and reports the error at the step the reference reports it.
+__device__ __noinline__ void coef_solve(const double* total, DevState* st, const TStore& T, double (*sm)[64],
+                                        int row_cw, int row_ww, int deferred) {
   const int s = st->s;
   double* Gcc = sm[0]; double* Goc = sm[1]; double* GoW = sm[2]; double* Goo = sm[3];
   double* GcW = sm[4]; double* GWW = sm[5]; double* Sc = sm[6]; double* So = sm[7];
@@ -328,8 +334,8 @@ __device__ __noinline__ void coef_solve(const double* total, DevState* st, const
     double* dst = b == 0 ? Gcc : b == 1 ? Goc : b == 2 ? GoW : b == 3 ? Goo : So;
     dst[e] = src[e];
   }
-  extract_block(total, 0, s, GcW);
-  extract_block(total, s, s, GWW);
+  extract_block(total, row_cw, s, GcW);
+  extract_block(total, row_ww, s, GWW);
   const int j = st->step + 1;        // 1-based step being solved
   const int has_old = st->has_old;
   // 1. lazy CholQR2 correction of the current block: Gcc = R2^T R2, Sc = R2^-1
@@ -341,7 +347,11 @@ __device__ __noinline__ void coef_solve(const double* total, DevState* st, const
   }
   __syncthreads();
   if (s_flag) {  // the stored block is not numerically full rank
-    set_status(st, KRY_ERR_DEFLATION);
+    if (deferred) {
+      if (tid() == 0) st->flags |= KRY_FLAG_FALLBACK;
+    } else {
+      set_status(st, KRY_ERR_DEFLATION);
+    }
     __syncthreads();
     return;
   }
@@ -521,7 +531,21 @@ __device__ __noinline__ void run_post(int post, const double* total, DevState* s
       __syncthreads();
       break;
     case POST_STEP:
-      coef_solve(total, st, T, sm);
+      coef_solve(total, st, T, sm, 0, s, 0);
+      break;
+    case POST_FUSED:
+      // [Goc | GoW | Gcc | GcW | GWW] as five 8x8 blocks (k_step): the
+      // carried blocks of POST_P, then the coefficient solve of step j+1
+      extract_block(total, 0, s, sm[0]);
+      extract_block(total, 8, s, sm[1]);
+      extract_block(total, 16, s, sm[2]);
+      if (tid() < 64) {
+        st->Goc[tid()] = sm[0][tid()];
+        st->GoW[tid()] = sm[1][tid()];
+        st->Gcc[tid()] = sm[2][tid()];
+      }
+      __syncthreads();
+      coef_solve(total, st, T, sm, 24, 32, 1);
       break;
     case POST_INIT: {
       extract_block(total, 0, s, sm[0]);
@@ -692,10 +716,11 @@ __device__ void finish_reduction(const double (&acc)[MP / 8][2], double* sX, dou
     total[e] = sum;
   }
   for (int e = NE + threadIdx.x; e < 256; e += blockDim.x) total[e] = 0.0;
+  constexpr int SMOFF = NE > 256 ? NE : 256;
   __syncthreads();
   if (threadIdx.x == 0) *ticket = 0u;
   // post routine on 8x8 smem scratch carved after `total`
-  double(*sm)[64] = reinterpret_cast<double(*)[64]>(sX + 256);
+  double(*sm)[64] = reinterpret_cast<double(*)[64]>(sX + SMOFF);
   run_post(post, total, st, T, sm);
 }
 
@@ -1478,5 +1503,7 @@ int launch_explicit_finish(cudaStream_t st, DevState* dst, const TStore& T, int 
   KRY_CUDA(cudaGetLastError());
   return KRY_OK;
 }
+
+#include "step.cuh"
 
 }  // namespace kry
