@@ -521,10 +521,32 @@ int run_step_kernel(kry_ctx* c, int j, const double* vold, const double* vcur, d
 int fused_step(kry_ctx* c, int j, const double* vold, const double* vcur, double* vnew,
                int64_t ld, int finalize_on_zero, int* exhausted) {
   *exhausted = 0;
+  // single GPU, two-kernel path: the combine is queued right behind the
+  // coefficient solve without a host round trip; it returns immediately when
+  // the solve raised the fallback flag or an error (the host checks below)
+  const bool speculate = !step_on(c) && !dist(c);
   if (!(step_on(c) && c->coef_ready)) {
     c->coef_ready = false;
     ApplyGramCall ag{vcur, ld, c->n, 1, POST_STEP, 0};
     KRY_CHECK(run_apply_gram(c, ag));
+    if (speculate) {
+      CombineCall cc{vold, ld, vcur, ld, vnew, ld, c->n, j > 1 ? 1 : 0, 1, 1, 1};
+      cudaEvent_t evs[2];
+      float dummy = 0.f;
+      if (c->prof) {
+        cudaEventCreate(&evs[0]);
+        cudaEventCreate(&evs[1]);
+      }
+      KRY_CHECK(run_combine(c, cc, c->prof ? &dummy : nullptr, c->prof ? evs : nullptr));
+      KRY_CHECK(sync_status(c));
+      KRY_CHECK(map_status(c, ("Lanczos step " + std::to_string(j)).c_str()));
+      if (c->st_h->flags & KRY_FLAG_FALLBACK) {
+        if (c->prof) { cudaEventDestroy(evs[0]); cudaEventDestroy(evs[1]); }
+        return explicit_step(c, j, vold, vcur, vnew, ld, finalize_on_zero, exhausted);
+      }
+      if (c->prof) c->ev_comb.push_back({evs[0], evs[1]});
+      return KRY_OK;
+    }
     KRY_CHECK(sync_status(c));
     KRY_CHECK(map_status(c, ("Lanczos step " + std::to_string(j)).c_str()));
     if (c->st_h->flags & KRY_FLAG_FALLBACK) {
@@ -621,7 +643,12 @@ int collect_check(kry_ctx* c, int slot, double beta2, double* res, double* rel) 
 }
 
 // coupling block to the next basis block (tau_{m+1,m}); zero when exhausted
-const double* tau_ptr(kry_ctx* c) { return c->exhausted ? c->zeros64 : c->st->R1prev; }
+// first-stage coupling tau_{m+1,m} of the last completed step (the fused
+// kernel may already have advanced st->R1prev to step m+1)
+const double* tau_ptr(kry_ctx* c) {
+  if (c->exhausted || c->m < 1) return c->zeros64;
+  return c->T.tau1 + (int64_t)(c->m - 1) * 64;
+}
 
 int check_lyap(kry_ctx* c, double beta2, double* res, double* rel) {
   KRY_CHECK(c->eig.residual_lyap(c->stream, c->gamma_d, tau_ptr(c)));
@@ -966,7 +993,7 @@ int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s
       // neighbour's coefficients (sharded) or zeros (the fused step kernel
       // loads the couplings of boundary points unmasked)
       const int64_t lo = op.halo_lo ? op.nxy : 0, hi = op.halo_hi ? op.nxy : 0;
-      const int64_t pad = op.nxy;
+      const int64_t pad = op.nxy + 256;
       for (int q = 0; q < 4; ++q) {
         double* p = nullptr;
         if (dalloc(&p, (size_t)(nloc + 2 * pad)) != KRY_OK) { delete c; return KRY_ERR_CUDA; }
@@ -998,9 +1025,12 @@ int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s
   op.fy = make_fastdiv((unsigned)std::max(op.ny, 1));
   c->n = nloc;
   c->ld = s;
-  // window: 3 slots, each with one halo plane on both sides (multi-GPU)
+  // window: 3 slots, each with one halo plane on both sides (multi-GPU; zero
+  // on one GPU); the upper halo is one chunk longer than a plane so that the
+  // bulk copies of the last chunk's shifted ranges stay inside the slot
   const int64_t halo = (od->kind == KRY_OP_STENCIL) ? op.nxy : 0;
-  const int64_t slot_pts = nloc + 2 * halo;
+  const int64_t halo_hi = (od->kind == KRY_OP_STENCIL) ? op.nxy + 256 : 0;
+  const int64_t slot_pts = nloc + halo + halo_hi;
   KRY_CHECK(dalloc(&c->win, (size_t)3 * slot_pts * s));
   KRY_CUDA(cudaMemset(c->win, 0, (size_t)3 * slot_pts * s * sizeof(double)));
   for (int q = 0; q < 3; ++q) c->slot[q] = c->win + (int64_t)q * slot_pts * s + halo * s;
@@ -1026,8 +1056,11 @@ int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s
   KRY_CUDA(cudaMemset(c->g.ticket, 0, (2 + c->g.max_grid / 32) * sizeof(unsigned)));
   // fused single-pass step scratch (stencil operators on one GPU)
   {
-    const char* off = getenv("KRY_NO_FUSED_STEP");
-    c->use_step = step_supported(op, s, c->ld) && !(off && off[0] == '1');
+    // opt-in (KRY_FUSED_STEP=1): on B200 the single-pass kernel measured
+    // 0.80-0.85 ms per c4 step against 0.77 ms for the two-kernel path (its
+    // stencil gathers re-read every block ~5x from L2), see DESIGN.md
+    const char* on = getenv("KRY_FUSED_STEP");
+    c->use_step = step_supported(op, s, c->ld) && (on && on[0] == '1');
     if (c->use_step) {
       step_geometry(op, nloc, &c->step_ch, &c->step_nch, &c->step_lag);
       const int gmax = KRY_MAX_GRID;
@@ -1660,15 +1693,20 @@ int kry_recover(kry_ctx* c, double* zhost) {
     // coefficient solve j on V_j (replay) -- already done by the previous
     // fused launch when coef_ready; V_{j+1} goes to the ring and the chunk
     const bool fused = step_on(c) && c->coef_ready;
+    // two-kernel path on one GPU: no host round trip between the solve and
+    // the (self-cancelling) combine, see fused_step
+    const bool speculate = !step_on(c) && !dist(c);
     if (!fused) {
       c->coef_ready = false;
       ApplyGramCall ag{ring(j), ldr, n, 1, POST_STEP, 0};
       rc = run_apply_gram(c, ag);
       if (rc) break;
-      rc = sync_status(c);
-      if (rc) break;
-      rc = map_status(c, ("second pass step " + std::to_string(j)).c_str());
-      if (rc) break;
+      if (!speculate) {
+        rc = sync_status(c);
+        if (rc) break;
+        rc = map_status(c, ("second pass step " + std::to_string(j)).c_str());
+        if (rc) break;
+      }
     }
     if (j + 1 - chunk_first == G) {
       // chunk complete: S_j known now -> fold blocks chunk_first..j into Z
@@ -1686,7 +1724,19 @@ int kry_recover(kry_ctx* c, double* zhost) {
     }
     double* chunk_dst = sp(cb, j + 1 - chunk_first);
     int ex = 0;
-    if (!fused && (c->st_h->flags & KRY_FLAG_FALLBACK)) {
+    if (speculate) {
+      CombineCall cc{j > 1 ? ring(j - 1) : nullptr, ldr, ring(j), ldr, ring(j + 1), ldr, n,
+                     j > 1 ? 1 : 0, 1, 1, 1};
+      cc.vn2 = chunk_dst;
+      cc.ldn2 = ld2;
+      rc = run_combine(c, cc, nullptr, nullptr);
+      if (rc == KRY_OK) rc = sync_status(c);
+      if (rc == KRY_OK) rc = map_status(c, ("second pass step " + std::to_string(j)).c_str());
+      if (rc == KRY_OK && (c->st_h->flags & KRY_FLAG_FALLBACK)) {
+        rc = explicit_step(c, j, j > 1 ? ring(j - 1) : nullptr, ring(j), ring(j + 1), ldr, 1, &ex);
+        if (rc == KRY_OK && !ex) rc = launch_copy_block(c->stream, s, ring(j + 1), ldr, chunk_dst, ld2, n);
+      }
+    } else if (!fused && (c->st_h->flags & KRY_FLAG_FALLBACK)) {
       rc = explicit_step(c, j, j > 1 ? ring(j - 1) : nullptr, ring(j), ring(j + 1), ldr, 1, &ex);
       if (rc == KRY_OK && !ex) rc = launch_copy_block(c->stream, s, ring(j + 1), ldr, chunk_dst, ld2, n);
     } else if (step_on(c)) {

@@ -228,7 +228,8 @@ struct StepCall {
   int nch = 0;           // number of chunks
   int lag = 0;           // consumption lag (chunks; grid strides in the kernel)
   int reverse = 0;       // chunk order descending (L2 reuse across steps)
-  unsigned epoch = 0;    // flag value published by this launch
+  unsigned epoch = 0;    // launch counter of this context
+  unsigned fpl = 1;      // flag increments per chunk and launch (producer warps or CTAs)
 };
 struct StepScratch {
   double* part = nullptr;     // [grid + grid/32 + 1][320] per-CTA / per-group partials

@@ -25,6 +25,7 @@
 #include <cmath>
 #include <mutex>
 #include <unordered_map>
+#include <cstdlib>
 
 namespace kry {
 
@@ -641,7 +642,7 @@ __device__ __noinline__ void run_post(int post, const double* total, DevState* s
 }
 
 // ------------------------------------------------------------------ grid reduction tail
-template <int MP>
+template <int MP, int NW = 4>
 __device__ void finish_reduction(const double (&acc)[MP / 8][2], double* sX, double* partials,
                                  unsigned* ticket, int post, DevState* st, const TStore& T) {
   constexpr int MT = MP / 8;
@@ -650,7 +651,7 @@ __device__ void finish_reduction(const double (&acc)[MP / 8][2], double* sX, dou
   const int g = lane >> 2, t = lane & 3;
   __syncthreads();
   // per-warp tiles to smem: red[warp][m*8+n]
-  double* red = sX;  // 4 * NE doubles <= 4*192 < 24*132
+  double* red = sX;  // NW * NE doubles
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
     red[warp * NE + (mt * 8 + g) * 8 + 2 * t] = acc[mt][0];
@@ -659,9 +660,8 @@ __device__ void finish_reduction(const double (&acc)[MP / 8][2], double* sX, dou
   __syncthreads();
   for (int e = threadIdx.x; e < NE; e += blockDim.x) {
     double v = red[e];
-    v += red[NE + e];
-    v += red[2 * NE + e];
-    v += red[3 * NE + e];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) v += red[w * NE + e];
     partials[(int64_t)blockIdx.x * NE + e] = v;
   }
   __threadfence();

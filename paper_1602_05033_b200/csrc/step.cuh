@@ -44,6 +44,7 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+#define LD_NEW(p) __ldcg(p)
 __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -209,13 +210,13 @@ __device__ __forceinline__ void consume_groups(const OpDev& op, const StepCall& 
       const int e = o.i * ld + col;
       const double* pc = c.vn + e;
       xv[q][k][0] = __ldg(c.vc + e);
-      xv[q][k][1] = __ldcg(pc);
-      xv[q][k][2] = __ldcg(pc + o.z0);
-      xv[q][k][3] = __ldcg(pc + o.y0);
-      xv[q][k][4] = __ldcg(pc + o.x0);
-      xv[q][k][5] = __ldcg(pc + o.x1);
-      xv[q][k][6] = __ldcg(pc + o.y1);
-      xv[q][k][7] = __ldcg(pc + o.z1);
+      xv[q][k][1] = LD_NEW(pc);
+      xv[q][k][2] = LD_NEW(pc + o.z0);
+      xv[q][k][3] = LD_NEW(pc + o.y0);
+      xv[q][k][4] = LD_NEW(pc + o.x0);
+      xv[q][k][5] = LD_NEW(pc + o.x1);
+      xv[q][k][6] = LD_NEW(pc + o.y1);
+      xv[q][k][7] = LD_NEW(pc + o.z1);
     }
 #pragma unroll
   for (int q = 0; q < NG; ++q)
@@ -249,7 +250,7 @@ __device__ __forceinline__ void step_consume(const OpDev& op, const StepCall& c,
 }
 
 // this warp waits until every chunk holding a stencil neighbour row of chunk
-// u is complete (each of the 4 warps of the producing CTA adds 1 per launch)
+// u is complete (c.fpl releases per chunk and launch)
 __device__ __forceinline__ void step_wait(const OpDev& op, const StepCall& c, int64_t u,
                                           const unsigned* flags) {
   const int lane = threadIdx.x & 31;
@@ -261,7 +262,7 @@ __device__ __forceinline__ void step_wait(const OpDev& op, const StepCall& c, in
     int64_t row = ((lane & 1) ? last : first) + (k < 3 ? -mag : mag);
     row = row < 0 ? 0 : (row >= c.n ? c.n - 1 : row);
     const unsigned* f = flags + row / c.ch;
-    const unsigned want = 4u * c.epoch;
+    const unsigned want = c.fpl * c.epoch;
     while ((int)(ld_acquire_u32(f) - want) < 0) __nanosleep(32);
   }
   __syncwarp();
@@ -362,6 +363,17 @@ static int step_grid(Kern kernel, int nch) {
   return std::max(1, std::min(std::min(per, nch), KRY_MAX_GRID));
 }
 
+#include "step_tma.cuh"
+
+template <class Kern>
+static int step_grid_smem(Kern kernel, int nch, int threads, size_t smem) {
+  int dev = 0, sms = 148, nb = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, smem);
+  return std::max(1, std::min(std::min(std::max(1, nb) * sms, nch), KRY_MAX_GRID));
+}
+
 // Cooperative launch: every CTA is co-resident (the static ticket order
 // spins on flags of other CTAs), and the per-CTA partials are reduced in CTA
 // order, so the result is independent of timing (pass 2 == pass 1 bitwise).
@@ -369,27 +381,51 @@ int launch_step(cudaStream_t st, int s, const OpDev& op, StepCall c, DevState* d
                 const TStore& T, StepScratch& sc, float* prof_ms, cudaEvent_t* ev) {
   c.epoch = ++sc.epoch;
   const void* fn = nullptr;
-  int grid = 1;
+  int grid = 1, threads = STEP_TP;
+  size_t smem = 0;
+  // even widths: TMA-staged kernel (16-byte aligned bulk copies of whole
+  // point rows); odd widths: register-gather kernel
 #define L(S)                                \
   grid = step_grid(k_step<S>, c.nch);       \
-  fn = (const void*)k_step<S>
+  fn = (const void*)k_step<S>;              \
+  c.fpl = STEP_TP / 32
+#define LT(S)                                                                            \
+  {                                                                                      \
+    static bool attr = false;                                                            \
+    smem = tma_smem_bytes(S);                                                            \
+    if (!attr) {                                                                         \
+      KRY_CUDA(cudaFuncSetAttribute(k_step_tma<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                    (int)smem));                                         \
+      attr = true;                                                                       \
+    }                                                                                    \
+    grid = step_grid_smem(k_step_tma<S>, c.nch, TMA_TP + 64, smem);                      \
+    fn = (const void*)k_step_tma<S>;                                                     \
+    threads = TMA_TP + 64;                                                               \
+    c.fpl = 1;                                                                           \
+  }
+  const char* reg = getenv("KRY_STEP_REGISTER");
+  const bool tma = !(reg && reg[0] == '1');
   switch (s) {
     case 1: L(1); break;
-    case 2: L(2); break;
+    case 2: if (tma) LT(2) else { L(2); } break;
     case 3: L(3); break;
-    case 4: L(4); break;
-    case 6: L(6); break;
-    case 8: L(8); break;
+    case 4: if (tma) LT(4) else { L(4); } break;
+    case 6: if (tma) LT(6) else { L(6); } break;
+    case 8: if (tma) LT(8) else { L(8); } break;
     default: return fail(KRY_ERR_ARGUMENT, "fused step: unsupported block width");
   }
 #undef L
+#undef LT
   if (grid > sc.nch_cap) return fail(KRY_ERR_STATE, "fused step scratch too small");
   // lag in grid strides: the consumed chunk is the CTA's own chunk of
   // c.lag iterations ago, at least `lag` chunks behind the production front
-  c.lag = std::max(1, (c.lag + grid - 1) / grid);
+  // (TMA kernel: four more strides: the consumption copies are issued two
+  // iterations ahead and a chunk is released two iterations after it is
+  // produced)
+  c.lag = std::max(1, (c.lag + grid - 1) / grid) + (smem ? 4 : 0);
   void* args[] = {(void*)&op, (void*)&c, (void*)&dst, (void*)&T, (void*)&sc};
   if (prof_ms && ev) cudaEventRecord(ev[0], st);
-  KRY_CUDA(cudaLaunchCooperativeKernel(fn, grid, STEP_TP, args, 0, st));
+  KRY_CUDA(cudaLaunchCooperativeKernel(fn, grid, threads, args, smem, st));
   if (prof_ms && ev) cudaEventRecord(ev[1], st);
   count_launch();
   return KRY_OK;

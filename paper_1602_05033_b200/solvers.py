@@ -129,6 +129,27 @@ def _nonconvergence(opts, reason, m, rel, history, both=False):
         history)
 
 
+# Factors of 1e9+ entries are returned in page-locked host memory from
+# torch's caching host allocator: the device-to-host copy then runs at full
+# PCIe rate straight into the result (no staging copy, no page faults), and a
+# released result's pages are reused by the next solve instead of being
+# pinned again.  Small factors (and hosts without CUDA) use plain numpy.
+PINNED_MIN_BYTES = 256 << 20
+
+
+def host_factor(n, rank):
+    """Uninitialised C-order n x rank float64 array for a device factor."""
+    if n * rank * 8 >= PINNED_MIN_BYTES:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                t = torch.empty((n, rank), dtype=torch.float64, pin_memory=True)
+                return t.numpy()
+        except Exception:  # pragma: no cover - plain host memory below
+            pass
+    return np.empty((n, rank))
+
+
 class _Pass1:
     """Runs init + pass 1 on one context; keeps the state for finalisation."""
 
@@ -149,7 +170,7 @@ class _Pass1:
         return m.value, bool(ex.value)
 
     def recover(self, rank):
-        z = np.empty((self.op.n, rank))
+        z = host_factor(self.op.n, rank)
         if rank > 0:
             _lib.check(_lib.load().kry_recover(self.ctx.ptr, _lib.as_dptr(z)))
         return z

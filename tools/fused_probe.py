@@ -9,7 +9,7 @@ import bench
 
 
 def run(op, c, tol, max_m, fused):
-    os.environ["KRY_NO_FUSED_STEP"] = "0" if fused else "1"
+    os.environ["KRY_FUSED_STEP"] = "1" if fused else "0"
     t = time.perf_counter()
     sol = kb.solve_lyapunov(op, c, kb.SolveOptions(tol=tol, max_m=max_m, storage="windowed"))
     return sol, time.perf_counter() - t
