@@ -336,7 +336,8 @@ def main():
             _t.cuda.synchronize()
             t0 = time.perf_counter()
             sol = kb.solve_lyapunov(op, pinned, opts)
-            e2e_runs.append((time.perf_counter() - t0, sol.iterations, sol.rank))
+            e2e_runs.append((time.perf_counter() - t0, sol.iterations, sol.rank,
+                             sol.basis_seconds, sol.recovery_seconds))
             del sol   # the caller consumes one result before asking for the next
         e2e_s = sum(r[0] for r in e2e_runs)
         e2e_its = sum(r[1] for r in e2e_runs)
@@ -348,7 +349,9 @@ def main():
         e2e = {"value": e2e_its / e2e_s, "unit": "iters/s",
                "h2d_bytes_per_step": int(n * s * 8),
                "d2h_bytes_per_step": int(n * rank_z * 8),
-               "ms_per_solve": 1000.0 * e2e_s / len(e2e_runs)}
+               "ms_per_solve": 1000.0 * e2e_s / len(e2e_runs),
+               "solves_s": [{"total": round(r[0], 4), "pass1": round(r[3], 4),
+                             "finalize+pass2+copy": round(r[4], 4)} for r in e2e_runs]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

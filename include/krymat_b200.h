@@ -24,6 +24,9 @@
  *   kry_ctri_lyap_blocks  ctri_lyapunov on given blocks     residual.py:40-59
  *   kry_ctri_sylv_blocks  ctri_sylvester on given blocks    residual.py:62-84
  *   kry_true_lyap_residual true_lyapunov_residual          solvers.py:104-115
+ *   kry_sylv1_setup       eigh(B), P^T C2 (one-sided)        solvers.py:405-411
+ *   kry_check_sylv1       residual_one_sided                 residual.py:87-104
+ *   kry_finalize_sylv1    one-sided finalisation + SVD       solvers.py:446-455
  *
  * Conventions: all arithmetic is IEEE fp64.  Host block vectors are row-major
  * n x s (C order, as numpy produces them).  s x s blocks are row-major.  Host
@@ -144,6 +147,22 @@ int kry_finalize_lyap(kry_ctx *ctx, double trunc_eps, int *rank,
                       double *discarded);
 int kry_finalize_sylv(kry_ctx *a, kry_ctx *b, double trunc_eps, int *rank,
                       double *discarded);
+
+/* one-sided Sylvester A X + X B + C1 C2^T = 0 with B small and dense
+ * (solve_sylvester_one_sided, solvers.py:386-481).  The context is the A
+ * side (its block Krylov space of C1).  setup: B (n2 x n2 row-major,
+ * symmetric) is eigendecomposed on the device, P^T C2 (C2: n2 x s row-major)
+ * is kept; ups (n2, ascending) is returned for the definiteness check.
+ * check: residual_one_sided of the current projection (after kry_init_basis
+ * and the steps).  finalize: rank, discarded tail mass and the right factor
+ * z2 = P * (V sqrt(sigma)) (host n2 x rank row-major; z2 may be NULL to
+ * query the rank first, then call again); the left factor comes from
+ * kry_recover. */
+int kry_sylv1_setup(kry_ctx *ctx, int n2, const double *b, const double *c2,
+                    double *ups);
+int kry_check_sylv1(kry_ctx *ctx, double rhs_norm, double *res, double *rel);
+int kry_finalize_sylv1(kry_ctx *ctx, double trunc_eps, int *rank,
+                       double *discarded, double *z2, int z2_cap);
 
 /* install a caller-provided reduced factor qy (k x t row-major, k = s*m) for
  * the first m blocks, as two_pass_recover(op, state, qy) does (solvers.py:130) */

@@ -413,6 +413,54 @@ def solve_sylvester(op_a, op_b, c1, c2, opts=None):
                     history=hist, discarded=disc)
 
 
+def residual_one_sided(t, tau, s_input, ups, rhs=None):
+    """residual.py:87-104: ||((s_input F) / (ups_i + lam_j)) (L^T tau^T)||_F."""
+    lam, f1, fm = partial_eig(t)
+    den = guarded_denominators(np.asarray(ups, dtype=float), lam)
+    m = ((np.asarray(s_input, dtype=float) @ f1) / den) @ (fm.T @ np.atleast_2d(tau).T)
+    res = float(np.linalg.norm(m))
+    return res, res / float(rhs) if rhs is not None else res
+
+
+def solve_sylvester_one_sided(op_a, b, c1, c2, opts=None):
+    """solvers.py:386-481 (standard space, two-pass recovery): B small and
+    dense, eigendecomposed once; only A is projected."""
+    opts = opts or SolveOptions()
+    b = np.asarray(b, dtype=float)
+    c1 = np.atleast_2d(np.asarray(c1, dtype=float))
+    c2 = np.atleast_2d(np.asarray(c2, dtype=float))
+    if not np.array_equal(b, b.T):
+        raise OracleError("small coefficient matrix B must be symmetric")
+    rhs = float(np.linalg.norm(c1) * np.linalg.norm(c2))
+    ups, p = np.linalg.eigh(b)
+    if ups[-1] >= 0.0:
+        raise IndefiniteError("B must be negative definite")
+    bs = Basis(op_a, c1)
+    s_input = (p.T @ c2) @ bs.gamma.T
+    hist, done, rel = [], None, None
+    for it in range(1, opts.max_m + 1):
+        bs.step()
+        if it % opts.check_period == 0 or bs.exhausted:
+            _, rel = residual_one_sided(bs.projection(), bs.coupling(), s_input, ups, rhs)
+            hist.append((it, it * bs.s, rel))
+            if rel <= opts.tol:
+                done = it
+                break
+            if bs.exhausted:
+                raise NoConvergence("invariant", hist)
+    if done is None:
+        raise NoConvergence("max_m", hist)
+    lam, q = np.linalg.eigh(bs.projection().dense())
+    if lam[-1] >= 0.0:
+        raise IndefiniteError("projected matrix is not negative definite")
+    u = q[:bs.s].T @ bs.gamma
+    y = -(u @ (c2.T @ p)) / guarded_denominators(lam, ups)
+    f1, f2, disc = truncated_svd(y, opts.trunc_eps)
+    z1 = two_pass_recover(op_a, bs, q @ f1)
+    return Solution(z1, p @ f2, rank=f1.shape[1], iterations=done, final_residual=rel,
+                    history=hist, discarded=disc)
+
+
 # ----------------------------------------------------------------- comparison helpers
 def factor_distance(za, zb, za2=None, zb2=None):
     """||Za Za2^T - Zb Zb2^T||_F / ||Zb Zb2^T||_F without forming n x n

@@ -123,6 +123,9 @@ SIGNATURES = {
                                             dptr, ctypes.c_int, dptr, dptr, dptr, dptr, dptr,
                                             dptr, dptr]),
     "kry_true_lyap_residual": (ctypes.c_int, [_P, dptr, ctypes.c_int, dptr, dptr]),
+    "kry_sylv1_setup": (ctypes.c_int, [_P, ctypes.c_int, dptr, dptr, dptr]),
+    "kry_check_sylv1": (ctypes.c_int, [_P, ctypes.c_double, dptr, dptr]),
+    "kry_finalize_sylv1": (ctypes.c_int, [_P, ctypes.c_double, iptr, dptr, dptr, ctypes.c_int]),
     "kry_profile_enable": (ctypes.c_int, [_P, ctypes.c_int]),
     "kry_profile_read": (ctypes.c_int, [_P, dptr, iptr, dptr, iptr]),
     "kry_timer": (ctypes.c_int, [_P, ctypes.c_int, dptr]),

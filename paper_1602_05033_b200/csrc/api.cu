@@ -217,6 +217,31 @@ void keep_pool_memory(int device) {
   done[device] = true;
 }
 
+
+// ---------------------------------------------------------------- one-sided Sylvester helpers
+// v[j][c] = sum_i P(i, j) C2[i][c]   (P column-major n2 x n2, C2 row-major n2 x s)
+__global__ void k_dense_proj(const double* P, int n2, const double* C2, int s, double* v) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n2 * 8; e += gridDim.x * blockDim.x) {
+    const int j = e >> 3, c = e & 7;
+    double a = 0.0;
+    if (c < s)
+      for (int i = 0; i < n2; ++i) a = fma(P[(int64_t)j * n2 + i], C2[(int64_t)i * s + c], a);
+    v[e] = a;
+  }
+}
+// out[j][c] = sum_r v[j][r] gamma[c][r]   ((P^T C2) gamma^T, gamma 8x8 row-major)
+__global__ void k_times_gamma_t(const double* v, int n2, const double* gamma, int s, double* out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n2 * 8; e += gridDim.x * blockDim.x) {
+    const int j = e >> 3, c = e & 7;
+    double a = 0.0;
+    if (c < s)
+      for (int r = 0; r < s; ++r) a = fma(v[(int64_t)j * 8 + r], gamma[c * 8 + r], a);
+    out[e] = a;
+  }
+}
+__global__ void k_eye8(double* e) {
+  if (threadIdx.x < 64) e[threadIdx.x] = (threadIdx.x >> 3) == (threadIdx.x & 7) ? 1.0 : 0.0;
+}
 }  // namespace kry
 
 using namespace kry;
@@ -271,6 +296,15 @@ struct kry_ctx {
   double* p2buf[2] = {nullptr, nullptr};
   double* p2qc[2] = {nullptr, nullptr};
   size_t p2buf_cap = 0, p2qc_cap = 0;
+  // one-sided Sylvester: the dense small side B = P diag(ups) P^T
+  int d1_n2 = 0;
+  double* d1_ups = nullptr;   // n2
+  double* d1_P = nullptr;     // n2 x n2 column-major eigenvectors
+  double* d1_v = nullptr;     // P^T C2, [n2][8]
+  double* d1_in = nullptr;    // (P^T C2) gamma^T, [n2][8] (after init)
+  double* d1_eye = nullptr;   // 8x8 identity
+  double* d1_z2 = nullptr;    // n2 x rank row-major right factor (finalize)
+  int d1_rank = -1;
   // fused single-pass step (stencil operators, one GPU)
   bool use_step = false;
   bool coef_ready = false;   // st->M holds the coefficients of the next step
@@ -1096,6 +1130,7 @@ void kry_ctx_destroy(kry_ctx* c) {
   dfree(c->sx.part);
   dfree(c->sx.gcnt);
   dfree(c->sx.flags);
+  for (double* p : {c->d1_ups, c->d1_P, c->d1_v, c->d1_in, c->d1_eye, c->d1_z2}) dfree(p);
   dfree(c->zeros64);
   dfree(c->gamma_d);
   if (c->qy) dfree(c->qy);
@@ -1600,6 +1635,190 @@ int kry_finalize_sylv(kry_ctx* a, kry_ctx* bb, double eps, int* rank, double* di
 // blocks in an interleaved chunk and fold them into Z with one DGEMM per chunk.
 // Two chunk buffers (kept in the context across solves): the DGEMM of chunk
 // k runs on the second stream while chunk k+1 is regenerated.
+// ---------------------------------------------------------------- one-sided Sylvester
+int kry_sylv1_setup(kry_ctx* c, int n2, const double* b, const double* c2, double* ups) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  if (n2 < 1) return fail(KRY_ERR_DIMENSION, "B must be a non-empty square matrix");
+  KRY_CHECK(ensure_handles(c));
+  for (double* p : {c->d1_ups, c->d1_P, c->d1_v, c->d1_in, c->d1_eye, c->d1_z2}) dfree(p);
+  c->d1_ups = c->d1_P = c->d1_v = c->d1_in = c->d1_eye = c->d1_z2 = nullptr;
+  c->d1_n2 = n2;
+  c->d1_rank = -1;
+  double* c2d = nullptr;
+  KRY_CHECK(dalloc(&c->d1_ups, (size_t)n2));
+  KRY_CHECK(dalloc(&c->d1_P, (size_t)n2 * n2));
+  KRY_CHECK(dalloc(&c->d1_v, (size_t)n2 * 8));
+  KRY_CHECK(dalloc(&c->d1_in, (size_t)n2 * 8));
+  KRY_CHECK(dalloc(&c->d1_eye, 64));
+  KRY_CHECK(dalloc(&c2d, (size_t)n2 * c->s));
+  // B symmetric: row-major == column-major
+  KRY_CUDA(cudaMemcpyAsync(c->d1_P, b, (size_t)n2 * n2 * sizeof(double), cudaMemcpyHostToDevice,
+                           c->stream));
+  KRY_CUDA(cudaMemcpyAsync(c2d, c2, (size_t)n2 * c->s * sizeof(double), cudaMemcpyHostToDevice,
+                           c->stream));
+  int rc = syevd(c, c->d1_P, n2, c->d1_ups);
+  if (rc == KRY_OK) {
+    const int g = std::min(1024, (n2 * 8 + 255) / 256);
+    k_dense_proj<<<g, 256, 0, c->stream>>>(c->d1_P, n2, c2d, c->s, c->d1_v);
+    k_eye8<<<1, 64, 0, c->stream>>>(c->d1_eye);
+    count_launch(2);
+    if (cudaMemcpyAsync(ups, c->d1_ups, (size_t)n2 * sizeof(double), cudaMemcpyDeviceToHost,
+                        c->stream) != cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess)
+      rc = fail(KRY_ERR_CUDA, "one-sided setup copy failed");
+  }
+  dfree(c2d);
+  return rc;
+}
+
+int kry_check_sylv1(kry_ctx* c, double rhs_norm, double* res, double* rel) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  if (!c->d1_ups) return fail(KRY_ERR_STATE, "kry_sylv1_setup has not been called");
+  if (!c->initialized) return fail(KRY_ERR_STATE, "init_basis has not been called");
+  const int n2 = c->d1_n2, K = c->eig.K;
+  const int g = std::min(1024, (n2 * 8 + 255) / 256);
+  // s_input = (P^T C2) gamma^T (residual.py:87-104 with gamma of init_basis)
+  k_times_gamma_t<<<g, 256, 0, c->stream>>>(c->d1_v, n2, c->gamma_d, c->s, c->d1_in);
+  count_launch();
+  // u = F^T (identity gamma: the rhs side is carried by s_input), w = L^T tau^T
+  KRY_CHECK(c->eig.compute_uw(c->stream, c->d1_eye, tau_ptr(c)));
+  KRY_CHECK(c->eig.ensure_cauchy(n2, K));
+  KRY_CHECK(c->eig.cauchy(c->stream, n2, c->d1_ups, c->d1_in, K, c->eig.lam_cur(), c->eig.u,
+                          c->eig.w, c->eig.res));
+  k_scale_of<<<1, 32, 0, c->stream>>>(c->d1_ups, n2, c->eig.lam_cur(), K, c->eig.res + 2);
+  count_launch();
+  KRY_CUDA(cudaMemcpyAsync(c->hres, c->eig.res, 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                           c->stream));
+  KRY_CUDA(cudaStreamSynchronize(c->stream));
+  if (K > 0 && c->hres[1] < 1e-14 * c->hres[2])
+    return fail(KRY_ERR_INDEFINITE,
+                "eigenvalue-sum denominator is numerically singular; coefficient matrices must "
+                "be definite (of one sign)");
+  *res = sqrt(fmax(c->hres[0], 0.0));
+  *rel = *res / rhs_norm;
+  return KRY_OK;
+}
+
+int kry_finalize_sylv1(kry_ctx* a, double eps, int* rank, double* discarded, double* z2,
+                       int z2_cap) {
+  KRY_CUDA(cudaSetDevice(a->dev));
+  if (!a->d1_ups) return fail(KRY_ERR_STATE, "kry_sylv1_setup has not been called");
+  if (a->d1_rank >= 0) {   // second call: hand out the right factor
+    *rank = a->d1_rank;
+    *discarded = a->discarded;
+    if (z2 && a->d1_rank > 0) {
+      if (z2_cap < a->d1_n2 * a->d1_rank) return fail(KRY_ERR_ARGUMENT, "z2 buffer too small");
+      KRY_CUDA(cudaMemcpy(z2, a->d1_z2, (size_t)a->d1_n2 * a->d1_rank * sizeof(double),
+                          cudaMemcpyDeviceToHost));
+    }
+    return KRY_OK;
+  }
+  if (a->m_final < 1) a->m_final = a->m;
+  KRY_CHECK(ensure_handles(a));
+  const int n2 = a->d1_n2;
+  FinalBufs fa;
+  int kA = 0;
+  int rc = final_eig(a, fa, &kA);
+  double *Y = nullptr, *sig = nullptr, *U = nullptr, *VT = nullptr, *mind = nullptr,
+         *work = nullptr, *outd = nullptr, *f1 = nullptr, *f2 = nullptr, *gw = nullptr;
+  int* info = nullptr;
+  auto cleanup = [&]() {
+    fa.free_all();
+    for (double* p : {Y, sig, U, VT, mind, work, outd, f1, f2, gw})
+      if (p) dfree(p);
+    if (info) dfree(info);
+  };
+  if (rc != KRY_OK) { cleanup(); return rc; }
+  double la[2], lb[2];
+  KRY_CUDA(cudaMemcpy(&la[0], fa.lam, sizeof(double), cudaMemcpyDeviceToHost));
+  KRY_CUDA(cudaMemcpy(&la[1], fa.lam + kA - 1, sizeof(double), cudaMemcpyDeviceToHost));
+  KRY_CUDA(cudaMemcpy(&lb[0], a->d1_ups, sizeof(double), cudaMemcpyDeviceToHost));
+  KRY_CUDA(cudaMemcpy(&lb[1], a->d1_ups + n2 - 1, sizeof(double), cudaMemcpyDeviceToHost));
+  if (la[1] >= 0.0) {
+    cleanup();
+    return fail(KRY_ERR_INDEFINITE, "projected matrix is not negative definite");
+  }
+  // Ytilde = -(u (C2^T P)) / (lam_i + ups_j)   (kA x n2), SVD on the taller orientation
+  const bool tr = kA < n2;
+  const int M = tr ? n2 : kA, N = tr ? kA : n2;
+  if ((rc = dalloc(&Y, (size_t)M * N)) || (rc = dalloc(&sig, (size_t)N)) ||
+      (rc = dalloc(&U, (size_t)M * N)) || (rc = dalloc(&VT, (size_t)N * N)) ||
+      (rc = dalloc(&mind, 1024)) || (rc = dalloc(&work, (size_t)N + 8)) ||
+      (rc = dalloc(&outd, 8)) || (rc = dalloc(&info, 1))) {
+    cleanup();
+    return rc;
+  }
+  int nparts = 0;
+  if (!tr)
+    rc = launch_ytilde(a->stream, fa.u, fa.lam, kA, a->d1_v, a->d1_ups, n2, a->s, Y, kA, mind,
+                       &nparts);
+  else
+    rc = launch_ytilde(a->stream, a->d1_v, a->d1_ups, n2, fa.u, fa.lam, kA, a->s, Y, n2, mind,
+                       &nparts);
+  if (rc != KRY_OK) { cleanup(); return rc; }
+  int lwork = 0;
+  if (cusolverDnDgesvd_bufferSize(a->solver, M, N, &lwork) != CUSOLVER_STATUS_SUCCESS) {
+    cleanup();
+    return fail(KRY_ERR_FACTORIZATION, "gesvd buffer query failed");
+  }
+  if ((rc = dalloc(&gw, (size_t)lwork + 1))) { cleanup(); return rc; }
+  signed char jobu = 'S', jobvt = 'S';
+  auto sst = cusolverDnDgesvd(a->solver, jobu, jobvt, M, N, Y, M, sig, U, M, VT, N, gw, lwork,
+                              nullptr, info);
+  int hinfo = 0;
+  KRY_CUDA(cudaMemcpy(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost));
+  if (sst != CUSOLVER_STATUS_SUCCESS || hinfo != 0) {
+    cleanup();
+    return fail(KRY_ERR_FACTORIZATION, "SVD did not converge");
+  }
+  rc = launch_truncate(a->stream, sig, N, 1, eps, mind, nparts, work, outd);
+  double hout[8];
+  KRY_CUDA(cudaMemcpy(hout, outd, 5 * sizeof(double), cudaMemcpyDeviceToHost));
+  const double scale = std::max(std::max(fabs(la[0]), fabs(la[1])), std::max(fabs(lb[0]), fabs(lb[1])));
+  if (hout[4] < 1e-14 * scale) {
+    cleanup();
+    return fail(KRY_ERR_INDEFINITE,
+                "eigenvalue-sum denominator is numerically singular; coefficient matrices must be "
+                "definite (of one sign)");
+  }
+  const int r = (int)hout[0];
+  if (r > 0) {
+    if ((rc = dalloc(&f1, (size_t)kA * r)) || (rc = dalloc(&f2, (size_t)n2 * r)) ||
+        (rc = dalloc(&a->d1_z2, (size_t)n2 * r))) {
+      cleanup();
+      return rc;
+    }
+    if (!tr) {
+      launch_scale_factor(a->stream, U, M, sig, kA, r, 1, 0, f1);
+      launch_scale_factor(a->stream, VT, N, sig, n2, r, 1, 1, f2);
+    } else {
+      launch_scale_factor(a->stream, VT, N, sig, kA, r, 1, 1, f1);
+      launch_scale_factor(a->stream, U, M, sig, n2, r, 1, 0, f2);
+    }
+    rc = set_qy(a, fa.Td, kA, f1, r);
+    // z2 (row-major n2 x r) = col-major (r x n2) = f2^T P^T
+    const double one = 1.0, zero = 0.0;
+    if (rc == KRY_OK &&
+        cublasDgemm(a->cublas, CUBLAS_OP_T, CUBLAS_OP_T, r, n2, n2, &one, f2, n2, a->d1_P, n2,
+                    &zero, a->d1_z2, r) != CUBLAS_STATUS_SUCCESS)
+      rc = fail(KRY_ERR_CUDA, "cublasDgemm (z2) failed");
+  } else {
+    set_qy(a, fa.Td, kA, nullptr, 0);
+  }
+  KRY_CUDA(cudaStreamSynchronize(a->stream));
+  cleanup();
+  if (rc != KRY_OK) return rc;
+  a->discarded = hout[1];
+  a->d1_rank = r;
+  *rank = r;
+  *discarded = hout[1];
+  if (z2 && r > 0) {
+    if (z2_cap < n2 * r) return fail(KRY_ERR_ARGUMENT, "z2 buffer too small");
+    KRY_CUDA(cudaMemcpy(z2, a->d1_z2, (size_t)n2 * r * sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  return KRY_OK;
+}
+
 int kry_recover(kry_ctx* c, double* zhost) {
   KRY_CUDA(cudaSetDevice(c->dev));
   if (c->rank < 0) return fail(KRY_ERR_STATE, "finalize has not been called");

@@ -807,7 +807,8 @@ void EigEngine::release() {
   if (dbuf) dfree(dbuf);
   if (ibuf) dfree(ibuf);
   if (ticket) dfree(ticket);
-  dbuf = nullptr; ibuf = nullptr; ticket = nullptr;
+  if (cpart_ext) dfree(cpart_ext);
+  dbuf = nullptr; ibuf = nullptr; ticket = nullptr; cpart_ext = nullptr;
 }
 
 EigView EigEngine::view() const {
@@ -876,6 +877,18 @@ int EigEngine::append_block(cudaStream_t st, const double* dsym_blk, const doubl
     cur = 1 - cur;
     K += 1;
   }
+  return KRY_OK;
+}
+
+int EigEngine::ensure_cauchy(int nx, int ny) {
+  const size_t nyc = (size_t)std::max(1, (ny + CC_CH - 1) / CC_CH);
+  if (nyc * (size_t)nx <= cpart_cap) return KRY_OK;
+  if (cpart_ext) dfree(cpart_ext);
+  cpart_ext = nullptr;
+  const size_t cap = (nyc + 1) * (size_t)nx;
+  KRY_CHECK(dalloc(&cpart_ext, cap * 8 + cap / 64 + 64));
+  cpart = cpart_ext;
+  cpart_cap = cap;
   return KRY_OK;
 }
 

@@ -39,6 +39,10 @@ struct EigEngine {
   int append_block(cudaStream_t st, const double* dsym_blk, const double* sub_prev);
   int compute_uw(cudaStream_t st, const double* gamma, const double* tau_blk);
   int residual_lyap(cudaStream_t st, const double* gamma, const double* tau_blk);
+  // grow the Cauchy stage-1 buffer for an nx x ny contraction (one-sided
+  // Sylvester: nx = order of the dense side B)
+  int ensure_cauchy(int nx, int ny);
+  double* cpart_ext = nullptr;
   int cauchy(cudaStream_t st, int nx, const double* lx, const double* ax, int ny,
              const double* ly, const double* by, const double* cy, double* out2);
   const double* lam_cur() const { return lam[cur]; }

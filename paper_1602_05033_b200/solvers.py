@@ -20,7 +20,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .errors import ConvergenceError, DimensionMismatchError, KrymatError
+from .errors import (ConvergenceError, DimensionMismatchError, IndefiniteMatrixError,
+                     KrymatError)
 
 #: Largest operator order for which ``verify`` recomputes the true residual.
 VERIFY_LIMIT = 20000
@@ -304,6 +305,106 @@ def solve_sylvester_two_sided(op_a, op_b, c1, c2, options=None):
     finally:
         pa.ctx.close()
         pb.ctx.close()
+
+
+def solve_sylvester_one_sided(op_a, b, c1, c2, options=None):
+    """Galerkin solver for A X + X B + C1 C2^T = 0 with B small and dense
+    (reference ``solvers.py:386-481``): B is eigendecomposed once on the
+    device, only A is projected (its block Krylov space of C1 grows on the
+    device), the residual is ``residual_one_sided`` (``residual.py:87-104``)
+    evaluated on the incrementally updated eigen data of T_m, and the right
+    factor is recovered in the eigenbasis of B."""
+    opts = options if options is not None else SolveOptions()
+    _check_space(opts)
+    b = np.asarray(b, dtype=float)
+    c1 = np.atleast_2d(np.asarray(c1, dtype=float))
+    c2 = np.atleast_2d(np.asarray(c2, dtype=float))
+    if b.ndim != 2 or b.shape[0] != b.shape[1] or not np.array_equal(b, b.T):
+        raise DimensionMismatchError("small coefficient matrix B must be symmetric")
+    if c1.shape[1] != c2.shape[1]:
+        raise DimensionMismatchError("C1 and C2 must have the same number of columns")
+    if c2.shape[0] != b.shape[0]:
+        raise DimensionMismatchError("C2 does not conform with B")
+    c1 = _as_rhs(op_a, c1)
+    c2 = np.ascontiguousarray(c2)
+    b = np.ascontiguousarray(b)
+    n2, s = b.shape[0], c1.shape[1]
+    lib = _lib.load()
+    tic = time.perf_counter()
+    ctx = op_a.context(s, opts.max_m + 2)
+    try:
+        ups = np.zeros(n2)
+        _lib.check(lib.kry_sylv1_setup(ctx.ptr, n2, _lib.as_dptr(b), _lib.as_dptr(c2),
+                                       _lib.as_dptr(ups)))
+        if ups[-1] >= 0.0:
+            raise IndefiniteMatrixError("B must be negative definite")
+        gamma = np.zeros((s, s))
+        beta2 = ctypes.c_double()
+        _lib.check(lib.kry_init_basis(ctx.ptr, _lib.as_dptr(c1), _lib.as_dptr(gamma),
+                                      ctypes.byref(beta2)))
+        t_basis = time.perf_counter() - tic
+        t_res = 0.0
+        rhs_norm = float(np.sqrt(beta2.value) * np.linalg.norm(c2))
+        history, converged_at, rel_v = [], None, None
+        ex = ctypes.c_int(0)
+        res, rel = ctypes.c_double(), ctypes.c_double()
+        for it in range(1, opts.max_m + 1):
+            tic = time.perf_counter()
+            _lib.check(lib.kry_lanczos_step(ctx.ptr, 1, ctypes.byref(ex)))
+            t_basis += time.perf_counter() - tic
+            if it % opts.check_period == 0 or ex.value:
+                tic = time.perf_counter()
+                _lib.check(lib.kry_check_sylv1(ctx.ptr, rhs_norm, ctypes.byref(res),
+                                               ctypes.byref(rel)))
+                t_res += time.perf_counter() - tic
+                rel_v = rel.value
+                history.append((it, it * s, rel_v, t_basis, t_res))
+                if rel_v <= opts.tol:
+                    converged_at = it
+                    break
+                if ex.value:
+                    raise ConvergenceError(
+                        "the Krylov space became invariant at m=%d without meeting the "
+                        "tolerance (residual %.3e)" % (it, rel_v), history)
+        if converged_at is None:
+            raise ConvergenceError(
+                "no convergence to %.1e within %d iterations (last residual %s)"
+                % (opts.tol, opts.max_m, "%.3e" % rel_v if rel_v is not None else "never checked"),
+                history)
+        tic = time.perf_counter()
+        rank, disc = ctypes.c_int(0), ctypes.c_double(0.0)
+        _lib.check(lib.kry_finalize_sylv1(ctx.ptr, float(opts.trunc_eps), ctypes.byref(rank),
+                                          ctypes.byref(disc), None, 0))
+        z2 = np.zeros((n2, rank.value))
+        if rank.value > 0:
+            _lib.check(lib.kry_finalize_sylv1(ctx.ptr, float(opts.trunc_eps), ctypes.byref(rank),
+                                              ctypes.byref(disc), _lib.as_dptr(z2), z2.size))
+        z1 = host_factor(op_a.n, rank.value)
+        if rank.value > 0:
+            _lib.check(lib.kry_recover(ctx.ptr, _lib.as_dptr(z1)))
+        t_rec = time.perf_counter() - tic
+        m, exh = ctypes.c_int(), ctypes.c_int()
+        lib.kry_ctx_info(ctx.ptr, None, None, ctypes.byref(m), ctypes.byref(exh))
+        verified = None
+        if opts.verify and op_a.n <= VERIFY_LIMIT:
+            verified = true_sylvester_residual(op_a, z1, z2, c1, c2, lambda v: b @ v) / rhs_norm
+        return LowRankSolution(
+            z1=z1,
+            z2=z2,
+            rank=rank.value,
+            iterations=converged_at,
+            space_dim=converged_at * s,
+            final_residual=rel_v,
+            history=history,
+            basis_seconds=t_basis,
+            residual_seconds=t_res,
+            recovery_seconds=t_rec,
+            peak_basis_vectors=_peak(opts.storage, m.value, bool(exh.value), s),
+            truncation_discarded=disc.value,
+            verified_residual=verified,
+        )
+    finally:
+        ctx.close()
 
 
 def true_lyapunov_residual(op, z, c):

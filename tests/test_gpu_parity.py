@@ -340,3 +340,79 @@ def test_config5_full_run_raises_with_survey_values():
     assert len(err.value.history) == 1500
     for m, v in ((175, 7.3e-5), (700, 4.6e-6), (975, 2.0e-6), (1100, 1.42e-6)):
         assert abs(h[m] - v) <= 0.05 * v, (m, h[m], v)
+
+
+# ------------------------------------------------------------------ one-sided Sylvester (§8(f) f1)
+def _sylv1_case(name):
+    from paper_1602_05033_b200 import problems as PP
+    g = gold("sylv1_" + name)
+    kind = "fd2d-exp" if name.startswith("exp") else "laplacian2d"
+    n = int(round(np.sqrt(g["c1"].shape[0])))
+    return g, PP.gen_fd2d(kind, n)
+
+
+@pytest.mark.parametrize("name", ["exp30", "lap40"])
+def test_one_sided_sylvester_matches_reference_run(name):
+    g, a = _sylv1_case(name)
+    sol = kb.solve_sylvester_one_sided(kb.SparseOperator(a), g["b"], g["c1"], g["c2"],
+                                       kb.SolveOptions(tol=float(g["tol"]), max_m=300,
+                                                       storage="windowed"))
+    assert sol.iterations == int(g["iterations"])
+    assert sol.rank == int(g["rank"])
+    # floor-adjusted criterion of SURVEY.md §8(c): the reference against
+    # itself with a reordered SpMM summation (oracle, same inputs) deviates
+    # by up to 7.6e-7 (lap40) / 0.24% (exp30, variable coefficients: chaotic
+    # late regime as config 3); the device reassociates every reduction, so
+    # it is held to 10x the running envelope of that self-noise (the config-3
+    # rule) plus 1e-9 relative
+    ref = g["history"][:, 2]
+    per = ko.solve_sylvester_one_sided(ReorderedOperator(a), g["b"], g["c1"], g["c2"],
+                                       ko.SolveOptions(tol=float(g["tol"]), max_m=300))
+    hp = np.array([r[2] for r in per.history])
+    k = min(len(hp), len(ref))
+    envelope = np.maximum.accumulate(np.abs(hp[:k] - ref[:k]))
+    envelope = np.concatenate([envelope, np.full(len(ref) - k, envelope[-1])])
+    h = np.array([r[2] for r in sol.history])
+    assert np.all(np.abs(h - ref) <= 1e-9 * ref + 10.0 * envelope + FLOOR), \
+        np.max(np.abs(h - ref) / ref)
+    om1 = P.sketch_omega(a.shape[0], 2)
+    om2 = P.sketch_omega(g["b"].shape[0], 2)
+    right = sol.z1 @ (sol.z2.T @ om2)
+    left = sol.z2 @ (sol.z1.T @ om1)
+    assert np.linalg.norm(right - g["sketch_right"]) <= 1e-8 * np.linalg.norm(g["sketch_right"])
+    assert np.linalg.norm(left - g["sketch_left"]) <= 1e-8 * np.linalg.norm(g["sketch_left"])
+    assert abs(sol.truncation_discarded - float(g["discarded"])) <= \
+        1e-6 * max(float(g["discarded"]), 1e-300) + 1e-13
+    assert sol.peak_basis_vectors == int(g["peak_basis_vectors"])
+
+
+def test_one_sided_sylvester_verify_and_oracle():
+    from paper_1602_05033_b200 import problems as PP
+    a = PP.gen_fd2d("fd2d-exp", 14)
+    b = (10.0 * PP.laplacian1d(9)).toarray()
+    rng = np.random.default_rng(3)
+    c1, c2 = rng.standard_normal((196, 2)), rng.standard_normal((9, 2))
+    sol = kb.solve_sylvester_one_sided(kb.SparseOperator(a), b, c1, c2,
+                                       kb.SolveOptions(tol=1e-10, max_m=80, verify=True))
+    ref = ko.solve_sylvester_one_sided(ko.SparseOperator(a), b, c1, c2,
+                                       ko.SolveOptions(tol=1e-10, max_m=80))
+    assert sol.iterations == ref.iterations and sol.rank == ref.rank
+    assert ko.factor_distance(sol.z1, ref.z1, sol.z2, ref.z2) <= 1e-8
+    # true residual of the truncated factor, relative to ||C1|| ||C2|| (the
+    # estimate converged below 1e-10; truncation and roundoff add ~1e-9)
+    assert sol.verified_residual is not None and sol.verified_residual <= 2e-8
+
+
+def test_one_sided_sylvester_input_errors():
+    from paper_1602_05033_b200 import problems as PP
+    op = kb.SparseOperator(PP.gen_fd2d("laplacian2d", 6))
+    c1 = np.ones((36, 1))
+    b = (PP.laplacian1d(4)).toarray()
+    with pytest.raises(kb.DimensionMismatchError):
+        kb.solve_sylvester_one_sided(op, b + np.triu(np.ones((4, 4)), 1), c1, np.ones((4, 1)))
+    with pytest.raises(kb.DimensionMismatchError):
+        kb.solve_sylvester_one_sided(op, b, c1, np.ones((5, 1)))
+    with pytest.raises(kb.DimensionMismatchError):
+        kb.solve_sylvester_one_sided(op, b, c1, np.ones((4, 2)))
+    with pytest.raises(kb.IndefiniteMatrixError):
+        kb.solve_sylvester_one_sided(op, -b, c1, np.ones((4, 1)))
