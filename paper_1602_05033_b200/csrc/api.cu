@@ -1843,9 +1843,13 @@ int kry_recover(kry_ctx* c, double* zhost) {
   // itself used to run on the interleaved layout: 64-byte rows at a
   // G*s*8-byte stride made its kernels 25-45% slower than in pass 1.)
   const size_t blk_bytes = (size_t)n * s * sizeof(double);
-  // two buffers within a quarter of the free memory (+ what is cached)
-  int64_t G = (int64_t)((fr / 4 + c->p2buf_cap * sizeof(double)) / blk_bytes) / 2;
-  if (G > 32) G = 32;
+  // two buffers within half of the free memory (+ what is cached); a chunk
+  // of G blocks is one DGEMM with K = G*s, and Z is read and written once
+  // per chunk (G = 64 at c4: 4 DGEMMs of K = 512 instead of 8 of K = 256)
+  int64_t gmax = 64;
+  if (const char* e = getenv("KRY_PASS2_CHUNK")) gmax = std::max(1, atoi(e));
+  int64_t G = (int64_t)((fr / 2 + c->p2buf_cap * sizeof(double)) / blk_bytes) / 2;
+  if (G > gmax) G = gmax;
   if (G > m) G = m;
   if (G < 1) G = 1;
   const int nbuf = (m > G) ? 2 : 1;
