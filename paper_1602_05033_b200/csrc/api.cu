@@ -308,6 +308,7 @@ struct kry_ctx {
   // fused single-pass step (stencil operators, one GPU)
   bool use_step = false;
   bool coef_ready = false;   // st->M holds the coefficients of the next step
+  bool pending_launch = false;  // step m+1's kernels are queued, not yet completed
   StepScratch sx{};
   int step_ch = 0, step_nch = 0, step_lag = 0;
   // multi-GPU
@@ -444,6 +445,13 @@ int reset_state(kry_ctx* c, int replay) {
                            c->stream));
   KRY_CUDA(cudaStreamSynchronize(c->stream));
   return KRY_OK;
+}
+
+// clear an error status left by a discarded speculative step
+void reset_state_status(kry_ctx* c) {
+  int zero = 0;
+  cudaMemcpyAsync(&c->st->status, &zero, sizeof(int), cudaMemcpyHostToDevice, c->stream);
+  cudaStreamSynchronize(c->stream);
 }
 
 // init from C (device, n x s, ld s) into slot `dst`
@@ -610,13 +618,52 @@ int fused_step(kry_ctx* c, int j, const double* vold, const double* vcur, double
 }
 
 // one Lanczos step with slot rotation (no eigen work)
+// Queue the kernels of step m+1 without waiting (single GPU, two-kernel
+// path): the pass-1 loop launches step m+1 before it issues the eigen work of
+// step m and collects the previous check, so the main stream never idles on
+// the host.  step_core completes it (status check, fallback).
+bool can_prelaunch(kry_ctx* c) {
+  return !step_on(c) && !dist(c) && c->initialized && !c->exhausted && !c->pending_launch &&
+         c->m + 2 <= c->T.cap;
+}
+int step_prelaunch(kry_ctx* c) {
+  if (!can_prelaunch(c)) return KRY_OK;
+  const int j = c->m + 1;
+  const double* vold = j > 1 ? slotp(c, c->i_old) : nullptr;
+  ApplyGramCall ag{slotp(c, c->i_cur), c->ld, c->n, 1, POST_STEP, 0};
+  KRY_CHECK(run_apply_gram(c, ag));
+  CombineCall cc{vold, c->ld, slotp(c, c->i_cur), c->ld, slotp(c, c->i_new), c->ld, c->n,
+                 j > 1 ? 1 : 0, 1, 1, 1};
+  cudaEvent_t evs[2];
+  float dummy = 0.f;
+  if (c->prof) {
+    cudaEventCreate(&evs[0]);
+    cudaEventCreate(&evs[1]);
+  }
+  KRY_CHECK(run_combine(c, cc, c->prof ? &dummy : nullptr, c->prof ? evs : nullptr));
+  if (c->prof) c->ev_comb.push_back({evs[0], evs[1]});
+  c->pending_launch = true;
+  return KRY_OK;
+}
+
 int step_core(kry_ctx* c, int finalize_on_zero, int* exhausted) {
   if (!c->initialized) return fail(KRY_ERR_STATE, "init_basis has not been called");
   if (c->exhausted) return fail(KRY_ERR_DEFLATION, "the Krylov space is already invariant");
   if (c->m + 2 > c->T.cap) return fail(KRY_ERR_STATE, "max_m capacity of the context exceeded");
   int ex = 0;
-  KRY_CHECK(fused_step(c, c->m + 1, slotp(c, c->i_old), slotp(c, c->i_cur), slotp(c, c->i_new),
-                       c->ld, finalize_on_zero, &ex));
+  if (c->pending_launch) {
+    // complete the queued step: a fallback (or error) made the combine a no-op
+    c->pending_launch = false;
+    const int j = c->m + 1;
+    KRY_CHECK(sync_status(c));
+    KRY_CHECK(map_status(c, ("Lanczos step " + std::to_string(j)).c_str()));
+    if (c->st_h->flags & KRY_FLAG_FALLBACK)
+      KRY_CHECK(explicit_step(c, j, j > 1 ? slotp(c, c->i_old) : nullptr, slotp(c, c->i_cur),
+                              slotp(c, c->i_new), c->ld, finalize_on_zero, &ex));
+  } else {
+    KRY_CHECK(fused_step(c, c->m + 1, slotp(c, c->i_old), slotp(c, c->i_cur),
+                         slotp(c, c->i_new), c->ld, finalize_on_zero, &ex));
+  }
   c->m += 1;
   if (ex) {
     c->exhausted = true;
@@ -645,8 +692,11 @@ int step_pass1(kry_ctx* c, int finalize_on_zero, int* exhausted) {
 // the residual check of iteration j with the staged coupling tau1[j-1].
 // The check result (sum |M|^2, min |denominator|, spectral scale) lands in
 // the pinned ring slot `slot`, signalled by ev_res[slot].
-int launch_eigen_step(kry_ctx* c, int j, bool check, bool exhausted_j, int slot) {
-  KRY_CUDA(cudaEventRecord(c->ev_t, c->stream));
+int launch_eigen_step(kry_ctx* c, int j, bool check, bool exhausted_j, int slot,
+                      bool recorded = false) {
+  // ev_t marks the completion of step j on the main stream (recorded by the
+  // caller before it queued step j+1, or here)
+  if (!recorded) KRY_CUDA(cudaEventRecord(c->ev_t, c->stream));
   KRY_CUDA(cudaStreamWaitEvent(c->estream, c->ev_t, 0));
   KRY_CHECK(c->eig.append_block(c->estream, c->T.dsym + (int64_t)(j - 1) * 64,
                                 j >= 2 ? c->T.sub + (int64_t)(j - 2) * 64 : nullptr));
@@ -1342,7 +1392,19 @@ int kry_solve_lyap_pass1(kry_ctx* c, double tol, int max_m, int check_period, do
     int ex = 0;
     rc = step_core(c, 1, &ex);
     if (rc) break;
+    // queue step it+1 before the host issues the eigen work of step it and
+    // waits for the previous check (a converged solve thereby computes up to
+    // two extra, discarded basis blocks)
+    KRY_CUDA(cudaEventRecord(c->ev_t, c->stream));
+    if (!ex && it < max_m) {
+      rc = step_prelaunch(c);
+      if (rc) break;
+    }
     t_basis += now_s() - t0;
+    const bool chk = (it % check_period == 0) || ex;
+    const int slot = it & 1;
+    rc = launch_eigen_step(c, it, chk, ex != 0, slot, true);
+    if (rc) break;
     if (pending > 0) {   // result of the previous iteration's check
       t0 = now_s();
       double res = 0.0;
@@ -1359,10 +1421,6 @@ int kry_solve_lyap_pass1(kry_ctx* c, double tol, int max_m, int check_period, do
       }
       pending = -1;
     }
-    const bool chk = (it % check_period == 0) || ex;
-    const int slot = it & 1;
-    rc = launch_eigen_step(c, it, chk, ex != 0, slot);
-    if (rc) break;
     if (chk) {
       pending = it;
       pending_slot = slot;
@@ -1395,6 +1453,18 @@ int kry_solve_lyap_pass1(kry_ctx* c, double tol, int max_m, int check_period, do
         *reason = 0;
         c->m_final = pending;
       }
+    }
+  }
+  if (c->pending_launch) {
+    // the speculative step past the decision: complete it so that the
+    // context state matches c->m; its own failure (if any) happened after
+    // the solve was decided and is not reported
+    const std::string keep = g_last_error;
+    int ex = 0;
+    if (step_core(c, 1, &ex) != KRY_OK) {
+      c->pending_launch = false;
+      g_last_error = keep;
+      reset_state_status(c);
     }
   }
   cudaStreamSynchronize(c->estream);

@@ -794,6 +794,29 @@ __device__ __forceinline__ void prefetch_rows(const double* base, int64_t ld, in
   prefetch_l2(reinterpret_cast<const void*>(a0), (uint32_t)bytes);
 }
 
+// Tile order of the persistent recurrence kernels.  Default (KRY_CONTIG_TILES
+// = 0): interleaved, tile = blockIdx + k * gridDim (the active tiles form a
+// compact wavefront).  KRY_CONTIG_TILES = 1: each CTA walks a contiguous
+// range, so the +-nx neighbour rows of a tile are rows this CTA loaded a
+// moment ago (L1 hits instead of L2 fills); the +-nx*ny planes are the rows
+// the CTAs a few ranges away are loading at the same time.
+#ifndef KRY_CONTIG_TILES
+#define KRY_CONTIG_TILES 0
+#endif
+struct TileOrder {
+  int64_t n, per, base;
+  __device__ explicit TileOrder(int64_t ntiles) : n(ntiles) {
+    per = (ntiles + gridDim.x - 1) / gridDim.x;
+    base = (int64_t)blockIdx.x * per;
+  }
+  __device__ bool valid(int64_t k) const {
+    return KRY_CONTIG_TILES ? (k < per && base + k < n) : (blockIdx.x + k * (int64_t)gridDim.x < n);
+  }
+  __device__ int64_t at(int64_t k) const {
+    return KRY_CONTIG_TILES ? base + k : blockIdx.x + k * (int64_t)gridDim.x;
+  }
+};
+
 __host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 // tile columns of the combine kernel: [V_{m-1} | V_m | A V_m | V_{m+1}] (+ zero padding
@@ -1030,11 +1053,14 @@ __global__ void __launch_bounds__(TP, COOP ? KRY_COMB_MINB : 2) k_combine(OpDev 
   // interleaved tile order: the active tiles form a compact wavefront, so the
   // +-nx*ny neighbour planes of a tile are in L2 (streamed as centre rows by
   // the CTAs ~nx*ny/TP tiles ahead / behind)
-  for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
+  const TileOrder ord(ntiles);
+  for (int64_t k = 0; ord.valid(k); ++k) {
+    const int64_t it = ord.at(k);
     const int64_t tile = c.reverse ? (ntiles - 1 - it) : it;
     const int64_t i64 = tile * TP + threadIdx.x;
-    if (threadIdx.x == 0 && it + gridDim.x < ntiles) {
-      const int64_t nt = c.reverse ? (ntiles - 1 - (it + gridDim.x)) : it + gridDim.x;
+    if (threadIdx.x == 0 && ord.valid(k + 1)) {
+      const int64_t nx_ = ord.at(k + 1);
+      const int64_t nt = c.reverse ? (ntiles - 1 - nx_) : nx_;
       prefetch_rows(c.vc, c.ldc, nt * TP, c.n);
       if (c.write_new && c.has_old) prefetch_rows(c.vo, c.ldo, nt * TP, c.n);
       if (!c.write_new) prefetch_rows(c.vn, c.ldn, nt * TP, c.n);
@@ -1151,11 +1177,14 @@ __global__ void __launch_bounds__(TP, COOP ? KRY_APPLY_MINB : 2) k_apply_gram(Op
   // interleaved tile order: the active tiles form a compact wavefront, so the
   // +-nx*ny neighbour planes of a tile are in L2 (streamed as centre rows by
   // the CTAs ~nx*ny/TP tiles ahead / behind)
-  for (int64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
+  const TileOrder ord(ntiles);
+  for (int64_t k = 0; ord.valid(k); ++k) {
+    const int64_t it = ord.at(k);
     const int64_t tile = c.reverse ? (ntiles - 1 - it) : it;
     const int64_t i64 = tile * TP + threadIdx.x;
-    if (threadIdx.x == 0 && it + gridDim.x < ntiles) {
-      const int64_t nt = c.reverse ? (ntiles - 1 - (it + gridDim.x)) : it + gridDim.x;
+    if (threadIdx.x == 0 && ord.valid(k + 1)) {
+      const int64_t nx_ = ord.at(k + 1);
+      const int64_t nt = c.reverse ? (ntiles - 1 - nx_) : nx_;
       prefetch_rows(c.v, c.ldv, nt * TP, c.n);
     }
     if constexpr (coop) {
