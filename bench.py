@@ -313,11 +313,16 @@ def main():
     its_total_all = its_total   # sharded: all ranks advance the same solve
     value = its_total_all / (ms_total / 1000.0)
     ctx.close()
-    # roofline of the fused recurrence kernel (k_combine): reads V_{m-1}, V_m,
-    # writes V_{m+1}: 3 * n * s * 8 algorithmic bytes per launch
+    # roofline of the recurrence kernel (k_combine): reads V_{m-1}, V_m and
+    # (single GPU, even s: the apply kernel's hand-off) A V_m, writes V_{m+1}:
+    # 4 (3 without the hand-off) * n * s * 8 bytes per launch.  The step as a
+    # whole moves 6 n s doubles (apply: read V_m, write A V_m); the
+    # three-term minimum is 3 n s.
     hbm, hbm_kind = peaks()
     comb_avg_ms = comb_ms.value / max(comb_n.value, 1)
-    bytes_launch = 3 * n * s * 8
+    handoff = (world == 1 and s % 2 == 0 and os.environ.get("KRY_NO_AV_HANDOFF") != "1"
+               and os.environ.get("KRY_FUSED_STEP") != "1")
+    bytes_launch = (4 if handoff else 3) * n * s * 8
     achieved = bytes_launch / (comb_avg_ms / 1000.0) / 1e9 if comb_avg_ms > 0 else 0.0
 
     e2e = None
@@ -387,12 +392,16 @@ def main():
         "phases_s": {"init": r0["init_s"], "pass1": r0["pass1_s"],
                      "checks_in_pass1": r0["check_s"],
                      "finalize": r0["finalize_s"], "pass2": r0["pass2_s"]},
-        "roofline": {"bound": "hbm", "kernel": "k_combine (fused stencil SpMM + 3-term "
-                     "recurrence + Gram)", "achieved": achieved, "peak": hbm,
+        "roofline": {"bound": "hbm", "kernel": "k_combine (three-term recurrence on DMMA + "
+                     "Gram, A V_m handed off by k_apply_gram)" if handoff else
+                     "k_combine (fused stencil SpMM + 3-term recurrence + Gram)",
+                     "achieved": achieved, "peak": hbm,
                      "peak_kind": hbm_kind, "unit": "GB/s",
                      "frac": achieved / hbm if hbm else None,
                      "traffic": captured_traffic(args.config),
                      "bytes_per_launch": bytes_launch, "avg_launch_ms": comb_avg_ms,
+                     "step_bytes": 6 * n * s * 8 if handoff else 4 * n * s * 8,
+                     "step_min_bytes": 3 * n * s * 8,
                      "launches": comb_n.value},
         "cpu_baseline": cpu,
         "e2e": e2e,

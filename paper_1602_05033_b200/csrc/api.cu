@@ -309,6 +309,7 @@ struct kry_ctx {
   bool use_step = false;
   bool coef_ready = false;   // st->M holds the coefficients of the next step
   bool pending_launch = false;  // step m+1's kernels are queued, not yet completed
+  double* wbuf = nullptr;       // A V_m handed from the apply to the combine kernel
   StepScratch sx{};
   int step_ch = 0, step_nch = 0, step_lag = 0;
   // multi-GPU
@@ -519,6 +520,21 @@ int explicit_step(kry_ctx* c, int j, const double* vold, const double* vcur, dou
   return KRY_OK;
 }
 
+// A V_m hand-off between the apply and the combine kernel (one GPU, stencil,
+// even s: the cooperative staging path): the combine then streams A V_m
+// (8 n s bytes from HBM) instead of gathering the 7-point stencil again
+// through L1/L2, which was its limiter (LSU data pipe 77 %).
+double* wbuf_of(kry_ctx* c) {
+  if (dist(c) || c->op.kind != KRY_OP_STENCIL || (c->s % 2) != 0 || c->ld != c->s) return nullptr;
+  const char* off = getenv("KRY_NO_AV_HANDOFF");
+  if (off && off[0] == '1') return nullptr;
+  if (!c->wbuf && dalloc(&c->wbuf, (size_t)c->n * c->s) != KRY_OK) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return c->wbuf;
+}
+
 // the fused single-pass kernel applies (stencil operator, one GPU, s != 5, 7)
 bool step_on(kry_ctx* c) { return c->use_step && !dist(c); }
 
@@ -570,9 +586,12 @@ int fused_step(kry_ctx* c, int j, const double* vold, const double* vcur, double
   if (!(step_on(c) && c->coef_ready)) {
     c->coef_ready = false;
     ApplyGramCall ag{vcur, ld, c->n, 1, POST_STEP, 0};
+    double* wb = (speculate && ld == c->s) ? wbuf_of(c) : nullptr;
+    ag.wout = wb;
     KRY_CHECK(run_apply_gram(c, ag));
     if (speculate) {
       CombineCall cc{vold, ld, vcur, ld, vnew, ld, c->n, j > 1 ? 1 : 0, 1, 1, 1};
+      cc.win = wb;
       cudaEvent_t evs[2];
       float dummy = 0.f;
       if (c->prof) {
@@ -631,9 +650,12 @@ int step_prelaunch(kry_ctx* c) {
   const int j = c->m + 1;
   const double* vold = j > 1 ? slotp(c, c->i_old) : nullptr;
   ApplyGramCall ag{slotp(c, c->i_cur), c->ld, c->n, 1, POST_STEP, 0};
+  double* wb = wbuf_of(c);
+  ag.wout = wb;
   KRY_CHECK(run_apply_gram(c, ag));
   CombineCall cc{vold, c->ld, slotp(c, c->i_cur), c->ld, slotp(c, c->i_new), c->ld, c->n,
                  j > 1 ? 1 : 0, 1, 1, 1};
+  cc.win = wb;
   cudaEvent_t evs[2];
   float dummy = 0.f;
   if (c->prof) {
@@ -1181,6 +1203,7 @@ void kry_ctx_destroy(kry_ctx* c) {
   dfree(c->sx.gcnt);
   dfree(c->sx.flags);
   for (double* p : {c->d1_ups, c->d1_P, c->d1_v, c->d1_in, c->d1_eye, c->d1_z2}) dfree(p);
+  dfree(c->wbuf);
   dfree(c->zeros64);
   dfree(c->gamma_d);
   if (c->qy) dfree(c->qy);
@@ -1992,6 +2015,7 @@ int kry_recover(kry_ctx* c, double* zhost) {
     if (!fused) {
       c->coef_ready = false;
       ApplyGramCall ag{ring(j), ldr, n, 1, POST_STEP, 0};
+      ag.wout = speculate ? wbuf_of(c) : nullptr;
       rc = run_apply_gram(c, ag);
       if (rc) break;
       if (!speculate) {
@@ -2022,6 +2046,7 @@ int kry_recover(kry_ctx* c, double* zhost) {
                      j > 1 ? 1 : 0, 1, 1, 1};
       cc.vn2 = chunk_dst;
       cc.ldn2 = ld2;
+      cc.win = wbuf_of(c);
       rc = run_combine(c, cc, nullptr, nullptr);
       if (rc == KRY_OK) rc = sync_status(c);
       if (rc == KRY_OK) rc = map_status(c, ("second pass step " + std::to_string(j)).c_str());

@@ -174,6 +174,7 @@ struct CombineCall {
   int post = POST_P;   // POST_NONE in multi-GPU mode (all-reduce, then k_post)
   double* vn2 = nullptr;   // optional second copy of V_{m+1} (pass-2 chunk buffer)
   int64_t ldn2 = 0;
+  const double* win = nullptr;   // A V_m stored by the apply kernel (n x s, ld s)
 };
 int launch_combine(cudaStream_t st, int s, const OpDev& op, const CombineCall& c,
                    DevState* dst, const TStore& T, GramScratch& g, int grid,
@@ -184,6 +185,7 @@ struct ApplyGramCall {
   int use_op;        // 1: X=[V|AV], Y=AV ; 0: X=[V], Y=V
   int post;          // PostMode
   int reverse;
+  double* wout = nullptr;   // also store A V (n x s, ld s) for the combine kernel
 };
 int launch_apply_gram(cudaStream_t st, int s, const OpDev& op,
                       const ApplyGramCall& c, DevState* dst, const TStore& T,

@@ -848,12 +848,16 @@ __device__ __forceinline__ void warp_gram(const double* sX, int r0, int x0, int 
 // ld == S).  The stencil is evaluated per column pair and the results are
 // written straight into the transposed smem tile:
 //   column groups: [col_o: V_{m-1}] (if col_o >= 0), [col_c: V_m], [col_w: A V_m]
+// `wout`: also store A V (apply kernel, for the combine that follows);
+// `win`: load A V instead of gathering the stencil (combine kernel).
 template <int S>
 __device__ __forceinline__ void stage_warp_coop(const OpDev& op, const double* __restrict__ vc,
                                                 int64_t ldc, const double* __restrict__ vo,
                                                 int64_t ldo, bool load_old, bool use_op,
                                                 int64_t n, int64_t tile_base, int r0,
-                                                double* sX, int col_o, int col_c, int col_w) {
+                                                double* sX, int col_o, int col_c, int col_w,
+                                                const double* __restrict__ win = nullptr,
+                                                double* __restrict__ wout = nullptr) {
   constexpr int CP = S / 2;
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -868,7 +872,9 @@ __device__ __forceinline__ void stage_warp_coop(const OpDev& op, const double* _
       const int off = 2 * cp;
       v = __ldg(reinterpret_cast<const double2*>(vc + i64 * ldc + off));
       if (load_old) o = __ldg(reinterpret_cast<const double2*>(vo + i64 * ldo + off));
-      if (use_op) {
+      if (use_op && win) {
+        w = __ldg(reinterpret_cast<const double2*>(win + i64 * S + off));
+      } else if (use_op) {
         const unsigned r = fdiv((unsigned)i, op.fx);
         const int x = i - (int)r * op.nx;
         const unsigned zq = fdiv(r, op.fy);
@@ -917,6 +923,7 @@ __device__ __forceinline__ void stage_warp_coop(const OpDev& op, const double* _
       }
     }
     const int c0 = 2 * cp;
+    if (wout && use_op && i64 < n) *reinterpret_cast<double2*>(wout + i64 * S + c0) = w;
     if (col_o >= 0) {
       sX[CB(col_o + c0) + row] = o.x;
       sX[CB(col_o + c0 + 1) + row] = o.y;
@@ -1073,7 +1080,7 @@ __global__ void __launch_bounds__(TP, COOP ? KRY_COMB_MINB : 2) k_combine(OpDev 
       else
 #endif
       stage_warp_coop<(S % 2 == 0) ? S : 2>(op, c.vc, c.ldc, c.vo, c.ldo, c.write_new && c.has_old,
-                                            c.use_op, c.n, tile * TP, r0, sX, 0, S, 2 * S);
+                                            c.use_op, c.n, tile * TP, r0, sX, 0, S, 2 * S, c.win);
       if (!c.write_new && i64 < c.n) {
         double vn[S];
         load_vec<S>(c.vn + i64 * c.ldn, vn);
@@ -1195,7 +1202,8 @@ __global__ void __launch_bounds__(TP, COOP ? KRY_APPLY_MINB : 2) k_apply_gram(Op
       else
 #endif
       stage_warp_coop<(S % 2 == 0) ? S : 2>(op, c.v, c.ldv, nullptr, 0, false, USE_OP != 0, c.n,
-                                            tile * TP, r0, sX, -1, 0, USE_OP ? S : -1);
+                                            tile * TP, r0, sX, -1, 0, USE_OP ? S : -1, nullptr,
+                                            c.wout);
     } else if (i64 < c.n) {
       double v[S];
       load_vec<S>(c.v + i64 * c.ldv, v);
