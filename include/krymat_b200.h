@@ -168,6 +168,13 @@ int kry_finalize_sylv1(kry_ctx *ctx, double trunc_eps, int *rank,
  * the first m blocks, as two_pass_recover(op, state, qy) does (solvers.py:130) */
 int kry_set_qy(kry_ctx *ctx, int m, int t, const double *qy);
 
+/* storage mode (SolveOptions.storage, solvers.py:49-73): stored != 0 keeps
+ * every basis block of pass 1 in device memory while it fits (chunked), so
+ * kry_recover assembles Z = V qy without regenerating the basis
+ * (_assemble_stored, solvers.py:125-127); it falls back to the two-pass
+ * regeneration when the memory runs out.  Set before kry_init_basis. */
+int kry_set_storage(kry_ctx *ctx, int stored);
+
 /* pass 2: regenerate the basis and accumulate Z = sum_i V_i qy_i.
  * z: host n x rank row-major (or NULL to keep Z on the device only). */
 int kry_recover(kry_ctx *ctx, double *z);

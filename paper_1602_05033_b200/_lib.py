@@ -113,6 +113,7 @@ SIGNATURES = {
     "kry_finalize_lyap": (ctypes.c_int, [_P, ctypes.c_double, iptr, dptr]),
     "kry_finalize_sylv": (ctypes.c_int, [_P, _P, ctypes.c_double, iptr, dptr]),
     "kry_recover": (ctypes.c_int, [_P, dptr]),
+    "kry_set_storage": (ctypes.c_int, [_P, ctypes.c_int]),
     "kry_set_qy": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, dptr]),
     "kry_get_factor": (ctypes.c_int, [_P, dptr]),
     "kry_partial_eig": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, dptr, dptr,

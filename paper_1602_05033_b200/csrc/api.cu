@@ -310,6 +310,13 @@ struct kry_ctx {
   bool coef_ready = false;   // st->M holds the coefficients of the next step
   bool pending_launch = false;  // step m+1's kernels are queued, not yet completed
   double* wbuf = nullptr;       // A V_m handed from the apply to the combine kernel
+  // storage="stored": pass 1 keeps every basis block in HBM (chunks of G
+  // blocks in the interleaved [point][G*s] DGEMM layout) and the factor is
+  // Z = V * qy without regenerating the basis (reference solvers.py:125-127)
+  bool store_req = false;       // requested by the caller
+  bool store_ok = false;        // every block so far is stored
+  int store_G = 16;
+  std::vector<double*> store_chunks;
   StepScratch sx{};
   int step_ch = 0, step_nch = 0, step_lag = 0;
   // multi-GPU
@@ -535,6 +542,36 @@ double* wbuf_of(kry_ctx* c) {
   return c->wbuf;
 }
 
+// ---------------------------------------------------------------- stored basis
+void store_drop(kry_ctx* c) {
+  for (double* p : c->store_chunks) dfree(p);
+  c->store_chunks.clear();
+  c->store_ok = false;
+}
+// destination of basis block `blk` (1-based) in the stored chunks, allocating
+// the chunk on first use; nullptr (and storage off for this solve) when the
+// device is out of memory or the path cannot store
+double* store_slot(kry_ctx* c, int blk, int64_t* ld2) {
+  if (!c->store_ok) return nullptr;
+  const int G = c->store_G;
+  const size_t q = (size_t)(blk - 1) / G;
+  while (c->store_chunks.size() <= q) {
+    double* p = nullptr;
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const size_t need = (size_t)c->n * G * c->s * sizeof(double);
+    // keep room for the factor Z and the finalisation
+    if (need + ((size_t)4 << 30) > fr || dalloc(&p, (size_t)c->n * G * c->s) != KRY_OK) {
+      cudaGetLastError();
+      store_drop(c);
+      return nullptr;
+    }
+    c->store_chunks.push_back(p);
+  }
+  *ld2 = (int64_t)G * c->s;
+  return c->store_chunks[q] + (int64_t)((blk - 1) % G) * c->s;
+}
+
 // the fused single-pass kernel applies (stencil operator, one GPU, s != 5, 7)
 bool step_on(kry_ctx* c) { return c->use_step && !dist(c); }
 
@@ -592,6 +629,7 @@ int fused_step(kry_ctx* c, int j, const double* vold, const double* vcur, double
     if (speculate) {
       CombineCall cc{vold, ld, vcur, ld, vnew, ld, c->n, j > 1 ? 1 : 0, 1, 1, 1};
       cc.win = wb;
+      if (c->store_ok && ld == c->s) cc.vn2 = store_slot(c, j + 1, &cc.ldn2);
       cudaEvent_t evs[2];
       float dummy = 0.f;
       if (c->prof) {
@@ -603,7 +641,10 @@ int fused_step(kry_ctx* c, int j, const double* vold, const double* vcur, double
       KRY_CHECK(map_status(c, ("Lanczos step " + std::to_string(j)).c_str()));
       if (c->st_h->flags & KRY_FLAG_FALLBACK) {
         if (c->prof) { cudaEventDestroy(evs[0]); cudaEventDestroy(evs[1]); }
-        return explicit_step(c, j, vold, vcur, vnew, ld, finalize_on_zero, exhausted);
+        KRY_CHECK(explicit_step(c, j, vold, vcur, vnew, ld, finalize_on_zero, exhausted));
+        if (!*exhausted && cc.vn2)
+          KRY_CHECK(launch_copy_block(c->stream, c->s, vnew, ld, cc.vn2, cc.ldn2, c->n));
+        return KRY_OK;
       }
       if (c->prof) c->ev_comb.push_back({evs[0], evs[1]});
       return KRY_OK;
@@ -656,6 +697,7 @@ int step_prelaunch(kry_ctx* c) {
   CombineCall cc{vold, c->ld, slotp(c, c->i_cur), c->ld, slotp(c, c->i_new), c->ld, c->n,
                  j > 1 ? 1 : 0, 1, 1, 1};
   cc.win = wb;
+  if (c->store_ok) cc.vn2 = store_slot(c, j + 1, &cc.ldn2);
   cudaEvent_t evs[2];
   float dummy = 0.f;
   if (c->prof) {
@@ -679,9 +721,13 @@ int step_core(kry_ctx* c, int finalize_on_zero, int* exhausted) {
     const int j = c->m + 1;
     KRY_CHECK(sync_status(c));
     KRY_CHECK(map_status(c, ("Lanczos step " + std::to_string(j)).c_str()));
-    if (c->st_h->flags & KRY_FLAG_FALLBACK)
+    if (c->st_h->flags & KRY_FLAG_FALLBACK) {
       KRY_CHECK(explicit_step(c, j, j > 1 ? slotp(c, c->i_old) : nullptr, slotp(c, c->i_cur),
                               slotp(c, c->i_new), c->ld, finalize_on_zero, &ex));
+      int64_t ld2 = 0;
+      double* dst = (!ex && c->store_ok) ? store_slot(c, j + 1, &ld2) : nullptr;
+      if (dst) KRY_CHECK(launch_copy_block(c->stream, c->s, slotp(c, c->i_new), c->ld, dst, ld2, c->n));
+    }
   } else {
     KRY_CHECK(fused_step(c, c->m + 1, slotp(c, c->i_old), slotp(c, c->i_cur),
                          slotp(c, c->i_new), c->ld, finalize_on_zero, &ex));
@@ -1204,6 +1250,7 @@ void kry_ctx_destroy(kry_ctx* c) {
   dfree(c->sx.flags);
   for (double* p : {c->d1_ups, c->d1_P, c->d1_v, c->d1_in, c->d1_eye, c->d1_z2}) dfree(p);
   dfree(c->wbuf);
+  for (double* p : c->store_chunks) dfree(p);
   dfree(c->zeros64);
   dfree(c->gamma_d);
   if (c->qy) dfree(c->qy);
@@ -1270,6 +1317,13 @@ static int init_basis_common(kry_ctx* c, double* gamma, double* beta2) {
   c->i_old = -1; c->i_cur = 0; c->i_new = 1;
   c->rank = -1;
   KRY_CHECK(do_init(c, c->slot[0], c->ld, 0));
+  store_drop(c);
+  if (c->store_req && !step_on(c) && !dist(c) && c->ld == c->s) {
+    c->store_ok = true;
+    int64_t ld2 = 0;
+    double* dst = store_slot(c, 1, &ld2);
+    if (dst) KRY_CHECK(launch_copy_block(c->stream, c->s, c->slot[0], c->ld, dst, ld2, c->n));
+  }
   c->beta2 = c->st_h->beta2;
   KRY_CUDA(cudaMemcpyAsync(c->gamma_d, c->st->gamma, 64 * sizeof(double),
                            cudaMemcpyDeviceToDevice, c->stream));
@@ -1912,6 +1966,12 @@ int kry_finalize_sylv1(kry_ctx* a, double eps, int* rank, double* discarded, dou
   return KRY_OK;
 }
 
+int kry_set_storage(kry_ctx* c, int stored) {
+  c->store_req = stored != 0;
+  if (!c->store_req) store_drop(c);
+  return KRY_OK;
+}
+
 int kry_recover(kry_ctx* c, double* zhost) {
   KRY_CUDA(cudaSetDevice(c->dev));
   if (c->rank < 0) return fail(KRY_ERR_STATE, "finalize has not been called");
@@ -1920,10 +1980,40 @@ int kry_recover(kry_ctx* c, double* zhost) {
   const int64_t n = c->n;
   if (c->Z && c->z_cap < n * std::max(r, 1)) { dfree(c->Z); c->Z = nullptr; }
   if (!c->Z) {
-    KRY_CHECK(dalloc(&c->Z, (size_t)n * std::max(r, 1)));
+    if (dalloc(&c->Z, (size_t)n * std::max(r, 1)) != KRY_OK) {
+      // the stored basis is in the way: drop it and regenerate (two pass)
+      if (!c->store_ok) return KRY_ERR_CUDA;
+      cudaGetLastError();
+      store_drop(c);
+      cudaDeviceSynchronize();
+      KRY_CHECK(dalloc(&c->Z, (size_t)n * std::max(r, 1)));
+    }
     c->z_cap = n * std::max(r, 1);
   }
   if (r == 0) return KRY_OK;
+  if (c->store_ok && (int64_t)c->store_chunks.size() * c->store_G >= m) {
+    // storage="stored": Z = sum_j V_j S_j qy_j over the stored chunks, one
+    // DGEMM per chunk (reference _assemble_stored, solvers.py:125-127)
+    const int G = c->store_G;
+    double* Qc = nullptr;
+    KRY_CHECK(dalloc(&Qc, (size_t)G * s * r));
+    cublasSetStream(c->cublas, c->stream);
+    int rc = KRY_OK;
+    for (int q = 0; rc == KRY_OK && q * G < m; ++q) {
+      const int blk0 = q * G, nblk = std::min(G, m - blk0);
+      rc = launch_chunk_coef(c->stream, c->T.S, c->qy, s, r, blk0, nblk, Qc);
+      const double one = 1.0, beta = q == 0 ? 0.0 : 1.0;
+      if (rc == KRY_OK &&
+          cublasDgemm(c->cublas, CUBLAS_OP_N, CUBLAS_OP_N, r, (int)n, nblk * s, &one, Qc, r,
+                      c->store_chunks[q], G * s, &beta, c->Z, r) != CUBLAS_STATUS_SUCCESS)
+        rc = fail(KRY_ERR_CUDA, "cublasDgemm (stored Z) failed");
+    }
+    if (rc == KRY_OK) rc = zhost ? copy_out(c, zhost, c->Z, (size_t)n * r * sizeof(double))
+                                 : (cudaStreamSynchronize(c->stream) == cudaSuccess ? KRY_OK
+                                                                                    : KRY_ERR_CUDA);
+    dfree(Qc);
+    return rc;
+  }
   Prefault pf;   // fault in the host factor's pages while pass 2 runs
   if (zhost) pf.begin(zhost, (size_t)n * r * sizeof(double));
   size_t fr = 0, tot = 0;

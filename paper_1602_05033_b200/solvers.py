@@ -7,10 +7,13 @@ The host keeps only bookkeeping; every n-sized and k^2-sized operation is a
 C-ABI call into libkrymat_b200.so (pass-1 loop with the cheap residual every
 ``check_period`` iterations, finalisation, pass-2 regeneration of the basis).
 
-Storage: the device always uses the two-pass (windowed) regeneration; its
-factor equals the stored-mode factor (the regeneration is bitwise
-deterministic, verified by the replay check).  ``peak_basis_vectors`` follows
-the reference's accounting for the requested mode (``basis.py:63-71``).
+Storage: ``storage="stored"`` (the reference default) keeps every basis block
+of pass 1 in device memory while it fits and assembles Z = V qy directly
+(``_assemble_stored``, ``solvers.py:125-127``); ``"windowed"`` (and stored
+runs that outgrow the device) regenerate the basis in a second pass, which
+is bitwise deterministic (replay check), so both give the same factor.
+``peak_basis_vectors`` follows the reference's accounting for the requested
+mode (``basis.py:63-71``).
 """
 
 import ctypes
@@ -154,11 +157,14 @@ def host_factor(n, rank):
 class _Pass1:
     """Runs init + pass 1 on one context; keeps the state for finalisation."""
 
-    def __init__(self, op, c, opts):
+    def __init__(self, op, c, opts, store=False):
         self.op = op
         self.c = c
         self.s = c.shape[1]
         self.ctx = op.context(self.s, opts.max_m + 2)
+        # storage="stored": keep the basis on the device while it fits (the
+        # factor is then assembled without regenerating the basis)
+        _lib.check(_lib.load().kry_set_storage(self.ctx.ptr, 1 if store else 0))
         self.gamma = np.zeros((self.s, self.s))
         beta2 = ctypes.c_double()
         _lib.check(_lib.load().kry_init_basis(self.ctx.ptr, _lib.as_dptr(c),
@@ -190,7 +196,7 @@ def solve_lyapunov(op, c, options=None):
     c = _as_rhs(op, c)
     lib = _lib.load()
     tic = time.perf_counter()
-    p1 = _Pass1(op, c, opts)
+    p1 = _Pass1(op, c, opts, store=opts.storage == "stored")
     t_init = time.perf_counter() - tic
     try:
         hist = np.zeros((opts.max_m + 1, 5))
@@ -228,7 +234,9 @@ def solve_lyapunov(op, c, options=None):
             basis_seconds=t_basis,
             residual_seconds=t_res,
             recovery_seconds=t_rec,
-            peak_basis_vectors=_peak(opts.storage, m, ex, p1.s),
+            # steps of the reference run = converged iterations (the device may
+            # have computed one or two discarded blocks beyond)
+            peak_basis_vectors=_peak(opts.storage, min(m, its.value), ex, p1.s),
             truncation_discarded=disc.value,
             verified_residual=verified,
         )
@@ -399,7 +407,7 @@ def solve_sylvester_one_sided(op_a, b, c1, c2, options=None):
             basis_seconds=t_basis,
             residual_seconds=t_res,
             recovery_seconds=t_rec,
-            peak_basis_vectors=_peak(opts.storage, m.value, bool(exh.value), s),
+            peak_basis_vectors=_peak(opts.storage, min(m.value, converged_at), bool(exh.value), s),
             truncation_discarded=disc.value,
             verified_residual=verified,
         )
