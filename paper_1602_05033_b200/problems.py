@@ -110,6 +110,33 @@ def stencil_operator(grid, slab=None, comm=None):
     return StencilOperator((grid[0], 1, grid[1]), cd, co, 0.0, co, slab=slab, comm=comm)
 
 
+def gen_fd3d_split(n):
+    """(A, B) of the 3-D operator (e^{-xy} u_x)_x + (e^{xy} u_y)_y + 10 u_zz
+    split as a Sylvester pair: A the 2-D part (n^2), B = 10 laplacian1d(n)
+    (reference problems.py:78-85)."""
+    return gen_fd2d("fd2d-exp", n), (10.0 * laplacian1d(n)).tocsr()
+
+
+def gen_operator(kind, n):
+    """Matrix (or pair) of a named problem kind (reference problems.py:101-109)."""
+    if kind in ("fd2d-exp", "fd2d-trig", "laplacian2d"):
+        return gen_fd2d(kind, n)
+    if kind == "laplacian1d":
+        return laplacian1d(n)
+    if kind == "fd3d-split":
+        return gen_fd3d_split(n)
+    raise ValueError("unknown problem kind %r" % kind)
+
+
+def gen_rhs(n, s, seed, normalize=True):
+    """Right-hand side block, entries uniform in (0, 1) from PCG64(seed),
+    scaled to unit Frobenius norm (reference problems.py:88-98)."""
+    c = np.random.default_rng(seed).random((n, s))
+    if normalize:
+        c /= np.linalg.norm(c)
+    return c
+
+
 WORKLOADS = ("c1", "c2", "c3", "c4", "c5")
 
 DESCRIPTIONS = {
