@@ -370,6 +370,8 @@ int allreduce_gram(kry_ctx* c) {
 
 int run_apply_gram(kry_ctx* c, ApplyGramCall ag) {
   const int post = ag.post;
+  if (!dist(c) && ag.use_op && post == POST_STEP && ag.ldv == c->s && apply_gl_ok(c->op, c->s))
+    return launch_apply_gl(c->stream, c->s, c->op, ag, c->st, c->T, c->g);
   if (dist(c)) ag.post = POST_NONE;
   KRY_CHECK(launch_apply_gram(c->stream, c->s, c->op, ag, c->st, c->T, c->g, c->grid));
   if (dist(c)) {

@@ -146,6 +146,7 @@ enum PostMode {
   POST_SCALE = 8,       // explicit path: scale2 = trace
   POST_W2 = 9,          // explicit path: w2 = trace, zero test
   POST_FUSED = 10,      // fused step kernel: carried blocks + deferred solve of step j+1
+  POST_STEP8 = 11,      // POST_STEP with W0^T W0 at row 8 (register-fragment apply kernel)
 };
 
 struct TStore {  // projected-matrix storage (device), slots of 64 doubles
@@ -243,6 +244,11 @@ struct StepScratch {
 // fused-step geometry for an operator of n local points
 void step_geometry(const OpDev& op, int64_t n, int* ch, int* nch, int* lag);
 bool step_supported(const OpDev& op, int s, int64_t ld);
+// apply + Gram with register DMMA fragments (no shared-memory staging): one
+// GPU, stencil, even s, V a ring slot with zero halos; stores A V to c.wout
+bool apply_gl_ok(const OpDev& op, int s);
+int launch_apply_gl(cudaStream_t st, int s, const OpDev& op, const ApplyGramCall& c,
+                    DevState* dst, const TStore& T, GramScratch& g);
 int launch_step(cudaStream_t st, int s, const OpDev& op, StepCall c, DevState* dst,
                 const TStore& T, StepScratch& sc, float* prof_ms, cudaEvent_t* ev);
 

@@ -534,6 +534,9 @@ __device__ __noinline__ void run_post(int post, const double* total, DevState* s
     case POST_STEP:
       coef_solve(total, st, T, sm, 0, s, 0);
       break;
+    case POST_STEP8:   // [V^T W0 | W0^T W0] as two 8-row blocks (k_apply_gl)
+      coef_solve(total, st, T, sm, 0, 8, 0);
+      break;
     case POST_FUSED:
       // [Goc | GoW | Gcc | GcW | GWW] as five 8x8 blocks (k_step): the
       // carried blocks of POST_P, then the coefficient solve of step j+1

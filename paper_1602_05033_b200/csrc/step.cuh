@@ -249,6 +249,103 @@ __device__ __forceinline__ void step_consume(const OpDev& op, const StepCall& c,
   }
 }
 
+// ---------------------------------------------------------------- apply kernel, register fragments
+// The coefficient-solve input of the two-kernel path, [V^T W0 | W0^T W0]
+// with W0 = A V, computed like the fused kernel's consumption: lane (g, t)
+// holds column g of points t and t + 4 of an 8-point group (8-byte loads,
+// 256 contiguous bytes per instruction), the stencil uses the zero-halo
+// redirection, both Grams are DMMAs straight from the registers, and W0 is
+// stored for the combine kernel.  No shared-memory staging (the staged
+// kernel spent ~30 % of its LSU wavefronts on the smem tile).
+template <int S, bool TAIL>
+__device__ __forceinline__ void apply_gl_group(const OpDev& op, const ApplyGramCall& c, int pb,
+                                               double (&acc)[2][2]) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int n = (int)c.n;
+  const int col = min(g, S - 1);
+  double v[2], w[2];
+  int ip[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const NbOff o = nb_off<TAIL>(op, pb + t + 4 * k, n, S);
+    ip[k] = pb + t + 4 * k;
+    const double* pc = c.v + o.i * S + col;
+    v[k] = __ldg(pc);
+    const double n0 = __ldg(pc + o.z0), n1 = __ldg(pc + o.y0), n2 = __ldg(pc + o.x0);
+    const double n3 = __ldg(pc + o.x1), n4 = __ldg(pc + o.y1), n5 = __ldg(pc + o.z1);
+    w[k] = stencil_val(op, o.i, v[k], n0, n1, n2, n3, n4, n5);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    if (c.wout && g < S && (!TAIL || ip[k] < n)) c.wout[(int64_t)ip[k] * S + g] = w[k];
+    dmma(acc[0][0], acc[0][1], v[k], w[k]);   // V^T W0
+    dmma(acc[1][0], acc[1][1], w[k], w[k]);   // W0^T W0
+  }
+}
+
+template <int S>
+__global__ void __launch_bounds__(128, 8) k_apply_gl(OpDev op, ApplyGramCall c, DevState* st,
+                                                     TStore T, double* partials,
+                                                     unsigned* ticket) {
+  __shared__ __align__(16) double sX[4 * 128 + 14 * 64 + 256];
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  const int warp = threadIdx.x >> 5;
+  const int64_t ntiles = (c.n + TP - 1) / TP;
+  const int n = (int)c.n;
+  const TileOrder ord(ntiles);
+  for (int64_t k = 0; ord.valid(k); ++k) {
+    const int64_t it = ord.at(k);
+    const int64_t tile = c.reverse ? (ntiles - 1 - it) : it;
+    if (threadIdx.x == 0 && ord.valid(k + 1)) {
+      const int64_t nx_ = ord.at(k + 1);
+      const int64_t nt = c.reverse ? (ntiles - 1 - nx_) : nx_;
+      prefetch_rows(c.v, c.ldv, nt * TP, c.n);
+    }
+    // this warp's 32 points = four 8-point groups
+    const int p0 = (int)(tile * TP) + warp * 32;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int pb = p0 + 8 * q;
+      if (pb >= n) break;
+      if (pb + 8 <= n)
+        apply_gl_group<S, false>(op, c, pb, acc);
+      else
+        apply_gl_group<S, true>(op, c, pb, acc);
+    }
+  }
+  finish_reduction<16>(acc, sX, partials, ticket, c.post, st, T);
+}
+
+bool apply_gl_ok(const OpDev& op, int s) {
+  if (op.kind != KRY_OP_STENCIL || op.halo_lo || op.halo_hi) return false;
+  if (s != 2 && s != 4 && s != 6 && s != 8) return false;
+  // opt-in (KRY_APPLY_GL=1): measured on par with the staged kernel on c4
+  // (whole solve 0.89-0.91 s either way), so the staged one stays default
+  const char* on = getenv("KRY_APPLY_GL");
+  return on && on[0] == '1';
+}
+
+int launch_apply_gl(cudaStream_t st, int s, const OpDev& op, const ApplyGramCall& c,
+                    DevState* dst, const TStore& T, GramScratch& g) {
+  ApplyGramCall cc = c;
+  cc.post = POST_STEP8;
+#define L(S)                                                                      \
+  k_apply_gl<S><<<resident_grid(k_apply_gl<S>, c.n), TP, 0, st>>>(op, cc, dst, T, \
+                                                                  g.partials, g.ticket + 1)
+  switch (s) {
+    case 2: L(2); break;
+    case 4: L(4); break;
+    case 6: L(6); break;
+    case 8: L(8); break;
+    default: return fail(KRY_ERR_ARGUMENT, "apply_gl: unsupported block width");
+  }
+#undef L
+  count_launch();
+  KRY_CUDA(cudaGetLastError());
+  return KRY_OK;
+}
+
 // this warp waits until every chunk holding a stencil neighbour row of chunk
 // u is complete (c.fpl releases per chunk and launch)
 __device__ __forceinline__ void step_wait(const OpDev& op, const StepCall& c, int64_t u,
