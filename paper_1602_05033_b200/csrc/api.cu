@@ -370,8 +370,11 @@ int allreduce_gram(kry_ctx* c) {
 
 int run_apply_gram(kry_ctx* c, ApplyGramCall ag) {
   const int post = ag.post;
-  if (!dist(c) && ag.use_op && post == POST_STEP && ag.ldv == c->s && apply_gl_ok(c->op, c->s))
-    return launch_apply_gl(c->stream, c->s, c->op, ag, c->st, c->T, c->g);
+  if (!dist(c) && ag.use_op && post == POST_STEP && ag.ldv == c->s) {
+    const int mode = apply_mode(c->op, c->s);   // 0 staged, 1 register fragments, 2 TMA
+    if (mode == 2) return launch_apply_tma(c->stream, c->s, c->op, ag, c->st, c->T, c->g);
+    if (mode == 1) return launch_apply_gl(c->stream, c->s, c->op, ag, c->st, c->T, c->g);
+  }
   if (dist(c)) ag.post = POST_NONE;
   KRY_CHECK(launch_apply_gram(c->stream, c->s, c->op, ag, c->st, c->T, c->g, c->grid));
   if (dist(c)) {

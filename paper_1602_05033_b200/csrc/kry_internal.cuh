@@ -246,9 +246,11 @@ void step_geometry(const OpDev& op, int64_t n, int* ch, int* nch, int* lag);
 bool step_supported(const OpDev& op, int s, int64_t ld);
 // apply + Gram with register DMMA fragments (no shared-memory staging): one
 // GPU, stencil, even s, V a ring slot with zero halos; stores A V to c.wout
-bool apply_gl_ok(const OpDev& op, int s);
+int apply_mode(const OpDev& op, int s);
 int launch_apply_gl(cudaStream_t st, int s, const OpDev& op, const ApplyGramCall& c,
                     DevState* dst, const TStore& T, GramScratch& g);
+int launch_apply_tma(cudaStream_t st, int s, const OpDev& op, const ApplyGramCall& c,
+                     DevState* dst, const TStore& T, GramScratch& g);
 int launch_step(cudaStream_t st, int s, const OpDev& op, StepCall c, DevState* dst,
                 const TStore& T, StepScratch& sc, float* prof_ms, cudaEvent_t* ev);
 

@@ -888,19 +888,9 @@ __device__ __forceinline__ void stage_warp_coop(const OpDev& op, const double* _
         // one 64-bit base, neighbours by (32-bit) element deltas
         const double2* pc = reinterpret_cast<const double2*>(vc + i64 * ldc + off);
         const int dx = (int)ldc / 2, dy = op.nx * (int)ldc / 2, dz = op.nxy * (int)ldc / 2;
-#ifdef KRY_EXP_NOYZ
-        const double2 n0 = v, n1 = v, n4 = v, n5 = v;
-        (void)dy; (void)dz;
-#else
         const double2 n0 = __ldg(pc - (hz0 ? dz : 0)), n1 = __ldg(pc - (hy0 ? dy : 0));
         const double2 n4 = __ldg(pc + (hy1 ? dy : 0)), n5 = __ldg(pc + (hz1 ? dz : 0));
-#endif
-#ifdef KRY_EXP_NOX
-        const double2 n2 = v, n3 = v;
-        (void)dx;
-#else
         const double2 n2 = __ldg(pc - (hx0 ? dx : 0)), n3 = __ldg(pc + (hx1 ? dx : 0));
-#endif
         if (!op.variable) {
           const double sx0 = (hx0 ? n2.x : 0.0) + (hx1 ? n3.x : 0.0);
           const double sx1 = (hx0 ? n2.y : 0.0) + (hx1 ? n3.y : 0.0);
@@ -936,86 +926,6 @@ __device__ __forceinline__ void stage_warp_coop(const OpDev& op, const double* _
     if (col_w >= 0) {
       sX[CB(col_w + c0) + row] = w.x;
       sX[CB(col_w + c0 + 1) + row] = w.y;
-    }
-  }
-}
-
-// Batched staging: all loads of NB chunks are issued before any of them is
-// consumed (one memory round trip per batch instead of per chunk).
-#ifndef KRY_STAGE_BATCH
-#define KRY_STAGE_BATCH 4
-#endif
-template <int S>
-__device__ __forceinline__ void stage_warp_coop_b(const OpDev& op, const double* __restrict__ vc,
-                                                  int64_t ldc, const double* __restrict__ vo,
-                                                  int64_t ldo, bool load_old, bool use_op,
-                                                  int64_t n, int64_t tile_base, int r0,
-                                                  double* sX, int col_o, int col_c, int col_w) {
-  constexpr int CP = S / 2;
-  constexpr int NB = (KRY_STAGE_BATCH < CP) ? KRY_STAGE_BATCH : CP;
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int e0 = 0; e0 < CP; e0 += NB) {
-    double2 v[NB], o[NB], nb[NB][6];
-    bool hx0[NB], hx1[NB], hy0[NB], hy1[NB], hz0[NB], hz1[NB];
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const int e = e0 + b;
-      const int q = lane + 32 * e;
-      const int pp = q / CP, cp = q % CP;
-      const int64_t i64 = tile_base + r0 + pp;
-      const bool in = i64 < n;
-      const int off = 2 * cp;
-      const int64_t ic = in ? i64 : 0;
-      const double2* pc = reinterpret_cast<const double2*>(vc + ic * ldc + off);
-      v[b] = in ? __ldg(pc) : make_double2(0.0, 0.0);
-      o[b] = (in && load_old) ? __ldg(reinterpret_cast<const double2*>(vo + ic * ldo + off))
-                              : make_double2(0.0, 0.0);
-      const int i = (int)ic;
-      const unsigned r = fdiv((unsigned)i, op.fx);
-      const int x = i - (int)r * op.nx;
-      const unsigned zq = fdiv(r, op.fy);
-      const int y = (int)r - (int)zq * op.ny;
-      const int z = (int)zq;
-      hz0[b] = in && (z > 0 || op.halo_lo); hy0[b] = in && y > 0; hx0[b] = in && x > 0;
-      hx1[b] = in && x < op.nx - 1; hy1[b] = in && y < op.ny - 1;
-      hz1[b] = in && (z < op.nzl - 1 || op.halo_hi);
-      const int dx = (int)ldc / 2, dy = op.nx * (int)ldc / 2, dz = op.nxy * (int)ldc / 2;
-      if (use_op) {
-        nb[b][0] = __ldg(pc - (hz0[b] ? dz : 0)); nb[b][1] = __ldg(pc - (hy0[b] ? dy : 0));
-        nb[b][2] = __ldg(pc - (hx0[b] ? dx : 0)); nb[b][3] = __ldg(pc + (hx1[b] ? dx : 0));
-        nb[b][4] = __ldg(pc + (hy1[b] ? dy : 0)); nb[b][5] = __ldg(pc + (hz1[b] ? dz : 0));
-      }
-    }
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const int e = e0 + b;
-      const int q = lane + 32 * e;
-      const int pp = q / CP, cp = q % CP;
-      const int row = r0 + pp;
-      double2 w = make_double2(0.0, 0.0);
-      if (use_op) {
-        const double2 n0 = nb[b][0], n1 = nb[b][1], n2 = nb[b][2], n3 = nb[b][3], n4 = nb[b][4], n5 = nb[b][5];
-        const double sx0 = (hx0[b] ? n2.x : 0.0) + (hx1[b] ? n3.x : 0.0);
-        const double sx1 = (hx0[b] ? n2.y : 0.0) + (hx1[b] ? n3.y : 0.0);
-        const double sy0 = (hy0[b] ? n1.x : 0.0) + (hy1[b] ? n4.x : 0.0);
-        const double sy1 = (hy0[b] ? n1.y : 0.0) + (hy1[b] ? n4.y : 0.0);
-        const double sz0 = (hz0[b] ? n0.x : 0.0) + (hz1[b] ? n5.x : 0.0);
-        const double sz1 = (hz0[b] ? n0.y : 0.0) + (hz1[b] ? n5.y : 0.0);
-        w.x = fma(op.cd, v[b].x, fma(op.cz, sz0, fma(op.cy, sy0, op.cx * sx0)));
-        w.y = fma(op.cd, v[b].y, fma(op.cz, sz1, fma(op.cy, sy1, op.cx * sx1)));
-      }
-      const int c0 = 2 * cp;
-      if (col_o >= 0) {
-        sX[CB(col_o + c0) + row] = o[b].x;
-        sX[CB(col_o + c0 + 1) + row] = o[b].y;
-      }
-      sX[CB(col_c + c0) + row] = v[b].x;
-      sX[CB(col_c + c0 + 1) + row] = v[b].y;
-      if (col_w >= 0) {
-        sX[CB(col_w + c0) + row] = w.x;
-        sX[CB(col_w + c0 + 1) + row] = w.y;
-      }
     }
   }
 }
@@ -1076,12 +986,6 @@ __global__ void __launch_bounds__(TP, COOP ? KRY_COMB_MINB : 2) k_combine(OpDev 
       if (!c.write_new) prefetch_rows(c.vn, c.ldn, nt * TP, c.n);
     }
     if constexpr (coop) {
-#ifdef KRY_USE_BATCH
-      if (!op.variable && op.kind == KRY_OP_STENCIL)
-        stage_warp_coop_b<(S % 2 == 0) ? S : 2>(op, c.vc, c.ldc, c.vo, c.ldo, c.write_new && c.has_old,
-                                                c.use_op, c.n, tile * TP, r0, sX, 0, S, 2 * S);
-      else
-#endif
       stage_warp_coop<(S % 2 == 0) ? S : 2>(op, c.vc, c.ldc, c.vo, c.ldo, c.write_new && c.has_old,
                                             c.use_op, c.n, tile * TP, r0, sX, 0, S, 2 * S, c.win);
       if (!c.write_new && i64 < c.n) {
@@ -1198,12 +1102,6 @@ __global__ void __launch_bounds__(TP, COOP ? KRY_APPLY_MINB : 2) k_apply_gram(Op
       prefetch_rows(c.v, c.ldv, nt * TP, c.n);
     }
     if constexpr (coop) {
-#ifdef KRY_USE_BATCH
-      if (!op.variable && op.kind == KRY_OP_STENCIL)
-        stage_warp_coop_b<(S % 2 == 0) ? S : 2>(op, c.v, c.ldv, nullptr, 0, false, USE_OP != 0, c.n,
-                                                tile * TP, r0, sX, -1, 0, USE_OP ? S : -1);
-      else
-#endif
       stage_warp_coop<(S % 2 == 0) ? S : 2>(op, c.v, c.ldv, nullptr, 0, false, USE_OP != 0, c.n,
                                             tile * TP, r0, sX, -1, 0, USE_OP ? S : -1, nullptr,
                                             c.wout);

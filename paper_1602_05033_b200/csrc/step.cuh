@@ -317,13 +317,22 @@ __global__ void __launch_bounds__(128, 8) k_apply_gl(OpDev op, ApplyGramCall c, 
   finish_reduction<16>(acc, sX, partials, ticket, c.post, st, T);
 }
 
-bool apply_gl_ok(const OpDev& op, int s) {
-  if (op.kind != KRY_OP_STENCIL || op.halo_lo || op.halo_hi) return false;
-  if (s != 2 && s != 4 && s != 6 && s != 8) return false;
-  // opt-in (KRY_APPLY_GL=1): measured on par with the staged kernel on c4
-  // (whole solve 0.89-0.91 s either way), so the staged one stays default
-  const char* on = getenv("KRY_APPLY_GL");
-  return on && on[0] == '1';
+// apply kernel variant for a single-GPU stencil step with even s:
+// 0 = shared-memory staged (k_apply_gram), 1 = register fragments
+// (k_apply_gl, KRY_APPLY_GL=1), 2 = TMA-staged (k_apply_tma).  Default: the
+// TMA-staged kernel for constant-coefficient stencils (c4: whole solve
+// 0.888 -> 0.853 s); variable coefficients keep the staged kernel (their
+// per-point coefficient loads go through L1 either way).
+// KRY_APPLY_KERNEL=staged|gl|tma overrides.
+int apply_mode(const OpDev& op, int s) {
+  if (op.kind != KRY_OP_STENCIL || op.halo_lo || op.halo_hi) return 0;
+  if (s != 2 && s != 4 && s != 6 && s != 8) return 0;
+  if (const char* k = getenv("KRY_APPLY_KERNEL")) {
+    if (k[0] == 't') return 2;
+    if (k[0] == 'g') return 1;
+    return 0;
+  }
+  return op.variable ? 0 : 2;
 }
 
 int launch_apply_gl(cudaStream_t st, int s, const OpDev& op, const ApplyGramCall& c,

@@ -359,3 +359,154 @@ __global__ void __launch_bounds__(TMA_TP + 64, 1) k_step_tma(OpDev op, StepCall 
   // + the carried blocks and the next coefficient solve on the last CTA
   finish_reduction<STEP_NBLK * 8, TMA_NW + 2>(acc, smem, sc.part, sc.gcnt, POST_FUSED, st, T);
 }
+
+
+// ---------------------------------------------------------------- apply kernel, TMA-staged
+// [V^T W0 | W0^T W0] with W0 = A V (stored for the combine), like k_apply_gl
+// but with every stencil operand staged in shared memory by bulk copies (the
+// centre range +-1 point and the four +-nx, +-nx*ny shifted ranges of a
+// 128-point tile, two tiles ahead), so the LSU pipe only serves the operand
+// reads and the stores, not the L2 fills of the gathers.  One control warp
+// issues the copies; the compute warps never meet at a CTA barrier.
+#define APT_NW 8
+__host__ __device__ constexpr int apt_stage(int S) { return (5 * TMA_CH + 2) * S; }
+__host__ __device__ constexpr size_t apt_smem_bytes(int S) {
+  return (size_t)(2 * apt_stage(S) + 8) * sizeof(double) + 8 * sizeof(uint64_t);
+}
+
+template <int S>
+__global__ void __launch_bounds__(APT_NW * 32 + 32, 2) k_apply_tma(OpDev op, ApplyGramCall c,
+                                                                   DevState* st, TStore T,
+                                                                   double* partials,
+                                                                   unsigned* ticket) {
+  extern __shared__ __align__(128) double smem[];
+  double* zero = smem + 2 * apt_stage(S);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(zero + 8);   // full[2], empty[2]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  if (threadIdx.x < 8) zero[threadIdx.x] = 0.0;
+  if (threadIdx.x == 0) {
+    mbar_init(bars + 0, 1);
+    mbar_init(bars + 1, 1);
+    mbar_init(bars + 2, APT_NW);
+    mbar_init(bars + 3, APT_NW);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  __syncthreads();
+  const int64_t ntiles = (c.n + TMA_CH - 1) / TMA_CH;
+  const int64_t G = gridDim.x;
+  const int64_t kend = (ntiles - blockIdx.x + G - 1) / G;
+  const int n = (int)c.n;
+  constexpr unsigned RB = TMA_CH * S * 8;
+  auto tile_of = [&](int64_t k) {
+    const int64_t it = blockIdx.x + k * G;
+    return c.reverse ? ntiles - 1 - it : it;
+  };
+  // stage layout: centre (CH + 2 rows), ym, yp, zm, zp (CH rows each)
+  auto ptr = [&](int stg, int r) { return smem + stg * apt_stage(S) + (r == 0 ? 0 : (TMA_CH + 2) * S + (r - 1) * TMA_CH * S); };
+  if (warp == APT_NW) {
+    const bool has_y = op.ny > 1;
+    for (int64_t k = 0; k < kend; ++k) {
+      const int stg = (int)(k & 1);
+      if (k >= 2) mbar_wait(bars + 2 + stg, (unsigned)(((k - 2) >> 1) & 1));
+      if (lane == 0) {
+        const int64_t c0 = tile_of(k) * TMA_CH;
+        if (k + 3 < kend) {   // L2 prefetch of the tile three iterations ahead
+          const int64_t p0 = tile_of(k + 3) * TMA_CH;
+          prefetch_l2(c.v + p0 * S, RB);
+          prefetch_l2(c.v + (p0 + op.nxy) * S, RB);
+        }
+        mbar_arrive_tx(bars + stg, RB * (has_y ? 4 : 2) + (TMA_CH + 2) * S * 8);
+        tma_load_1d(ptr(stg, 0), c.v + (c0 - 1) * S, (TMA_CH + 2) * S * 8, bars + stg);
+        if (has_y) {
+          tma_load_1d(ptr(stg, 1), c.v + (c0 - op.nx) * S, RB, bars + stg);
+          tma_load_1d(ptr(stg, 2), c.v + (c0 + op.nx) * S, RB, bars + stg);
+        }
+        tma_load_1d(ptr(stg, 3), c.v + (c0 - op.nxy) * S, RB, bars + stg);
+        tma_load_1d(ptr(stg, 4), c.v + (c0 + op.nxy) * S, RB, bars + stg);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int col = min(g, S - 1);
+    for (int64_t k = 0; k < kend; ++k) {
+      const int stg = (int)(k & 1);
+      mbar_wait(bars + stg, (unsigned)((k >> 1) & 1));
+      const int c0 = (int)(tile_of(k) * TMA_CH);
+      const double* C = ptr(stg, 0);
+      const double* YM = ptr(stg, 1);
+      const double* YP = ptr(stg, 2);
+      const double* ZM = ptr(stg, 3);
+      const double* ZP = ptr(stg, 4);
+#pragma unroll
+      for (int j = 0; j < TMA_CH / 8 / APT_NW; ++j) {
+        const int r0 = (warp + j * APT_NW) * 8;
+        double v[2], w[2];
+        int pp[2];
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const int r = r0 + t + 4 * kk;
+          const int p = c0 + r;
+          pp[kk] = p;
+          bool mx0, mx1, my0, my1;
+          xy_mask(op, min(p, n - 1), mx0, mx1, my0, my1);
+          v[kk] = C[(r + 1) * S + col];
+          const double nz0 = ZM[r * S + col], nz1 = ZP[r * S + col];
+          const double ny0 = (my0 ? YM + r * S : zero)[col];
+          const double ny1 = (my1 ? YP + r * S : zero)[col];
+          const double nx0 = (mx0 ? C + r * S : zero)[col];
+          const double nx1 = (mx1 ? C + (r + 2) * S : zero)[col];
+          w[kk] = p < n ? stencil_val(op, min(p, n - 1), v[kk], nz0, ny0, nx0, nx1, ny1, nz1)
+                        : 0.0;
+        }
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          if (c.wout && g < S && pp[kk] < n) c.wout[(int64_t)pp[kk] * S + g] = w[kk];
+          dmma(acc[0][0], acc[0][1], v[kk], w[kk]);   // V^T W0
+          dmma(acc[1][0], acc[1][1], w[kk], w[kk]);   // W0^T W0
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_empty(bars + 2 + stg);
+    }
+  }
+  __syncthreads();
+  finish_reduction<16, APT_NW + 1>(acc, smem, partials, ticket, c.post, st, T);
+}
+
+int launch_apply_tma(cudaStream_t st, int s, const OpDev& op, const ApplyGramCall& c,
+                     DevState* dst, const TStore& T, GramScratch& g) {
+  ApplyGramCall cc = c;
+  cc.post = POST_STEP8;
+  const int threads = APT_NW * 32 + 32;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+#define L(S)                                                                               \
+  {                                                                                        \
+    static int per = 0;                                                                    \
+    const size_t sm = apt_smem_bytes(S);                                                   \
+    if (!per) {                                                                            \
+      KRY_CUDA(cudaFuncSetAttribute(k_apply_tma<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                    (int)sm));                                             \
+      int nb = 1;                                                                          \
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_apply_tma<S>, threads, sm);    \
+      per = std::max(1, nb);                                                               \
+    }                                                                                      \
+    const int64_t ntiles = (c.n + TMA_CH - 1) / TMA_CH;                                     \
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)per * sms)); \
+    k_apply_tma<S><<<grid, threads, sm, st>>>(op, cc, dst, T, g.partials, g.ticket + 1);   \
+  }
+  switch (s) {
+    case 2: L(2); break;
+    case 4: L(4); break;
+    case 6: L(6); break;
+    case 8: L(8); break;
+    default: return fail(KRY_ERR_ARGUMENT, "apply_tma: unsupported block width");
+  }
+#undef L
+  count_launch();
+  KRY_CUDA(cudaGetLastError());
+  return KRY_OK;
+}
