@@ -429,7 +429,15 @@ __global__ void __launch_bounds__(APT_NW * 32 + 32, 2) k_apply_tma(OpDev op, App
       __syncwarp();
     }
   } else {
-    const int col = min(g, S - 1);
+    // operand reads in the production layout (lane (g, t) = point perm(g),
+    // columns {2t, 2t+1}; 16-byte shared loads without bank conflicts), the
+    // stencil per column pair, A V stored as 512 contiguous bytes per warp,
+    // then V and W0 transposed by a DMMA with a permuted identity (exact)
+    // into the Gram fragment layout (column g of points t and 4 + (t+1)%4)
+    const int col = min(2 * t, S - 2);
+    const double e0 = (g == 2 * t && 2 * t < S) ? 1.0 : 0.0;          // k-step h = 0
+    const double e1 = (g == 2 * t + 1 && 2 * t + 1 < S) ? 1.0 : 0.0;  // k-step h = 1
+    const int pg = (g & 1) ? 4 + (((g >> 1) + 1) & 3) : (g >> 1);
     for (int64_t k = 0; k < kend; ++k) {
       const int stg = (int)(k & 1);
       mbar_wait(bars + stg, (unsigned)((k >> 1) & 1));
@@ -442,30 +450,32 @@ __global__ void __launch_bounds__(APT_NW * 32 + 32, 2) k_apply_tma(OpDev op, App
 #pragma unroll
       for (int j = 0; j < TMA_CH / 8 / APT_NW; ++j) {
         const int r0 = (warp + j * APT_NW) * 8;
-        double v[2], w[2];
-        int pp[2];
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {
-          const int r = r0 + t + 4 * kk;
-          const int p = c0 + r;
-          pp[kk] = p;
-          bool mx0, mx1, my0, my1;
-          xy_mask(op, min(p, n - 1), mx0, mx1, my0, my1);
-          v[kk] = C[(r + 1) * S + col];
-          const double nz0 = ZM[r * S + col], nz1 = ZP[r * S + col];
-          const double ny0 = (my0 ? YM + r * S : zero)[col];
-          const double ny1 = (my1 ? YP + r * S : zero)[col];
-          const double nx0 = (mx0 ? C + r * S : zero)[col];
-          const double nx1 = (mx1 ? C + (r + 2) * S : zero)[col];
-          w[kk] = p < n ? stencil_val(op, min(p, n - 1), v[kk], nz0, ny0, nx0, nx1, ny1, nz1)
-                        : 0.0;
+        const int r = r0 + pg;
+        const int p = c0 + r;
+        bool mx0, mx1, my0, my1;
+        xy_mask(op, min(p, n - 1), mx0, mx1, my0, my1);
+        auto ld2 = [&](const double* row) { return *reinterpret_cast<const double2*>(row + col); };
+        const double2 v = ld2(C + (r + 1) * S);
+        const double2 z0 = ld2(ZM + r * S), z1 = ld2(ZP + r * S);
+        const double2 y0 = ld2(my0 ? YM + r * S : zero), y1 = ld2(my1 ? YP + r * S : zero);
+        const double2 x0 = ld2(mx0 ? C + r * S : zero), x1 = ld2(mx1 ? C + (r + 2) * S : zero);
+        double2 w = make_double2(0.0, 0.0);
+        if (p < n) {
+          const int pc = min(p, n - 1);
+          w.x = stencil_val(op, pc, v.x, z0.x, y0.x, x0.x, x1.x, y1.x, z1.x);
+          w.y = stencil_val(op, pc, v.y, z0.y, y0.y, x0.y, x1.y, y1.y, z1.y);
+          if (c.wout && 2 * t < S)
+            *reinterpret_cast<double2*>(c.wout + (int64_t)p * S + 2 * t) = w;
         }
-#pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {
-          if (c.wout && g < S && pp[kk] < n) c.wout[(int64_t)pp[kk] * S + g] = w[kk];
-          dmma(acc[0][0], acc[0][1], v[kk], w[kk]);   // V^T W0
-          dmma(acc[1][0], acc[1][1], w[kk], w[kk]);   // W0^T W0
-        }
+        double vt0 = 0.0, vt1 = 0.0, wt0 = 0.0, wt1 = 0.0;
+        dmma(vt0, vt1, e0, v.x);
+        dmma(vt0, vt1, e1, v.y);
+        dmma(wt0, wt1, e0, w.x);
+        dmma(wt0, wt1, e1, w.y);
+        dmma(acc[0][0], acc[0][1], vt0, wt0);   // V^T W0, points t
+        dmma(acc[0][0], acc[0][1], vt1, wt1);   //         points 4 + (t+1)%4
+        dmma(acc[1][0], acc[1][1], wt0, wt0);   // W0^T W0
+        dmma(acc[1][0], acc[1][1], wt1, wt1);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_empty(bars + 2 + stg);
