@@ -219,12 +219,18 @@ __global__ void __launch_bounds__(1024) k_eig_deflate(EigView e, int K, const do
     db += td;
   }
   __syncthreads();
+  // rotated deflations can break the order of the deflated list locally;
+  // the (usually sorted) list is checked by the whole block, and only a
+  // disordered one goes through the serial insertion-sort fix-up (the
+  // single-thread scan over ~K/2 deflated entries dominated this kernel)
+  int unsorted = 0;
+  for (int i = 1 + threadIdx.x; i < db; i += blockDim.x)
+    unsorted |= (e.def_lam[i] < e.def_lam[i - 1]) ? 1 : 0;
+  unsorted = __syncthreads_or(unsorted);
   if (threadIdx.x == 0) {
     e.counts[0] = pb;
     e.counts[1] = db;
-    // rotated deflations can break the order of the deflated list locally:
-    // insertion-sort fix-up (rare, local disorder only)
-    for (int i = 1; i < db; ++i) {
+    for (int i = 1; unsorted && i < db; ++i) {
       double v = e.def_lam[i];
       if (v >= e.def_lam[i - 1]) continue;
       int ix = e.def_idx[i];
