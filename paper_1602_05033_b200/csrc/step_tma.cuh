@@ -368,7 +368,9 @@ __global__ void __launch_bounds__(TMA_TP + 64, 1) k_step_tma(OpDev op, StepCall 
 // 128-point tile, two tiles ahead), so the LSU pipe only serves the operand
 // reads and the stores, not the L2 fills of the gathers.  One control warp
 // issues the copies; the compute warps never meet at a CTA barrier.
+#ifndef APT_NW
 #define APT_NW 8
+#endif
 __host__ __device__ constexpr int apt_stage(int S) { return (5 * TMA_CH + 2) * S; }
 __host__ __device__ constexpr size_t apt_smem_bytes(int S) {
   return (size_t)(2 * apt_stage(S) + 8) * sizeof(double) + 8 * sizeof(uint64_t);
