@@ -937,6 +937,11 @@ template <int S, bool COOP>
 #ifndef KRY_COMB_MINB
 #define KRY_COMB_MINB 5
 #endif
+// resident CTAs per SM of the combine kernel (0 = occupancy limit); a cap
+// leaves room for the eigen stream's kernels next to the HBM-bound combine
+#ifndef KRY_COMB_CAP
+#define KRY_COMB_CAP 0
+#endif
 #ifndef KRY_APPLY_MINB
 #define KRY_APPLY_MINB 8
 #endif
@@ -1279,7 +1284,7 @@ int gram_grid_for(int64_t n) {
 // persistent grid = resident CTAs (occupancy x SMs), capped by the tile count,
 // so the grid-stride tile loop runs in exactly one wave
 template <class Kern>
-static int resident_grid(Kern kernel, int64_t n) {
+static int resident_grid(Kern kernel, int64_t n, int cap_per_sm = 0) {
   static std::mutex mu;
   static std::unordered_map<const void*, int> cache;
   int per_sm = 0;
@@ -1291,6 +1296,7 @@ static int resident_grid(Kern kernel, int64_t n) {
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, TP, 0);
+      if (cap_per_sm > 0) nb = std::min(nb, cap_per_sm);
       per_sm = std::max(1, nb) * sms;
       cache[(const void*)kernel] = per_sm;
     } else {
@@ -1323,7 +1329,7 @@ int launch_combine(cudaStream_t st, int s, const OpDev& op, const CombineCall& c
                     (!c.has_old || c.ldo % 2 == 0);
   if (coop) {
 #define L(S)                                                                 \
-  k_combine<S, true><<<resident_grid(k_combine<S, true>, c.n), TP, 0, st>>>( \
+  k_combine<S, true><<<resident_grid(k_combine<S, true>, c.n, KRY_COMB_CAP), TP, 0, st>>>( \
       op, c, dst, T, g.partials, g.ticket + 0)
     KRY_DISPATCH_S(s, L);
 #undef L
