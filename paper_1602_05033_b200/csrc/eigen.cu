@@ -747,12 +747,26 @@ __global__ void __launch_bounds__(128) k_cauchy_sum(int nx, int nyc, int nmin, c
   __syncthreads();
   if (!s_last) return;
   __threadfence();
+  // the last CTA: block-parallel sum of the CTA partials (fixed per-thread
+  // stride and tree order, so the value is reproducible) and min of the
+  // denominator mins (a single-thread sweep here cost ~10 us per check)
+  double tot = 0.0, mn = 1e300;
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) tot += __ldcg(partials + b);
+  for (int b = threadIdx.x; b < nmin; b += blockDim.x) mn = fmin(mn, __ldcg(pmin + b));
+  __shared__ double rm[128];
+  rs[threadIdx.x] = tot;
+  rm[threadIdx.x] = mn;
+  __syncthreads();
+  for (int o = 64; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      rs[threadIdx.x] += rs[threadIdx.x + o];
+      rm[threadIdx.x] = fmin(rm[threadIdx.x], rm[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
-    double tot = 0.0, mn = 1e300;
-    for (unsigned b = 0; b < gridDim.x; ++b) tot += __ldcg(partials + b);
-    for (int b = 0; b < nmin; ++b) mn = fmin(mn, __ldcg(pmin + b));
-    res[0] = tot;
-    res[1] = mn;
+    res[0] = rs[0];
+    res[1] = rm[0];
     *ticket = 0u;
   }
 }

@@ -68,14 +68,30 @@ __global__ void k_ytilde(const double* u, const double* lx, int nx, const double
 // k stored ascending (desc=0: eigenvalues from syevd) or descending (desc=1:
 // singular values).  out[0] = rank, out[1] = discarded, out[2] = min value,
 // out[3] = max |value|, out[4] = min denominator over parts.
+template <bool SM>
 __global__ void k_truncate(const double* ev, int k, int desc, double eps, const double* mind_part,
                            int nparts, double* work, double* out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  // cumulative squares from the smallest (the reference's lam[::-1] order)
+  if (blockIdx.x != 0) return;
+  // the squares, smallest first (the reference's lam[::-1] order), staged in
+  // shared memory by the whole block (SM); the cumulative sum itself stays
+  // sequential (np.cumsum order, which decides the rank at the eps boundary)
+  extern __shared__ double sq[];
+  if (SM) {
+    for (int l = threadIdx.x; l < k; l += blockDim.x) {
+      const double x = desc ? ev[k - 1 - l] : ev[l];
+      sq[l] = x * x;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
   double acc = 0.0;
   for (int l = 0; l < k; ++l) {
-    const double x = desc ? ev[k - 1 - l] : ev[l];
-    acc += x * x;
+    if (SM) {
+      acc += sq[l];
+    } else {
+      const double x = desc ? ev[k - 1 - l] : ev[l];
+      acc += x * x;
+    }
     work[l] = acc;              // work[l] = sum of the l+1 smallest
   }
   int rank = 0;
@@ -166,7 +182,18 @@ int launch_ytilde(cudaStream_t st, const double* u, const double* lx, int nx, co
 }
 int launch_truncate(cudaStream_t st, const double* ev, int k, int desc, double eps,
                     const double* mind_part, int nparts, double* work, double* out) {
-  k_truncate<<<1, 32, 0, st>>>(ev, k, desc, eps, mind_part, nparts, work, out);
+  const size_t smb = (size_t)k * sizeof(double);
+  if (smb <= (size_t)200 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_truncate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
+      attr = true;
+    }
+    k_truncate<true><<<1, 256, smb, st>>>(ev, k, desc, eps, mind_part, nparts, work, out);
+  } else {
+    k_truncate<false><<<1, 32, 0, st>>>(ev, k, desc, eps, mind_part, nparts, work, out);
+  }
   count_launch();
   KRY_CUDA(cudaGetLastError());
   return KRY_OK;
