@@ -34,6 +34,9 @@
 namespace kry {
 
 static constexpr double EPS = 2.220446049250313e-16;
+#ifndef KRY_SECULAR_W8
+#define KRY_SECULAR_W8 0
+#endif
 
 // ------------------------------------------------------------------ block scan helpers
 __device__ __forceinline__ int warp_incl_scan(int v) {
@@ -861,7 +864,11 @@ int EigEngine::append_block(cudaStream_t st, const double* dsym_blk, const doubl
     }
     // K+1 roots at most, one CTA each; threads per root grow with K
     if (K >= 1024) {
+#if KRY_SECULAR_W8
+      if (K <= 256 * 8) k_eig_secular<8, 8><<<K + 1, 256, 0, st>>>(v);
+#else
       if (K <= 128 * 16) k_eig_secular<4, 16><<<K + 1, 128, 0, st>>>(v);
+#endif
       else k_eig_secular<4, 0><<<K + 1, 128, 0, st>>>(v);
     } else if (K >= 256) {
       k_eig_secular<2, 16><<<K + 1, 64, 0, st>>>(v);
