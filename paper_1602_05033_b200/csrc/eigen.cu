@@ -864,7 +864,9 @@ int EigEngine::append_block(cudaStream_t st, const double* dsym_blk, const doubl
     }
     // K+1 roots at most, one CTA each; threads per root grow with K
     if (K >= 1024) {
-#if KRY_SECULAR_W8
+#if KRY_SECULAR_W8 == 2
+      if (K <= 64 * 32) k_eig_secular<2, 32><<<K + 1, 64, 0, st>>>(v);
+#elif KRY_SECULAR_W8
       if (K <= 256 * 8) k_eig_secular<8, 8><<<K + 1, 256, 0, st>>>(v);
 #else
       if (K <= 128 * 16) k_eig_secular<4, 16><<<K + 1, 128, 0, st>>>(v);
