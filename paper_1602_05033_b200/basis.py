@@ -18,6 +18,7 @@ import numpy as np
 from . import _lib
 from .errors import DeflationUnsupportedError, DimensionMismatchError
 from .kernels import BlockTridiagonal
+from .operators import require_device
 
 #: Relative size of a residual block treated as zero (reference basis.py:30).
 ZERO_BLOCK_TOL = 1e-13
@@ -143,6 +144,7 @@ def init_basis(op, c, space="standard", storage="stored", fact=None, max_m=1000)
     ``max_m`` bounds the number of steps the device context can hold."""
     if space != "standard":
         raise NotImplementedError("extended Krylov spaces are outside the B200 hot path")
+    require_device(op)
     c = np.ascontiguousarray(np.asarray(c, dtype=float))
     if c.ndim != 2 or c.shape[0] != op.n:
         raise DimensionMismatchError(

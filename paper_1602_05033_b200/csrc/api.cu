@@ -319,6 +319,11 @@ struct kry_ctx {
   std::vector<double*> store_chunks;
   StepScratch sx{};
   int step_ch = 0, step_nch = 0, step_lag = 0;
+  // phase timing of the pass-1 loop (CUDA events, reused across solves):
+  // per iteration one completion event on the Lanczos stream and a begin/end
+  // pair on the eigen/check stream
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pool;
+  std::vector<cudaEvent_t> ev_step;
   // multi-GPU
   int nranks = 1, rank_id = 0;
   ncclComm_t comm = nullptr;
@@ -831,6 +836,7 @@ int check_sylv(kry_ctx* a, kry_ctx* b, double rhs_norm, double* res, double* rel
   KRY_CHECK(b->eig.compute_uw(b->stream, b->gamma_d, tau_ptr(b)));
   KRY_CUDA(cudaStreamSynchronize(b->stream));
   const int kA = a->eig.K, kB = b->eig.K;
+  KRY_CHECK(a->eig.ensure_cauchy(std::max(kA, kB), 0));
   // ||sd^T f||^2: rows over B, sum over A with c = f
   KRY_CHECK(a->eig.cauchy(a->stream, kB, b->eig.lam_cur(), b->eig.u, kA, a->eig.lam_cur(),
                           a->eig.u, a->eig.w, a->eig.res));
@@ -1105,15 +1111,9 @@ int kry_device_count(int* count) {
 int64_t kry_launch_count(void) { return g_launches.load(); }
 void kry_reset_launch_count(void) { g_launches = 0; }
 
-int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s, int max_m) {
-  *out = nullptr;
-  if (s < 1 || s > KRY_SMAX) return fail(KRY_ERR_ARGUMENT, "block width s must be in 1..8");
-  if (max_m < 1) return fail(KRY_ERR_ARGUMENT, "max_m must be >= 1");
-  if (od->n < 1 || od->n > ((int64_t)1 << 31) - 1)
-    return fail(KRY_ERR_DIMENSION, "operator order out of range");
-  KRY_CUDA(cudaSetDevice(device));
-  keep_pool_memory(device);
-  kry_ctx* c = new kry_ctx();
+// body of kry_ctx_create on a freshly allocated context; on failure the
+// caller tears the partial context down (streams, pinned buffers, window)
+static int ctx_create_body(kry_ctx* c, int device, const kry_operator_desc* od, int s, int max_m) {
   c->dev = device;
   c->s = s;
   c->max_m = max_m;
@@ -1128,10 +1128,8 @@ int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s
   op.kind = od->kind;
   int64_t nloc = od->n;
   if (od->kind == KRY_OP_STENCIL) {
-    if (od->nx < 1 || od->ny < 1 || od->nz < 1 || od->nx * od->ny * od->nz != od->n) {
-      delete c;
+    if (od->nx < 1 || od->ny < 1 || od->nz < 1 || od->nx * od->ny * od->nz != od->n)
       return fail(KRY_ERR_DIMENSION, "stencil grid does not match the operator order");
-    }
     int64_t z0 = od->z_begin, z1 = od->z_end;
     if (z1 <= z0) { z0 = 0; z1 = od->nz; }
     op.nx = (int)od->nx;
@@ -1153,7 +1151,7 @@ int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s
       const int64_t pad = op.nxy + 256;
       for (int q = 0; q < 4; ++q) {
         double* p = nullptr;
-        if (dalloc(&p, (size_t)(nloc + 2 * pad)) != KRY_OK) { delete c; return KRY_ERR_CUDA; }
+        if (dalloc(&p, (size_t)(nloc + 2 * pad)) != KRY_OK) return KRY_ERR_CUDA;
         c->op_mem.push_back(p);
         KRY_CUDA(cudaMemset(p, 0, (nloc + 2 * pad) * sizeof(double)));
         KRY_CUDA(cudaMemcpy(p + pad - lo, src[q] + z0 * op.nxy - lo,
@@ -1175,7 +1173,6 @@ int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s
     op.rp = rp; op.ci = ci; op.va = va;
     op.nx = 1; op.ny = 1; op.nzl = 1; op.nxy = 1;
   } else {
-    delete c;
     return fail(KRY_ERR_ARGUMENT, "unknown operator kind");
   }
   op.fx = make_fastdiv((unsigned)std::max(op.nx, 1));
@@ -1209,8 +1206,9 @@ int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s
   c->g.max_grid = KRY_MAX_GRID;
   // per-CTA partials + per-group totals of the two-level grid reduction
   KRY_CHECK(dalloc(&c->g.partials, (size_t)(c->g.max_grid + c->g.max_grid / 32 + 1) * 24 * 8));
-  KRY_CHECK(dalloc(&c->g.ticket, 2 + c->g.max_grid / 32));
-  KRY_CUDA(cudaMemset(c->g.ticket, 0, (2 + c->g.max_grid / 32) * sizeof(unsigned)));
+  // one disjoint counter block per reduction site (combine, apply, pair Gram)
+  KRY_CHECK(dalloc(&c->g.ticket, (size_t)KRY_TICKET_SITES * KRY_TICKET_STRIDE));
+  KRY_CUDA(cudaMemset(c->g.ticket, 0, (size_t)KRY_TICKET_SITES * KRY_TICKET_STRIDE * sizeof(unsigned)));
   // fused single-pass step scratch (stencil operators on one GPU)
   {
     // opt-in (KRY_FUSED_STEP=1): on B200 the single-pass kernel measured
@@ -1233,6 +1231,26 @@ int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s
   KRY_CHECK(dalloc(&c->gamma_d, 64));
   KRY_CUDA(cudaMemset(c->zeros64, 0, 64 * sizeof(double)));
   KRY_CHECK(c->eig.init(s, s * (max_m + 2), device));
+  return KRY_OK;
+}
+
+int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s, int max_m) {
+  *out = nullptr;
+  if (s < 1 || s > KRY_SMAX) return fail(KRY_ERR_ARGUMENT, "block width s must be in 1..8");
+  if (max_m < 1) return fail(KRY_ERR_ARGUMENT, "max_m must be >= 1");
+  if (od->n < 1 || od->n > ((int64_t)1 << 31) - 1)
+    return fail(KRY_ERR_DIMENSION, "operator order out of range");
+  KRY_CUDA(cudaSetDevice(device));
+  keep_pool_memory(device);
+  kry_ctx* c = new kry_ctx();
+  const int rc = ctx_create_body(c, device, od, s, max_m);
+  if (rc != KRY_OK) {
+    const std::string keep = g_last_error;
+    cudaGetLastError();
+    kry_ctx_destroy(c);
+    g_last_error = keep;
+    return rc;
+  }
   *out = c;
   return KRY_OK;
 }
@@ -1240,13 +1258,13 @@ int kry_ctx_create(kry_ctx** out, int device, const kry_operator_desc* od, int s
 void kry_ctx_destroy(kry_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->dev);
-  cudaStreamSynchronize(c->stream);
+  if (c->stream) cudaStreamSynchronize(c->stream);
   for (void* p : c->op_mem) dfree(p);
   dfree(c->win);
   dfree(c->C);
   dfree(c->st);
-  cudaFreeHost(c->st_h);
-  cudaFreeHost(c->hres);
+  if (c->st_h) cudaFreeHost(c->st_h);
+  if (c->hres) cudaFreeHost(c->hres);
   dfree(c->tmem);
   dfree(c->g.partials);
   dfree(c->g.ticket);
@@ -1267,16 +1285,16 @@ void kry_ctx_destroy(kry_ctx* c) {
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->halo_buf) dfree(c->halo_buf);
   if (c->t_ev[0]) { cudaEventDestroy(c->t_ev[0]); cudaEventDestroy(c->t_ev[1]); }
-  cudaStreamSynchronize(c->estream);
-  cudaEventDestroy(c->ev_t);
-  cudaEventDestroy(c->ev_res[0]);
-  cudaEventDestroy(c->ev_res[1]);
-  cudaStreamDestroy(c->estream);
+  if (c->estream) cudaStreamSynchronize(c->estream);
+  for (cudaEvent_t e : {c->ev_t, c->ev_res[0], c->ev_res[1]})
+    if (e) cudaEventDestroy(e);
+  for (auto& e : c->ev_pool) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  if (c->estream) cudaStreamDestroy(c->estream);
   for (int b = 0; b < 2; ++b) {
     if (c->p2buf[b]) dfree(c->p2buf[b]);
     if (c->p2qc[b]) dfree(c->p2qc[b]);
   }
-  cudaStreamDestroy(c->stream);
+  if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
 
@@ -1316,6 +1334,9 @@ int kry_apply(kry_ctx* c, const double* v, double* y, int ncols) {
 
 static int init_basis_common(kry_ctx* c, double* gamma, double* beta2) {
   c->m = 0;
+  c->m_final = 0;
+  c->coef_ready = false;
+  c->pending_launch = false;
   c->exhausted = false;
   c->initialized = false;
   c->eig.reset();
@@ -1444,6 +1465,31 @@ int kry_check_sylv(kry_ctx* a, kry_ctx* b, double rhs_norm, double* res, double*
   return check_sylv(a, b, rhs_norm, res, rel);
 }
 
+// timing events for `n` iterations (+1 start event on the Lanczos stream)
+static int ensure_timing_events(kry_ctx* c, int n) {
+  while ((int)c->ev_pool.size() < n) {
+    cudaEvent_t a, b;
+    KRY_CUDA(cudaEventCreate(&a));
+    KRY_CUDA(cudaEventCreate(&b));
+    c->ev_pool.push_back({a, b});
+  }
+  while ((int)c->ev_step.size() < n + 1) {
+    cudaEvent_t a;
+    KRY_CUDA(cudaEventCreate(&a));
+    c->ev_step.push_back(a);
+  }
+  return KRY_OK;
+}
+
+static double ev_seconds(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+    cudaGetLastError();
+    return 0.0;
+  }
+  return 1e-3 * ms;
+}
+
 int kry_solve_lyap_pass1(kry_ctx* c, double tol, int max_m, int check_period, double* history,
                          int* n_history, int* iterations, double* final_rel, int* reason) {
   KRY_CUDA(cudaSetDevice(c->dev));
@@ -1453,46 +1499,91 @@ int kry_solve_lyap_pass1(kry_ctx* c, double tol, int max_m, int check_period, do
   // Lanczos step j+1 runs on the main stream; its result is read one
   // iteration later (a converged solve therefore computes one extra,
   // discarded basis block).
-  double t_basis = 0.0, t_res = 0.0;
+  //
+  // Phase times (history columns 3-4, reference solvers.py:224-236) are
+  // device times from CUDA events: basis = Lanczos-stream time between the
+  // completions of consecutive steps, residual = eigen-stream time of the
+  // eigen-data append + check of each iteration (the reference's check time
+  // includes its partial eigendecomposition).  The two streams overlap, so
+  // their sum can exceed the wall time of the loop.
+  KRY_CHECK(ensure_timing_events(c, max_m + 2));
+  KRY_CUDA(cudaEventRecord(c->ev_step[0], c->stream));
+  std::vector<int> row_it;
   int nh = 0;
   *iterations = 0;
   *reason = 1;
   *n_history = 0;
   double rel = INFINITY;
   int pending = -1, pending_slot = 0;
+  int last_it = 0;   // iterations whose events were recorded
   auto record = [&](int it, double r) {
     double* row = history + (size_t)nh * 5;
-    row[0] = it; row[1] = (double)it * c->s; row[2] = r; row[3] = t_basis; row[4] = t_res;
+    row[0] = it; row[1] = (double)it * c->s; row[2] = r; row[3] = 0.0; row[4] = 0.0;
+    row_it.push_back(it);
     ++nh;
     *n_history = nh;
     *final_rel = r;
   };
+  // the check of iteration `pending` decides the solve when a later step fails
+  // (the reference never computes the steps past its converged iteration)
+  auto rescue = [&](int rc_step) -> int {
+    if (pending <= 0) return rc_step;
+    const std::string keep = g_last_error;
+    double res = 0.0, r2 = INFINITY;
+    if (collect_check(c, pending_slot, c->beta2, &res, &r2) != KRY_OK) {
+      g_last_error = keep;
+      return rc_step;
+    }
+    record(pending, r2);
+    rel = r2;
+    const int p = pending;
+    pending = -1;
+    if (r2 <= tol) {
+      *iterations = p;
+      *reason = 0;
+      c->m_final = p;
+      c->pending_launch = false;
+      reset_state_status(c);
+      return KRY_OK;
+    }
+    g_last_error = keep;
+    return rc_step;
+  };
   int rc = KRY_OK;
   bool done = false;
   for (int it = 1; it <= max_m && !done; ++it) {
-    double t0 = now_s();
     int ex = 0;
     rc = step_core(c, 1, &ex);
-    if (rc) break;
+    if (rc) {
+      rc = rescue(rc);
+      done = true;
+      break;
+    }
     // queue step it+1 before the host issues the eigen work of step it and
     // waits for the previous check (a converged solve thereby computes up to
     // two extra, discarded basis blocks)
     KRY_CUDA(cudaEventRecord(c->ev_t, c->stream));
+    KRY_CUDA(cudaEventRecord(c->ev_step[it], c->stream));
     if (!ex && it < max_m) {
       rc = step_prelaunch(c);
-      if (rc) break;
+      if (rc) {
+        rc = rescue(rc);
+        done = true;
+        break;
+      }
     }
-    t_basis += now_s() - t0;
     const bool chk = (it % check_period == 0) || ex;
     const int slot = it & 1;
+    KRY_CUDA(cudaStreamWaitEvent(c->estream, c->ev_t, 0));
+    KRY_CUDA(cudaEventRecord(c->ev_pool[it].first, c->estream));
     rc = launch_eigen_step(c, it, chk, ex != 0, slot, true);
     if (rc) break;
+    KRY_CUDA(cudaEventRecord(c->ev_pool[it].second, c->estream));
+    last_it = it;
     if (pending > 0) {   // result of the previous iteration's check
-      t0 = now_s();
       double res = 0.0;
       rc = collect_check(c, pending_slot, c->beta2, &res, &rel);
       if (rc) break;
-      t_res += now_s() - t0;
       record(pending, rel);
       if (rel <= tol) {
         *iterations = pending;
@@ -1508,11 +1599,9 @@ int kry_solve_lyap_pass1(kry_ctx* c, double tol, int max_m, int check_period, do
       pending_slot = slot;
     }
     if (ex) {   // invariant subspace: this check decides
-      t0 = now_s();
       double res = 0.0;
       rc = collect_check(c, slot, c->beta2, &res, &rel);
       if (rc) break;
-      t_res += now_s() - t0;
       record(it, rel);
       pending = -1;
       if (rel <= tol) {
@@ -1550,6 +1639,23 @@ int kry_solve_lyap_pass1(kry_ctx* c, double tol, int max_m, int check_period, do
     }
   }
   cudaStreamSynchronize(c->estream);
+  cudaStreamSynchronize(c->stream);
+  // cumulative device phase times at each history row
+  {
+    double tb = 0.0, tr = 0.0;
+    int q = 0, i = 1;
+    for (int r = 0; r < nh; ++r) {
+      const int upto = std::min(row_it[r], last_it);
+      for (; i <= upto; ++i) {
+        tb += ev_seconds(c->ev_step[i - 1], c->ev_step[i]);
+        tr += ev_seconds(c->ev_pool[i].first, c->ev_pool[i].second);
+      }
+      history[(size_t)r * 5 + 3] = tb;
+      history[(size_t)r * 5 + 4] = tr;
+      ++q;
+    }
+    (void)q;
+  }
   if (rc != KRY_OK) return rc;
   if (*reason == 0) return KRY_OK;
   return fail(KRY_ERR_CONVERGENCE, *reason == 2 ? "invariant" : "max_m");
@@ -2343,6 +2449,7 @@ int kry_ctri_sylv_blocks(int device, int s, int m1, const double* diag1, const d
   KRY_CHECK(B.eig.compute_uw(B.st, g2, tq2));
   KRY_CUDA(cudaStreamSynchronize(B.st));
   const int kA = A.eig.K, kB = B.eig.K;
+  KRY_CHECK(A.eig.ensure_cauchy(std::max(kA, kB), 0));
   KRY_CHECK(A.eig.cauchy(A.st, kB, B.eig.lam_cur(), B.eig.u, kA, A.eig.lam_cur(), A.eig.u,
                          A.eig.w, A.eig.res));
   KRY_CHECK(A.eig.cauchy(A.st, kA, A.eig.lam_cur(), A.eig.u, kB, B.eig.lam_cur(), B.eig.u,

@@ -661,88 +661,138 @@ __global__ void k_uw(const double* F, const double* L, int64_t km, int k, int s,
   }
 }
 
-// out_x = sum_y (a_x . b_y) / (lx_x + ly_y) c_y, res[0] = sum_x |out_x|^2,
-// res[1] = min |lx + ly|.  Stage 1 splits BOTH x and y over CTAs (grid
-// x-tiles x y-chunks; the first version split only x: 16 CTAs at k = 2056,
-// 119 us per check) and writes partial out_x per y-chunk; stage 2 sums the
-// chunks in a fixed order per x and reduces |out_x|^2 with a last-CTA tail.
-#define CC_CH 128
-template <int S>
-__global__ void __launch_bounds__(128) k_cauchy_part(int nx, const double* lx, const double* ax,
-                                                     int ny, const double* ly, const double* by,
-                                                     const double* cy, double* part, double* pmin) {
-  __shared__ double sl[CC_CH], sb[CC_CH][S], sc[CC_CH][S];
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y0 = blockIdx.y * CC_CH;
-  const bool active = x < nx;
-  double a[S], acc[S];
-  double lxx = 0.0;
-#pragma unroll
-  for (int q = 0; q < S; ++q) { a[q] = active ? ax[(int64_t)x * 8 + q] : 0.0; acc[q] = 0.0; }
-  if (active) lxx = lx[x];
-  const int yy = y0 + threadIdx.x;
-  if (yy < ny) {
-    sl[threadIdx.x] = ly[yy];
-#pragma unroll
-    for (int q = 0; q < S; ++q) {
-      sb[threadIdx.x][q] = by[(int64_t)yy * 8 + q];
-      sc[threadIdx.x][q] = cy[(int64_t)yy * 8 + q];
-    }
-  }
-  __syncthreads();
-  double mind = 1e300;
-  const int cnt = min(CC_CH, ny - y0);
-  if (active) {
-    for (int q = 0; q < cnt; ++q) {
-      double dot = 0.0;
-#pragma unroll
-      for (int r = 0; r < S; ++r) dot = fma(a[r], sb[q][r], dot);
-      const double den = lxx + sl[q];
-      mind = fmin(mind, fabs(den));
-      const double gq = dot / den;
-#pragma unroll
-      for (int r = 0; r < S; ++r) acc[r] = fma(gq, sc[q][r], acc[r]);
-    }
-    double* o = part + ((int64_t)blockIdx.y * nx + x) * 8;
-#pragma unroll
-    for (int r = 0; r < S; ++r) o[r] = acc[r];
-  }
-  // per-CTA min denominator
-  __shared__ double rm[4];
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mind = fmin(mind, __shfl_xor_sync(0xffffffffu, mind, o));
-  if ((threadIdx.x & 31) == 0) rm[threadIdx.x >> 5] = mind;
-  __syncthreads();
-  if (threadIdx.x == 0)
-    pmin[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = fmin(fmin(rm[0], rm[1]), fmin(rm[2], rm[3]));
+// out_x = sum_y (a_x . b_y) / (lx_x + ly_y) c_y ;  res[0] = sum_x |out_x|^2,
+// res[1] = min_{x,y} |lx_x + ly_y|  (reference residual.py:52-57, the guard of
+// kernels.py:31-45).
+//
+// One kernel, DMMA (mma.sync m8n8k4 f64) for both s-deep products, the k^2
+// reciprocals on the DFMA pipe in between -- the structure of attention:
+//   P  = A_x B_y^T            (8 x-rows x 8 y-cols, k = s: 1 or 2 DMMAs)
+//   P' = P / (lx_x + ly_y)     (elementwise, on the accumulator fragment)
+//   M += P' C_y               (k = the 8 y's: 2 DMMAs, N = s columns)
+// The accumulator of the first product is directly the A operand of the
+// second: lane (g, t) holds P[g][2t], P[g][2t+1], and the second product
+// takes its k-steps over the y parity (k-step h <-> y = 2t + h), so no lane
+// exchange is needed; the B operand of k-step h is C[y0 + 2t + h][g].
+// A CTA owns 16 x-rows (two 8-row fragments per warp, two independent DMMA
+// chains) and sweeps ALL y: its 16 warps take y-tiles in a fixed stride and
+// their partial M are summed through shared memory in warp order, so no
+// split-y partial pass exists and the result is deterministic.  The minimum
+// |lx + ly| is exact and cheap because ly is sorted ascending (eigenvalues):
+// per x only the two neighbours of -lx in ly can be closest.
+#define CC_XR 16     // x rows per CTA
+#define CC_NW 16     // warps per CTA
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
 template <int S>
-__global__ void __launch_bounds__(128) k_cauchy_sum(int nx, int nyc, int nmin, const double* part,
-                                                    const double* pmin, double* partials,
-                                                    unsigned* ticket, double* res) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  double ss = 0.0;
-  if (x < nx) {
-    double acc[S];
+__global__ void __launch_bounds__(32 * CC_NW) k_cauchy_mma(int nx, const double* __restrict__ lx,
+                                                           const double* __restrict__ ax, int ny,
+                                                           const double* __restrict__ ly,
+                                                           const double* __restrict__ by,
+                                                           const double* __restrict__ cy,
+                                                           double* part, unsigned* ticket,
+                                                           double* res) {
+  constexpr int KS = (S + 3) / 4;   // k-steps of the first product
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int x0 = blockIdx.x * CC_XR;
+  // A fragments of the two 8-row x tiles: A[g][t] = a[x0 + 8f + g][4 ks + t]
+  double fa[2][KS], flx[2];
+  bool vx[2];
 #pragma unroll
-    for (int r = 0; r < S; ++r) acc[r] = 0.0;
-    for (int c = 0; c < nyc; ++c) {
-      const double* o = part + ((int64_t)c * nx + x) * 8;
+  for (int f = 0; f < 2; ++f) {
+    const int x = x0 + 8 * f + g;
+    vx[f] = x < nx;
+    flx[f] = vx[f] ? lx[x] : 0.0;
 #pragma unroll
-      for (int r = 0; r < S; ++r) acc[r] += __ldcg(o + r);
+    for (int ks = 0; ks < KS; ++ks) {
+      const int col = 4 * ks + t;
+      fa[f][ks] = (vx[f] && col < S) ? ax[(int64_t)x * 8 + col] : 0.0;
+    }
+  }
+  double m[2][2] = {{0.0, 0.0}, {0.0, 0.0}};   // M[x0 + 8f + g][2t + j]
+  const int nyt = (ny + 7) >> 3;
+  for (int yt = warp; yt < nyt; yt += CC_NW) {
+    const int y0 = yt * 8;
+    // B operand of the first product: B[k = t][n = g] = b[y0 + g][4 ks + t]
+    double fb[KS];
+    {
+      const int y = y0 + g;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int col = 4 * ks + t;
+        fb[ks] = (y < ny && col < S) ? __ldg(by + (int64_t)y * 8 + col) : 0.0;
+      }
+    }
+    // B operand of the second product, k-step h: C[y0 + 2t + h][g]; and ly
+    double fc[2], fl[2];
+    bool vy[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int y = y0 + 2 * t + h;
+      vy[h] = y < ny;
+      fc[h] = (vy[h] && g < S) ? __ldg(cy + (int64_t)y * 8 + g) : 0.0;
+      fl[h] = vy[h] ? __ldg(ly + y) : 0.0;
     }
 #pragma unroll
-    for (int r = 0; r < S; ++r) ss = fma(acc[r], acc[r], ss);
+    for (int f = 0; f < 2; ++f) {
+      double p0 = 0.0, p1 = 0.0;   // P[g][2t], P[g][2t+1]
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) dmma884(p0, p1, fa[f][ks], fb[ks]);
+      const bool ok = vx[f];
+      p0 = (ok && vy[0]) ? p0 * frcp(flx[f] + fl[0]) : 0.0;
+      p1 = (ok && vy[1]) ? p1 * frcp(flx[f] + fl[1]) : 0.0;
+      dmma884(m[f][0], m[f][1], p0, fc[0]);
+      dmma884(m[f][0], m[f][1], p1, fc[1]);
+    }
   }
-  __shared__ double rs[128];
-  rs[threadIdx.x] = ss;
+  // fixed-order sum of the warps' partial M, then |M_x|^2 of the CTA
+  __shared__ double sm[CC_NW][CC_XR][8];
+  __shared__ double s_min[CC_XR];
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    sm[warp][8 * f + g][2 * t] = m[f][0];
+    sm[warp][8 * f + g][2 * t + 1] = m[f][1];
+  }
+  if (warp == 1 && lane < CC_XR) {
+    // exact min |lx + ly| of this row: the neighbours of -lx in sorted ly
+    const int x = x0 + lane;
+    double mn = 1e300;
+    if (x < nx && ny > 0) {
+      const double v = lx[x];
+      int lo = 0, hi = ny;   // first index with ly >= -v
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (ly[mid] < -v) lo = mid + 1; else hi = mid;
+      }
+      if (lo < ny) mn = fmin(mn, fabs(v + ly[lo]));
+      if (lo > 0) mn = fmin(mn, fabs(v + ly[lo - 1]));
+    }
+    s_min[lane] = mn;
+  }
   __syncthreads();
-  for (int o = 64; o > 0; o >>= 1) {
-    if (threadIdx.x < o) rs[threadIdx.x] += rs[threadIdx.x + o];
-    __syncthreads();
+  if (warp == 0) {
+    double ss = 0.0;
+    for (int e = lane; e < CC_XR * 8; e += 32) {
+      const int r = e >> 3, col = e & 7;
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < CC_NW; ++w) v += sm[w][r][col];
+      if (col < S) ss = fma(v, v, ss);
+    }
+    ss = warp_sum(ss);
+    double mn = lane < CC_XR ? s_min[lane] : 1e300;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if (lane == 0) {
+      part[2 * blockIdx.x] = ss;
+      part[2 * blockIdx.x + 1] = mn;
+    }
   }
-  if (threadIdx.x == 0) partials[blockIdx.x] = rs[0];
+  // last CTA: fixed-order reduction of the CTA partials
   __threadfence();
   __syncthreads();
   __shared__ unsigned s_last;
@@ -750,18 +800,17 @@ __global__ void __launch_bounds__(128) k_cauchy_sum(int nx, int nyc, int nmin, c
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // the last CTA: block-parallel sum of the CTA partials (fixed per-thread
-  // stride and tree order, so the value is reproducible) and min of the
-  // denominator mins (a single-thread sweep here cost ~10 us per check)
+  __shared__ double rs[32 * CC_NW], rm[32 * CC_NW];
   double tot = 0.0, mn = 1e300;
-  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) tot += __ldcg(partials + b);
-  for (int b = threadIdx.x; b < nmin; b += blockDim.x) mn = fmin(mn, __ldcg(pmin + b));
-  __shared__ double rm[128];
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+    tot += __ldcg(part + 2 * b);
+    mn = fmin(mn, __ldcg(part + 2 * b + 1));
+  }
   rs[threadIdx.x] = tot;
   rm[threadIdx.x] = mn;
   __syncthreads();
-  for (int o = 64; o > 0; o >>= 1) {
-    if (threadIdx.x < o) {
+  for (int o = blockDim.x >> 1; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
       rs[threadIdx.x] += rs[threadIdx.x + o];
       rm[threadIdx.x] = fmin(rm[threadIdx.x], rm[threadIdx.x + o]);
     }
@@ -797,9 +846,9 @@ int EigEngine::init(int s_, int kmax_, int device) {
   const size_t nch_max = (nk + E4_CH - 1) / E4_CH + 1;
   const size_t vpart_n = nch_max * (nk + 8) * 16;
   doubles += vpart_n;             // E4 partial sums
-  // Cauchy stage-1 partials: [y-chunk][x][8] for x, y up to 2 kmax, + mins
-  cpart_cap = ((2 * nk + CC_CH - 1) / CC_CH + 1) * (2 * nk);
-  doubles += cpart_cap * 8 + cpart_cap / 64 + 64;
+  // Cauchy per-CTA partials (sum, min) for x up to 2 kmax
+  cpart_cap = 2 * ((2 * nk + CC_XR - 1) / CC_XR) + 64;
+  doubles += cpart_cap;
   KRY_CHECK(dalloc(&dbuf, doubles));
   KRY_CUDA(cudaMemset(dbuf, 0, doubles * sizeof(double)));
   double* p = dbuf;
@@ -814,7 +863,7 @@ int EigEngine::init(int s_, int kmax_, int device) {
   partials = p; p += 4096;
   res = p; p += 16;
   vpart = p; p += vpart_n;
-  cpart = p; p += cpart_cap * 8 + cpart_cap / 64 + 64;
+  cpart = p; p += cpart_cap;
   size_t ints = 5 * nk + 8;
   KRY_CHECK(dalloc(&ibuf, ints));
   KRY_CUDA(cudaMemset(ibuf, 0, ints * sizeof(int)));
@@ -910,34 +959,30 @@ int EigEngine::append_block(cudaStream_t st, const double* dsym_blk, const doubl
 }
 
 int EigEngine::ensure_cauchy(int nx, int ny) {
-  const size_t nyc = (size_t)std::max(1, (ny + CC_CH - 1) / CC_CH);
-  if (nyc * (size_t)nx <= cpart_cap) return KRY_OK;
+  (void)ny;
+  const size_t need = 2 * (size_t)((nx + CC_XR - 1) / CC_XR) + 64;   // per-CTA (sum, min)
+  if (need <= cpart_cap) return KRY_OK;
   if (cpart_ext) dfree(cpart_ext);
   cpart_ext = nullptr;
-  const size_t cap = (nyc + 1) * (size_t)nx;
-  KRY_CHECK(dalloc(&cpart_ext, cap * 8 + cap / 64 + 64));
+  KRY_CHECK(dalloc(&cpart_ext, need));
   cpart = cpart_ext;
-  cpart_cap = cap;
+  cpart_cap = need;
   return KRY_OK;
 }
 
 int EigEngine::cauchy(cudaStream_t st, int nx, const double* lx, const double* ax, int ny,
                       const double* ly, const double* by, const double* cy, double* out2) {
-  const int gx = std::max(1, (nx + 127) / 128);
-  const int nyc = std::max(1, (ny + CC_CH - 1) / CC_CH);
-  if (gx > 4096 || (size_t)nyc * nx > cpart_cap) return fail(KRY_ERR_STATE, "residual grid too large");
-  double* pmin = cpart + cpart_cap * 8;
-  dim3 g1(gx, nyc);
-#define L(S)                                                                                    \
-  k_cauchy_part<S><<<g1, 128, 0, st>>>(nx, lx, ax, ny, ly, by, cy, cpart, pmin);               \
-  k_cauchy_sum<S><<<gx, 128, 0, st>>>(nx, nyc, gx * nyc, cpart, pmin, partials, ticket, out2)
+  const int gx = std::max(1, (nx + CC_XR - 1) / CC_XR);
+  if ((size_t)2 * gx > cpart_cap) return fail(KRY_ERR_STATE, "residual grid too large");
+#define L(S) \
+  k_cauchy_mma<S><<<gx, 32 * CC_NW, 0, st>>>(nx, lx, ax, ny, ly, by, cy, cpart, ticket, out2)
   switch (s) {
     case 1: L(1); break; case 2: L(2); break; case 3: L(3); break; case 4: L(4); break;
     case 5: L(5); break; case 6: L(6); break; case 7: L(7); break; case 8: L(8); break;
     default: return fail(KRY_ERR_ARGUMENT, "block width s must be 1..8");
   }
 #undef L
-  count_launch(2);
+  count_launch(1);
   KRY_CUDA(cudaGetLastError());
   return KRY_OK;
 }

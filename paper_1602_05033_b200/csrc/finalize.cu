@@ -184,11 +184,13 @@ int launch_truncate(cudaStream_t st, const double* ev, int k, int desc, double e
                     const double* mind_part, int nparts, double* work, double* out) {
   const size_t smb = (size_t)k * sizeof(double);
   if (smb <= (size_t)200 * 1024) {
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[64] = {false};   // the attribute is per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!attr[dev & 63]) {
       cudaFuncSetAttribute(k_truncate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            200 * 1024);
-      attr = true;
+      attr[dev & 63] = true;
     }
     k_truncate<true><<<1, 256, smb, st>>>(ev, k, desc, eps, mind_part, nparts, work, out);
   } else {

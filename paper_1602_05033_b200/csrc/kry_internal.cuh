@@ -19,6 +19,9 @@
 #define KRY_SMAX 8
 #define KRY_SS 64
 #define KRY_MAX_GRID (148 * 16)
+// grid-reduction counters: [0] top level, [1 + group] per group of 32 CTAs
+#define KRY_TICKET_STRIDE (2 + KRY_MAX_GRID / 32)
+#define KRY_TICKET_SITES 3
 
 namespace kry {
 
@@ -161,7 +164,7 @@ struct TStore {  // projected-matrix storage (device), slots of 64 doubles
 
 struct GramScratch {
   double* partials;   // [grid][24*8]
-  unsigned* ticket;   // one counter per reduction site
+  unsigned* ticket;   // KRY_TICKET_SITES disjoint blocks of KRY_TICKET_STRIDE counters
   int max_grid;
 };
 

@@ -1286,19 +1286,21 @@ int gram_grid_for(int64_t n) {
 template <class Kern>
 static int resident_grid(Kern kernel, int64_t n, int cap_per_sm = 0) {
   static std::mutex mu;
-  static std::unordered_map<const void*, int> cache;
+  static std::unordered_map<const void*, int> cache[64];   // per device
   int per_sm = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
   {
     std::lock_guard<std::mutex> lock(mu);
-    auto it = cache.find((const void*)kernel);
-    if (it == cache.end()) {
-      int dev = 0, sms = 148, nb = 1;
-      cudaGetDevice(&dev);
+    auto& cd = cache[dev & 63];
+    auto it = cd.find((const void*)kernel);
+    if (it == cd.end()) {
+      int sms = 148, nb = 1;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, TP, 0);
       if (cap_per_sm > 0) nb = std::min(nb, cap_per_sm);
       per_sm = std::max(1, nb) * sms;
-      cache[(const void*)kernel] = per_sm;
+      cd[(const void*)kernel] = per_sm;
     } else {
       per_sm = it->second;
     }
@@ -1352,7 +1354,7 @@ int launch_apply_gram(cudaStream_t st, int s, const OpDev& op, const ApplyGramCa
   const bool coop = (s % 2 == 0) && (op.kind == KRY_OP_STENCIL || !c.use_op) && (c.ldv % 2 == 0);
 #define LA(S, U, C)                                                                    \
   k_apply_gram<S, U, C><<<resident_grid(k_apply_gram<S, U, C>, c.n), TP, 0, st>>>( \
-      op, c, dst, T, g.partials, g.ticket + 1)
+      op, c, dst, T, g.partials, g.ticket + 1 * KRY_TICKET_STRIDE)
   if (c.use_op && coop) {
 #define L(S) LA(S, 1, true)
     KRY_DISPATCH_S(s, L);
@@ -1382,7 +1384,7 @@ int launch_pair_gram(cudaStream_t st, int s, const double* x, int64_t ldx, const
   (void)grid;
 #define L(S)                                                       \
   k_pair_gram<S><<<resident_grid(k_pair_gram<S>, n), TP, 0, st>>>( \
-      x, ldx, y, ldy, n, post, dst, T, g.partials, g.ticket + 2)
+      x, ldx, y, ldy, n, post, dst, T, g.partials, g.ticket + 2 * KRY_TICKET_STRIDE)
   KRY_DISPATCH_S(s, L);
 #undef L
   count_launch();

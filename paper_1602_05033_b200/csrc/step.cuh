@@ -341,7 +341,7 @@ int launch_apply_gl(cudaStream_t st, int s, const OpDev& op, const ApplyGramCall
   cc.post = POST_STEP8;
 #define L(S)                                                                      \
   k_apply_gl<S><<<resident_grid(k_apply_gl<S>, c.n), TP, 0, st>>>(op, cc, dst, T, \
-                                                                  g.partials, g.ticket + 1)
+                                                                  g.partials, g.ticket + 1 * KRY_TICKET_STRIDE)
   switch (s) {
     case 2: L(2); break;
     case 4: L(4); break;
@@ -450,14 +450,16 @@ bool step_supported(const OpDev& op, int s, int64_t ld) {
 template <class Kern>
 static int step_grid(Kern kernel, int nch) {
   static std::mutex mu;
-  static std::unordered_map<const void*, int> cache;
+  static std::unordered_map<const void*, int> cache_dev[64];   // per device
   int per = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
   {
     std::lock_guard<std::mutex> lock(mu);
+    auto& cache = cache_dev[dev & 63];
     auto it = cache.find((const void*)kernel);
     if (it == cache.end()) {
-      int dev = 0, sms = 148, nb = 1;
-      cudaGetDevice(&dev);
+      int sms = 148, nb = 1;
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, STEP_TP, 0);
       per = std::max(1, nb) * sms;
@@ -497,7 +499,10 @@ int launch_step(cudaStream_t st, int s, const OpDev& op, StepCall c, DevState* d
   c.fpl = STEP_TP / 32
 #define LT(S)                                                                            \
   {                                                                                      \
-    static bool attr = false;                                                            \
+    static bool attr_dev[64] = {false};   /* per device */                               \
+    int adev = 0;                                                                        \
+    cudaGetDevice(&adev);                                                                \
+    bool& attr = attr_dev[adev & 63];                                                    \
     smem = tma_smem_bytes(S);                                                            \
     if (!attr) {                                                                         \
       KRY_CUDA(cudaFuncSetAttribute(k_step_tma<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, \

@@ -497,7 +497,8 @@ int launch_apply_tma(cudaStream_t st, int s, const OpDev& op, const ApplyGramCal
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
 #define L(S)                                                                               \
   {                                                                                        \
-    static int per = 0;                                                                    \
+    static int per_dev[64] = {0};   /* attribute + occupancy are per device */             \
+    int& per = per_dev[dev & 63];                                                          \
     const size_t sm = apt_smem_bytes(S);                                                   \
     if (!per) {                                                                            \
       KRY_CUDA(cudaFuncSetAttribute(k_apply_tma<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -508,7 +509,7 @@ int launch_apply_tma(cudaStream_t st, int s, const OpDev& op, const ApplyGramCal
     }                                                                                      \
     const int64_t ntiles = (c.n + TMA_CH - 1) / TMA_CH;                                     \
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)per * sms)); \
-    k_apply_tma<S><<<grid, threads, sm, st>>>(op, cc, dst, T, g.partials, g.ticket + 1);   \
+    k_apply_tma<S><<<grid, threads, sm, st>>>(op, cc, dst, T, g.partials, g.ticket + 1 * KRY_TICKET_STRIDE);   \
   }
   switch (s) {
     case 2: L(2); break;

@@ -54,6 +54,20 @@ class LinearOperator:
         raise NotImplementedError("operator has no inverse-apply capability")
 
 
+def require_device(op):
+    """The device solvers need an operator that lives on the GPU
+    (SparseOperator / StencilOperator).  A host-only LinearOperator (the
+    reference's plug-in protocol, operators.py:65-79, whose ``apply`` is
+    Python code) cannot feed the device recurrence: it is rejected with a
+    typed error instead of failing later on a missing attribute."""
+    if not callable(getattr(op, "context", None)):
+        raise TypeError(
+            "%s is not a device operator: the B200 solvers need a SparseOperator "
+            "(or StencilOperator) whose products run on the GPU; wrap the matrix "
+            "with paper_1602_05033_b200.SparseOperator(a)" % type(op).__name__)
+    return op
+
+
 def _grid_from_offsets(n, pos):
     """(nx, nxy) such that the positive offsets are a subset of {1, nx, nxy}."""
     p = [int(v) for v in pos]

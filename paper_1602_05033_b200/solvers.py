@@ -23,6 +23,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
+from .operators import require_device as _require_device
 from .errors import (ConvergenceError, DimensionMismatchError, IndefiniteMatrixError,
                      KrymatError)
 
@@ -158,7 +159,7 @@ class _Pass1:
     """Runs init + pass 1 on one context; keeps the state for finalisation."""
 
     def __init__(self, op, c, opts, store=False):
-        self.op = op
+        self.op = _require_device(op)
         self.c = c
         self.s = c.shape[1]
         self.ctx = op.context(self.s, opts.max_m + 2)
@@ -193,6 +194,7 @@ def solve_lyapunov(op, c, options=None):
     """
     opts = options if options is not None else SolveOptions()
     _check_space(opts)
+    _require_device(op)
     c = _as_rhs(op, c)
     lib = _lib.load()
     tic = time.perf_counter()
@@ -254,6 +256,8 @@ def solve_sylvester_two_sided(op_a, op_b, c1, c2, options=None):
     c2 = np.atleast_2d(np.asarray(c2, dtype=float))
     if c1.shape[1] != c2.shape[1]:
         raise DimensionMismatchError("C1 and C2 must have the same number of columns")
+    _require_device(op_a)
+    _require_device(op_b)
     c1 = _as_rhs(op_a, c1)
     c2 = _as_rhs(op_b, c2)
     lib = _lib.load()
@@ -333,6 +337,7 @@ def solve_sylvester_one_sided(op_a, b, c1, c2, options=None):
         raise DimensionMismatchError("C1 and C2 must have the same number of columns")
     if c2.shape[0] != b.shape[0]:
         raise DimensionMismatchError("C2 does not conform with B")
+    _require_device(op_a)
     c1 = _as_rhs(op_a, c1)
     c2 = np.ascontiguousarray(c2)
     b = np.ascontiguousarray(b)
@@ -418,6 +423,7 @@ def solve_sylvester_one_sided(op_a, b, c1, c2, options=None):
 def true_lyapunov_residual(op, z, c):
     """||A Z Z^T + Z Z^T A + C C^T||_F from small Gram matrices, on the device
     (reference ``solvers.py:104-115``)."""
+    _require_device(op)
     z = np.ascontiguousarray(np.atleast_2d(np.asarray(z, dtype=float)))
     c = np.ascontiguousarray(np.atleast_2d(np.asarray(c, dtype=float)))
     ctx = op.context(c.shape[1], 1)

@@ -1,0 +1,317 @@
+"""Reference-derived goldens for the long configs.
+
+Test infrastructure only; runs in the build container (needs /root/reference,
+which never travels to the GPU box).  Three stages:
+
+1. ``lanczos <cfg> <variant> <out.npz>`` drives the REFERENCE's own
+   ``init_basis`` + ``lanczos_step`` (``krymat/basis.py:192-252``, with
+   ``on_zero_residual="finalize"`` as ``solve_lyapunov`` calls it,
+   ``solvers.py:224-227``) for ``steps`` iterations and stores every projected
+   block (symmetrised diagonal blocks, QR coupling blocks), gamma and the
+   normalisation.  ``variant`` = ``csr`` (the reference ``SparseOperator``) or
+   one of the reordered-summation operators below: the reference algorithm
+   against itself with only the SpMM summation order changed is the roundoff
+   floor of the parity protocol (§8(c) item 1).
+   For config 5 with variant ``csr`` the run continues with the fixed-depth
+   factor at m = 1500: the reference's finalisation (``solvers.py:254-264``,
+   ``truncated_spd_factor`` ``kernels.py:309-331``) and its own
+   ``two_pass_recover`` (``solvers.py:130-169``), recipe of
+   ``tests/test_acceptance.py:190-215``; the factor is stored as the seeded
+   sketch Z (Zᵀ Ω) on 4096 sampled rows (as the c4 golden).
+2. ``residuals <out_dir> <blocks.npz> ...`` (run where a GPU is available; CPU works
+   but takes hours at k = 6000) evaluates the paper's residual formula at
+   EVERY m from the stored reference blocks with a dense symmetric
+   eigensolver in fp64 instead of the reference's band reduction +
+   tridiagonal solver (``residual.py:40-84``).  The surrogate is the same
+   formula on an independent eigensolver; stage 3 pins it.
+3. ``crosscheck <blocks.npz> <m,...>`` runs the reference's own
+   ``ctri_lyapunov`` / ``ctri_sylvester`` on the stored blocks at sampled m
+   and stores the values, so the test can pin the surrogate history to the
+   reference's residual function.
+
+    OPENBLAS_NUM_THREADS=1 python tests/golden/make_golden_blocks.py \
+        lanczos c5 csr tests/golden/c5_blocks.npz          # ~3 h (pass 2 incl.)
+    ... lanczos c5 upd tests/golden/c5_blocks_upd.npz      # ~50 min
+"""
+
+import os
+import sys
+import time
+
+sys.dont_write_bytecode = True
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import scipy.sparse as sp  # noqa: E402
+
+
+def _ref():
+    sys.path.insert(0, "/root/reference/pkg/src")
+    import krymat  # noqa: F401
+    return krymat
+
+
+class Reordered:
+    """A CSR operator with an exact-arithmetic-equal, different summation
+    order.  ``upd``: (U v + D v) + L v; ``ldu``: L v + (D v + U v);
+    ``dlu``: D v + (L v + U v); ``lud``: (L v + U v) + D v; ``rev``: the CSR
+    row sums in reversed column order.  Satisfies the reference
+    LinearOperator protocol (``n``, ``definite``, ``apply``;
+    operators.py:65-79)."""
+
+    definite = True
+
+    def __init__(self, a, order):
+        a = sp.csr_matrix(a)
+        self.n = a.shape[0]
+        self.lo = sp.tril(a, -1).tocsr()
+        self.up = sp.triu(a, 1).tocsr()
+        self.d = a.diagonal().copy()
+        self.order = order
+        if order == "rev":   # columns of every row stored in descending order
+            coo = a.tocoo()
+            key = np.lexsort((-coo.col, coo.row))
+            self.rev = sp.csr_matrix((coo.data[key], coo.col[key], a.indptr.copy()),
+                                     shape=a.shape)
+
+    def can_solve(self):
+        return False
+
+    def apply(self, v):
+        dv = self.d[:, None] * v
+        if self.order == "upd":
+            return (self.up @ v + dv) + self.lo @ v
+        if self.order == "ldu":
+            return self.lo @ v + (dv + self.up @ v)
+        if self.order == "dlu":
+            return dv + (self.lo @ v + self.up @ v)
+        if self.order == "lud":
+            return (self.lo @ v + self.up @ v) + dv
+        if self.order == "rev":
+            return self.rev @ v
+        raise ValueError(self.order)
+
+
+def _operators(cfg_name, variant):
+    krymat = _ref()
+    from tests.golden.make_golden import ref_laplacian3d, ref_varcoef2d
+    import krymat.problems as kp
+    if cfg_name == "c5":
+        mats = [kp.gen_fd2d("laplacian2d", 2000)]
+    elif cfg_name == "c3":
+        mats = [ref_varcoef2d(300), ref_laplacian3d(40)]
+    elif cfg_name == "c4":
+        mats = [ref_laplacian3d(200)]
+    else:
+        raise ValueError(cfg_name)
+    if variant == "csr":
+        return [krymat.SparseOperator(a) for a in mats]
+    return [Reordered(a, variant) for a in mats]
+
+
+def _blocks(state):
+    s = state.ell
+    m = state.n_t_blocks
+    diag = np.array([0.5 * (d + d.T) for d in state.diag_raw[:m]])
+    sub = np.array(state.sub[:m]) if m else np.zeros((0, s, s))
+    return diag, sub
+
+
+def lanczos(cfg_name, variant, out_path, steps=None):
+    krymat = _ref()
+    from krymat.basis import init_basis, lanczos_step
+    from oracle import problems as P
+    cfg = P.build_config(cfg_name, with_matrix=False)
+    ops = _operators(cfg_name, variant)
+    steps = steps or {"c5": 1500, "c3": 700, "c4": 300}[cfg_name]
+    rhs = [cfg["c"]] if cfg_name != "c3" else [cfg["c1"], cfg["c2"]]
+    states, windows = [], []
+    tic = time.perf_counter()
+    for op, c in zip(ops, rhs):
+        w, st = init_basis(op, c, storage="windowed")
+        windows.append(w)
+        states.append(st)
+    step_secs = []
+    for it in range(1, steps + 1):
+        t0 = time.perf_counter()
+        for op, w, st in zip(ops, windows, states):
+            if not st.exhausted:
+                lanczos_step(op, w, st, on_zero_residual="finalize")
+        step_secs.append(time.perf_counter() - t0)
+        if it % 50 == 0:
+            print("%s/%s: step %d  %.2f s/step" % (cfg_name, variant, it,
+                                                   np.mean(step_secs[-50:])),
+                  flush=True)
+    out = {"steps": np.int64(steps), "step_seconds": np.array(step_secs),
+           "wall_seconds": np.float64(time.perf_counter() - tic),
+           "variant": np.array(variant), "tol": np.float64(cfg["tol"])}
+    sides = ("a",) if cfg_name != "c3" else ("a", "b")
+    for side, st in zip(sides, states):
+        out["diag_" + side], out["sub_" + side] = _blocks(st)
+        out["gamma_" + side] = np.asarray(st.gamma)
+    if cfg_name == "c3":
+        out["rhs_norm"] = np.float64(np.linalg.norm(cfg["c1"]) *
+                                     np.linalg.norm(cfg["c2"]))
+    else:
+        out["beta2"] = np.float64(np.linalg.norm(cfg["c"]) ** 2)
+    np.savez_compressed(out_path, **out)
+    print("wrote", out_path, flush=True)
+    if cfg_name == "c5" and variant == "csr":
+        _fixed_depth_factor(ops[0], windows[0], states[0], out, out_path)
+
+
+def _fixed_depth_factor(op, window, state, out, out_path):
+    """Reference finalisation + two-pass recovery at the final depth."""
+    from krymat.kernels import guarded_denominators, truncated_spd_factor
+    from krymat.solvers import two_pass_recover
+    from oracle import problems as P
+    from threadpoolctl import threadpool_limits
+    tic = time.perf_counter()
+    t_dense = state.projected_matrix().to_dense()
+    lam, q = np.linalg.eigh(t_dense)
+    denom = guarded_denominators(lam, lam)
+    u = q[: state.gamma.shape[0], :].T @ state.gamma
+    ytilde = -(u @ u.T) / denom
+    ytilde = 0.5 * (ytilde + ytilde.T)
+    fac = truncated_spd_factor(ytilde)
+    qy = q @ fac.factor
+    print("c5 fixed depth: rank %d discarded %.3e" % (fac.rank,
+                                                       fac.discarded_mass),
+          flush=True)
+    with threadpool_limits(2):
+        z = two_pass_recover(op, state, qy, window)
+    n = z.shape[0]
+    omega = P.sketch_omega(n, 2)
+    sk = z @ (z.T @ omega)
+    rows = np.sort(np.random.default_rng(7).choice(n, 4096, replace=False))
+    out["rank"] = np.int64(fac.rank)
+    out["discarded"] = np.float64(fac.discarded_mass)
+    out["sketch_rows"] = rows
+    out["sketch"] = sk[rows]
+    out["x_norm_fro"] = np.float64(np.linalg.norm(z.T @ z))
+    out["factor_seconds"] = np.float64(time.perf_counter() - tic)
+    np.savez_compressed(out_path, **out)
+    print("wrote factor", out_path, flush=True)
+
+
+# ---------------------------------------------------------------- stage 2
+
+def _eigh(t_dense):
+    try:
+        import torch
+        if torch.cuda.is_available():
+            lam, q = torch.linalg.eigh(torch.from_numpy(t_dense).cuda())
+            return lam.cpu().numpy(), q.cpu().numpy()
+    except ImportError:
+        pass
+    return np.linalg.eigh(t_dense)
+
+
+def _dense(diag, sub, m):
+    s = diag.shape[1]
+    k = m * s
+    t = np.zeros((k, k))
+    for i in range(m):
+        t[i * s:(i + 1) * s, i * s:(i + 1) * s] = diag[i]
+        if i + 1 < m:
+            t[(i + 1) * s:(i + 2) * s, i * s:(i + 1) * s] = sub[i]
+            t[i * s:(i + 1) * s, (i + 1) * s:(i + 2) * s] = sub[i].T
+    return t
+
+
+def _partial(diag, sub, m):
+    s = diag.shape[1]
+    lam, q = _eigh(_dense(diag, sub, m))
+    return lam, q[:s], q[-s:]
+
+
+def lyap_residual(diag, sub, gamma, beta2, m):
+    """residual.py:40-59 on a dense eigendecomposition of T_m."""
+    lam, first, last = _partial(diag, sub, m)
+    denom = lam[:, None] + lam[None, :]
+    u = first.T @ gamma
+    w = last.T @ sub[m - 1].T
+    mm = ((u @ u.T) / denom) @ w
+    res = float(np.sqrt(2.0) * np.linalg.norm(mm))
+    return res / beta2
+
+
+def sylv_residual(d, m):
+    """residual.py:62-84 on dense eigendecompositions of T_m and J_m."""
+    lam, fa, la = _partial(d["diag_a"], d["sub_a"], m)
+    ups, fb, lb = _partial(d["diag_b"], d["sub_b"], m)
+    denom = lam[:, None] + ups[None, :]
+    u = fa.T @ d["gamma_a"]
+    v = fb.T @ d["gamma_b"]
+    f = la.T @ d["sub_a"][m - 1].T
+    g = lb.T @ d["sub_b"][m - 1].T
+    sd = (u @ v.T) / denom
+    res = float(np.sqrt(np.linalg.norm(sd.T @ f) ** 2 +
+                        np.linalg.norm(sd @ g) ** 2))
+    return res / float(d["rhs_norm"])
+
+
+def residuals(out_dir, paths):
+    os.makedirs(out_dir, exist_ok=True)
+    for path in paths:
+        d = dict(np.load(path))
+        steps = int(d["steps"])
+        hist = np.zeros(steps)
+        tic = time.perf_counter()
+        for m in range(1, steps + 1):
+            if "diag_b" in d:
+                hist[m - 1] = sylv_residual(d, m)
+            else:
+                hist[m - 1] = lyap_residual(d["diag_a"], d["sub_a"],
+                                            d["gamma_a"], float(d["beta2"]), m)
+            if m % 100 == 0:
+                print(path, m, hist[m - 1], time.perf_counter() - tic,
+                      flush=True)
+        out = os.path.join(out_dir, os.path.basename(path)[:-4] + "_hist.npz")
+        np.savez_compressed(out, surrogate_history=hist)
+        print("wrote surrogate history", out, flush=True)
+
+
+# ---------------------------------------------------------------- stage 3
+
+def crosscheck(path, ms):
+    krymat = _ref()
+    from krymat.kernels import BlockTridiagonal
+    from krymat.residual import ctri_lyapunov, ctri_sylvester
+    d = dict(np.load(path))
+    vals = []
+    for m in ms:
+        tic = time.perf_counter()
+        ta = BlockTridiagonal(d["diag_a"].shape[1], list(d["diag_a"][:m]),
+                              list(d["sub_a"][:m - 1]))
+        if "diag_b" in d:
+            tb = BlockTridiagonal(d["diag_b"].shape[1], list(d["diag_b"][:m]),
+                                  list(d["sub_b"][:m - 1]))
+            rv = ctri_sylvester(ta, tb, d["gamma_a"], d["gamma_b"],
+                                d["sub_a"][m - 1], d["sub_b"][m - 1],
+                                rhs_norm=float(d["rhs_norm"]))
+        else:
+            rv = ctri_lyapunov(ta, d["gamma_a"], d["sub_a"][m - 1],
+                               rhs_norm=float(d["beta2"]))
+        vals.append(rv.relative)
+        print("crosscheck m=%d rel=%.16e (%.1f s)"
+              % (m, rv.relative, time.perf_counter() - tic), flush=True)
+    out = path[:-4] + "_xc.npz"
+    np.savez_compressed(out, crosscheck_m=np.array(ms, dtype=np.int64),
+                        crosscheck_rel=np.array(vals))
+    print("wrote crosscheck", out, flush=True)
+
+
+if __name__ == "__main__":
+    mode = sys.argv[1]
+    if mode == "lanczos":
+        steps = int(sys.argv[5]) if len(sys.argv) > 5 else None
+        lanczos(sys.argv[2], sys.argv[3], sys.argv[4], steps)
+    elif mode == "residuals":
+        residuals(sys.argv[2], sys.argv[3:])
+    elif mode == "crosscheck":
+        crosscheck(sys.argv[2], [int(x) for x in sys.argv[3].split(",")])
+    else:
+        raise SystemExit(__doc__)
