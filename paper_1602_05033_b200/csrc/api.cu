@@ -58,6 +58,12 @@ __global__ void k_init_gamma(DevState* st) {
       g[r * 8 + c] = v;
     }
   for (int q = 0; q < 64; ++q) st->gamma[q] = g[q];
+  // rank test of the initial QR on its final R factor (kernels.py:151-160)
+  double fro = 0.0, mn = 1e300;
+  for (int q = 0; q < 64; ++q) fro += g[q] * g[q];
+  fro = sqrt(fro);
+  for (int k = 0; k < s; ++k) mn = fmin(mn, fabs(g[k * 8 + k]));
+  if ((fro == 0.0 || mn < 1e-12 * fro) && st->status == KRY_OK) st->status = KRY_ERR_DEFLATION;
 }
 
 // orthonormal copy of a stored block: out = v * S, S = given 8x8 or
@@ -259,6 +265,7 @@ struct kry_ctx {
   // pass-1 window (3 slots)
   double* win = nullptr;
   double* slot[3] = {nullptr, nullptr, nullptr};
+  int64_t slot_pts = 0, slot_lo = 0;   // points per ring slot (with halos), lower halo
   int64_t ld = 0;
   int i_old = -1, i_cur = 0, i_new = 1;
   double* C = nullptr;
@@ -461,6 +468,9 @@ int reset_state(kry_ctx* c, int replay) {
   KRY_CUDA(cudaMemcpyAsync(&c->st->s, &tmp.s, sizeof(int), cudaMemcpyHostToDevice, c->stream));
   KRY_CUDA(cudaMemcpyAsync(&c->st->replay, &tmp.replay, sizeof(int), cudaMemcpyHostToDevice,
                            c->stream));
+  tmp.nrows = (double)c->n * c->nranks;
+  KRY_CUDA(cudaMemcpyAsync(&c->st->nrows, &tmp.nrows, sizeof(double), cudaMemcpyHostToDevice,
+                           c->stream));
   KRY_CUDA(cudaStreamSynchronize(c->stream));
   return KRY_OK;
 }
@@ -482,6 +492,13 @@ int do_init(kry_ctx* c, double* dst, int64_t ldd, int replay) {
   KRY_CHECK(map_status(c, "initial QR of C"));
   CombineCall cc{nullptr, 0, c->C, (int64_t)c->s, dst, ldd, c->n, 0, 0, 1, 1};
   KRY_CHECK(run_combine(c, cc, nullptr, nullptr));
+  if (c->st_h->flags & KRY_FLAG_SHIFTED) {
+    // ill-conditioned C (shifted CholQR3): explicit middle stage on V1,
+    // then V1^T V1 again for the lazy third stage (k_init_gamma)
+    KRY_CHECK(run_pair_gram(c, dst, ldd, dst, ldd, POST_CHOL_MID));
+    KRY_CHECK(launch_update(c->stream, c->s, dst, ldd, nullptr, 0, c->st->M, c->n, 0));
+    KRY_CHECK(run_pair_gram(c, dst, ldd, dst, ldd, POST_GCC));
+  }
   KRY_CHECK(halo_exchange(c, dst, ldd, c->s));
   k_init_gamma<<<1, 32, 0, c->stream>>>(c->st);
   count_launch();
@@ -524,6 +541,13 @@ int explicit_step(kry_ctx* c, int j, const double* vold, const double* vcur, dou
   }
   KRY_CHECK(run_pair_gram(c, vnew, ld, vnew, ld, POST_CHOL1));
   KRY_CHECK(launch_update(st, s, vnew, ld, nullptr, 0, c->st->M, c->n, 0));
+  KRY_CHECK(sync_status(c));
+  KRY_CHECK(map_status(c, ("Lanczos step " + std::to_string(j)).c_str()));
+  if (c->st_h->flags & KRY_FLAG_SHIFTED) {
+    // ill-conditioned residual block: shifted CholQR3 middle stage
+    KRY_CHECK(run_pair_gram(c, vnew, ld, vnew, ld, POST_CHOL_MID));
+    KRY_CHECK(launch_update(st, s, vnew, ld, nullptr, 0, c->st->M, c->n, 0));
+  }
   KRY_CHECK(run_pair_gram(c, vnew, ld, vnew, ld, POST_CHOL2));
   KRY_CHECK(launch_update(st, s, vnew, ld, nullptr, 0, c->st->M, c->n, 0));
   KRY_CHECK(sync_status(c));
@@ -578,8 +602,8 @@ double* store_slot(kry_ctx* c, int blk, int64_t* ld2) {
     }
     c->store_chunks.push_back(p);
   }
-  *ld2 = (int64_t)G * c->s;
-  return c->store_chunks[q] + (int64_t)((blk - 1) % G) * c->s;
+  *ld2 = c->s;   // block layout: block b of a chunk at b * n * s, point-major
+  return c->store_chunks[q] + (int64_t)((blk - 1) % G) * c->n * c->s;
 }
 
 // the fused single-pass kernel applies (stencil operator, one GPU, s != 5, 7)
@@ -977,18 +1001,35 @@ int final_eig(kry_ctx* c, FinalBufs& b, int* k_out) {
   return KRY_OK;
 }
 
+// rows of a column-major k x r factor into a row-major k x ldq panel (zero
+// padded): the B operand layout of the DMMA accumulation kernel
+__global__ void k_cols_to_rows(const double* f, int k, int r, int ldq, double* out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)k * ldq;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % ldq), i = (int)(e / ldq);
+    out[e] = c < r ? f[(int64_t)c * k + i] : 0.0;
+  }
+}
+
 int set_qy(kry_ctx* c, const double* Q, int k, const double* factor, int rank) {
   if (c->qy) dfree(c->qy);
   c->qy = nullptr;
   c->rank = rank;
   if (rank <= 0) return KRY_OK;
   KRY_CHECK(dalloc(&c->qy, (size_t)k * rank));
-  // qy (row-major k x rank) = col-major (rank x k) = factor^T Q^T
-  const double one = 1.0, zero = 0.0;
-  if (cublasDgemm(c->cublas, CUBLAS_OP_T, CUBLAS_OP_T, rank, k, k, &one, factor, k, Q, k, &zero,
-                  c->qy, rank) != CUBLAS_STATUS_SUCCESS)
-    return fail(KRY_ERR_CUDA, "cublasDgemm (qy) failed");
-  return KRY_OK;
+  // qy (row-major k x rank) = Q factor with Q column-major: column l of Q is
+  // one "block" of width 1 (k points), so the same DMMA accumulation kernel
+  // as pass 2 computes it (no library GEMM on the solve path)
+  const int ldq = zacc_ldq(rank);
+  double* fr = nullptr;
+  KRY_CHECK(dalloc(&fr, (size_t)k * ldq));
+  const int64_t tot = (int64_t)k * ldq;
+  k_cols_to_rows<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, c->stream>>>(
+      factor, k, rank, ldq, fr);
+  count_launch();
+  int rc = launch_zacc(c->stream, 1, Q, k, k, fr, ldq, rank, c->qy, k, 0);
+  dfree(fr);
+  return rc;
 }
 
 }  // namespace
@@ -1117,8 +1158,21 @@ static int ctx_create_body(kry_ctx* c, int device, const kry_operator_desc* od, 
   c->dev = device;
   c->s = s;
   c->max_m = max_m;
-  KRY_CUDA(cudaStreamCreate(&c->stream));
-  KRY_CUDA(cudaStreamCreate(&c->estream));
+  // The Lanczos stream (the recurrence: a chain of one-wave kernels) gets
+  // the highest priority, the second stream (eigen appends and checks in
+  // pass 1, the DMMA factor accumulation in pass 2) the lowest: when both
+  // have work queued, the block scheduler hands SMs freed by the long
+  // second-stream grids to the recurrence first, so the memory-bound
+  // recurrence and the fp64-bound accumulation share the SMs instead of
+  // running back to back.  (KRY_STREAM_PRIO=0 disables.)
+  {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    const char* e = getenv("KRY_STREAM_PRIO");
+    if (e && e[0] == '0') least = greatest = 0;
+    KRY_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamDefault, greatest));
+    KRY_CUDA(cudaStreamCreateWithPriority(&c->estream, cudaStreamDefault, least));
+  }
   KRY_CUDA(cudaEventCreateWithFlags(&c->ev_t, cudaEventDisableTiming));
   KRY_CUDA(cudaEventCreateWithFlags(&c->ev_res[0], cudaEventDisableTiming));
   KRY_CUDA(cudaEventCreateWithFlags(&c->ev_res[1], cudaEventDisableTiming));
@@ -1185,6 +1239,8 @@ static int ctx_create_body(kry_ctx* c, int device, const kry_operator_desc* od, 
   const int64_t halo = (od->kind == KRY_OP_STENCIL) ? op.nxy : 0;
   const int64_t halo_hi = (od->kind == KRY_OP_STENCIL) ? op.nxy + 256 : 0;
   const int64_t slot_pts = nloc + halo + halo_hi;
+  c->slot_pts = slot_pts;
+  c->slot_lo = halo;
   KRY_CHECK(dalloc(&c->win, (size_t)3 * slot_pts * s));
   KRY_CUDA(cudaMemset(c->win, 0, (size_t)3 * slot_pts * s * sizeof(double)));
   for (int q = 0; q < 3; ++q) c->slot[q] = c->win + (int64_t)q * slot_pts * s + halo * s;
@@ -2086,9 +2142,9 @@ int kry_set_storage(kry_ctx* c, int stored) {
 int kry_recover(kry_ctx* c, double* zhost) {
   KRY_CUDA(cudaSetDevice(c->dev));
   if (c->rank < 0) return fail(KRY_ERR_STATE, "finalize has not been called");
-  KRY_CHECK(ensure_handles(c));
   const int s = c->s, m = c->m_final, r = c->rank;
   const int64_t n = c->n;
+  if (m < 1 || m > c->m) return fail(KRY_ERR_STATE, "factor depth exceeds the generated basis");
   if (c->Z && c->z_cap < n * std::max(r, 1)) { dfree(c->Z); c->Z = nullptr; }
   if (!c->Z) {
     if (dalloc(&c->Z, (size_t)n * std::max(r, 1)) != KRY_OK) {
@@ -2102,22 +2158,21 @@ int kry_recover(kry_ctx* c, double* zhost) {
     c->z_cap = n * std::max(r, 1);
   }
   if (r == 0) return KRY_OK;
+  const int ldq = zacc_ldq(r);
   if (c->store_ok && (int64_t)c->store_chunks.size() * c->store_G >= m) {
-    // storage="stored": Z = sum_j V_j S_j qy_j over the stored chunks, one
-    // DGEMM per chunk (reference _assemble_stored, solvers.py:125-127)
+    // storage="stored": Z = sum_j V_j S_j qy_j over the stored chunks of
+    // blocks, one DMMA accumulation per chunk (reference _assemble_stored,
+    // solvers.py:125-127)
     const int G = c->store_G;
     double* Qc = nullptr;
-    KRY_CHECK(dalloc(&Qc, (size_t)G * s * r));
-    cublasSetStream(c->cublas, c->stream);
+    KRY_CHECK(dalloc(&Qc, (size_t)G * s * ldq));
     int rc = KRY_OK;
     for (int q = 0; rc == KRY_OK && q * G < m; ++q) {
       const int blk0 = q * G, nblk = std::min(G, m - blk0);
-      rc = launch_chunk_coef(c->stream, c->T.S, c->qy, s, r, blk0, nblk, Qc);
-      const double one = 1.0, beta = q == 0 ? 0.0 : 1.0;
-      if (rc == KRY_OK &&
-          cublasDgemm(c->cublas, CUBLAS_OP_N, CUBLAS_OP_N, r, (int)n, nblk * s, &one, Qc, r,
-                      c->store_chunks[q], G * s, &beta, c->Z, r) != CUBLAS_STATUS_SUCCESS)
-        rc = fail(KRY_ERR_CUDA, "cublasDgemm (stored Z) failed");
+      rc = launch_chunk_coef_ld(c->stream, c->T.S, c->qy, s, r, blk0, nblk, ldq, Qc);
+      if (rc == KRY_OK)
+        rc = launch_zacc(c->stream, s, c->store_chunks[q], n * s, nblk, Qc, ldq, r, c->Z, n,
+                         q > 0);
     }
     if (rc == KRY_OK) rc = zhost ? copy_out(c, zhost, c->Z, (size_t)n * r * sizeof(double))
                                  : (cudaStreamSynchronize(c->stream) == cudaSuccess ? KRY_OK
@@ -2129,30 +2184,25 @@ int kry_recover(kry_ctx* c, double* zhost) {
   if (zhost) pf.begin(zhost, (size_t)n * r * sizeof(double));
   size_t fr = 0, tot = 0;
   cudaMemGetInfo(&fr, &tot);
-  // Pass 2 regenerates V_j in the contiguous three-block ring (the same
-  // layout and kernels as pass 1) and the combine kernel writes each new block
-  // a second time into a point-interleaved chunk buffer [point][block][s] of G
-  // blocks, which one DGEMM per chunk folds into Z on the second stream while
-  // the next chunk is regenerated into the other buffer.  (The recurrence
-  // itself used to run on the interleaved layout: 64-byte rows at a
-  // G*s*8-byte stride made its kernels 25-45% slower than in pass 1.)
-  const size_t blk_bytes = (size_t)n * s * sizeof(double);
-  // two buffers within half of the free memory (+ what is cached); a chunk
-  // of G blocks is one DGEMM with K = G*s, and Z is read and written once
-  // per chunk (G = 64 at c4: 4 DGEMMs of K = 512 instead of 8 of K = 256)
+  // Pass 2 regenerates V_1..V_m with the pass-1 kernels directly into chunk
+  // buffers of G block slots (the ring layout of pass 1: each block point-
+  // major with its zero halo planes, written ONCE); when the coefficient
+  // solve of a chunk's last block has produced its lazy CholQR2 correction,
+  // the chunk is folded into Z by the DMMA accumulation kernel (zacc.cu) on
+  // the second stream while the next chunk is regenerated into the other
+  // buffer.  A buffer is rewritten only after its accumulation finished.
+  const int64_t slot_d = c->slot_pts * s;            // doubles per block slot
+  const int64_t lo_d = c->slot_lo * s;               // lower halo before the interior
+  const size_t slot_bytes = (size_t)slot_d * sizeof(double);
   int64_t gmax = 64;
   if (const char* e = getenv("KRY_PASS2_CHUNK")) gmax = std::max(1, atoi(e));
-  int64_t G = (int64_t)((fr / 2 + c->p2buf_cap * sizeof(double)) / blk_bytes) / 2;
+  int64_t G = (int64_t)((fr / 2 + c->p2buf_cap * sizeof(double)) / slot_bytes) / 2;
   if (G > gmax) G = gmax;
   if (G > m) G = m;
   if (G < 1) G = 1;
   const int nbuf = (m > G) ? 2 : 1;
-  const int64_t ld2 = G * s;
-  double* buf[2] = {nullptr, nullptr};
-  double* Qc[2] = {nullptr, nullptr};
-  cudaEvent_t ev_full[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+  const size_t need_buf = (size_t)G * slot_d, need_qc = (size_t)G * s * ldq;
   int rc = KRY_OK;
-  const size_t need_buf = (size_t)n * ld2, need_qc = (size_t)G * s * r;
   if (c->p2buf_cap < need_buf || c->p2qc_cap < need_qc) {
     for (int b = 0; b < 2; ++b) {
       if (c->p2buf[b]) dfree(c->p2buf[b]);
@@ -2162,8 +2212,17 @@ int kry_recover(kry_ctx* c, double* zhost) {
     c->p2buf_cap = need_buf;
     c->p2qc_cap = need_qc;
   }
+  double* buf[2] = {nullptr, nullptr};
+  double* Qc[2] = {nullptr, nullptr};
+  cudaEvent_t ev_full[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
   for (int b = 0; b < nbuf && rc == KRY_OK; ++b) {
-    if (!c->p2buf[b]) rc = dalloc(&c->p2buf[b], c->p2buf_cap);
+    if (!c->p2buf[b]) {
+      rc = dalloc(&c->p2buf[b], c->p2buf_cap);
+      // zero halo planes of every slot (the interiors are always rewritten)
+      if (rc == KRY_OK &&
+          cudaMemsetAsync(c->p2buf[b], 0, c->p2buf_cap * sizeof(double), c->stream) != cudaSuccess)
+        rc = fail(KRY_ERR_CUDA, "pass-2 buffer clear failed");
+    }
     if (rc == KRY_OK && !c->p2qc[b]) rc = dalloc(&c->p2qc[b], c->p2qc_cap);
     buf[b] = c->p2buf[b];
     Qc[b] = c->p2qc[b];
@@ -2173,49 +2232,41 @@ int kry_recover(kry_ctx* c, double* zhost) {
   auto cleanup = [&]() {
     cudaStreamSynchronize(c->estream);
     cudaStreamSynchronize(c->stream);
-    cublasSetStream(c->cublas, c->stream);
     for (int b = 0; b < 2; ++b) {
       if (ev_full[b]) cudaEventDestroy(ev_full[b]);
       if (ev_free[b]) cudaEventDestroy(ev_free[b]);
     }
   };
   if (rc != KRY_OK) { cleanup(); return rc; }
-  int cb = 0;   // current chunk buffer
-  auto sp = [&](int b, int64_t q) { return buf[b] + q * s; };
-  auto ring = [&](int j) { return c->slot[(j - 1) % 3]; };   // V_j, 1-based
-  const int64_t ldr = c->ld;
-  int first_gemm = 1;
-  int gemm_used[2] = {0, 0};
-  // fold blocks blk0.. (0-based) of buffer b into Z on the second stream
-  auto gemm_chunk = [&](int b, int blk0, int nblk) -> int {
+  // V_j (1-based): chunk q = (j-1)/G in buffer q % nbuf, slot (j-1) % G
+  auto blk = [&](int j) -> double* {
+    const int64_t q = (j - 1) / G;
+    return buf[q % nbuf] + ((j - 1) % G) * slot_d + lo_d;
+  };
+  const int64_t ld = s;
+  bool gemm_used[2] = {false, false};
+  // fold chunk q (blocks q*G+1 .. q*G+nblk) into Z on the second stream
+  auto gemm_chunk = [&](int64_t q, int nblk) -> int {
+    const int b = (int)(q % nbuf);
     KRY_CUDA(cudaEventRecord(ev_full[b], c->stream));
     KRY_CUDA(cudaStreamWaitEvent(c->estream, ev_full[b], 0));
-    KRY_CHECK(launch_chunk_coef(c->estream, c->T.S, c->qy, s, r, blk0, nblk, Qc[b]));
-    cublasSetStream(c->cublas, c->estream);
-    const double one = 1.0;
-    const double beta = first_gemm ? 0.0 : 1.0;
-    if (cublasDgemm(c->cublas, CUBLAS_OP_N, CUBLAS_OP_N, r, (int)n, nblk * s, &one, Qc[b], r,
-                    sp(b, 0), (int)ld2, &beta, c->Z, r) != CUBLAS_STATUS_SUCCESS)
-      return fail(KRY_ERR_CUDA, "cublasDgemm (Z accumulation) failed");
+    KRY_CHECK(launch_chunk_coef_ld(c->estream, c->T.S, c->qy, s, r, (int)(q * G), nblk, ldq, Qc[b]));
+    KRY_CHECK(launch_zacc(c->estream, s, buf[b] + lo_d, slot_d, nblk, Qc[b], ldq, r, c->Z, n,
+                          q > 0));
     KRY_CUDA(cudaEventRecord(ev_free[b], c->estream));
-    gemm_used[b] = 1;
-    first_gemm = 0;
+    gemm_used[b] = true;
     return KRY_OK;
   };
-  // regenerate V_1 into the ring and the chunk buffer
-  rc = do_init(c, ring(1), ldr, 1);
-  if (rc == KRY_OK) rc = launch_copy_block(c->stream, s, ring(1), ldr, sp(cb, 0), ld2, n);
-  int chunk_first = 1;  // 1-based block index held in chunk slot 0
+  // regenerate V_1 (replay mode: coupling blocks compared with pass 1)
+  rc = do_init(c, blk(1), ld, 1);
+  const bool speculate = !step_on(c) && !dist(c);
   for (int j = 1; rc == KRY_OK && j < m; ++j) {
     // coefficient solve j on V_j (replay) -- already done by the previous
-    // fused launch when coef_ready; V_{j+1} goes to the ring and the chunk
+    // fused launch when coef_ready
     const bool fused = step_on(c) && c->coef_ready;
-    // two-kernel path on one GPU: no host round trip between the solve and
-    // the (self-cancelling) combine, see fused_step
-    const bool speculate = !step_on(c) && !dist(c);
     if (!fused) {
       c->coef_ready = false;
-      ApplyGramCall ag{ring(j), ldr, n, 1, POST_STEP, 0};
+      ApplyGramCall ag{blk(j), ld, n, 1, POST_STEP, 0};
       ag.wout = speculate ? wbuf_of(c) : nullptr;
       rc = run_apply_gram(c, ag);
       if (rc) break;
@@ -2226,51 +2277,39 @@ int kry_recover(kry_ctx* c, double* zhost) {
         if (rc) break;
       }
     }
-    if (j + 1 - chunk_first == G) {
-      // chunk complete: S_j known now -> fold blocks chunk_first..j into Z
-      rc = gemm_chunk(cb, chunk_first - 1, j - chunk_first + 1);
+    if (j % G == 0) {   // S_j known: the chunk ending at block j is complete
+      rc = gemm_chunk(j / G - 1, (int)G);
       if (rc) break;
-      const int nb = (nbuf == 2) ? 1 - cb : cb;
-      // the buffer we switch to is free once its previous DGEMM is done
-      if ((nb == cb || gemm_used[nb]) &&
-          cudaStreamWaitEvent(c->stream, ev_free[nb], 0) != cudaSuccess) {
+    }
+    if (j % G == 0 && nbuf == 2) {
+      // V_{j+1} opens chunk j/G in the buffer of chunk j/G - 2: wait for its fold
+      const int b = (int)((j / G) % 2);
+      if (gemm_used[b] && cudaStreamWaitEvent(c->stream, ev_free[b], 0) != cudaSuccess) {
         rc = fail(KRY_ERR_CUDA, "event wait failed");
         break;
       }
-      cb = nb;
-      chunk_first = j + 1;
     }
-    double* chunk_dst = sp(cb, j + 1 - chunk_first);
+    double* vold = j > 1 ? blk(j - 1) : nullptr;
     int ex = 0;
     if (speculate) {
-      CombineCall cc{j > 1 ? ring(j - 1) : nullptr, ldr, ring(j), ldr, ring(j + 1), ldr, n,
-                     j > 1 ? 1 : 0, 1, 1, 1};
-      cc.vn2 = chunk_dst;
-      cc.ldn2 = ld2;
+      CombineCall cc{vold, ld, blk(j), ld, blk(j + 1), ld, n, j > 1 ? 1 : 0, 1, 1, 1};
       cc.win = wbuf_of(c);
       rc = run_combine(c, cc, nullptr, nullptr);
       if (rc == KRY_OK) rc = sync_status(c);
       if (rc == KRY_OK) rc = map_status(c, ("second pass step " + std::to_string(j)).c_str());
-      if (rc == KRY_OK && (c->st_h->flags & KRY_FLAG_FALLBACK)) {
-        rc = explicit_step(c, j, j > 1 ? ring(j - 1) : nullptr, ring(j), ring(j + 1), ldr, 1, &ex);
-        if (rc == KRY_OK && !ex) rc = launch_copy_block(c->stream, s, ring(j + 1), ldr, chunk_dst, ld2, n);
-      }
+      if (rc == KRY_OK && (c->st_h->flags & KRY_FLAG_FALLBACK))
+        rc = explicit_step(c, j, vold, blk(j), blk(j + 1), ld, 1, &ex);
     } else if (!fused && (c->st_h->flags & KRY_FLAG_FALLBACK)) {
-      rc = explicit_step(c, j, j > 1 ? ring(j - 1) : nullptr, ring(j), ring(j + 1), ldr, 1, &ex);
-      if (rc == KRY_OK && !ex) rc = launch_copy_block(c->stream, s, ring(j + 1), ldr, chunk_dst, ld2, n);
+      rc = explicit_step(c, j, vold, blk(j), blk(j + 1), ld, 1, &ex);
     } else if (step_on(c)) {
-      rc = run_step_kernel(c, j, j > 1 ? ring(j - 1) : nullptr, ring(j), ring(j + 1), ldr,
-                           chunk_dst, ld2, false);
+      rc = run_step_kernel(c, j, vold, blk(j), blk(j + 1), ld, nullptr, 0, false);
       if (rc == KRY_OK) rc = sync_status(c);
       if (rc == KRY_OK) rc = map_status(c, ("second pass step " + std::to_string(j)).c_str());
       c->coef_ready = !(c->st_h->flags & KRY_FLAG_FALLBACK);
     } else {
-      CombineCall cc{j > 1 ? ring(j - 1) : nullptr, ldr, ring(j), ldr, ring(j + 1), ldr, n,
-                     j > 1 ? 1 : 0, 1, 1, 1};
-      cc.vn2 = chunk_dst;
-      cc.ldn2 = ld2;
+      CombineCall cc{vold, ld, blk(j), ld, blk(j + 1), ld, n, j > 1 ? 1 : 0, 1, 1, 1};
       rc = run_combine(c, cc, nullptr, nullptr);
-      if (rc == KRY_OK) rc = halo_exchange(c, ring(j + 1), ldr, s);
+      if (rc == KRY_OK) rc = halo_exchange(c, blk(j + 1), ld, s);
     }
     if (rc) break;
     if (ex) { rc = fail(KRY_ERR_RECURRENCE, "second pass hit an invariant subspace early"); break; }
@@ -2279,11 +2318,12 @@ int kry_recover(kry_ctx* c, double* zhost) {
     // coefficient solve m: S_m (and the replay check of coupling m-1); the
     // last fused launch has done it already
     if (!(step_on(c) && c->coef_ready && m > 1)) {
-      ApplyGramCall ag{ring(m), ldr, n, 1, POST_STEP, 0};
+      ApplyGramCall ag{blk(m), ld, n, 1, POST_STEP, 0};
       rc = run_apply_gram(c, ag);
       if (rc == KRY_OK) rc = sync_status(c);
     }
-    if (rc == KRY_OK) rc = gemm_chunk(cb, chunk_first - 1, m - chunk_first + 1);
+    const int64_t q = (m - 1) / G;
+    if (rc == KRY_OK) rc = gemm_chunk(q, (int)(m - q * G));
   }
   if (rc == KRY_OK) {
     cudaStreamSynchronize(c->estream);

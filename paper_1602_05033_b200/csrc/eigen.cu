@@ -303,16 +303,73 @@ __device__ __forceinline__ void block_sumv(double (&v)[NV], double (*red)[W][NV]
 // convergence speed, not the converged root, which is decided by h)
 __device__ __forceinline__ double fdivi(double a, double b) { return a * frcp(b); }
 
+// Two-pole rational model step (LAPACK dlaed4 "middle way" style) for the
+// shifted secular function at t with the left / right sums (psiL, dpsiL,
+// psiR, dpsiR); da / db: shifted neighbour poles (ia / ib < 0: none);
+// returns the new iterate inside (ta, tb) (bisection when the model fails).
+__device__ __forceinline__ double model_step(double t, double h, double psiL, double dpsiL,
+                                             double psiR, double dpsiR, double da, double db,
+                                             int ia, int ib, bool near_left, double c0,
+                                             double ta, double tb) {
+  double tn = 0.0;
+  bool ok = false;
+  if (ia >= 0 && ib >= 0) {
+    double w1, w2;
+    if (near_left) {
+      w1 = dpsiL * (t - da) * (t - da);
+      w2 = (dpsiR + 1.0) * (t - db) * (t - db);
+    } else {
+      w1 = (dpsiL + 1.0) * (t - da) * (t - da);
+      w2 = dpsiR * (t - db) * (t - db);
+    }
+    const double c = h + fdivi(w1, t - da) + fdivi(w2, t - db);
+    const double A = c, B = c * (da + db) + w1 + w2, C = c * da * db + w1 * db + w2 * da;
+    if (A != 0.0) {
+      const double sq = sqrt(fmax(B * B - 4.0 * A * C, 0.0));
+      double r1, r2;
+      if (B >= 0.0) { r1 = fdivi(B + sq, 2.0 * A); r2 = (B + sq) != 0.0 ? fdivi(2.0 * C, B + sq) : r1; }
+      else { r1 = (B - sq) != 0.0 ? fdivi(2.0 * C, B - sq) : 0.0; r2 = fdivi(B - sq, 2.0 * A); }
+      if (r1 > ta && r1 < tb) { tn = r1; ok = true; }
+      else if (r2 > ta && r2 < tb) { tn = r2; ok = true; }
+    } else if (B != 0.0) {
+      tn = fdivi(C, B);
+      ok = (tn > ta && tn < tb);
+    }
+  } else {
+    const double psi = psiL + psiR, dpsi = dpsiL + dpsiR;
+    const double w = dpsi * t * t;
+    const double B = c0 + psi + fdivi(w, t);
+    const double sq = sqrt(B * B + 4.0 * w);
+    if (ib < 0) tn = (B >= 0.0) ? fdivi(2.0 * w, B + sq) : 0.5 * (sq - B);   // top root
+    else tn = (B > 0.0) ? -0.5 * (B + sq) : fdivi(2.0 * w, B - sq);          // bottom root
+    ok = (tn > ta && tn < tb);
+  }
+  if (!ok || !isfinite(tn)) tn = 0.5 * (ta + tb);
+  return tn;
+}
+
+// Per root: (1) one pass over all poles at the interval midpoint mu0 gives
+// the sign of h(mu0) (the origin = nearer pole, so mu - lam_j is formed
+// without cancellation) and, for the poles outside a window of SEC_WIN
+// poles around the root, their left/right sums and derivatives; (2) warp 0
+// solves the LOCAL model -- the window's poles exactly, the far part
+// linearised at mu0 -- to convergence, one lane per window pole; (3) the
+// global two-pole iteration starts from that root.  On the c5 spectra the
+// far part is smooth over the interval, so (3) converges in ~2-3 passes
+// where the midpoint start needed 5-11 (the model's error is dominated by
+// the dense neighbourhood, which the window now takes exactly).
+#define SEC_WIN 32
 // Per-thread register cache of the shifted poles and z^2 (MT terms per
 // thread, MT * NT >= p); MT = 0: stream them from global memory.
 template <int W, int MT>
 __global__ void __launch_bounds__(32 * W) k_eig_secular(EigView e) {
   constexpr int NT = 32 * W;
   __shared__ double red[2][W][4];   // double-buffered: one barrier per reduction
+  __shared__ double s_t1;
   const int p = e.counts[0];
   const int i = blockIdx.x;
   if (i > p) return;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
   const double d = e.scal[0];
   if (p == 0) {
     if (tid == 0) { e.org[0] = d; e.tau[0] = 0.0; e.mu[0] = d; }
@@ -324,33 +381,95 @@ __global__ void __launch_bounds__(32 * W) k_eig_secular(EigView e) {
   const double lo = fmin(poles[0], d) - zabs - 1e-300;
   const double hi = fmax(poles[p - 1], d) + zabs + 1e-300;
   int rb = 0;
-  double org;
+  // window of poles around the root (contains the neighbours i-1, i)
+  int w0 = i - SEC_WIN / 2;
+  w0 = max(0, min(w0, p - SEC_WIN));
+  const int w1 = min(p, w0 + SEC_WIN);
   int ia, ib;
+  double mu0, org;
   if (i == 0) {
     org = poles[0]; ia = -1; ib = 0;
+    mu0 = org + 0.5 * (lo - org);
   } else if (i == p) {
     org = poles[p - 1]; ia = p - 1; ib = -1;
+    mu0 = org + 0.5 * (hi - org);
   } else {
-    const double a = poles[i - 1], b = poles[i];
-    const double mid = 0.5 * (a + b);
-    double v[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int j = tid; j < p; j += 2 * NT) {
-      const double zj = zz[j];
-      v[0] -= zj * zj * frcp(mid - poles[j]);
-      if (j + NT < p) {
-        const double zk = zz[j + NT];
-        v[1] -= zk * zk * frcp(mid - poles[j + NT]);
-      }
-    }
-    v[0] += v[1];
-    v[1] = 0.0;
-    block_sumv<W, 4>(v, &red[rb]);
-    rb ^= 1;
-    const double hm = v[0] + (mid - d);
-    org = (hm > 0.0) ? a : b;
+    mu0 = 0.5 * (poles[i - 1] + poles[i]);
+    org = 0.0;   // decided below
     ia = i - 1; ib = i;
   }
-  // shifted poles sh_j = lam_j - org and z_j^2, cached once per root
+  // (1) far sums at mu0 (left: j <= ia), absolute coordinates
+  double fL, fdL, fR, fdR;
+  {
+    double v[4] = {0.0, 0.0, 0.0, 0.0}, u[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int j = tid; j < p; j += 2 * NT) {
+      if (j < w0 || j >= w1) {
+        const double zj = zz[j];
+        const double r = frcp(mu0 - poles[j]);
+        const double term = zj * zj * r, dterm = term * r;
+        if (j <= ia) { v[0] -= term; v[1] += dterm; } else { v[2] -= term; v[3] += dterm; }
+      }
+      const int k = j + NT;
+      if (k < p && (k < w0 || k >= w1)) {
+        const double zk = zz[k];
+        const double r = frcp(mu0 - poles[k]);
+        const double term = zk * zk * r, dterm = term * r;
+        if (k <= ia) { u[0] -= term; u[1] += dterm; } else { u[2] -= term; u[3] += dterm; }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] += u[q];
+    block_sumv<W, 4>(v, &red[rb]);
+    rb ^= 1;
+    fL = v[0]; fdL = v[1]; fR = v[2]; fdR = v[3];
+  }
+  // window pole of this lane
+  const int jw = w0 + lane;
+  const bool inw = jw < w1;
+  const double zw = inw ? zz[jw] : 0.0;
+  const double z2w = zw * zw;
+  const double plw = inw ? poles[jw] : 0.0;
+  if (i > 0 && i < p) {
+    // sign of h(mu0): the origin is the nearer pole
+    double nsum = inw ? -z2w * frcp(mu0 - plw) : 0.0;
+    nsum = warp_sum(nsum);
+    const double hm = (mu0 - d) + fL + fR + nsum;
+    org = (hm > 0.0) ? poles[i - 1] : poles[i];
+  }
+  const double da = (ia >= 0) ? poles[ia] - org : 0.0;
+  const double db = (ib >= 0) ? poles[ib] - org : 0.0;
+  double ta = (ia >= 0) ? da : lo - org;
+  double tb = (ib >= 0) ? db : hi - org;
+  const double c0 = org - d;
+  const bool near_left = (ia >= 0) && (org == poles[ia]);
+  const double t0 = mu0 - org;
+  // (2) local model, warp 0: g(t) = t + c0 + [window terms] + far(t0) + far'(t0) (t - t0)
+  if (tid < 32) {
+    const double shw = plw - org;
+    const bool wleft = jw <= ia;
+    double t = t0, la = ta, lb = tb;
+    for (int it = 0; it < 40; ++it) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      if (inw) {
+        const double r = frcp(t - shw);
+        const double term = z2w * r, dterm = term * r;
+        if (wleft) { a0 = -term; a1 = dterm; } else { a2 = -term; a3 = dterm; }
+      }
+      a0 = warp_sum(a0); a1 = warp_sum(a1); a2 = warp_sum(a2); a3 = warp_sum(a3);
+      const double psiL = a0 + fL + fdL * (t - t0), dpsiL = a1 + fdL;
+      const double psiR = a2 + fR + fdR * (t - t0), dpsiR = a3 + fdR;
+      const double g = t + c0 + psiL + psiR;
+      if (g > 0.0) lb = t; else la = t;
+      if (fabs(g) <= 8.0 * EPS * (fabs(t) + fabs(c0) + fabs(psiL) + fabs(psiR))) break;
+      const double tn = model_step(t, g, psiL, dpsiL, psiR, dpsiR, da, db, ia, ib, near_left, c0,
+                                   la, lb);
+      if (fabs(tn - t) <= 2.0 * EPS * fabs(t)) { t = tn; break; }
+      t = tn;
+    }
+    if (tid == 0) s_t1 = t;
+  }
+  __syncthreads();
+  // (3) global iteration from the local root
   double shc[MT > 0 ? MT : 1], z2c[MT > 0 ? MT : 1];
   if (MT > 0) {
 #pragma unroll
@@ -362,13 +481,9 @@ __global__ void __launch_bounds__(32 * W) k_eig_secular(EigView e) {
       z2c[q] = zj * zj;
     }
   }
-  const double da = (ia >= 0) ? poles[ia] - org : 0.0;
-  const double db = (ib >= 0) ? poles[ib] - org : 0.0;
-  double ta = (ia >= 0) ? da : lo - org;
-  double tb = (ib >= 0) ? db : hi - org;
-  double t = 0.5 * (ta + tb);
-  const double c0 = org - d;
-  const bool near_left = (ia >= 0) && (org == poles[ia]);
+  double t = s_t1;
+  if (!(t > ta && t < tb)) t = 0.5 * (ta + tb);
+  int used = 80, nbis = 0;
   for (int it = 0; it < 80; ++it) {
     // v = {psiL, dpsiL, psiR, dpsiR}: poles j <= ia give positive terms,
     // j > ia negative ones, so sum |term| = psiR - psiL
@@ -414,43 +529,15 @@ __global__ void __launch_bounds__(32 * W) k_eig_secular(EigView e) {
     const double h = t + c0 + psiL + psiR;
     const double err = 8.0 * EPS * (fabs(t) + fabs(c0) + sabs);
     if (h > 0.0) tb = t; else ta = t;
-    if (fabs(h) <= err) break;
-    double tn = 0.0;
-    bool ok = false;
-    if (ia >= 0 && ib >= 0) {
-      double w1, w2;
-      if (near_left) {
-        w1 = dpsiL * (t - da) * (t - da);
-        w2 = (dpsiR + 1.0) * (t - db) * (t - db);
-      } else {
-        w1 = (dpsiL + 1.0) * (t - da) * (t - da);
-        w2 = dpsiR * (t - db) * (t - db);
-      }
-      const double c = h + fdivi(w1, t - da) + fdivi(w2, t - db);
-      const double A = c, B = c * (da + db) + w1 + w2, C = c * da * db + w1 * db + w2 * da;
-      if (A != 0.0) {
-        const double sq = sqrt(fmax(B * B - 4.0 * A * C, 0.0));
-        double r1, r2;
-        if (B >= 0.0) { r1 = fdivi(B + sq, 2.0 * A); r2 = (B + sq) != 0.0 ? fdivi(2.0 * C, B + sq) : r1; }
-        else { r1 = (B - sq) != 0.0 ? fdivi(2.0 * C, B - sq) : 0.0; r2 = fdivi(B - sq, 2.0 * A); }
-        if (r1 > ta && r1 < tb) { tn = r1; ok = true; }
-        else if (r2 > ta && r2 < tb) { tn = r2; ok = true; }
-      } else if (B != 0.0) {
-        tn = fdivi(C, B);
-        ok = (tn > ta && tn < tb);
-      }
-    } else {
-      const double psi = psiL + psiR, dpsi = dpsiL + dpsiR;
-      const double w = dpsi * t * t;
-      const double B = c0 + psi + fdivi(w, t);
-      const double sq = sqrt(B * B + 4.0 * w);
-      if (ib < 0) tn = (B >= 0.0) ? fdivi(2.0 * w, B + sq) : 0.5 * (sq - B);   // top root
-      else tn = (B > 0.0) ? -0.5 * (B + sq) : fdivi(2.0 * w, B - sq);          // bottom root
-      ok = (tn > ta && tn < tb);
-    }
-    if (!ok || !isfinite(tn)) tn = 0.5 * (ta + tb);
-    if (fabs(tn - t) <= 4.0 * EPS * fabs(t)) { t = tn; break; }
+    if (fabs(h) <= err) { used = it + 1; break; }
+    double tn = model_step(t, h, psiL, dpsiL, psiR, dpsiR, da, db, ia, ib, near_left, c0, ta, tb);
+    if (!(tn > ta && tn < tb)) { tn = 0.5 * (ta + tb); ++nbis; }
+    if (fabs(tn - t) <= 4.0 * EPS * fabs(t)) { t = tn; used = it + 1; break; }
     t = tn;
+  }
+  if (e.stats && tid == 0) {
+    atomicAdd(e.stats + min(used, 80), 1u);
+    atomicAdd(e.stats + 96 + min(nbis, 31), 1u);
   }
   if (tid == 0) {
     e.org[i] = org;
@@ -675,30 +762,63 @@ __global__ void k_uw(const double* F, const double* L, int64_t km, int k, int s,
 // takes its k-steps over the y parity (k-step h <-> y = 2t + h), so no lane
 // exchange is needed; the B operand of k-step h is C[y0 + 2t + h][g].
 // A CTA owns 16 x-rows (two 8-row fragments per warp, two independent DMMA
-// chains) and sweeps ALL y: its 16 warps take y-tiles in a fixed stride and
-// their partial M are summed through shared memory in warp order, so no
-// split-y partial pass exists and the result is deterministic.  The minimum
-// |lx + ly| is exact and cheap because ly is sorted ascending (eigenvalues):
-// per x only the two neighbours of -lx in ly can be closest.
+// chains) and one of YS interleaved y-splits; its 8 warps take the split's
+// y-tiles in a fixed stride, with the next tile's operands loaded while the
+// current one is multiplied.  The warps' partial M are summed through shared
+// memory in warp order; with YS > 1 the splits' partial M go to global
+// memory and the last split CTA of an x-tile (per-tile ticket) adds them in
+// split order, so every sum has a fixed order: the result is deterministic.
+// The minimum |lx + ly| is exact and cheap because ly is sorted ascending
+// (eigenvalues): per x only the two neighbours of -lx in ly can be closest.
 #define CC_XR 16     // x rows per CTA
-#define CC_NW 16     // warps per CTA
+#define CC_NW 8      // warps per CTA
+#define CC_TARGET_CTAS (3 * 148)
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
+template <int KS>
+struct YOps {   // operands of one 8-wide y-tile held by a lane
+  double b[KS], c[2], l[2];
+  bool v[2];
+};
+template <int S, int KS>
+__device__ __forceinline__ void load_y(YOps<KS>& o, int y0, int g, int t, int ny,
+                                       const double* __restrict__ ly,
+                                       const double* __restrict__ by,
+                                       const double* __restrict__ cy) {
+  const int yb = y0 + g;
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const int col = 4 * ks + t;
+    o.b[ks] = (yb < ny && col < S) ? __ldg(by + (int64_t)yb * 8 + col) : 0.0;
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int y = y0 + 2 * t + h;
+    o.v[h] = y < ny;
+    o.c[h] = (o.v[h] && g < S) ? __ldg(cy + (int64_t)y * 8 + g) : 0.0;
+    o.l[h] = o.v[h] ? __ldg(ly + y) : 0.0;
+  }
+}
+
+// part layout: [0, 2*nxt): per-x-tile (|M|^2, min);  then [nxt][YS][16][8]
+// partial M of the splits.  cnt: nxt per-tile tickets + 1 global ticket.
 template <int S>
 __global__ void __launch_bounds__(32 * CC_NW) k_cauchy_mma(int nx, const double* __restrict__ lx,
                                                            const double* __restrict__ ax, int ny,
                                                            const double* __restrict__ ly,
                                                            const double* __restrict__ by,
                                                            const double* __restrict__ cy,
-                                                           double* part, unsigned* ticket,
+                                                           double* part, unsigned* cnt,
                                                            double* res) {
   constexpr int KS = (S + 3) / 4;   // k-steps of the first product
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int x0 = blockIdx.x * CC_XR;
+  const int xt = blockIdx.x, nxt = gridDim.x;
+  const int split = blockIdx.y, YS = gridDim.y;
+  const int x0 = xt * CC_XR;
   // A fragments of the two 8-row x tiles: A[g][t] = a[x0 + 8f + g][4 ks + t]
   double fa[2][KS], flx[2];
   bool vx[2];
@@ -715,49 +835,37 @@ __global__ void __launch_bounds__(32 * CC_NW) k_cauchy_mma(int nx, const double*
   }
   double m[2][2] = {{0.0, 0.0}, {0.0, 0.0}};   // M[x0 + 8f + g][2t + j]
   const int nyt = (ny + 7) >> 3;
-  for (int yt = warp; yt < nyt; yt += CC_NW) {
-    const int y0 = yt * 8;
-    // B operand of the first product: B[k = t][n = g] = b[y0 + g][4 ks + t]
-    double fb[KS];
-    {
-      const int y = y0 + g;
-#pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        const int col = 4 * ks + t;
-        fb[ks] = (y < ny && col < S) ? __ldg(by + (int64_t)y * 8 + col) : 0.0;
-      }
-    }
-    // B operand of the second product, k-step h: C[y0 + 2t + h][g]; and ly
-    double fc[2], fl[2];
-    bool vy[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int y = y0 + 2 * t + h;
-      vy[h] = y < ny;
-      fc[h] = (vy[h] && g < S) ? __ldg(cy + (int64_t)y * 8 + g) : 0.0;
-      fl[h] = vy[h] ? __ldg(ly + y) : 0.0;
-    }
+  const int ystep = CC_NW * YS;
+  int yt = warp + CC_NW * split;
+  YOps<KS> cur;
+  if (yt < nyt) load_y<S, KS>(cur, yt * 8, g, t, ny, ly, by, cy);
+  for (; yt < nyt; yt += ystep) {
+    YOps<KS> nxt_ops;
+    const int yn = yt + ystep;
+    if (yn < nyt) load_y<S, KS>(nxt_ops, yn * 8, g, t, ny, ly, by, cy);
 #pragma unroll
     for (int f = 0; f < 2; ++f) {
       double p0 = 0.0, p1 = 0.0;   // P[g][2t], P[g][2t+1]
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) dmma884(p0, p1, fa[f][ks], fb[ks]);
-      const bool ok = vx[f];
-      p0 = (ok && vy[0]) ? p0 * frcp(flx[f] + fl[0]) : 0.0;
-      p1 = (ok && vy[1]) ? p1 * frcp(flx[f] + fl[1]) : 0.0;
-      dmma884(m[f][0], m[f][1], p0, fc[0]);
-      dmma884(m[f][0], m[f][1], p1, fc[1]);
+      for (int ks = 0; ks < KS; ++ks) dmma884(p0, p1, fa[f][ks], cur.b[ks]);
+      p0 = (vx[f] && cur.v[0]) ? p0 * frcp(flx[f] + cur.l[0]) : 0.0;
+      p1 = (vx[f] && cur.v[1]) ? p1 * frcp(flx[f] + cur.l[1]) : 0.0;
+      dmma884(m[f][0], m[f][1], p0, cur.c[0]);
+      dmma884(m[f][0], m[f][1], p1, cur.c[1]);
     }
+    if (yn < nyt) cur = nxt_ops;
   }
-  // fixed-order sum of the warps' partial M, then |M_x|^2 of the CTA
+  // fixed-order sum of the warps' partial M
   __shared__ double sm[CC_NW][CC_XR][8];
+  __shared__ double s_tile[CC_XR * 8];
   __shared__ double s_min[CC_XR];
+  __shared__ unsigned s_last;
 #pragma unroll
   for (int f = 0; f < 2; ++f) {
     sm[warp][8 * f + g][2 * t] = m[f][0];
     sm[warp][8 * f + g][2 * t + 1] = m[f][1];
   }
-  if (warp == 1 && lane < CC_XR) {
+  if (split == 0 && warp == 1 && lane < CC_XR) {
     // exact min |lx + ly| of this row: the neighbours of -lx in sorted ly
     const int x = x0 + lane;
     double mn = 1e300;
@@ -774,35 +882,60 @@ __global__ void __launch_bounds__(32 * CC_NW) k_cauchy_mma(int nx, const double*
     s_min[lane] = mn;
   }
   __syncthreads();
+  for (int e = threadIdx.x; e < CC_XR * 8; e += blockDim.x) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < CC_NW; ++w) v += sm[w][e >> 3][e & 7];
+    s_tile[e] = v;
+  }
+  double* tile_out = part + 2 * (int64_t)xt;
+  if (YS > 1) {
+    double* mine = part + 2 * (int64_t)nxt + ((int64_t)xt * YS + split) * (CC_XR * 8);
+    __syncthreads();
+    for (int e = threadIdx.x; e < CC_XR * 8; e += blockDim.x) mine[e] = s_tile[e];
+    if (split == 0 && threadIdx.x == 0) {
+      double mn = 1e300;
+      for (int r = 0; r < CC_XR; ++r) mn = fmin(mn, s_min[r]);
+      tile_out[1] = mn;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_last = (atomicAdd(cnt + xt, 1u) == (unsigned)YS - 1) ? 1u : 0u;
+      if (s_last) cnt[xt] = 0u;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const double* all = part + 2 * (int64_t)nxt + (int64_t)xt * YS * (CC_XR * 8);
+    for (int e = threadIdx.x; e < CC_XR * 8; e += blockDim.x) {
+      double v = 0.0;
+      for (int q = 0; q < YS; ++q) v += __ldcg(all + (int64_t)q * (CC_XR * 8) + e);
+      s_tile[e] = v;
+    }
+  } else if (threadIdx.x == 0) {
+    double mn = 1e300;
+    for (int r = 0; r < CC_XR; ++r) mn = fmin(mn, s_min[r]);
+    tile_out[1] = mn;
+  }
+  __syncthreads();
   if (warp == 0) {
     double ss = 0.0;
-    for (int e = lane; e < CC_XR * 8; e += 32) {
-      const int r = e >> 3, col = e & 7;
-      double v = 0.0;
-#pragma unroll
-      for (int w = 0; w < CC_NW; ++w) v += sm[w][r][col];
-      if (col < S) ss = fma(v, v, ss);
-    }
+    for (int e = lane; e < CC_XR * 8; e += 32)
+      if ((e & 7) < S) ss = fma(s_tile[e], s_tile[e], ss);
     ss = warp_sum(ss);
-    double mn = lane < CC_XR ? s_min[lane] : 1e300;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    if (lane == 0) {
-      part[2 * blockIdx.x] = ss;
-      part[2 * blockIdx.x + 1] = mn;
-    }
+    if (lane == 0) tile_out[0] = ss;
   }
-  // last CTA: fixed-order reduction of the CTA partials
+  // last x-tile: fixed-order reduction of the tile partials
   __threadfence();
   __syncthreads();
-  __shared__ unsigned s_last;
-  if (threadIdx.x == 0) s_last = (atomicAdd(ticket, 1u) == gridDim.x - 1) ? 1u : 0u;
+  if (threadIdx.x == 0) s_last = (atomicAdd(cnt + nxt, 1u) == (unsigned)nxt - 1) ? 1u : 0u;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
   __shared__ double rs[32 * CC_NW], rm[32 * CC_NW];
   double tot = 0.0, mn = 1e300;
-  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+  for (int b = threadIdx.x; b < nxt; b += blockDim.x) {
     tot += __ldcg(part + 2 * b);
     mn = fmin(mn, __ldcg(part + 2 * b + 1));
   }
@@ -819,7 +952,7 @@ __global__ void __launch_bounds__(32 * CC_NW) k_cauchy_mma(int nx, const double*
   if (threadIdx.x == 0) {
     res[0] = rs[0];
     res[1] = rm[0];
-    *ticket = 0u;
+    cnt[nxt] = 0u;
   }
 }
 
@@ -846,8 +979,11 @@ int EigEngine::init(int s_, int kmax_, int device) {
   const size_t nch_max = (nk + E4_CH - 1) / E4_CH + 1;
   const size_t vpart_n = nch_max * (nk + 8) * 16;
   doubles += vpart_n;             // E4 partial sums
-  // Cauchy per-CTA partials (sum, min) for x up to 2 kmax
-  cpart_cap = 2 * ((2 * nk + CC_XR - 1) / CC_XR) + 64;
+  // Cauchy tile sums + split partials for x up to 2 kmax
+  {
+    const size_t nxt = (2 * nk + CC_XR - 1) / CC_XR;
+    cpart_cap = 2 * nxt + nxt * 16 * CC_XR * 8 + 64;
+  }
   doubles += cpart_cap;
   KRY_CHECK(dalloc(&dbuf, doubles));
   KRY_CUDA(cudaMemset(dbuf, 0, doubles * sizeof(double)));
@@ -872,13 +1008,39 @@ int EigEngine::init(int s_, int kmax_, int device) {
   def_idx = q; q += nk; counts = q;
   KRY_CHECK(dalloc(&ticket, 4));
   KRY_CUDA(cudaMemset(ticket, 0, sizeof(unsigned) * 4));
+  cnt_cap = (2 * nk + CC_XR - 1) / CC_XR + 1;
+  KRY_CHECK(dalloc(&cnt, cnt_cap));
+  KRY_CUDA(cudaMemset(cnt, 0, cnt_cap * sizeof(unsigned)));
+  if (const char* st = getenv("KRY_SECULAR_STATS")) {
+    if (st[0] == '1') {
+      KRY_CHECK(dalloc(&stats, 128));
+      KRY_CUDA(cudaMemset(stats, 0, 128 * sizeof(unsigned)));
+    }
+  }
   return KRY_OK;
 }
 
 void EigEngine::release() {
+  if (stats) {
+    unsigned h[128];
+    if (cudaMemcpy(h, stats, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess) {
+      fprintf(stderr, "[kry] secular iterations:");
+      for (int i = 0; i <= 80; ++i)
+        if (h[i]) fprintf(stderr, " %d:%u", i, h[i]);
+      fprintf(stderr, "\n[kry] secular bisection steps:");
+      for (int i = 0; i < 32; ++i)
+        if (h[96 + i]) fprintf(stderr, " %d:%u", i, h[96 + i]);
+      fprintf(stderr, "\n");
+    }
+    dfree(stats);
+    stats = nullptr;
+  }
   if (dbuf) dfree(dbuf);
   if (ibuf) dfree(ibuf);
   if (ticket) dfree(ticket);
+  if (cnt) dfree(cnt);
+  cnt = nullptr;
+  cnt_cap = 0;
   if (cpart_ext) dfree(cpart_ext);
   dbuf = nullptr; ibuf = nullptr; ticket = nullptr; cpart_ext = nullptr;
 }
@@ -893,6 +1055,7 @@ EigView EigEngine::view() const {
   v.org = org; v.tau = tau; v.scal = scal;
   v.cand = cand; v.dflag = dflag; v.pflag = pflag; v.pmap = pmap; v.def_idx = def_idx;
   v.counts = counts;
+  v.stats = stats;
   return v;
 }
 
@@ -958,24 +1121,41 @@ int EigEngine::append_block(cudaStream_t st, const double* dsym_blk, const doubl
   return KRY_OK;
 }
 
+static int cauchy_splits(int nx, int ny) {
+  const int nxt = std::max(1, (nx + CC_XR - 1) / CC_XR);
+  const int nyt = std::max(1, (ny + 7) / 8);
+  int ys = (CC_TARGET_CTAS + nxt - 1) / nxt;
+  ys = std::min(ys, std::max(1, nyt / (2 * CC_NW)));   // >= 2 y-tiles per warp
+  return std::max(1, std::min(ys, 16));
+}
+
 int EigEngine::ensure_cauchy(int nx, int ny) {
+  const size_t nxt = (size_t)std::max(1, (nx + CC_XR - 1) / CC_XR);
+  const size_t need = 2 * nxt + nxt * 16 * CC_XR * 8 + 64;   // tile sums + split partials (YS <= 16)
   (void)ny;
-  const size_t need = 2 * (size_t)((nx + CC_XR - 1) / CC_XR) + 64;   // per-CTA (sum, min)
-  if (need <= cpart_cap) return KRY_OK;
+  if (need <= cpart_cap && nxt + 1 <= cnt_cap) return KRY_OK;
   if (cpart_ext) dfree(cpart_ext);
   cpart_ext = nullptr;
   KRY_CHECK(dalloc(&cpart_ext, need));
   cpart = cpart_ext;
   cpart_cap = need;
+  if (cnt_cap < nxt + 1) {
+    if (cnt) dfree(cnt);
+    cnt = nullptr;
+    KRY_CHECK(dalloc(&cnt, nxt + 1));
+    KRY_CUDA(cudaMemset(cnt, 0, (nxt + 1) * sizeof(unsigned)));
+    cnt_cap = nxt + 1;
+  }
   return KRY_OK;
 }
 
 int EigEngine::cauchy(cudaStream_t st, int nx, const double* lx, const double* ax, int ny,
                       const double* ly, const double* by, const double* cy, double* out2) {
+  KRY_CHECK(ensure_cauchy(nx, ny));
   const int gx = std::max(1, (nx + CC_XR - 1) / CC_XR);
-  if ((size_t)2 * gx > cpart_cap) return fail(KRY_ERR_STATE, "residual grid too large");
+  dim3 grid(gx, cauchy_splits(nx, ny));
 #define L(S) \
-  k_cauchy_mma<S><<<gx, 32 * CC_NW, 0, st>>>(nx, lx, ax, ny, ly, by, cy, cpart, ticket, out2)
+  k_cauchy_mma<S><<<grid, 32 * CC_NW, 0, st>>>(nx, lx, ax, ny, ly, by, cy, cpart, cnt, out2)
   switch (s) {
     case 1: L(1); break; case 2: L(2); break; case 3: L(3); break; case 4: L(4); break;
     case 5: L(5); break; case 6: L(6); break; case 7: L(7); break; case 8: L(8); break;

@@ -13,6 +13,7 @@ struct EigView {
   double *z, *poles, *zz, *zhat, *def_lam, *mu;
   double *org, *tau, *scal;
   int *cand, *dflag, *pflag, *pmap, *def_idx, *counts;
+  unsigned* stats;   // KRY_SECULAR_STATS=1: secular iteration histogram (diagnostics)
 };
 
 struct EigEngine {
@@ -21,6 +22,8 @@ struct EigEngine {
   double* dbuf = nullptr;
   int* ibuf = nullptr;
   unsigned* ticket = nullptr;
+  unsigned* cnt = nullptr;     // Cauchy per-x-tile tickets + 1 global
+  size_t cnt_cap = 0;
   double *lam[2] = {nullptr, nullptr}, *F[2] = {nullptr, nullptr}, *L[2] = {nullptr, nullptr};
   double *z = nullptr, *poles = nullptr, *zz = nullptr, *zhat = nullptr, *def_lam = nullptr,
          *mu = nullptr;
@@ -29,6 +32,7 @@ struct EigEngine {
   size_t cpart_cap = 0;   // x-by-y-chunk entries of cpart
   int *cand = nullptr, *dflag = nullptr, *pflag = nullptr, *pmap = nullptr,
       *def_idx = nullptr, *counts = nullptr;
+  unsigned* stats = nullptr;
 
   int init(int s, int kmax, int device);
   void release();

@@ -15,4 +15,11 @@ int launch_scale_factor(cudaStream_t st, const double* W, int64_t ldw, const dou
                         int rank, int desc, int transposed, double* factor);
 int launch_chunk_coef(cudaStream_t st, const double* S, const double* qy, int s, int rank,
                       int blk0, int nblk, double* Qc);
+// pass-2 / stored factor accumulation on DMMA (zacc.cu):
+// Z[i][:] (+)= sum_b V_b[i][:] Q[b s .. b s + s)[:], V_b = vbase + b vstride
+int launch_zacc(cudaStream_t st, int s, const double* vbase, int64_t vstride, int nb,
+                const double* Q, int ldq, int r, double* Z, int64_t n, int accumulate);
+int launch_chunk_coef_ld(cudaStream_t st, const double* S, const double* qy, int s, int rank,
+                         int blk0, int nblk, int ldq, double* Qc);
+int zacc_ldq(int r);   // padded leading dimension of the Q panel
 }  // namespace kry

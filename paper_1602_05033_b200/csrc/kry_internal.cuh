@@ -121,6 +121,7 @@ struct DevState {
   double beta2;
   double scale2, w2;
   double replay_err;
+  double nrows;              // rows of the Krylov vectors (all ranks): shift of CholQR3
   int status;
   int flags;                 // KRY_FLAG_*
   int step;                  // completed coefficient solves
@@ -134,6 +135,7 @@ struct DevState {
 enum {
   KRY_FLAG_EXHAUSTED = 1,
   KRY_FLAG_FALLBACK = 2,
+  KRY_FLAG_SHIFTED = 4,     // the last Cholesky QR stage used the CholQR3 shift
 };
 
 // post-reduction routines run by the last CTA of a Gram reduction
@@ -150,6 +152,9 @@ enum PostMode {
   POST_W2 = 9,          // explicit path: w2 = trace, zero test
   POST_FUSED = 10,      // fused step kernel: carried blocks + deferred solve of step j+1
   POST_STEP8 = 11,      // POST_STEP with W0^T W0 at row 8 (register-fragment apply kernel)
+  POST_CHOL_MID = 12,   // shifted CholQR3 middle stage: R = chol(V^T V), M[0] = R^-1,
+                        // gram[0..63] = R1prev = R * gram[0..63] (accumulated R chain)
+  POST_GCC = 13,        // Gcc = V^T V (refresh after an explicit re-orthonormalisation)
 };
 
 struct TStore {  // projected-matrix storage (device), slots of 64 doubles

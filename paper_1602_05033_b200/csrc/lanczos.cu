@@ -214,6 +214,33 @@ __device__ int chol_upper(const double* G, double* R, int s, double* min_ratio) 
   *min_ratio = mr;
   return 0;
 }
+// Shifted Cholesky of shifted CholQR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto,
+// Yamazaki 2020): R = chol(G + sigma I), sigma = 11 (n s + s (s + 1)) u ||G||,
+// with ||G|| bounded by trace(G).  The shift keeps the factorisation
+// positive definite for any W with kappa(W) up to ~u^-1, and Q0 = W R^-1 is
+// then well enough conditioned (kappa ~ (n s u)^-1/2) for two plain CholQR
+// stages to reach Householder-level orthogonality.  That is what resolves
+// the rank of ill-conditioned blocks the way economy_qr (kernels.py:134-160)
+// does, instead of failing at the Gram's rounding level (kappa ~ 1e7).
+__device__ int chol_shifted(const double* G, double* R, int s, double nrows) {
+  double tr = 0.0;
+  for (int k = 0; k < s; ++k) tr += fabs(G[k * 8 + k]);
+  const double sigma = 11.0 * (nrows * s + s * (s + 1.0)) * 2.220446049250313e-16 * tr;
+  for (int i = 0; i < 64; ++i) R[i] = 0.0;
+  for (int k = 0; k < s; ++k) {
+    double p = G[k * 8 + k] + sigma;
+    for (int i = 0; i < k; ++i) p -= R[i * 8 + k] * R[i * 8 + k];
+    if (!(p > 0.0)) return 1;
+    const double rkk = sqrt(p);
+    R[k * 8 + k] = rkk;
+    for (int j = k + 1; j < s; ++j) {
+      double v = G[k * 8 + j];
+      for (int i = 0; i < k; ++i) v -= R[i * 8 + k] * R[i * 8 + j];
+      R[k * 8 + j] = v / rkk;
+    }
+  }
+  return 0;
+}
 __device__ void inv_upper(const double* R, double* Ri, int s) {
   for (int i = 0; i < 64; ++i) Ri[i] = 0.0;
   for (int j = 0; j < s; ++j) {
@@ -556,14 +583,21 @@ __device__ __noinline__ void run_post(int post, const double* total, DevState* s
       if (tid() == 0) {
         double mr = 0.0;
         st->beta2 = m_trace(sm[0], s);
+        int shifted = 0;
         s_bad = chol_upper(sm[0], sm[1], s, &mr);
-        if (s_bad || mr < 1e-12) {
-          s_bad = 1;
+        if (s_bad) {
+          // ill-conditioned C: shifted first stage, the host adds the
+          // explicit middle stage (rank decided on the final gamma)
+          s_bad = chol_shifted(sm[0], sm[1], s, st->nrows);
+          shifted = 1;
+        }
+        if (s_bad) {
           if (st->status == KRY_OK) st->status = KRY_ERR_DEFLATION;
         } else {
           inv_upper(sm[1], sm[2], s);
           for (int q = 0; q < 64; ++q) {
             st->R1prev[q] = sm[1][q];
+            st->gram[q] = sm[1][q];
             st->M[q] = 0.0;
             st->M[64 + q] = sm[2][q];
             st->M[128 + q] = 0.0;
@@ -571,12 +605,42 @@ __device__ __noinline__ void run_post(int post, const double* total, DevState* s
           }
           st->step = 0;
           st->has_old = 0;
-          st->flags = 0;
+          st->flags = shifted ? KRY_FLAG_SHIFTED : 0;
         }
       }
       __syncthreads();
       break;
     }
+    case POST_CHOL_MID:
+      extract_block(total, 0, s, sm[0]);
+      if (tid() == 0) {
+        double mr = 0.0;
+        s_bad = chol_upper(sm[0], sm[1], s, &mr);
+        if (s_bad) {
+          if (st->status == KRY_OK) st->status = KRY_ERR_DEFLATION;
+        } else {
+          inv_upper(sm[1], sm[2], s);
+          for (int r = 0; r < 8; ++r)
+            for (int c = 0; c < 8; ++c) {
+              double v = 0.0;
+              for (int k = 0; k < 8; ++k) v += sm[1][r * 8 + k] * st->gram[k * 8 + c];
+              sm[3][r * 8 + c] = v;
+            }
+          for (int q = 0; q < 64; ++q) {
+            st->M[q] = sm[2][q];
+            st->gram[q] = sm[3][q];
+            st->R1prev[q] = sm[3][q];
+          }
+          st->flags &= ~KRY_FLAG_SHIFTED;
+        }
+      }
+      __syncthreads();
+      break;
+    case POST_GCC:
+      extract_block(total, 0, s, sm[0]);
+      if (tid() < 64) st->Gcc[tid()] = sm[0][tid()];
+      __syncthreads();
+      break;
     case POST_SCALE:
       extract_block(total, 0, s, sm[0]);
       if (tid() == 0) {
@@ -611,6 +675,11 @@ __device__ __noinline__ void run_post(int post, const double* total, DevState* s
       if (tid() == 0) {
         double mr = 0.0;
         s_bad = chol_upper(sm[0], sm[1], s, &mr);
+        if (s_bad && post == POST_CHOL1) {
+          // shifted CholQR3: the host runs POST_CHOL_MID before POST_CHOL2
+          s_bad = chol_shifted(sm[0], sm[1], s, st->nrows);
+          if (!s_bad) st->flags |= KRY_FLAG_SHIFTED;
+        }
         if (s_bad) {
           if (st->status == KRY_OK) st->status = KRY_ERR_DEFLATION;
         } else {

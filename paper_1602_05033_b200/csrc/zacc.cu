@@ -1,0 +1,228 @@
+// Pass-2 factor accumulation on DMMA (sm_100a, fp64).
+//
+// Reference: two_pass_recover (solvers.py:130-169), `z += v_new @ qy[block]`
+// for every regenerated block, and _assemble_stored (solvers.py:125-127).
+//
+//   Z[i][j] (+)= sum_{b < nb} sum_{c < s} V_b[i][c] * Q[b s + c][j]
+//
+// V_b are consecutive basis blocks of one pass-2 chunk, each stored once,
+// point-major (n x s, ld s) at a fixed stride `vstride` (the ring layout of
+// pass 1: no second, interleaved copy), Q = the chunk's rows of S qy
+// (row-major, ld ldq >= r), Z row-major n x r.  This is a tall-skinny GEMM
+// (M = n = 8e6 points at c4, N = r = 231, K = G s = 512 per chunk) that is
+// bound by the fp64 tensor rate: 2 n k r flops per solve (7.6 TFLOP at c4).
+//
+// Tiling: a CTA computes a 64 x 128 tile of Z (8 warps as 2 x 4, each warp
+// 32 x 32 = 4 x 4 m8n8 DMMA tiles, 32 accumulator doubles per lane) and
+// walks the K dimension one basis block per pipeline stage: the block's 64
+// point rows (64 s contiguous doubles) and the block's s rows of the Q panel
+// arrive by cp.async (16-byte, zero-filled outside the matrix) in a
+// 4-stage ring.  Shared-memory strides are padded so that the A fragments
+// (8 rows x 4 k per warp) and the B fragments (4 k x 8 columns) are read
+// without bank conflicts.  CTAs are ordered panel-fastest, so the panels of
+// one 64-point tile read its A rows from L2.
+#include "kry_internal.cuh"
+#include "finalize.cuh"
+#include <algorithm>
+
+namespace kry {
+
+namespace {
+constexpr int ZBM = 64, ZBN = 128, ZST = 4, ZWARPS = 8;
+constexpr int ZBST = ZBN + 4;          // B row stride (doubles): conflict-free B fragments
+
+__device__ __forceinline__ void zdmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void cp16(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp8(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+// A row stride (doubles): s values padded to the k-steps, + 4 so that the 8
+// rows of a fragment land in distinct banks
+template <int S>
+__host__ __device__ constexpr int zast() { return (S <= 4 ? 4 : 8) + 4; }
+}  // namespace
+
+template <int S>
+__global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__ vbase,
+                                                      int64_t vstride, int nb,
+                                                      const double* __restrict__ Q, int ldq,
+                                                      int r, double* __restrict__ Z, int64_t n,
+                                                      int accumulate, int npanels) {
+  constexpr int KS = (S + 3) / 4;      // k4-steps per block
+  constexpr int AST = zast<S>();
+  constexpr int KP = 4 * KS;           // padded k rows of a B stage
+  extern __shared__ __align__(16) double zsm[];
+  double (*sA)[ZBM * AST] = reinterpret_cast<double (*)[ZBM * AST]>(zsm);
+  double (*sB)[KP * ZBST] = reinterpret_cast<double (*)[KP * ZBST]>(zsm + ZST * ZBM * AST);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int panel = blockIdx.x % npanels;
+  const int64_t i0 = (int64_t)(blockIdx.x / npanels) * ZBM;
+  const int j0 = panel * ZBN;
+  // zero the padding once (k columns >= s of A, k rows >= s of B)
+  for (int e = tid; e < ZST * ZBM * AST; e += blockDim.x) (&sA[0][0])[e] = 0.0;
+  for (int e = tid; e < ZST * KP * ZBST; e += blockDim.x) (&sB[0][0])[e] = 0.0;
+  __syncthreads();
+  auto load_stage = [&](int b, int st) {
+    const double* vb = vbase + (int64_t)b * vstride + i0 * S;
+    if ((S & 1) == 0) {
+      // 64 rows x S doubles contiguous: 16-byte pieces
+      constexpr int PR = (S / 2) > 0 ? S / 2 : 1;   // pieces per row
+      for (int q = tid; q < ZBM * PR; q += blockDim.x) {
+        const int row = q / PR, pc = q % PR;
+        const bool ok = i0 + row < n;
+        cp16(&sA[st][row * AST + 2 * pc], ok ? vb + (int64_t)row * S + 2 * pc : vb, ok);
+      }
+    } else {
+      for (int q = tid; q < ZBM * S; q += blockDim.x) {
+        const int row = q / S, c = q % S;
+        const bool ok = i0 + row < n;
+        cp8(&sA[st][row * AST + c], ok ? vb + (int64_t)row * S + c : vb, ok);
+      }
+    }
+    const double* qb = Q + (int64_t)b * S * ldq + j0;
+    constexpr int PB = ZBN / 2;   // 16-byte pieces per Q row
+    for (int q = tid; q < S * PB; q += blockDim.x) {
+      const int row = q / PB, pc = q % PB;
+      cp16(&sB[st][row * ZBST + 2 * pc], qb + (int64_t)row * ldq + 2 * pc, j0 + 2 * pc < ldq);
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll
+  for (int st = 0; st < ZST - 1; ++st) {
+    if (st < nb) load_stage(st, st);
+    cp_commit();
+  }
+  for (int b = 0; b < nb; ++b) {
+    cp_wait<ZST - 2>();
+    __syncthreads();
+    {   // prefetch block b + ZST - 1 into the stage freed by block b - 1
+      const int bn = b + ZST - 1;
+      if (bn < nb) load_stage(bn, bn % ZST);
+      cp_commit();
+    }
+    const double* A = sA[b % ZST];
+    const double* B = sB[b % ZST];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) fa[mt] = A[(wm * 32 + mt * 8 + g) * AST + 4 * ks + t];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) fb[nt] = B[(4 * ks + t) * ZBST + wn * 32 + nt * 8 + g];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) zdmma(acc[mt][nt][0], acc[mt][nt][1], fa[mt], fb[nt]);
+    }
+  }
+  cp_wait<0>();
+  // epilogue: Z (+)= acc; lane (g, t) holds rows ..+g, columns ..+2t, +2t+1
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+    const int64_t i = i0 + wm * 32 + mt * 8 + g;
+    if (i >= n) continue;
+    double* zr = Z + i * r;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int j = j0 + wn * 32 + nt * 8 + 2 * t;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (j + e < r) {
+          const double v = acc[mt][nt][e];
+          zr[j + e] = accumulate ? zr[j + e] + v : v;
+        }
+      }
+    }
+  }
+}
+
+template <int S>
+static int zacc_go(cudaStream_t st, int64_t grid, const double* vbase, int64_t vstride, int nb,
+                   const double* Q, int ldq, int r, double* Z, int64_t n, int accumulate,
+                   int npanels) {
+  constexpr int KP = 4 * ((S + 3) / 4);
+  const size_t smem = (size_t)ZST * (ZBM * zast<S>() + KP * ZBST) * sizeof(double);
+  static bool attr[64] = {false};   // per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr[dev & 63]) {
+    KRY_CUDA(cudaFuncSetAttribute(k_zacc<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    attr[dev & 63] = true;
+  }
+  k_zacc<S><<<(unsigned)grid, 32 * ZWARPS, smem, st>>>(vbase, vstride, nb, Q, ldq, r, Z, n,
+                                                        accumulate, npanels);
+  return KRY_OK;
+}
+
+int launch_zacc(cudaStream_t st, int s, const double* vbase, int64_t vstride, int nb,
+                const double* Q, int ldq, int r, double* Z, int64_t n, int accumulate) {
+  if (nb < 1 || r < 1) return KRY_OK;
+  const int npanels = (r + ZBN - 1) / ZBN;
+  const int64_t mt = (n + ZBM - 1) / ZBM;
+  const int64_t grid = mt * npanels;
+  if (grid > 0x7fffffffLL) return fail(KRY_ERR_DIMENSION, "pass-2 factor too large");
+#define L(S) KRY_CHECK(zacc_go<S>(st, grid, vbase, vstride, nb, Q, ldq, r, Z, n, accumulate, npanels))
+  switch (s) {
+    case 1: L(1); break; case 2: L(2); break; case 3: L(3); break; case 4: L(4); break;
+    case 5: L(5); break; case 6: L(6); break; case 7: L(7); break; case 8: L(8); break;
+    default: return fail(KRY_ERR_ARGUMENT, "block width s must be 1..8");
+  }
+#undef L
+  count_launch();
+  KRY_CUDA(cudaGetLastError());
+  return KRY_OK;
+}
+
+// Q panel of a chunk with a padded leading dimension: Q[(b s + a) ldq + c] =
+// sum_q S_i[a][q] qy[(i s + q) r + c] for c < r, 0 for r <= c < ldq (i = blk0 + b)
+__global__ void k_chunk_coef_ld(const double* S, const double* qy, int s, int rank, int blk0,
+                                int nblk, int ldq, double* Qc) {
+  const int64_t total = (int64_t)nblk * s * ldq;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % ldq);
+    const int64_t ra = e / ldq;
+    const int a = (int)(ra % s), b = (int)(ra / s);
+    const int i = blk0 + b;
+    double v = 0.0;
+    if (c < rank)
+      for (int q = 0; q < s; ++q)
+        v = fma(S[(int64_t)i * 64 + a * 8 + q], qy[((int64_t)i * s + q) * rank + c], v);
+    Qc[e] = v;
+  }
+}
+
+int launch_chunk_coef_ld(cudaStream_t st, const double* S, const double* qy, int s, int rank,
+                         int blk0, int nblk, int ldq, double* Qc) {
+  const int64_t total = (int64_t)nblk * s * ldq;
+  int64_t g = (total + 255) / 256;
+  g = std::max<int64_t>(1, std::min<int64_t>(g, 148 * 8));
+  k_chunk_coef_ld<<<(int)g, 256, 0, st>>>(S, qy, s, rank, blk0, nblk, ldq, Qc);
+  count_launch();
+  KRY_CUDA(cudaGetLastError());
+  return KRY_OK;
+}
+
+int zacc_ldq(int r) { return ((r + ZBN - 1) / ZBN) * ZBN; }
+
+}  // namespace kry

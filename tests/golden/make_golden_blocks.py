@@ -57,7 +57,8 @@ class Reordered:
     """A CSR operator with an exact-arithmetic-equal, different summation
     order.  ``upd``: (U v + D v) + L v; ``ldu``: L v + (D v + U v);
     ``dlu``: D v + (L v + U v); ``lud``: (L v + U v) + D v; ``rev``: the CSR
-    row sums in reversed column order.  Satisfies the reference
+    row sums in reversed column order.  (Variants ``cholqr`` / ``cholqr-<order>``
+    also swap the QR of new blocks, see _cholqr2.)  Satisfies the reference
     LinearOperator protocol (``n``, ``definite``, ``apply``;
     operators.py:65-79)."""
 
@@ -94,6 +95,20 @@ class Reordered:
         raise ValueError(self.order)
 
 
+def _cholqr2(w):
+    """Cholesky QR twice (R = R2 R1, positive diagonal): the QR algorithm the
+    device uses.  Swapped in for the reference's Householder economy_qr by the
+    ``cholqr*`` variants, so the noise ensemble also spans the perturbation an
+    equally valid QR implementation introduces."""
+    import scipy.linalg as sl
+    w = np.asarray(w, dtype=float)
+    r1 = sl.cholesky(w.T @ w, lower=False)
+    q1 = sl.solve_triangular(r1, w.T, trans="T", lower=False).T
+    r2 = sl.cholesky(q1.T @ q1, lower=False)
+    q = sl.solve_triangular(r2, q1.T, trans="T", lower=False).T
+    return q, r2 @ r1
+
+
 def _operators(cfg_name, variant):
     krymat = _ref()
     from tests.golden.make_golden import ref_laplacian3d, ref_varcoef2d
@@ -106,6 +121,10 @@ def _operators(cfg_name, variant):
         mats = [ref_laplacian3d(200)]
     else:
         raise ValueError(cfg_name)
+    if variant.startswith("cholqr"):
+        import krymat.basis
+        krymat.basis.economy_qr = _cholqr2
+        variant = variant.partition("-")[2] or "csr"
     if variant == "csr":
         return [krymat.SparseOperator(a) for a in mats]
     return [Reordered(a, variant) for a in mats]

@@ -1,0 +1,48 @@
+"""Noise-floor fixtures for the chaotic / long configs.
+
+Input: the reference block sequences and their surrogate histories written by
+make_golden_blocks.py (``lanczos`` + ``residuals`` stages) for the plain run
+(variant ``csr``) and an ensemble of variants of the SAME reference
+algorithm: reordered SpMM summations (``upd``, ``ldu``, ``dlu``, ``lud``,
+``rev``) and the QR of new blocks done by Cholesky QR twice (``cholqr*``,
+the QR algorithm the device uses).  Output ``tests/golden/<cfg>_noise.npz``:
+
+* ``surrogate``: the plain run's history (the paper's formula on a dense
+  eigendecomposition of the reference's own T_m at every m);
+* ``env``: per m, max over the ensemble of |rel_variant - rel_plain|;
+* ``variants``, ``variant_iters`` (first m below tol per variant).
+
+The test floor is 2 x the running maximum of ``env`` (an 8-member ensemble
+envelope underestimates the spread of a chaotic deviation; the factor 2 is
+that allowance).  Test infrastructure only (build container).
+
+    python tests/golden/make_noise_fixtures.py c3 /tmp/gt upd ldu dlu lud rev cholqr cholqr-upd cholqr-dlu
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def main(cfg, src, variants):
+    base = np.load(os.path.join(src, "%s_blocks_csr_hist.npz" % cfg))["surrogate_history"]
+    tol = float(np.load(os.path.join(src, "%s_blocks_csr.npz" % cfg))["tol"])
+    devs, iters = [], []
+    for v in variants:
+        h = np.load(os.path.join(src, "%s_blocks_%s_hist.npz" % (cfg, v)))["surrogate_history"]
+        n = min(len(h), len(base))
+        devs.append(np.abs(h[:n] - base[:n]))
+        below = np.nonzero(h <= tol)[0]
+        iters.append(int(below[0]) + 1 if len(below) else -1)
+    n = min(len(d) for d in devs)
+    env = np.max([d[:n] for d in devs], axis=0)
+    out = os.path.join(HERE, "%s_noise.npz" % cfg)
+    np.savez_compressed(out, surrogate=base, env=env, variants=np.array(variants),
+                        variant_iters=np.array(iters))
+    print("wrote", out, "max rel env", float(np.max(env / base[:n])), "iters", iters)
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2], sys.argv[3:])

@@ -262,21 +262,23 @@ def test_config3_sylvester_parity_with_reference_run():
     assert sol.iterations == int(g["iterations"]) == 681
     assert sol.rank == int(g["rank"])
     # Config 3's history is chaotic once Ritz values converge (m > ~100): the
-    # reference algorithm against ITSELF with a reordered SpMM summation
-    # deviates by up to 2.7% (tests/golden/c3_selfnoise.npz).  Floor-adjusted
-    # criterion: |d| <= 1e-9 rel + 4 x running max of the
-    # reference's self-deviation; early iterations stay at ~1e-14.  The
-    # factor 10: the self-noise run perturbs only the SpMM summation order,
-    # the device reassociates every reduction (Gram blocks, stencil, eigen
-    # updates), so its initial perturbation is a few times larger; in the
-    # chaotic regime the deviation scales linearly with it (measured ratio
-    # device/self-noise 2.6-2.7 at m = 100-110, where both are still tiny).
+    # reference algorithm against ITSELF deviates by up to 3.7% in the late
+    # history.  Calibrated floor (SURVEY.md §8(c) protocol,
+    # tests/golden/c3_noise.npz, make_noise_fixtures.py): an ensemble of 8
+    # runs of the reference's own init_basis + lanczos_step on the same
+    # inputs, with reordered SpMM summations and with Cholesky QR in place of
+    # Householder QR (both exact-arithmetic identities), gives per m the
+    # largest deviation from the plain run; the bar is 1e-9 rel + 2 x its
+    # running maximum (the factor 2 allows for the spread an 8-member
+    # ensemble underestimates).  The first 60 iterations are held to
+    # 1e-9 rel + 2e-16.
     ref = g["history"][:, 2]
-    selfn = np.abs(gold("c3_selfnoise")["history"][:, 2] - ref)
-    envelope = np.maximum.accumulate(selfn)
+    env = gold("c3_noise")["env"][:len(ref)]
+    envelope = np.maximum.accumulate(env)
     h = np.array([r[2] for r in sol.history])
-    assert np.all(np.abs(h - ref) <= 1e-9 * ref + 10.0 * envelope + FLOOR)
-    assert np.all(np.abs(h[:60] - ref[:60]) <= 1e-9 * ref[:60] + FLOOR)
+    dev = np.abs(h - ref)
+    assert np.all(dev <= 1e-9 * ref + 2.0 * envelope + FLOOR), np.max(dev / (1e-9 * ref + envelope))
+    assert np.all(dev[:60] <= 1e-9 * ref[:60] + FLOOR)
     om2 = P.sketch_omega(cfg["b"].shape[0], 2)
     om1 = P.sketch_omega(cfg["a"].shape[0], 2)
     right = sol.z1 @ (sol.z2.T @ om2)
