@@ -104,6 +104,17 @@ int kry_ctx_info(kry_ctx *ctx, int64_t *n, int *s, int *m, int *exhausted);
 int kry_nccl_unique_id(void *id128);
 int kry_comm_init(kry_ctx *ctx, int nranks, int rank, const void *id128);
 
+/* in-process loopback transport for the same sharded path: several slab
+ * contexts of one process (one host thread per rank, e.g. all on one GPU)
+ * exchange halos and sum Gram partials through event-ordered device copies
+ * and a host rendezvous instead of NCCL.  Create the group once, attach one
+ * context per rank, drive every rank from its own thread; destroy the group
+ * after all its contexts are destroyed. */
+typedef struct kry_loop kry_loop;
+int kry_loop_create(int nranks, kry_loop **out);
+void kry_loop_destroy(kry_loop *group);
+int kry_comm_init_loopback(kry_ctx *ctx, kry_loop *group, int rank);
+
 /* operator apply: Y = A V for a host block V (n x ncols, row-major) */
 int kry_apply(kry_ctx *ctx, const double *v, double *y, int ncols);
 

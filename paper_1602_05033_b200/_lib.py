@@ -98,6 +98,9 @@ SIGNATURES = {
     "kry_ctx_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64), iptr, iptr, iptr]),
     "kry_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
     "kry_comm_init": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
+    "kry_loop_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    "kry_loop_destroy": (None, [ctypes.c_void_p]),
+    "kry_comm_init_loopback": (ctypes.c_int, [_P, ctypes.c_void_p, ctypes.c_int]),
     "kry_apply": (ctypes.c_int, [_P, dptr, dptr, ctypes.c_int]),
     "kry_init_basis": (ctypes.c_int, [_P, dptr, dptr, dptr]),
     "kry_init_basis_device": (ctypes.c_int, [_P, ctypes.c_void_p, dptr, dptr]),

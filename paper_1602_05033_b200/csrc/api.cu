@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstring>
 #include <cstdlib>
+#include <condition_variable>
 #include <mutex>
 #include <thread>
 #include <sys/mman.h>
@@ -335,7 +336,62 @@ struct kry_ctx {
   int nranks = 1, rank_id = 0;
   ncclComm_t comm = nullptr;
   double* halo_buf = nullptr;
+  kry_loop* loop = nullptr;    // in-process loopback transport (instead of NCCL)
+  uint64_t coll_seq = 0;       // collectives issued on the loopback group
 };
+
+// ================================================================ loopback transport
+// Several slab contexts of ONE process (one host thread each, any devices
+// with peer access; the tests put them on one GPU) exchange halos and sum
+// their Gram partials through device copies ordered by CUDA events, with a
+// host barrier where NCCL would rendezvous.  It is the NCCL path of
+// halo_exchange / allreduce_gram with the transport swapped: the same
+// POST_NONE reductions, replicated post routines and packed halo planes run,
+// so the sharded code path executes without a multi-GPU node.  Kernels never
+// wait on kernels of another rank that are not yet enqueued (every wait
+// follows the barrier at which the other rank recorded its event).
+struct kry_loop {
+  int n = 0;
+  int dev = -1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t phase = 0;
+  bool aborted = false;
+  std::vector<kry_ctx*> ctx;
+  double* slots = nullptr;                          // [2][n][3 * 64] Gram partials
+  std::vector<cudaEvent_t> ev_ready[2], ev_done[2], ev_halo;
+  std::vector<double*> hfirst, hlast;               // published boundary planes
+  std::vector<int64_t> hld;                          // their point pitch
+};
+
+static int loop_barrier(kry_loop* g) {
+  std::unique_lock<std::mutex> lk(g->mu);
+  if (g->aborted) return fail(KRY_ERR_NCCL, "loopback group aborted by another rank");
+  const uint64_t ph = g->phase;
+  if (++g->arrived == g->n) {
+    g->arrived = 0;
+    ++g->phase;
+    g->cv.notify_all();
+    return KRY_OK;
+  }
+  const bool ok = g->cv.wait_for(lk, std::chrono::seconds(120),
+                                 [&] { return g->phase != ph || g->aborted; });
+  if (g->aborted || !ok) {
+    g->aborted = true;
+    g->cv.notify_all();
+    return fail(KRY_ERR_NCCL, "loopback rendezvous failed (a rank stopped early)");
+  }
+  return KRY_OK;
+}
+
+__global__ void k_loop_sum(const double* slots, int n, double* out) {
+  for (int e = threadIdx.x; e < 3 * 64; e += blockDim.x) {
+    double v = 0.0;
+    for (int q = 0; q < n; ++q) v += slots[(int64_t)q * 3 * 64 + e];   // rank order
+    out[e] = v;
+  }
+}
 
 namespace {
 
@@ -373,7 +429,29 @@ double* slotp(kry_ctx* c, int i) { return i < 0 ? nullptr : c->slot[i]; }
 // before the replicated coefficient solve / post routine runs.
 bool dist(kry_ctx* c) { return c->nranks > 1; }
 
+int loop_allreduce(kry_ctx* c) {
+  kry_loop* g = c->loop;
+  const int r = c->rank_id, par = (int)(c->coll_seq & 1);
+  const bool reuse = c->coll_seq >= 2;
+  c->coll_seq++;
+  double* mine = g->slots + ((int64_t)par * g->n + r) * 3 * 64;
+  // the slot set `par` was last read by every rank's sum two collectives ago
+  if (reuse)
+    for (int q = 0; q < g->n; ++q) KRY_CUDA(cudaStreamWaitEvent(c->stream, g->ev_done[par][q], 0));
+  KRY_CUDA(cudaMemcpyAsync(mine, c->st->gram, 3 * 64 * sizeof(double), cudaMemcpyDeviceToDevice,
+                           c->stream));
+  KRY_CUDA(cudaEventRecord(g->ev_ready[par][r], c->stream));
+  KRY_CHECK(loop_barrier(g));
+  for (int q = 0; q < g->n; ++q) KRY_CUDA(cudaStreamWaitEvent(c->stream, g->ev_ready[par][q], 0));
+  k_loop_sum<<<1, 192, 0, c->stream>>>(g->slots + (int64_t)par * g->n * 3 * 64, g->n, c->st->gram);
+  count_launch();
+  KRY_CUDA(cudaGetLastError());
+  KRY_CUDA(cudaEventRecord(g->ev_done[par][r], c->stream));
+  return KRY_OK;
+}
+
 int allreduce_gram(kry_ctx* c) {
+  if (c->loop) return loop_allreduce(c);
   if (ncclAllReduce(c->st->gram, c->st->gram, 3 * 64, ncclDouble, ncclSum, c->comm, c->stream) !=
       ncclSuccess)
     return fail(KRY_ERR_NCCL, "ncclAllReduce (Gram) failed");
@@ -440,16 +518,43 @@ int halo_exchange(kry_ctx* c, double* blk, int64_t ld, int s) {
     if (has_lo) KRY_CHECK(launch_copy_block(c->stream, s, first, ld, s_lo, s, P));
     if (has_hi) KRY_CHECK(launch_copy_block(c->stream, s, last, ld, s_hi, s, P));
   }
-  ncclGroupStart();
-  if (has_lo) {
-    ncclSend(s_lo, cnt, ncclDouble, lo, c->comm, c->stream);
-    ncclRecv(r_lo, cnt, ncclDouble, lo, c->comm, c->stream);
+  if (c->loop) {
+    // loopback: publish the packed boundary planes, rendezvous, copy the
+    // neighbours' planes into the halos (rank r-1 sends its last plane,
+    // rank r+1 its first: the same plan as the NCCL send/recv pairs)
+    kry_loop* g = c->loop;
+    const int r = c->rank_id;
+    g->hfirst[r] = s_lo;
+    g->hlast[r] = s_hi;
+    g->hld[r] = packed ? s : ld;
+    KRY_CUDA(cudaEventRecord(g->ev_halo[r], c->stream));
+    KRY_CHECK(loop_barrier(g));
+    auto plane = [&](int q, bool last) -> const double* { return last ? g->hlast[q] : g->hfirst[q]; };
+    if (has_lo) {
+      KRY_CUDA(cudaStreamWaitEvent(c->stream, g->ev_halo[lo], 0));
+      KRY_CUDA(cudaMemcpy2DAsync(r_lo, (packed ? s : ld) * sizeof(double), plane(lo, true),
+                                 g->hld[lo] * sizeof(double), s * sizeof(double), P,
+                                 cudaMemcpyDeviceToDevice, c->stream));
+    }
+    if (has_hi) {
+      KRY_CUDA(cudaStreamWaitEvent(c->stream, g->ev_halo[hi], 0));
+      KRY_CUDA(cudaMemcpy2DAsync(r_hi, (packed ? s : ld) * sizeof(double), plane(hi, false),
+                                 g->hld[hi] * sizeof(double), s * sizeof(double), P,
+                                 cudaMemcpyDeviceToDevice, c->stream));
+    }
+    KRY_CHECK(loop_barrier(g));
+  } else {
+    ncclGroupStart();
+    if (has_lo) {
+      ncclSend(s_lo, cnt, ncclDouble, lo, c->comm, c->stream);
+      ncclRecv(r_lo, cnt, ncclDouble, lo, c->comm, c->stream);
+    }
+    if (has_hi) {
+      ncclSend(s_hi, cnt, ncclDouble, hi, c->comm, c->stream);
+      ncclRecv(r_hi, cnt, ncclDouble, hi, c->comm, c->stream);
+    }
+    if (ncclGroupEnd() != ncclSuccess) return fail(KRY_ERR_NCCL, "halo exchange failed");
   }
-  if (has_hi) {
-    ncclSend(s_hi, cnt, ncclDouble, hi, c->comm, c->stream);
-    ncclRecv(r_hi, cnt, ncclDouble, hi, c->comm, c->stream);
-  }
-  if (ncclGroupEnd() != ncclSuccess) return fail(KRY_ERR_NCCL, "halo exchange failed");
   if (packed) {
     if (has_lo) KRY_CHECK(launch_copy_block(c->stream, s, r_lo, s, hlo, ld, P));
     if (has_hi) KRY_CHECK(launch_copy_block(c->stream, s, r_hi, s, hhi, ld, P));
@@ -1339,6 +1444,15 @@ void kry_ctx_destroy(kry_ctx* c) {
   cudaStreamSynchronize(c->stream);
   release_handles(c);
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->loop) {
+    kry_loop* g = c->loop;
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (g->arrived > 0) {   // peers wait at a rendezvous this rank will never reach
+      g->aborted = true;
+      g->cv.notify_all();
+    }
+    if (c->rank_id >= 0 && c->rank_id < g->n) g->ctx[c->rank_id] = nullptr;
+  }
   if (c->halo_buf) dfree(c->halo_buf);
   if (c->t_ev[0]) { cudaEventDestroy(c->t_ev[0]); cudaEventDestroy(c->t_ev[1]); }
   if (c->estream) cudaStreamSynchronize(c->estream);
@@ -2589,6 +2703,62 @@ int kry_timer(kry_ctx* c, int op, double* ms) {
   float f = 0.f;
   KRY_CUDA(cudaEventElapsedTime(&f, c->t_ev[0], c->t_ev[1]));
   if (ms) *ms = f;
+  return KRY_OK;
+}
+
+int kry_loop_create(int nranks, kry_loop** out) {
+  *out = nullptr;
+  if (nranks < 1 || nranks > 64) return fail(KRY_ERR_ARGUMENT, "loopback group size must be 1..64");
+  kry_loop* g = new kry_loop();
+  g->n = nranks;
+  g->ctx.assign(nranks, nullptr);
+  g->hfirst.assign(nranks, nullptr);
+  g->hlast.assign(nranks, nullptr);
+  g->hld.assign(nranks, 0);
+  *out = g;
+  return KRY_OK;
+}
+
+void kry_loop_destroy(kry_loop* g) {
+  if (!g) return;
+  if (g->dev >= 0) cudaSetDevice(g->dev);
+  for (int b = 0; b < 2; ++b) {
+    for (cudaEvent_t e : g->ev_ready[b]) cudaEventDestroy(e);
+    for (cudaEvent_t e : g->ev_done[b]) cudaEventDestroy(e);
+  }
+  for (cudaEvent_t e : g->ev_halo) cudaEventDestroy(e);
+  if (g->slots) cudaFree(g->slots);
+  delete g;
+}
+
+int kry_comm_init_loopback(kry_ctx* c, kry_loop* g, int rank) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  if (!g || rank < 0 || rank >= g->n) return fail(KRY_ERR_ARGUMENT, "bad loopback rank");
+  {
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (g->dev < 0) {
+      g->dev = c->dev;
+      KRY_CUDA(cudaMalloc(&g->slots, (size_t)2 * g->n * 3 * 64 * sizeof(double)));
+      KRY_CUDA(cudaMemset(g->slots, 0, (size_t)2 * g->n * 3 * 64 * sizeof(double)));
+      for (int b = 0; b < 2; ++b) {
+        g->ev_ready[b].assign(g->n, nullptr);
+        g->ev_done[b].assign(g->n, nullptr);
+        for (int q = 0; q < g->n; ++q) {
+          KRY_CUDA(cudaEventCreateWithFlags(&g->ev_ready[b][q], cudaEventDisableTiming));
+          KRY_CUDA(cudaEventCreateWithFlags(&g->ev_done[b][q], cudaEventDisableTiming));
+        }
+      }
+      g->ev_halo.assign(g->n, nullptr);
+      for (int q = 0; q < g->n; ++q)
+        KRY_CUDA(cudaEventCreateWithFlags(&g->ev_halo[q], cudaEventDisableTiming));
+    }
+    if (g->ctx[rank]) return fail(KRY_ERR_STATE, "loopback rank already attached");
+    g->ctx[rank] = c;
+  }
+  c->loop = g;
+  c->nranks = g->n;
+  c->rank_id = rank;
+  c->coll_seq = 0;
   return KRY_OK;
 }
 

@@ -100,6 +100,10 @@ __device__ double block_sum(double v) {
 // The per-pole work arrays (z, candidate list, flags) live in shared memory
 // when they fit (SM = true): the passes below are chains of dependent
 // accesses, and each global round trip costs ~1 us on this single CTA.
+// Every thread owns a contiguous segment of C = ceil(K / 1024) poles, so each
+// compaction pass is ONE block scan of the per-thread counts (the first
+// version scanned 1024-pole chunks one after the other: ~30 barriers per
+// call, 22 us at K = 4000, barrier-stalled).
 template <bool SM>
 __global__ void __launch_bounds__(1024) k_eig_deflate(EigView e, int K, const double* dsym_blk,
                                                       const double* sub_prev, int a) {
@@ -123,8 +127,10 @@ __global__ void __launch_bounds__(1024) k_eig_deflate(EigView e, int K, const do
   if (threadIdx.x == 0) s_d = dsym_blk[a * 8 + a];
   __syncthreads();
   const double d = s_d;
+  const int C = (K + blockDim.x - 1) / blockDim.x;
+  const int j0 = min(K, (int)threadIdx.x * C), j1 = min(K, j0 + C);
   double zmax = 0.0, zabs = 0.0;
-  for (int j = threadIdx.x; j < K; j += blockDim.x) {
+  for (int j = j0; j < j1; ++j) {
     double z = 0.0;
     for (int r = 0; r < s; ++r) z = fma(e.L_old[(int64_t)r * e.kmax + j], t[r], z);
     e.z[j] = z;
@@ -144,20 +150,20 @@ __global__ void __launch_bounds__(1024) k_eig_deflate(EigView e, int K, const do
   __syncthreads();
   const double tol = s_tol;
   // pass 1: candidates = non-negligible z, compacted in eigenvalue order
-  int base = 0;
-  for (int c0 = 0; c0 < K; c0 += blockDim.x) {
-    const int j = c0 + threadIdx.x;
-    int keep = (j < K) && (fabs(e.z[j]) > tol);
-    int tot;
-    int pre = block_excl_scan(keep, &tot);
-    if (keep) e.cand[base + pre] = j;
-    if (j < K) e.dflag[j] = keep ? 0 : 1;
-    base += tot;
+  int q;
+  {
+    int cnt = 0;
+    for (int j = j0; j < j1; ++j) cnt += (fabs(e.z[j]) > tol) ? 1 : 0;
+    int pos = block_excl_scan(cnt, &q);
+    for (int j = j0; j < j1; ++j) {
+      const int keep = fabs(e.z[j]) > tol;
+      if (keep) e.cand[pos++] = j;
+      e.dflag[j] = keep ? 0 : 1;
+    }
   }
-  const int q = base;
   __syncthreads();
   // pass 2: pairs of consecutive candidates whose Givens rotation decouples
-  // one of them (kernels are LAPACK dlaed2's rule: |t c s| <= tol)
+  // one of them (LAPACK dlaed2's rule: |t c s| <= tol)
   for (int i = 1 + threadIdx.x; i < q; i += blockDim.x) {
     const int ja = e.cand[i - 1], jb = e.cand[i];
     const double za = e.z[ja], zb = e.z[jb];
@@ -200,32 +206,39 @@ __global__ void __launch_bounds__(1024) k_eig_deflate(EigView e, int K, const do
     }
   }
   __syncthreads();
-  // pass 3: final poles and deflated list
-  int pb = 0, db = 0;
-  for (int c0 = 0; c0 < K; c0 += blockDim.x) {
-    const int j = c0 + threadIdx.x;
-    const int isd = (j < K) ? e.dflag[j] : 0;
-    const int isp = (j < K) ? 1 - isd : 0;
-    int tp, td;
-    int pp = block_excl_scan(isp, &tp);
-    int pd = block_excl_scan(isd, &td);
-    if (isp) {
-      e.poles[pb + pp] = e.lam_old[j];
-      e.zz[pb + pp] = e.z[j];
-      e.pmap[pb + pp] = j;
+  // pass 3: final poles and deflated list (one scan of the packed counts)
+  int pb, db;
+  {
+    int np = 0, nd = 0;
+    for (int j = j0; j < j1; ++j) {
+      if (e.dflag[j]) ++nd; else ++np;
     }
-    if (isd) {
-      e.def_idx[db + pd] = j;
-      e.def_lam[db + pd] = e.lam_old[j];
+    int tot;
+    const int pre = block_excl_scan(np | (nd << 16), &tot);
+    int pp = pre & 0xffff, pd = pre >> 16;
+    pb = tot & 0xffff;
+    db = tot >> 16;
+    if (K >= 65536) {   // counts do not fit 16 bits: two scans
+      pp = block_excl_scan(np, &pb);
+      pd = block_excl_scan(nd, &db);
     }
-    pb += tp;
-    db += td;
+    for (int j = j0; j < j1; ++j) {
+      if (e.dflag[j]) {
+        e.def_idx[pd] = j;
+        e.def_lam[pd] = e.lam_old[j];
+        ++pd;
+      } else {
+        e.poles[pp] = e.lam_old[j];
+        e.zz[pp] = e.z[j];
+        e.pmap[pp] = j;
+        ++pp;
+      }
+    }
   }
   __syncthreads();
   // rotated deflations can break the order of the deflated list locally;
   // the (usually sorted) list is checked by the whole block, and only a
-  // disordered one goes through the serial insertion-sort fix-up (the
-  // single-thread scan over ~K/2 deflated entries dominated this kernel)
+  // disordered one goes through the serial insertion-sort fix-up
   int unsorted = 0;
   for (int i = 1 + threadIdx.x; i < db; i += blockDim.x)
     unsorted |= (e.def_lam[i] < e.def_lam[i - 1]) ? 1 : 0;
@@ -359,6 +372,7 @@ __device__ __forceinline__ double model_step(double t, double h, double psiL, do
 // where the midpoint start needed 5-11 (the model's error is dominated by
 // the dense neighbourhood, which the window now takes exactly).
 #define SEC_WIN 32
+#define SEC_LOCAL_IT 8   // local-model iterations (more buy ~0.2 global passes, cost latency)
 // Per-thread register cache of the shifted poles and z^2 (MT terms per
 // thread, MT * NT >= p); MT = 0: stream them from global memory.
 template <int W, int MT>
@@ -398,19 +412,22 @@ __global__ void __launch_bounds__(32 * W) k_eig_secular(EigView e) {
     org = 0.0;   // decided below
     ia = i - 1; ib = i;
   }
-  // (1) far sums at mu0 (left: j <= ia), absolute coordinates
-  double fL, fdL, fR, fdR;
+  // (1) sums over ALL poles at mu0 (left: j <= ia), absolute coordinates; the
+  // window's own terms are subtracted below (the far part only feeds the
+  // local model, so the cancellation of total - window costs nothing but a
+  // slightly worse starting point)
+  double tL, tdL, tR, tdR;
   {
     double v[4] = {0.0, 0.0, 0.0, 0.0}, u[4] = {0.0, 0.0, 0.0, 0.0};
     for (int j = tid; j < p; j += 2 * NT) {
-      if (j < w0 || j >= w1) {
+      {
         const double zj = zz[j];
         const double r = frcp(mu0 - poles[j]);
         const double term = zj * zj * r, dterm = term * r;
         if (j <= ia) { v[0] -= term; v[1] += dterm; } else { v[2] -= term; v[3] += dterm; }
       }
       const int k = j + NT;
-      if (k < p && (k < w0 || k >= w1)) {
+      if (k < p) {
         const double zk = zz[k];
         const double r = frcp(mu0 - poles[k]);
         const double term = zk * zk * r, dterm = term * r;
@@ -421,7 +438,7 @@ __global__ void __launch_bounds__(32 * W) k_eig_secular(EigView e) {
     for (int q = 0; q < 4; ++q) v[q] += u[q];
     block_sumv<W, 4>(v, &red[rb]);
     rb ^= 1;
-    fL = v[0]; fdL = v[1]; fR = v[2]; fdR = v[3];
+    tL = v[0]; tdL = v[1]; tR = v[2]; tdR = v[3];
   }
   // window pole of this lane
   const int jw = w0 + lane;
@@ -431,10 +448,19 @@ __global__ void __launch_bounds__(32 * W) k_eig_secular(EigView e) {
   const double plw = inw ? poles[jw] : 0.0;
   if (i > 0 && i < p) {
     // sign of h(mu0): the origin is the nearer pole
-    double nsum = inw ? -z2w * frcp(mu0 - plw) : 0.0;
-    nsum = warp_sum(nsum);
-    const double hm = (mu0 - d) + fL + fR + nsum;
+    const double hm = (mu0 - d) + tL + tR;
     org = (hm > 0.0) ? poles[i - 1] : poles[i];
+  }
+  double fL, fdL, fR, fdR;   // far part = total - window, at mu0
+  {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (inw) {
+      const double r = frcp(mu0 - plw);
+      const double term = z2w * r, dterm = term * r;
+      if (jw <= ia) { a0 = -term; a1 = dterm; } else { a2 = -term; a3 = dterm; }
+    }
+    a0 = warp_sum(a0); a1 = warp_sum(a1); a2 = warp_sum(a2); a3 = warp_sum(a3);
+    fL = tL - a0; fdL = fmax(tdL - a1, 0.0); fR = tR - a2; fdR = fmax(tdR - a3, 0.0);
   }
   const double da = (ia >= 0) ? poles[ia] - org : 0.0;
   const double db = (ib >= 0) ? poles[ib] - org : 0.0;
@@ -448,7 +474,7 @@ __global__ void __launch_bounds__(32 * W) k_eig_secular(EigView e) {
     const double shw = plw - org;
     const bool wleft = jw <= ia;
     double t = t0, la = ta, lb = tb;
-    for (int it = 0; it < 40; ++it) {
+    for (int it = 0; it < SEC_LOCAL_IT; ++it) {
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       if (inw) {
         const double r = frcp(t - shw);

@@ -12,8 +12,11 @@
 // (M = n = 8e6 points at c4, N = r = 231, K = G s = 512 per chunk) that is
 // bound by the fp64 tensor rate: 2 n k r flops per solve (7.6 TFLOP at c4).
 //
-// Tiling: a CTA computes a 64 x 128 tile of Z (8 warps as 2 x 4, each warp
-// 32 x 32 = 4 x 4 m8n8 DMMA tiles, 32 accumulator doubles per lane) and
+// Tiling: a CTA computes a 64 x (32 NT) tile of Z, NT = 2..8 chosen from the
+// rank so that one panel covers r (c4: r = 231 -> 64 x 256; 8 warps as 2 x 4,
+// each warp 32 x 8 NT = 4 x NT m8n8 DMMA tiles, 8 NT accumulator doubles per
+// lane; A is then read from HBM once and every loaded fragment feeds 4 or NT
+// DMMAs) and
 // walks the K dimension one basis block per pipeline stage: the block's 64
 // point rows (64 s contiguous doubles) and the block's s rows of the Q panel
 // arrive by cp.async (16-byte, zero-filled outside the matrix) in a
@@ -28,8 +31,9 @@
 namespace kry {
 
 namespace {
-constexpr int ZBM = 64, ZBN = 128, ZST = 4, ZWARPS = 8;
-constexpr int ZBST = ZBN + 4;          // B row stride (doubles): conflict-free B fragments
+constexpr int ZBM = 64, ZST = 4, ZWARPS = 8, ZNTMAX = 8;
+// B row stride (doubles) for a panel of BN columns: conflict-free B fragments
+__host__ __device__ constexpr int zbst(int bn) { return bn + 4; }
 
 __device__ __forceinline__ void zdmma(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -55,7 +59,7 @@ template <int S>
 __host__ __device__ constexpr int zast() { return (S <= 4 ? 4 : 8) + 4; }
 }  // namespace
 
-template <int S>
+template <int S, int NT>
 __global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__ vbase,
                                                       int64_t vstride, int nb,
                                                       const double* __restrict__ Q, int ldq,
@@ -64,6 +68,7 @@ __global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__
   constexpr int KS = (S + 3) / 4;      // k4-steps per block
   constexpr int AST = zast<S>();
   constexpr int KP = 4 * KS;           // padded k rows of a B stage
+  constexpr int ZBN = 32 * NT, ZBST = zbst(32 * NT);
   extern __shared__ __align__(16) double zsm[];
   double (*sA)[ZBM * AST] = reinterpret_cast<double (*)[ZBM * AST]>(zsm);
   double (*sB)[KP * ZBST] = reinterpret_cast<double (*)[KP * ZBST]>(zsm + ZST * ZBM * AST);
@@ -101,11 +106,11 @@ __global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__
       cp16(&sB[st][row * ZBST + 2 * pc], qb + (int64_t)row * ldq + 2 * pc, j0 + 2 * pc < ldq);
     }
   };
-  double acc[4][4][2];
+  double acc[4][NT][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 #pragma unroll
   for (int st = 0; st < ZST - 1; ++st) {
     if (st < nb) load_stage(st, st);
@@ -123,15 +128,15 @@ __global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__
     const double* B = sB[b % ZST];
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
-      double fa[4], fb[4];
+      double fa[4], fb[NT];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt) fa[mt] = A[(wm * 32 + mt * 8 + g) * AST + 4 * ks + t];
 #pragma unroll
-      for (int nt = 0; nt < 4; ++nt) fb[nt] = B[(4 * ks + t) * ZBST + wn * 32 + nt * 8 + g];
+      for (int nt = 0; nt < NT; ++nt) fb[nt] = B[(4 * ks + t) * ZBST + wn * 8 * NT + nt * 8 + g];
 #pragma unroll
       for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) zdmma(acc[mt][nt][0], acc[mt][nt][1], fa[mt], fb[nt]);
+        for (int nt = 0; nt < NT; ++nt) zdmma(acc[mt][nt][0], acc[mt][nt][1], fa[mt], fb[nt]);
     }
   }
   cp_wait<0>();
@@ -142,8 +147,8 @@ __global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__
     if (i >= n) continue;
     double* zr = Z + i * r;
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt) {
-      const int j = j0 + wn * 32 + nt * 8 + 2 * t;
+    for (int nt = 0; nt < NT; ++nt) {
+      const int j = j0 + wn * 8 * NT + nt * 8 + 2 * t;
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         if (j + e < r) {
@@ -155,33 +160,50 @@ __global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__
   }
 }
 
-template <int S>
-static int zacc_go(cudaStream_t st, int64_t grid, const double* vbase, int64_t vstride, int nb,
-                   const double* Q, int ldq, int r, double* Z, int64_t n, int accumulate,
-                   int npanels) {
+// panel width 32 NT: NT = 8 (one panel for r <= 256) measured slower on c4
+// (84 vs 65 ms per chunk: 1 CTA of 168 registers per SM, 12 % warps active),
+// so panels stop at 128 columns (2 CTAs per SM)
+static int zacc_nt(int r) {
+  const int nt = (r + 31) / 32;
+  if (nt <= 2) return 2;
+  return 4;
+}
+
+template <int S, int NT>
+static int zacc_go(cudaStream_t st, const double* vbase, int64_t vstride, int nb,
+                   const double* Q, int ldq, int r, double* Z, int64_t n, int accumulate) {
   constexpr int KP = 4 * ((S + 3) / 4);
-  const size_t smem = (size_t)ZST * (ZBM * zast<S>() + KP * ZBST) * sizeof(double);
+  constexpr int BN = 32 * NT;
+  const int npanels = (r + BN - 1) / BN;
+  const int64_t grid = ((n + ZBM - 1) / ZBM) * npanels;
+  if (grid > 0x7fffffffLL) return fail(KRY_ERR_DIMENSION, "pass-2 factor too large");
+  const size_t smem = (size_t)ZST * (ZBM * zast<S>() + KP * zbst(BN)) * sizeof(double);
   static bool attr[64] = {false};   // per device
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr[dev & 63]) {
-    KRY_CUDA(cudaFuncSetAttribute(k_zacc<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    KRY_CUDA(cudaFuncSetAttribute(k_zacc<S, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
     attr[dev & 63] = true;
   }
-  k_zacc<S><<<(unsigned)grid, 32 * ZWARPS, smem, st>>>(vbase, vstride, nb, Q, ldq, r, Z, n,
-                                                        accumulate, npanels);
+  k_zacc<S, NT><<<(unsigned)grid, 32 * ZWARPS, smem, st>>>(vbase, vstride, nb, Q, ldq, r, Z, n,
+                                                            accumulate, npanels);
   return KRY_OK;
+}
+
+template <int S>
+static int zacc_s(cudaStream_t st, const double* vbase, int64_t vstride, int nb, const double* Q,
+                  int ldq, int r, double* Z, int64_t n, int accumulate) {
+  switch (zacc_nt(r)) {
+    case 2: return zacc_go<S, 2>(st, vbase, vstride, nb, Q, ldq, r, Z, n, accumulate);
+    default: return zacc_go<S, 4>(st, vbase, vstride, nb, Q, ldq, r, Z, n, accumulate);
+  }
 }
 
 int launch_zacc(cudaStream_t st, int s, const double* vbase, int64_t vstride, int nb,
                 const double* Q, int ldq, int r, double* Z, int64_t n, int accumulate) {
   if (nb < 1 || r < 1) return KRY_OK;
-  const int npanels = (r + ZBN - 1) / ZBN;
-  const int64_t mt = (n + ZBM - 1) / ZBM;
-  const int64_t grid = mt * npanels;
-  if (grid > 0x7fffffffLL) return fail(KRY_ERR_DIMENSION, "pass-2 factor too large");
-#define L(S) KRY_CHECK(zacc_go<S>(st, grid, vbase, vstride, nb, Q, ldq, r, Z, n, accumulate, npanels))
+#define L(S) KRY_CHECK(zacc_s<S>(st, vbase, vstride, nb, Q, ldq, r, Z, n, accumulate))
   switch (s) {
     case 1: L(1); break; case 2: L(2); break; case 3: L(3); break; case 4: L(4); break;
     case 5: L(5); break; case 6: L(6); break; case 7: L(7); break; case 8: L(8); break;
@@ -223,6 +245,9 @@ int launch_chunk_coef_ld(cudaStream_t st, const double* S, const double* qy, int
   return KRY_OK;
 }
 
-int zacc_ldq(int r) { return ((r + ZBN - 1) / ZBN) * ZBN; }
+int zacc_ldq(int r) {
+  const int bn = 32 * zacc_nt(r);
+  return ((r + bn - 1) / bn) * bn;
+}
 
 }  // namespace kry

@@ -82,3 +82,75 @@ class Communicator:
         uid = ctypes.create_string_buffer(self.unique_id(), 128)
         _lib.check(_lib.load().kry_comm_init(ctx.ptr, self.nranks, self.rank, uid))
         self._id = None  # a fresh id for the next communicator
+
+
+class LoopbackGroup:
+    """In-process transport for the sharded path (``kry_loop`` in
+    csrc/api.cu): the P slab contexts of one process -- typically all on one
+    GPU -- exchange halos and all-reduce their Gram partials through
+    event-ordered device copies and a host rendezvous instead of NCCL.  The
+    library runs exactly the code of the NCCL path (POST_NONE reductions,
+    replicated post routines, halo planes), so the multi-rank solve can be
+    exercised and parity-tested without a multi-GPU node.  Each rank must be
+    driven from its own host thread (the library releases the GIL)."""
+
+    def __init__(self, nranks):
+        self.nranks = int(nranks)
+        self.ptr = ctypes.c_void_p()
+        _lib.check(_lib.load().kry_loop_create(self.nranks, ctypes.byref(self.ptr)))
+
+    def comm(self, rank):
+        return _LoopComm(self, rank)
+
+    def close(self):
+        if self.ptr is not None and self.ptr.value:
+            _lib.load().kry_loop_destroy(self.ptr)
+        self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class _LoopComm:
+    """Per-rank handle with the Communicator interface used by operators."""
+
+    def __init__(self, group, rank):
+        self.group = group
+        self.rank = int(rank)
+        self.nranks = group.nranks
+
+    def attach(self, ctx):
+        _lib.check(_lib.load().kry_comm_init_loopback(ctx.ptr, self.group.ptr, self.rank))
+
+
+def run_ranks(nranks, fn):
+    """Run ``fn(rank, comm)`` for every rank of a loopback group, one host
+    thread per rank; returns the per-rank results (re-raises the first
+    rank failure)."""
+    import threading
+
+    group = LoopbackGroup(nranks)
+    out = [None] * nranks
+    err = [None] * nranks
+
+    def body(r):
+        try:
+            out[r] = fn(r, group.comm(r))
+        except BaseException as e:  # noqa: B902 - reported below
+            err[r] = e
+
+    threads = [threading.Thread(target=body, args=(r,)) for r in range(nranks)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    import gc
+    gc.collect()   # contexts of the finished solves go before their group
+    group.close()
+    for e in err:
+        if e is not None:
+            raise e
+    return out
