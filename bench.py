@@ -38,6 +38,25 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def _ncu_bytes(path):
+    d = json.load(open(path))
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    tot = 0.0
+    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        tot += float(d[k]["value"].replace(",", "")) * scale[d[k]["unit"]]
+    return tot
+
+
+def step_traffic(config):
+    """DRAM bytes of one pass-1 step (k_apply_tma + k_combine launches) from
+    the committed ncu --set full captures (profiles/), or None."""
+    try:
+        return (_ncu_bytes(os.path.join(ROOT, "profiles", "r1_k_apply_tma_%s_ncu.json" % config))
+                + _ncu_bytes(os.path.join(ROOT, "profiles", "r1_k_combine_%s_ncu.json" % config)))
+    except Exception:
+        return None
+
+
 def captured_traffic(config):
     """DRAM bytes per k_combine launch from the committed ncu --set full
     capture of this config (profiles/r1_k_combine_<config>_ncu.json), or None."""
@@ -161,71 +180,128 @@ def timed_solve_device(kb, lib, ctx, c_dev_ptr, opts, s, prof=True):
         t3 = time.perf_counter()
     return dict(ms=ms.value, iterations=its.value, rank=rank.value, rel=rel.value,
                 init_s=t_init, pass1_s=t1 - t0, finalize_s=t2 - t1, pass2_s=t3 - t2,
-                check_s=float(hist[nh.value - 1, 4]) if nh.value else 0.0)
+                check_s=float(hist[nh.value - 1, 4]) if nh.value else 0.0,
+                basis_s=float(hist[nh.value - 1, 3]) if nh.value else 0.0,
+                basis_its=int(hist[nh.value - 1, 0]) if nh.value else 0)
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 def cpu_sample(cfg_name, threads):
-    """Bounded sample of the reference algorithm (oracle port) on the host:
-    block-Lanczos steps of the numpy restatement on the full-size input,
-    plus one cTri check at the reference's own T_m (golden) truncated to a
-    representative depth.  Returns iterations/s and a description."""
-    os.environ.setdefault("OMP_NUM_THREADS", str(threads))
+    """Bounded sample of the reference algorithm (the oracle port, a numpy
+    restatement of the reference pinned to its goldens) on the host with
+    ``threads`` BLAS threads, extrapolated to the full solve:
+
+    * pass-1 steps: block-Lanczos steps (SpMM + MGS twice + Householder QR,
+      basis.py:223-252) on the full-size input;
+    * pass-2 steps: the same regeneration + the factor update
+      ``z += v @ qy[block]`` of two_pass_recover (solvers.py:158-169) with the
+      reference's rank (the golden), which is what makes the reference's
+      recovery ~2x its basis time (c4 golden: 4,827 s vs 2,480 s);
+    * one cTri check (band reduction + tridiagonal eig + contraction,
+      residual.py:40-59) on the reference's own T_m at depth m_chk, scaled
+      ~m^2 to every iteration (SURVEY.md §6);
+    * the finalisation (two dense eighs of order k = s m, solvers.py:254-264).
+    Returns (iterations/s, description, seconds spent)."""
+    from threadpoolctl import threadpool_limits
     from oracle import krymat_oracle as ko
     from oracle import problems as P
 
+    spent = time.perf_counter()
     cfg = P.build_config(cfg_name)
     op = ko.SparseOperator(cfg["a"])
     c = cfg.get("c", cfg.get("c1"))
-    bs = ko.Basis(op, c)
-    nsteps = 2 if cfg_name in ("c4", "c5") else 10
-    t0 = time.perf_counter()
-    for _ in range(nsteps):
-        bs.step()
-    t_step = (time.perf_counter() - t0) / nsteps
-    # check cost at depth m_chk on the reference's own projection (golden)
     gpath = os.path.join(ROOT, "tests", "golden", cfg_name + ".npz")
-    t_chk, m_chk = None, None
-    iters_ref = None
-    if os.path.exists(gpath):
-        g = np.load(gpath)
-        s = g["t_diag"].shape[1]
-        m_all = g["t_diag"].shape[0]
-        iters_ref = int(g["iterations"]) if "iterations" in g else m_all
-        m_chk = max(1, min(m_all, 64 if s >= 4 else 200))
-        t = ko.BlockTri(s, [0.5 * (d + d.T) for d in g["t_diag"][:m_chk]],
-                        list(g["t_off"][:m_chk - 1]))
-        t1 = time.perf_counter()
-        ko.ctri_lyapunov(t, g["gamma"], g["t_off"][m_chk - 1] if m_chk < m_all else g["tau"])
-        t_chk = time.perf_counter() - t1
+    g = np.load(gpath) if os.path.exists(gpath) else None
+    with threadpool_limits(threads):
+        bs = ko.Basis(op, c)
+        nsteps = 2 if cfg_name in ("c4", "c5") else 10
+        t0 = time.perf_counter()
+        for _ in range(nsteps):
+            bs.step()
+        t_step = (time.perf_counter() - t0) / nsteps
+        nsteps2 = 1 if cfg_name in ("c4", "c5") else nsteps
+        s = c.shape[1]
+        rank = int(g["rank"]) if g is not None and "rank" in g else 8 * s
+        qy = np.random.default_rng(0).standard_normal(((nsteps2 + 1) * s, rank))
+        z = np.zeros((op.n, rank))
+        v = bs.blocks[-1]
+        t0 = time.perf_counter()
+        for i in range(nsteps2):
+            w, _, _ = ko.mgs_twice(op.apply(v), None, v)
+            vn, _ = ko.economy_qr(w)
+            z += vn @ qy[i * s:(i + 1) * s]
+            v = vn
+        t_step2 = (time.perf_counter() - t0) / nsteps2
+        del z
+        t_chk = m_chk = iters_ref = None
+        t_fin = 0.0
+        if g is not None:
+            m_all = g["t_diag"].shape[0]
+            iters_ref = int(g["iterations"]) if "iterations" in g else m_all
+            m_chk = max(1, min(m_all, 64 if s >= 4 else 200))
+            t = ko.BlockTri(s, [0.5 * (d + d.T) for d in g["t_diag"][:m_chk]],
+                            list(g["t_off"][:m_chk - 1]))
+            t1 = time.perf_counter()
+            ko.ctri_lyapunov(t, g["gamma"], g["t_off"][m_chk - 1] if m_chk < m_all else g["tau"])
+            t_chk = time.perf_counter() - t1
+            k = s * iters_ref
+            a = np.random.default_rng(1).standard_normal((k, k))
+            a = a + a.T
+            t1 = time.perf_counter()
+            np.linalg.eigh(a)
+            t_fin = 2.0 * (time.perf_counter() - t1)
+    spent = time.perf_counter() - spent
     if t_chk is not None and iters_ref:
-        # check cost grows ~ m^2 (SURVEY §6); pass 2 repeats the steps
         m = iters_ref
         checks = sum(t_chk * (j / m_chk) ** 2 for j in range(1, m + 1))
-        total = 2 * m * t_step + checks
+        total = m * t_step + checks + t_fin + m * t_step2
         value = m / total
-        desc = ("%d block-Lanczos steps of the numpy port on the full %s input (%.2f s/step) "
-                "+ one cTri check at m=%d on the reference's own T_m (%.2f s); "
-                "extrapolated to the reference's %d iterations with check cost ~ m^2 and "
-                "pass 2 = pass-1 steps: time-to-tol %.0f s" %
-                (nsteps, cfg_name, t_step, m_chk, t_chk, m, total))
+        desc = ("%d threads (%s): %d pass-1 block-Lanczos steps of the numpy port on the full %s "
+                "input (%.2f s/step), %d pass-2 steps incl. the rank-%d factor update (%.2f "
+                "s/step), one cTri check at m=%d on the reference's own T_m (%.2f s), two "
+                "eighs of order %d (%.1f s); extrapolated to the reference's %d iterations "
+                "(checks ~ m^2): time-to-tol %.0f s" %
+                (threads, cpu_model(), nsteps, cfg_name, t_step, nsteps2, rank, t_step2, m_chk,
+                 t_chk, s * m, t_fin, m, total))
     else:
-        value = 1.0 / t_step
-        desc = "%d block-Lanczos steps (no checks) of the numpy port" % nsteps
-    return value, desc, nsteps * t_step + (t_chk or 0.0)
+        value = 1.0 / (t_step + t_step2)
+        desc = "%d threads: %d block-Lanczos steps (no checks) of the numpy port" % (threads,
+                                                                                    nsteps)
+    return value, desc, spent
+
+
+def cpu_legs(cfg_name):
+    """The reference on all host threads and on one (more
+    threads can be slower); the faster leg is the baseline."""
+    allt = os.cpu_count() or 1
+    legs = []
+    for th in sorted({allt, 1}, reverse=True):
+        v, desc, spent = cpu_sample(cfg_name, th)
+        legs.append({"threads": th, "value": v, "sample": desc, "seconds": round(spent, 1)})
+    best = max(legs, key=lambda x: x["value"])
+    return best, legs
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    threads = os.cpu_count() or 1
-    vals = []
-    desc = ""
-    t_all = 0.0
+    vals, legs_all = [], []
+    best = None
     for _ in range(max(1, args.steps)):
-        v, desc, t = cpu_sample(args.config, threads)
-        vals.append(v)
-        t_all += t
+        best, legs = cpu_legs(args.config)
+        vals.append(best["value"])
+        legs_all = legs
     value = float(np.median(vals))
     line = {
         "impl": "reference",
@@ -242,8 +318,9 @@ def run_reference(args):
         "dtype": "f64",
         "data": "synthetic (seeded, SURVEY.md §8(d))",
         "config": {"workload": args.config, "desc": CONFIG_DOC[args.config]},
-        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": threads, "kind": "port",
-                         "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": best["threads"],
+                         "kind": "port", "sample": best["sample"], "cpu_model": cpu_model(),
+                         "legs": legs_all},
         "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -310,9 +387,18 @@ def main():
     launches = _lib.launch_count()
     comb_ms, comb_n = ctypes.c_double(), ctypes.c_int()
     lib.kry_profile_read(ctx.ptr, ctypes.byref(comb_ms), ctypes.byref(comb_n), None, None)
+    zacc_ms, zacc_fl, zacc_n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+    lib.kry_profile_zacc(ctx.ptr, ctypes.byref(zacc_ms), ctypes.byref(zacc_fl),
+                         ctypes.byref(zacc_n))
     lib.kry_profile_enable(ctx.ptr, 0)
     torch.cuda.synchronize()
     clk = clocks.stop()
+    # the residual contraction on the final eigen data (k = s m), and the
+    # device's measured fp64 peaks (untimed, after the timed region)
+    chk_ms, chk_k = ctypes.c_double(), ctypes.c_int()
+    chk_ok = lib.kry_profile_check(ctx.ptr, 20, ctypes.byref(chk_ms), ctypes.byref(chk_k)) == 0
+    dfma, dmma = ctypes.c_double(), ctypes.c_double()
+    lib.kry_fp64_peak(local, ctypes.byref(dfma), ctypes.byref(dmma))
     ms_total = sum(r["ms"] for r in runs)
     its_total = sum(r["iterations"] for r in runs)
     if dist:
@@ -322,17 +408,44 @@ def main():
     its_total_all = its_total   # sharded: all ranks advance the same solve
     value = its_total_all / (ms_total / 1000.0)
     ctx.close()
-    # roofline of the recurrence kernel (k_combine): reads V_{m-1}, V_m and
-    # (single GPU, even s: the apply kernel's hand-off) A V_m, writes V_{m+1}:
-    # 4 (3 without the hand-off) * n * s * 8 bytes per launch.  The step as a
-    # whole moves 6 n s doubles (apply: read V_m, write A V_m); the
-    # three-term minimum is 3 n s.
+    # Roofline: the unit is one pass-1 block-Lanczos step,
+    # B_iter = 24 n s bytes (read V_{m-1}, V_m, write V_{m+1}: the three-term
+    # minimum; constant stencil, no operator bytes); achieved = B_iter / the
+    # device time per step on the Lanczos stream (CUDA events, pass 1,
+    # excluding the check stream).  The step kernels themselves move 48 n s
+    # (k_apply_tma: read V_m, write A V_m; k_combine: read V_{m-1}, V_m,
+    # A V_m, write V_{m+1}), so this is at most 0.5 of the copy peak by
+    # construction; the kernel-level DRAM fractions are listed beside it.
     hbm, hbm_kind = peaks()
+    r_last = runs[-1]
+    b_iter = 24 * n * s
+    t_step = r_last["basis_s"] / max(r_last["basis_its"], 1)
+    achieved = b_iter / t_step / 1e9 if t_step > 0 else 0.0
     comb_avg_ms = comb_ms.value / max(comb_n.value, 1)
     handoff = (world == 1 and s % 2 == 0 and os.environ.get("KRY_NO_AV_HANDOFF") != "1"
                and os.environ.get("KRY_FUSED_STEP") != "1")
     bytes_launch = (4 if handoff else 3) * n * s * 8
-    achieved = bytes_launch / (comb_avg_ms / 1000.0) / 1e9 if comb_avg_ms > 0 else 0.0
+    comb_gbs = bytes_launch / (comb_avg_ms / 1000.0) / 1e9 if comb_avg_ms > 0 else 0.0
+    kernels = [{"kernel": "k_combine (3-term recurrence + Gram on DMMA)", "bound": "hbm",
+                "bytes_per_launch": bytes_launch, "avg_launch_ms": comb_avg_ms,
+                "achieved": comb_gbs, "unit": "GB/s", "frac": comb_gbs / hbm if hbm else None,
+                "traffic": captured_traffic(args.config), "launches": comb_n.value}]
+    fp64_peak = dmma.value if dmma.value > 0 else None
+    if zacc_n.value:
+        tf = zacc_fl.value / (zacc_ms.value / 1000.0) / 1e12
+        kernels.append({"kernel": "k_zacc (pass-2 factor accumulation Z += V Q, DMMA)",
+                        "bound": "tensor (fp64 DMMA)", "flops_total": zacc_fl.value,
+                        "ms_total": zacc_ms.value, "launches": zacc_n.value, "achieved": tf,
+                        "unit": "TFLOP/s", "peak": fp64_peak,
+                        "frac": tf / fp64_peak if fp64_peak else None})
+    if chk_ok and chk_ms.value > 0:
+        k = chk_k.value
+        fl = 4.0 * s * k * k + k * k
+        tf = fl / (chk_ms.value / 1000.0) / 1e12
+        kernels.append({"kernel": "cheap residual: k_uw + k_cauchy_mma (4 s k^2 + k^2 flop, "
+                        "divisions counted once)", "bound": "fp64", "k": k,
+                        "avg_ms": chk_ms.value, "achieved": tf, "unit": "TFLOP/s",
+                        "peak": fp64_peak, "frac": tf / fp64_peak if fp64_peak else None})
 
     e2e = None
     if not args.no_e2e:
@@ -374,9 +487,10 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            v, desc, _ = cpu_sample(args.config, os.cpu_count() or 1)
-            cpu = {"value": v, "unit": "iters/s", "cores": os.cpu_count() or 1, "kind": "port",
-                   "sample": desc}
+            best, legs = cpu_legs(args.config)
+            cpu = {"value": best["value"], "unit": "iters/s", "cores": best["threads"],
+                   "kind": "port", "sample": best["sample"], "cpu_model": cpu_model(),
+                   "legs": legs}
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unit": "iters/s", "cores": 0, "kind": "port",
                    "sample": "failed: %s" % exc}
@@ -405,17 +519,19 @@ def main():
         "phases_s": {"init": r0["init_s"], "pass1": r0["pass1_s"],
                      "checks_in_pass1": r0["check_s"],
                      "finalize": r0["finalize_s"], "pass2": r0["pass2_s"]},
-        "roofline": {"bound": "hbm", "kernel": "k_combine (three-term recurrence on DMMA + "
-                     "Gram, A V_m handed off by k_apply_gram)" if handoff else
-                     "k_combine (fused stencil SpMM + 3-term recurrence + Gram)",
-                     "achieved": achieved, "peak": hbm,
-                     "peak_kind": hbm_kind, "unit": "GB/s",
+        "roofline": {"bound": "hbm", "kernel": "pass-1 block-Lanczos step (k_apply_tma + "
+                     "k_combine)", "unit_bytes": b_iter,
+                     "definition": "SURVEY 8(d): B_iter = 24 n s bytes per step / device time "
+                     "per step on the Lanczos stream (CUDA events)",
+                     "achieved": achieved, "peak": hbm, "peak_kind": hbm_kind, "unit": "GB/s",
                      "frac": achieved / hbm if hbm else None,
-                     "traffic": captured_traffic(args.config),
-                     "bytes_per_launch": bytes_launch, "avg_launch_ms": comb_avg_ms,
-                     "step_bytes": 6 * n * s * 8 if handoff else 4 * n * s * 8,
-                     "step_min_bytes": 3 * n * s * 8,
-                     "launches": comb_n.value},
+                     "traffic": step_traffic(args.config),
+                     "step_ms": 1000.0 * t_step,
+                     "pass1_loop_frac": (b_iter * r_last["iterations"] / r_last["pass1_s"] / 1e9
+                                         / hbm) if r_last["pass1_s"] > 0 else None,
+                     "fp64_peak_tflops": {"dmma": dmma.value, "dfma": dfma.value,
+                                          "how": "kry_fp64_peak, one-wave microbenchmark"},
+                     "kernels": kernels},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

@@ -213,6 +213,14 @@ int kry_true_lyap_residual(kry_ctx *ctx, const double *z, int t,
 int kry_profile_enable(kry_ctx *ctx, int enable);
 int kry_profile_read(kry_ctx *ctx, double *combine_ms_total, int *combine_launches,
                      double *apply_ms_total, int *apply_launches);
+/* measurement: fp64 DFMA / DMMA peak of the device (TFLOP/s, one-wave
+ * microbenchmark), and the average time of the cheap residual (u, w and the
+ * Cauchy contraction) on the context's current eigen data (k = its order) */
+int kry_fp64_peak(int device, double *dfma_tflops, double *dmma_tflops);
+int kry_profile_check(kry_ctx *ctx, int reps, double *ms, int *k);
+/* pass-2 factor-accumulation launches recorded while profiling is enabled:
+ * total device ms, total flops (2 n K r per chunk), launch count */
+int kry_profile_zacc(kry_ctx *ctx, double *ms_total, double *flops_total, int *launches);
 /* CUDA-event timer on the context's stream: op 0 records the start, op 1
  * records the stop, synchronises and returns the elapsed milliseconds */
 int kry_timer(kry_ctx *ctx, int op, double *ms);

@@ -98,6 +98,13 @@ SIGNATURES = {
     "kry_ctx_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64), iptr, iptr, iptr]),
     "kry_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
     "kry_comm_init": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
+    "kry_fp64_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                     ctypes.POINTER(ctypes.c_double)]),
+    "kry_profile_check": (ctypes.c_int, [_P, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                         ctypes.POINTER(ctypes.c_int)]),
+    "kry_profile_zacc": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_double),
+                                        ctypes.POINTER(ctypes.c_double),
+                                        ctypes.POINTER(ctypes.c_int)]),
     "kry_loop_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
     "kry_loop_destroy": (None, [ctypes.c_void_p]),
     "kry_comm_init_loopback": (ctypes.c_int, [_P, ctypes.c_void_p, ctypes.c_int]),

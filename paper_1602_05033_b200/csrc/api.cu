@@ -295,6 +295,8 @@ struct kry_ctx {
   // profiling
   bool prof = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_comb;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_zacc;   // pass-2 accumulations
+  double zacc_flops = 0.0;
   double prof_comb_ms = 0.0;
   int prof_comb_n = 0;
   cudaEvent_t t_ev[2] = {nullptr, nullptr};
@@ -1352,7 +1354,7 @@ static int ctx_create_body(kry_ctx* c, int device, const kry_operator_desc* od, 
   KRY_CHECK(dalloc(&c->C, (size_t)nloc * s));
   KRY_CHECK(dalloc(&c->st, 1));
   KRY_CUDA(cudaMallocHost(&c->st_h, sizeof(DevState)));
-  KRY_CUDA(cudaMallocHost(&c->hres, 16 * sizeof(double)));
+  KRY_CUDA(cudaMallocHost(&c->hres, 32 * sizeof(double)));
   const int cap = max_m + 3;
   KRY_CHECK(dalloc(&c->tmem, (size_t)6 * cap * 64));
   KRY_CUDA(cudaMemset(c->tmem, 0, (size_t)6 * cap * 64 * sizeof(double)));
@@ -1441,6 +1443,7 @@ void kry_ctx_destroy(kry_ctx* c) {
   if (c->Z) dfree(c->Z);
   c->eig.release();
   for (auto& e : c->ev_comb) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  for (auto& e : c->ev_zacc) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   cudaStreamSynchronize(c->stream);
   release_handles(c);
   if (c->comm) ncclCommDestroy(c->comm);
@@ -1831,6 +1834,39 @@ int kry_solve_lyap_pass1(kry_ctx* c, double tol, int max_m, int check_period, do
   return fail(KRY_ERR_CONVERGENCE, *reason == 2 ? "invariant" : "max_m");
 }
 
+// Sylvester check of iteration j queued on a->estream after the eigen
+// appends of both sides (b's on b->estream, joined by ev_b); result into the
+// pinned ring slot `slot` of a (sum |M|^2 of both contractions, min |den|).
+static int launch_sylv_check(kry_ctx* a, kry_ctx* b, const double* tau_a, const double* tau_b,
+                             int slot) {
+  cudaStream_t st = a->estream;
+  KRY_CHECK(a->eig.compute_uw(st, a->gamma_d, tau_a));
+  KRY_CHECK(b->eig.compute_uw(st, b->gamma_d, tau_b));
+  const int kA = a->eig.K, kB = b->eig.K;
+  KRY_CHECK(a->eig.ensure_cauchy(std::max(kA, kB), 0));
+  KRY_CHECK(a->eig.cauchy(st, kB, b->eig.lam_cur(), b->eig.u, kA, a->eig.lam_cur(), a->eig.u,
+                          a->eig.w, a->eig.res));
+  KRY_CHECK(a->eig.cauchy(st, kA, a->eig.lam_cur(), a->eig.u, kB, b->eig.lam_cur(), b->eig.u,
+                          b->eig.w, a->eig.res + 4));
+  k_scale_of<<<1, 32, 0, st>>>(a->eig.lam_cur(), kA, b->eig.lam_cur(), kB, a->eig.res + 2);
+  count_launch();
+  KRY_CUDA(cudaMemcpyAsync(a->hres + 8 * slot, a->eig.res, 6 * sizeof(double),
+                           cudaMemcpyDeviceToHost, st));
+  KRY_CUDA(cudaEventRecord(a->ev_res[slot], st));
+  return KRY_OK;
+}
+
+static int collect_sylv(kry_ctx* a, int slot, double rhs_norm, double* rel) {
+  KRY_CUDA(cudaEventSynchronize(a->ev_res[slot]));
+  const double* h = a->hres + 8 * slot;
+  if (fmin(h[1], h[5]) < 1e-14 * h[2])
+    return fail(KRY_ERR_INDEFINITE,
+                "eigenvalue-sum denominator is numerically singular; coefficient matrices must "
+                "be definite (of one sign)");
+  *rel = sqrt(fmax(h[0] + h[4], 0.0)) / rhs_norm;
+  return KRY_OK;
+}
+
 int kry_solve_sylv_pass1(kry_ctx* a, kry_ctx* b, double tol, int max_m, int check_period,
                          double* history, int* n_history, int* iterations, double* final_rel,
                          int* reason) {
@@ -1838,46 +1874,179 @@ int kry_solve_sylv_pass1(kry_ctx* a, kry_ctx* b, double tol, int max_m, int chec
   if (!a->initialized || !b->initialized) return fail(KRY_ERR_STATE, "init_basis has not been called");
   if (max_m > a->max_m || max_m > b->max_m)
     return fail(KRY_ERR_ARGUMENT, "max_m exceeds the context capacity");
+  // Pipelined like the Lyapunov loop: both sides' Lanczos steps run on their
+  // main streams (step j+1 is queued before the host collects the check of
+  // j), the eigen appends on the sides' second streams, the two-sided check
+  // on a's second stream once b's appends are in (ev_t of b) -- b's next
+  // appends wait for that check to have read b's eigen data.  Phase times
+  // are CUDA-event device times (basis: both recurrences; residual: the
+  // appends + check window on a's second stream).
   const double rhs_norm = sqrt(a->beta2) * sqrt(b->beta2);
-  double t_basis = 0.0, t_res = 0.0;
-  int nh = 0;
+  KRY_CHECK(ensure_timing_events(a, max_m + 2));
+  KRY_CHECK(ensure_timing_events(b, max_m + 2));
+  KRY_CUDA(cudaEventRecord(a->ev_step[0], a->stream));
+  KRY_CUDA(cudaEventRecord(b->ev_step[0], b->stream));
+  cudaEvent_t ev_chk = nullptr;   // a's check finished reading b's eigen data
+  KRY_CUDA(cudaEventCreateWithFlags(&ev_chk, cudaEventDisableTiming));
+  std::vector<int> row_it, a_step(max_m + 2, 0), b_step(max_m + 2, 0);
+  std::vector<int> ma_at(max_m + 2, 0), mb_at(max_m + 2, 0);
+  int nh = 0, last_it = 0;
   *iterations = 0;
   *reason = 1;
+  *n_history = 0;
   double rel = INFINITY;
-  for (int it = 1; it <= max_m; ++it) {
-    double t0 = now_s();
-    int ex = 0;
-    if (!a->exhausted) KRY_CHECK(step_pass1(a, 1, &ex));
-    if (!b->exhausted) KRY_CHECK(step_pass1(b, 1, &ex));
-    KRY_CUDA(cudaStreamSynchronize(a->stream));
-    KRY_CUDA(cudaStreamSynchronize(b->stream));
-    t_basis += now_s() - t0;
+  int pending = -1, pending_slot = 0;
+  auto record = [&](int it, double r) {
+    double* row = history + (size_t)nh * 5;
+    row[0] = it; row[1] = (double)it * a->s; row[2] = r; row[3] = 0.0; row[4] = 0.0;
+    row_it.push_back(it);
+    ++nh;
+    *n_history = nh;
+    *final_rel = r;
+  };
+  auto converge = [&](int it) {
+    *iterations = it;
+    *reason = 0;
+    a->m_final = ma_at[it];
+    b->m_final = mb_at[it];
+  };
+  auto rescue = [&](int rc_step) -> int {
+    if (pending <= 0) return rc_step;
+    const std::string keep = g_last_error;
+    double r2 = INFINITY;
+    if (collect_sylv(a, pending_slot, rhs_norm, &r2) != KRY_OK) { g_last_error = keep; return rc_step; }
+    record(pending, r2);
+    const int p = pending;
+    pending = -1;
+    if (r2 <= tol) {
+      converge(p);
+      a->pending_launch = b->pending_launch = false;
+      reset_state_status(a);
+      reset_state_status(b);
+      return KRY_OK;
+    }
+    g_last_error = keep;
+    return rc_step;
+  };
+  int rc = KRY_OK;
+  bool done = false;
+  for (int it = 1; it <= max_m && !done; ++it) {
+    int exa = 0, exb = 0;
+    const bool sa = !a->exhausted, sb = !b->exhausted;
+    if (sa) rc = step_core(a, 1, &exa);
+    if (rc == KRY_OK && sb) rc = step_core(b, 1, &exb);
+    if (rc) { rc = rescue(rc); done = true; break; }
+    a_step[it] = sa;
+    b_step[it] = sb;
+    ma_at[it] = a->m;
+    mb_at[it] = b->m;
+    if (sa) {
+      KRY_CUDA(cudaEventRecord(a->ev_t, a->stream));
+      KRY_CUDA(cudaEventRecord(a->ev_step[it], a->stream));
+    }
+    if (sb) {
+      KRY_CUDA(cudaEventRecord(b->ev_t, b->stream));
+      KRY_CUDA(cudaEventRecord(b->ev_step[it], b->stream));
+    }
+    if (it < max_m) {
+      if (sa && !exa) rc = step_prelaunch(a);
+      if (rc == KRY_OK && sb && !exb) rc = step_prelaunch(b);
+      if (rc) { rc = rescue(rc); done = true; break; }
+    }
     const bool both = a->exhausted && b->exhausted;
-    if (it % check_period == 0 || both) {
-      t0 = now_s();
-      double res = 0.0;
-      KRY_CHECK(check_sylv(a, b, rhs_norm, &res, &rel));
-      t_res += now_s() - t0;
-      double* row = history + (size_t)nh * 5;
-      row[0] = it; row[1] = (double)it * a->s; row[2] = rel; row[3] = t_basis; row[4] = t_res;
-      ++nh;
-      *n_history = nh;
-      *final_rel = rel;
+    const bool chk = (it % check_period == 0) || both;
+    const int slot = it & 1;
+    // eigen appends of block row `it` of each side that stepped
+    KRY_CUDA(cudaEventRecord(a->ev_pool[it].first, a->estream));
+    if (sa) {
+      KRY_CUDA(cudaStreamWaitEvent(a->estream, a->ev_t, 0));
+      const int j = a->m;
+      rc = a->eig.append_block(a->estream, a->T.dsym + (int64_t)(j - 1) * 64,
+                               j >= 2 ? a->T.sub + (int64_t)(j - 2) * 64 : nullptr);
+      if (rc) break;
+    }
+    if (sb) {
+      KRY_CUDA(cudaStreamWaitEvent(b->estream, b->ev_t, 0));
+      KRY_CUDA(cudaStreamWaitEvent(b->estream, ev_chk, 0));
+      const int j = b->m;
+      rc = b->eig.append_block(b->estream, b->T.dsym + (int64_t)(j - 1) * 64,
+                               j >= 2 ? b->T.sub + (int64_t)(j - 2) * 64 : nullptr);
+      if (rc) break;
+      KRY_CUDA(cudaEventRecord(b->ev_t, b->estream));
+      KRY_CUDA(cudaStreamWaitEvent(a->estream, b->ev_t, 0));
+    }
+    if (chk) {
+      rc = launch_sylv_check(a, b, tau_ptr(a), tau_ptr(b), slot);
+      if (rc) break;
+      KRY_CUDA(cudaEventRecord(ev_chk, a->estream));
+    }
+    KRY_CUDA(cudaEventRecord(a->ev_pool[it].second, a->estream));
+    last_it = it;
+    if (pending > 0) {   // the previous iteration's check
+      rc = collect_sylv(a, pending_slot, rhs_norm, &rel);
+      if (rc) break;
+      record(pending, rel);
       if (rel <= tol) {
-        *iterations = it;
-        *reason = 0;
-        a->m_final = a->m;
-        b->m_final = b->m;
-        return KRY_OK;
+        converge(pending);
+        done = true;
+        break;
       }
-      if (both) {
-        *reason = 2;
-        return fail(KRY_ERR_CONVERGENCE, "invariant");
+      pending = -1;
+    }
+    if (chk) {
+      pending = it;
+      pending_slot = slot;
+    }
+    if (both) {   // both spaces invariant: this check decides
+      rc = collect_sylv(a, slot, rhs_norm, &rel);
+      if (rc) break;
+      record(it, rel);
+      pending = -1;
+      if (rel <= tol) converge(it);
+      else *reason = 2;
+      done = true;
+    }
+  }
+  if (rc == KRY_OK && !done && pending > 0) {
+    rc = collect_sylv(a, pending_slot, rhs_norm, &rel);
+    if (rc == KRY_OK) {
+      record(pending, rel);
+      if (rel <= tol) converge(pending);
+    }
+  }
+  for (kry_ctx* c : {a, b}) {
+    if (c->pending_launch) {   // the speculative step past the decision
+      const std::string keep = g_last_error;
+      int ex = 0;
+      if (step_core(c, 1, &ex) != KRY_OK) {
+        c->pending_launch = false;
+        g_last_error = keep;
+        reset_state_status(c);
       }
     }
   }
-  *n_history = nh;
-  return fail(KRY_ERR_CONVERGENCE, "max_m");
+  cudaStreamSynchronize(a->estream);
+  cudaStreamSynchronize(b->estream);
+  cudaStreamSynchronize(a->stream);
+  cudaStreamSynchronize(b->stream);
+  {
+    double tb = 0.0, tr = 0.0;
+    int i = 1;
+    for (int r = 0; r < nh; ++r) {
+      const int upto = std::min(row_it[r], last_it);
+      for (; i <= upto; ++i) {
+        if (a_step[i]) tb += ev_seconds(a->ev_step[i - 1], a->ev_step[i]);
+        if (b_step[i]) tb += ev_seconds(b->ev_step[i - 1], b->ev_step[i]);
+        tr += ev_seconds(a->ev_pool[i].first, a->ev_pool[i].second);
+      }
+      history[(size_t)r * 5 + 3] = tb;
+      history[(size_t)r * 5 + 4] = tr;
+    }
+  }
+  cudaEventDestroy(ev_chk);
+  if (rc != KRY_OK) return rc;
+  if (*reason == 0) return KRY_OK;
+  return fail(KRY_ERR_CONVERGENCE, *reason == 2 ? "invariant" : "max_m");
 }
 
 int kry_finalize_lyap(kry_ctx* c, double eps, int* rank, double* discarded) {
@@ -2365,8 +2534,19 @@ int kry_recover(kry_ctx* c, double* zhost) {
     KRY_CUDA(cudaEventRecord(ev_full[b], c->stream));
     KRY_CUDA(cudaStreamWaitEvent(c->estream, ev_full[b], 0));
     KRY_CHECK(launch_chunk_coef_ld(c->estream, c->T.S, c->qy, s, r, (int)(q * G), nblk, ldq, Qc[b]));
+    cudaEvent_t pe[2] = {nullptr, nullptr};
+    if (c->prof) {
+      cudaEventCreate(&pe[0]);
+      cudaEventCreate(&pe[1]);
+      cudaEventRecord(pe[0], c->estream);
+    }
     KRY_CHECK(launch_zacc(c->estream, s, buf[b] + lo_d, slot_d, nblk, Qc[b], ldq, r, c->Z, n,
                           q > 0));
+    if (c->prof) {
+      cudaEventRecord(pe[1], c->estream);
+      c->ev_zacc.push_back({pe[0], pe[1]});
+      c->zacc_flops += 2.0 * (double)n * nblk * s * r;
+    }
     KRY_CUDA(cudaEventRecord(ev_free[b], c->estream));
     gemm_used[b] = true;
     return KRY_OK;
@@ -2670,6 +2850,23 @@ int kry_profile_enable(kry_ctx* c, int enable) {
   c->prof = enable != 0;
   for (auto& e : c->ev_comb) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   c->ev_comb.clear();
+  for (auto& e : c->ev_zacc) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  c->ev_zacc.clear();
+  c->zacc_flops = 0.0;
+  return KRY_OK;
+}
+
+int kry_profile_zacc(kry_ctx* c, double* ms_total, double* flops_total, int* launches) {
+  KRY_CUDA(cudaStreamSynchronize(c->estream));
+  double tot = 0.0;
+  for (auto& e : c->ev_zacc) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e.first, e.second);
+    tot += ms;
+  }
+  if (ms_total) *ms_total = tot;
+  if (flops_total) *flops_total = c->zacc_flops;
+  if (launches) *launches = (int)c->ev_zacc.size();
   return KRY_OK;
 }
 
@@ -2780,4 +2977,105 @@ int kry_comm_init(kry_ctx* c, int nranks, int rank, const void* id128) {
   return KRY_OK;
 }
 
+}  // extern "C"
+
+// ================================================================ measurement helpers
+namespace kry {
+// fp64 peak microbenchmark (the roofline denominator of the fp64 kernels,
+// tools/fp64_peak.cu is the standalone copy): independent DFMA chains and
+// independent DMMA m8n8k4 chains on a one-wave grid, best of 5 launches
+constexpr int PK_CH = 8;
+__global__ void k_peak_dfma(double* out, int iters, double a, double b) {
+  double x[PK_CH];
+#pragma unroll
+  for (int c = 0; c < PK_CH; ++c) x[c] = threadIdx.x * 1e-3 + c;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < PK_CH; ++c) x[c] = fma(x[c], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < PK_CH; ++c) s += x[c];
+  if (s == 12345.678) out[0] = s;
+}
+__global__ void k_peak_dmma(double* out, int iters) {
+  double acc[PK_CH][2];
+  const double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+#pragma unroll
+  for (int c = 0; c < PK_CH; ++c) acc[c][0] = acc[c][1] = 0.0;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < PK_CH; ++c)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(acc[c][0]), "+d"(acc[c][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < PK_CH; ++c) s += acc[c][0] + acc[c][1];
+  if (s == 12345.678) out[0] = s;
+}
+}  // namespace kry
+
+extern "C" {
+int kry_fp64_peak(int device, double* dfma_tflops, double* dmma_tflops) {
+  KRY_CUDA(cudaSetDevice(device));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  double* out = nullptr;
+  KRY_CHECK(dalloc(&out, 8));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int T = 256, B = sms * 8, it = 20000;
+  auto best = [&](auto launch) {
+    float b = 1e30f;
+    launch();
+    cudaDeviceSynchronize();
+    for (int r = 0; r < 5; ++r) {
+      cudaEventRecord(e0);
+      launch();
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      b = std::min(b, ms);
+    }
+    return b;
+  };
+  const float ms_f = best([&] { k_peak_dfma<<<B, T>>>(out, it, 0.999999, 1e-7); });
+  const float ms_m = best([&] { k_peak_dmma<<<B, T>>>(out, it / 4); });
+  count_launch(12);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  dfree(out);
+  KRY_CUDA(cudaGetLastError());
+  const double thr = (double)T * B;
+  if (dfma_tflops) *dfma_tflops = thr * it * PK_CH * 2.0 / (ms_f * 1e-3) / 1e12;
+  if (dmma_tflops) *dmma_tflops = thr / 32.0 * (it / 4) * PK_CH * 512.0 / (ms_m * 1e-3) / 1e12;
+  return KRY_OK;
+}
+
+// time the cheap residual (the Cauchy contraction + u/w, the check's fp64
+// part) on the context's current eigen data: average ms over `reps` launches
+// on the eigen stream (CUDA events) and the order k it ran at
+int kry_profile_check(kry_ctx* c, int reps, double* ms, int* k) {
+  KRY_CUDA(cudaSetDevice(c->dev));
+  if (c->m < 1 || c->eig.K < 1) return fail(KRY_ERR_STATE, "no eigen data to time");
+  cudaEvent_t e0, e1;
+  KRY_CUDA(cudaEventCreate(&e0));
+  KRY_CUDA(cudaEventCreate(&e1));
+  const double* tau = tau_ptr(c);
+  KRY_CHECK(c->eig.residual_lyap(c->estream, c->gamma_d, tau));   // warm
+  KRY_CUDA(cudaEventRecord(e0, c->estream));
+  for (int r = 0; r < reps; ++r) KRY_CHECK(c->eig.residual_lyap(c->estream, c->gamma_d, tau));
+  KRY_CUDA(cudaEventRecord(e1, c->estream));
+  KRY_CUDA(cudaEventSynchronize(e1));
+  float f = 0.f;
+  cudaEventElapsedTime(&f, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (ms) *ms = f / std::max(reps, 1);
+  if (k) *k = c->eig.K;
+  return KRY_OK;
+}
 }  // extern "C"

@@ -17,10 +17,10 @@
 // each warp 32 x 8 NT = 4 x NT m8n8 DMMA tiles, 8 NT accumulator doubles per
 // lane; A is then read from HBM once and every loaded fragment feeds 4 or NT
 // DMMAs) and
-// walks the K dimension one basis block per pipeline stage: the block's 64
-// point rows (64 s contiguous doubles) and the block's s rows of the Q panel
-// arrive by cp.async (16-byte, zero-filled outside the matrix) in a
-// 4-stage ring.  Shared-memory strides are padded so that the A fragments
+// walks the K dimension a few basis blocks per pipeline stage (>= 8 k values
+// between barriers): each block's 64 point rows (64 s contiguous doubles)
+// and its s rows of the Q panel arrive by cp.async (16-byte, zero-filled
+// outside the matrix) in a 3-stage ring.  Shared-memory strides are padded so that the A fragments
 // (8 rows x 4 k per warp) and the B fragments (4 k x 8 columns) are read
 // without bank conflicts.  CTAs are ordered panel-fastest, so the panels of
 // one 64-point tile read its A rows from L2.
@@ -31,7 +31,7 @@
 namespace kry {
 
 namespace {
-constexpr int ZBM = 64, ZST = 4, ZWARPS = 8, ZNTMAX = 8;
+constexpr int ZBM = 64, ZST = 3, ZWARPS = 8, ZNTMAX = 8;
 // B row stride (doubles) for a panel of BN columns: conflict-free B fragments
 __host__ __device__ constexpr int zbst(int bn) { return bn + 4; }
 
@@ -57,6 +57,8 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 // rows of a fragment land in distinct banks
 template <int S>
 __host__ __device__ constexpr int zast() { return (S <= 4 ? 4 : 8) + 4; }
+// basis blocks per pipeline stage: >= 8 k values between barriers
+__host__ __device__ constexpr int zbps(int s) { return s >= 8 ? 2 : (s >= 4 ? 4 : 8); }
 }  // namespace
 
 template <int S, int NT>
@@ -68,10 +70,12 @@ __global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__
   constexpr int KS = (S + 3) / 4;      // k4-steps per block
   constexpr int AST = zast<S>();
   constexpr int KP = 4 * KS;           // padded k rows of a B stage
+  constexpr int BPS = zbps(S);         // basis blocks per pipeline stage
   constexpr int ZBN = 32 * NT, ZBST = zbst(32 * NT);
+  constexpr int ASZ = ZBM * AST, BSZ = KP * ZBST;   // per block of a stage
   extern __shared__ __align__(16) double zsm[];
-  double (*sA)[ZBM * AST] = reinterpret_cast<double (*)[ZBM * AST]>(zsm);
-  double (*sB)[KP * ZBST] = reinterpret_cast<double (*)[KP * ZBST]>(zsm + ZST * ZBM * AST);
+  double* sA = zsm;                                  // [ZST][BPS][ASZ]
+  double* sB = zsm + ZST * BPS * ASZ;                // [ZST][BPS][BSZ]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;
@@ -79,31 +83,39 @@ __global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__
   const int64_t i0 = (int64_t)(blockIdx.x / npanels) * ZBM;
   const int j0 = panel * ZBN;
   // zero the padding once (k columns >= s of A, k rows >= s of B)
-  for (int e = tid; e < ZST * ZBM * AST; e += blockDim.x) (&sA[0][0])[e] = 0.0;
-  for (int e = tid; e < ZST * KP * ZBST; e += blockDim.x) (&sB[0][0])[e] = 0.0;
+  for (int e = tid; e < ZST * BPS * ASZ; e += blockDim.x) sA[e] = 0.0;
+  for (int e = tid; e < ZST * BPS * BSZ; e += blockDim.x) sB[e] = 0.0;
   __syncthreads();
-  auto load_stage = [&](int b, int st) {
-    const double* vb = vbase + (int64_t)b * vstride + i0 * S;
-    if ((S & 1) == 0) {
-      // 64 rows x S doubles contiguous: 16-byte pieces
-      constexpr int PR = (S / 2) > 0 ? S / 2 : 1;   // pieces per row
-      for (int q = tid; q < ZBM * PR; q += blockDim.x) {
-        const int row = q / PR, pc = q % PR;
-        const bool ok = i0 + row < n;
-        cp16(&sA[st][row * AST + 2 * pc], ok ? vb + (int64_t)row * S + 2 * pc : vb, ok);
+  // stage `st` <- blocks grp*BPS .. grp*BPS+BPS-1 (zero-filled past nb)
+  auto load_stage = [&](int grp, int st) {
+#pragma unroll
+    for (int bb = 0; bb < BPS; ++bb) {
+      const int b = grp * BPS + bb;
+      const bool bok = b < nb;
+      double* dA = sA + ((int64_t)st * BPS + bb) * ASZ;
+      double* dB = sB + ((int64_t)st * BPS + bb) * BSZ;
+      const double* vb = vbase + (int64_t)(bok ? b : 0) * vstride + i0 * S;
+      if ((S & 1) == 0) {
+        // 64 rows x S doubles contiguous: 16-byte pieces
+        constexpr int PR = (S / 2) > 0 ? S / 2 : 1;   // pieces per row
+        for (int q = tid; q < ZBM * PR; q += blockDim.x) {
+          const int row = q / PR, pc = q % PR;
+          const bool ok = bok && i0 + row < n;
+          cp16(&dA[row * AST + 2 * pc], ok ? vb + (int64_t)row * S + 2 * pc : vbase, ok);
+        }
+      } else {
+        for (int q = tid; q < ZBM * S; q += blockDim.x) {
+          const int row = q / S, c = q % S;
+          const bool ok = bok && i0 + row < n;
+          cp8(&dA[row * AST + c], ok ? vb + (int64_t)row * S + c : vbase, ok);
+        }
       }
-    } else {
-      for (int q = tid; q < ZBM * S; q += blockDim.x) {
-        const int row = q / S, c = q % S;
-        const bool ok = i0 + row < n;
-        cp8(&sA[st][row * AST + c], ok ? vb + (int64_t)row * S + c : vb, ok);
+      const double* qb = Q + (int64_t)(bok ? b : 0) * S * ldq + j0;
+      constexpr int PB = ZBN / 2;   // 16-byte pieces per Q row
+      for (int q = tid; q < S * PB; q += blockDim.x) {
+        const int row = q / PB, pc = q % PB;
+        cp16(&dB[row * ZBST + 2 * pc], qb + (int64_t)row * ldq + 2 * pc, bok);
       }
-    }
-    const double* qb = Q + (int64_t)b * S * ldq + j0;
-    constexpr int PB = ZBN / 2;   // 16-byte pieces per Q row
-    for (int q = tid; q < S * PB; q += blockDim.x) {
-      const int row = q / PB, pc = q % PB;
-      cp16(&sB[st][row * ZBST + 2 * pc], qb + (int64_t)row * ldq + 2 * pc, j0 + 2 * pc < ldq);
     }
   };
   double acc[4][NT][2];
@@ -111,32 +123,36 @@ __global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int ng = (nb + BPS - 1) / BPS;
 #pragma unroll
   for (int st = 0; st < ZST - 1; ++st) {
-    if (st < nb) load_stage(st, st);
+    if (st < ng) load_stage(st, st);
     cp_commit();
   }
-  for (int b = 0; b < nb; ++b) {
+  for (int gi = 0; gi < ng; ++gi) {
     cp_wait<ZST - 2>();
     __syncthreads();
-    {   // prefetch block b + ZST - 1 into the stage freed by block b - 1
-      const int bn = b + ZST - 1;
-      if (bn < nb) load_stage(bn, bn % ZST);
+    {   // prefetch group gi + ZST - 1 into the stage freed by group gi - 1
+      const int gn = gi + ZST - 1;
+      if (gn < ng) load_stage(gn, gn % ZST);
       cp_commit();
     }
-    const double* A = sA[b % ZST];
-    const double* B = sB[b % ZST];
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      double fa[4], fb[NT];
+    for (int bb = 0; bb < BPS; ++bb) {
+      const double* A = sA + ((int64_t)(gi % ZST) * BPS + bb) * ASZ;
+      const double* B = sB + ((int64_t)(gi % ZST) * BPS + bb) * BSZ;
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) fa[mt] = A[(wm * 32 + mt * 8 + g) * AST + 4 * ks + t];
+      for (int ks = 0; ks < KS; ++ks) {
+        double fa[4], fb[NT];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) fb[nt] = B[(4 * ks + t) * ZBST + wn * 8 * NT + nt * 8 + g];
+        for (int mt = 0; mt < 4; ++mt) fa[mt] = A[(wm * 32 + mt * 8 + g) * AST + 4 * ks + t];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
+        for (int nt = 0; nt < NT; ++nt) fb[nt] = B[(4 * ks + t) * ZBST + wn * 8 * NT + nt * 8 + g];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) zdmma(acc[mt][nt][0], acc[mt][nt][1], fa[mt], fb[nt]);
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) zdmma(acc[mt][nt][0], acc[mt][nt][1], fa[mt], fb[nt]);
+      }
     }
   }
   cp_wait<0>();
@@ -174,10 +190,11 @@ static int zacc_go(cudaStream_t st, const double* vbase, int64_t vstride, int nb
                    const double* Q, int ldq, int r, double* Z, int64_t n, int accumulate) {
   constexpr int KP = 4 * ((S + 3) / 4);
   constexpr int BN = 32 * NT;
+  constexpr int BPS = zbps(S);
   const int npanels = (r + BN - 1) / BN;
   const int64_t grid = ((n + ZBM - 1) / ZBM) * npanels;
   if (grid > 0x7fffffffLL) return fail(KRY_ERR_DIMENSION, "pass-2 factor too large");
-  const size_t smem = (size_t)ZST * (ZBM * zast<S>() + KP * zbst(BN)) * sizeof(double);
+  const size_t smem = (size_t)ZST * BPS * (ZBM * zast<S>() + KP * zbst(BN)) * sizeof(double);
   static bool attr[64] = {false};   // per device
   int dev = 0;
   cudaGetDevice(&dev);

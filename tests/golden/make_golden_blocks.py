@@ -18,7 +18,7 @@ which never travels to the GPU box).  Three stages:
    ``two_pass_recover`` (``solvers.py:130-169``), recipe of
    ``tests/test_acceptance.py:190-215``; the factor is stored as the seeded
    sketch Z (Zᵀ Ω) on 4096 sampled rows (as the c4 golden).
-2. ``residuals <out_dir> <blocks.npz> ...`` (run where a GPU is available; CPU works
+2. ``residuals [--stride=k] <out_dir> <blocks.npz> ...`` (run where a GPU is available; CPU works
    but takes hours at k = 6000) evaluates the paper's residual formula at
    EVERY m from the stored reference blocks with a dense symmetric
    eigensolver in fp64 instead of the reference's band reduction +
@@ -272,14 +272,19 @@ def sylv_residual(d, m):
     return res / float(d["rhs_norm"])
 
 
-def residuals(out_dir, paths):
+def residuals(out_dir, paths, stride=1):
+    """Surrogate history at every m (stride 1), or at m = 1..60 and every
+    ``stride``-th m after (NaN elsewhere; enough for the noise ensemble,
+    whose envelope is a running maximum)."""
     os.makedirs(out_dir, exist_ok=True)
     for path in paths:
         d = dict(np.load(path))
         steps = int(d["steps"])
-        hist = np.zeros(steps)
+        hist = np.full(steps, np.nan)
         tic = time.perf_counter()
         for m in range(1, steps + 1):
+            if m > 60 and m % stride and m != steps:
+                continue
             if "diag_b" in d:
                 hist[m - 1] = sylv_residual(d, m)
             else:
@@ -329,7 +334,12 @@ if __name__ == "__main__":
         steps = int(sys.argv[5]) if len(sys.argv) > 5 else None
         lanczos(sys.argv[2], sys.argv[3], sys.argv[4], steps)
     elif mode == "residuals":
-        residuals(sys.argv[2], sys.argv[3:])
+        args = sys.argv[2:]
+        stride = 1
+        if args and args[0].startswith("--stride="):
+            stride = int(args[0].split("=")[1])
+            args = args[1:]
+        residuals(args[0], args[1:], stride)
     elif mode == "crosscheck":
         crosscheck(sys.argv[2], [int(x) for x in sys.argv[3].split(",")])
     else:

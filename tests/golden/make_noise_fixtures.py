@@ -33,7 +33,16 @@ def main(cfg, src, variants):
     for v in variants:
         h = np.load(os.path.join(src, "%s_blocks_%s_hist.npz" % (cfg, v)))["surrogate_history"]
         n = min(len(h), len(base))
-        devs.append(np.abs(h[:n] - base[:n]))
+        dv = np.abs(h[:n] - base[:n])
+        # strided variant histories (NaN between samples): the deviation at an
+        # unsampled m is bounded by the larger of its sampled neighbours
+        have = np.nonzero(np.isfinite(dv))[0]
+        if len(have) < n:
+            nxt = np.searchsorted(have, np.arange(n))
+            prv = np.clip(nxt - 1, 0, len(have) - 1)
+            nxt = np.clip(nxt, 0, len(have) - 1)
+            dv = np.where(np.isfinite(dv), dv, np.maximum(dv[have[prv]], dv[have[nxt]]))
+        devs.append(dv)
         below = np.nonzero(h <= tol)[0]
         iters.append(int(below[0]) + 1 if len(below) else -1)
     n = min(len(d) for d in devs)
