@@ -2528,6 +2528,21 @@ int kry_recover(kry_ctx* c, double* zhost) {
   };
   const int64_t ld = s;
   bool gemm_used[2] = {false, false};
+  // SM sharing: while the accumulation of chunk q-1 runs (one persistent CTA
+  // per SM, a DMMA-bound grid-stride GEMM) the regeneration of chunk q runs
+  // with grids capped to what fits next to it on every SM, so both kernels
+  // are resident at once instead of taking turns (KRY_P2_SHARE=0 disables)
+  int sms = 148, cap_apply = 0, cap_comb = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev);
+  bool share = nbuf == 2 && !dist(c);
+  if (const char* e = getenv("KRY_P2_SHARE")) share = share && e[0] != '0';
+  if (share) {
+    int zr = 0;
+    size_t zs = 0;
+    zacc_footprint(s, r, &zr, &zs);
+    pass2_caps(c->op, s, zr, zs, &cap_apply, &cap_comb);
+  }
+  const int nchunks = (int)((m + G - 1) / G);
   // fold chunk q (blocks q*G+1 .. q*G+nblk) into Z on the second stream
   auto gemm_chunk = [&](int64_t q, int nblk) -> int {
     const int b = (int)(q % nbuf);
@@ -2540,8 +2555,9 @@ int kry_recover(kry_ctx* c, double* zhost) {
       cudaEventCreate(&pe[1]);
       cudaEventRecord(pe[0], c->estream);
     }
+    const bool last = q == nchunks - 1;   // nothing left to overlap: the full grid
     KRY_CHECK(launch_zacc(c->estream, s, buf[b] + lo_d, slot_d, nblk, Qc[b], ldq, r, c->Z, n,
-                          q > 0));
+                          q > 0, (share && !last) ? sms : 0));
     if (c->prof) {
       cudaEventRecord(pe[1], c->estream);
       c->ev_zacc.push_back({pe[0], pe[1]});
@@ -2558,10 +2574,13 @@ int kry_recover(kry_ctx* c, double* zhost) {
     // coefficient solve j on V_j (replay) -- already done by the previous
     // fused launch when coef_ready
     const bool fused = step_on(c) && c->coef_ready;
+    // regeneration of chunk >= 1 shares the SMs with the previous chunk's fold
+    const bool shared = share && j >= G;
     if (!fused) {
       c->coef_ready = false;
       ApplyGramCall ag{blk(j), ld, n, 1, POST_STEP, 0};
       ag.wout = speculate ? wbuf_of(c) : nullptr;
+      ag.grid_cap = shared ? cap_apply : 0;
       rc = run_apply_gram(c, ag);
       if (rc) break;
       if (!speculate) {
@@ -2588,6 +2607,7 @@ int kry_recover(kry_ctx* c, double* zhost) {
     if (speculate) {
       CombineCall cc{vold, ld, blk(j), ld, blk(j + 1), ld, n, j > 1 ? 1 : 0, 1, 1, 1};
       cc.win = wbuf_of(c);
+      cc.grid_cap = shared ? cap_comb : 0;
       rc = run_combine(c, cc, nullptr, nullptr);
       if (rc == KRY_OK) rc = sync_status(c);
       if (rc == KRY_OK) rc = map_status(c, ("second pass step " + std::to_string(j)).c_str());
@@ -3055,8 +3075,9 @@ int kry_fp64_peak(int device, double* dfma_tflops, double* dmma_tflops) {
   return KRY_OK;
 }
 
-// time the cheap residual (the Cauchy contraction + u/w, the check's fp64
-// part) on the context's current eigen data: average ms over `reps` launches
+// time the residual contraction (k_cauchy_mma, the check's fp64 part; u, w
+// computed once before) on the context's current eigen data: average ms over
+// `reps` launches
 // on the eigen stream (CUDA events) and the order k it ran at
 int kry_profile_check(kry_ctx* c, int reps, double* ms, int* k) {
   KRY_CUDA(cudaSetDevice(c->dev));
@@ -3065,9 +3086,12 @@ int kry_profile_check(kry_ctx* c, int reps, double* ms, int* k) {
   KRY_CUDA(cudaEventCreate(&e0));
   KRY_CUDA(cudaEventCreate(&e1));
   const double* tau = tau_ptr(c);
-  KRY_CHECK(c->eig.residual_lyap(c->estream, c->gamma_d, tau));   // warm
+  KRY_CHECK(c->eig.residual_lyap(c->estream, c->gamma_d, tau));   // u, w + warm
   KRY_CUDA(cudaEventRecord(e0, c->estream));
-  for (int r = 0; r < reps; ++r) KRY_CHECK(c->eig.residual_lyap(c->estream, c->gamma_d, tau));
+  const int K = c->eig.K;
+  for (int r = 0; r < reps; ++r)   // the contraction kernel alone
+    KRY_CHECK(c->eig.cauchy(c->estream, K, c->eig.lam_cur(), c->eig.u, K, c->eig.lam_cur(),
+                            c->eig.u, c->eig.w, c->eig.res));
   KRY_CUDA(cudaEventRecord(e1, c->estream));
   KRY_CUDA(cudaEventSynchronize(e1));
   float f = 0.f;

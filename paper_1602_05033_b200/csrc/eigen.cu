@@ -177,6 +177,13 @@ __global__ void __launch_bounds__(1024) k_eig_deflate(EigView e, int K, const do
   // runs of flagged pairs are processed sequentially (one thread per run)
   for (int i = 1 + threadIdx.x; i < q; i += blockDim.x) {
     if (!e.pflag[i] || e.pflag[i - 1]) continue;
+    if (e.stats) {
+      int len = 0;
+      for (int k = i; k < q && e.pflag[k]; ++k) ++len;
+      atomicAdd(e.stats + 130, 1u);                       // runs
+      atomicAdd(e.stats + 131, (unsigned)len);            // rotated pairs
+      atomicMax(e.stats + 132, (unsigned)len);            // longest run
+    }
     int prev = e.cand[i - 1];
     for (int k = i; k < q && e.pflag[k]; ++k) {
       const int cur = e.cand[k];
@@ -246,6 +253,12 @@ __global__ void __launch_bounds__(1024) k_eig_deflate(EigView e, int K, const do
   if (threadIdx.x == 0) {
     e.counts[0] = pb;
     e.counts[1] = db;
+    if (e.stats) {
+      atomicAdd(e.stats + 133, 1u);                       // calls
+      atomicAdd(e.stats + 134, unsorted ? 1u : 0u);       // serial re-sorts
+      atomicAdd(e.stats + 135, (unsigned)db);             // deflated poles
+      atomicAdd(e.stats + 136, (unsigned)q);              // candidates
+    }
     for (int i = 1; unsorted && i < db; ++i) {
       double v = e.def_lam[i];
       if (v >= e.def_lam[i - 1]) continue;
@@ -787,8 +800,8 @@ __global__ void k_uw(const double* F, const double* L, int64_t km, int k, int s,
 // second: lane (g, t) holds P[g][2t], P[g][2t+1], and the second product
 // takes its k-steps over the y parity (k-step h <-> y = 2t + h), so no lane
 // exchange is needed; the B operand of k-step h is C[y0 + 2t + h][g].
-// A CTA owns 16 x-rows (two 8-row fragments per warp, two independent DMMA
-// chains) and one of YS interleaved y-splits; its 8 warps take the split's
+// A CTA owns 32 x-rows (four 8-row fragments per warp: four independent DMMA
+// chains per loaded y-tile) and one of YS interleaved y-splits; its 8 warps take the split's
 // y-tiles in a fixed stride, with the next tile's operands loaded while the
 // current one is multiplied.  The warps' partial M are summed through shared
 // memory in warp order; with YS > 1 the splits' partial M go to global
@@ -796,9 +809,9 @@ __global__ void k_uw(const double* F, const double* L, int64_t km, int k, int s,
 // split order, so every sum has a fixed order: the result is deterministic.
 // The minimum |lx + ly| is exact and cheap because ly is sorted ascending
 // (eigenvalues): per x only the two neighbours of -lx in ly can be closest.
-#define CC_XR 16     // x rows per CTA
+#define CC_XR 32     // x rows per CTA (CC_XR / 8 fragments per warp)
 #define CC_NW 8      // warps per CTA
-#define CC_TARGET_CTAS (3 * 148)
+#define CC_TARGET_CTAS (2 * 148)   // one wave at 2 CTAs per SM (96 registers)
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
@@ -845,11 +858,12 @@ __global__ void __launch_bounds__(32 * CC_NW) k_cauchy_mma(int nx, const double*
   const int xt = blockIdx.x, nxt = gridDim.x;
   const int split = blockIdx.y, YS = gridDim.y;
   const int x0 = xt * CC_XR;
-  // A fragments of the two 8-row x tiles: A[g][t] = a[x0 + 8f + g][4 ks + t]
-  double fa[2][KS], flx[2];
-  bool vx[2];
+  // A fragments of the XF 8-row x tiles: A[g][t] = a[x0 + 8f + g][4 ks + t]
+  constexpr int XF = CC_XR / 8;
+  double fa[XF][KS], flx[XF];
+  bool vx[XF];
 #pragma unroll
-  for (int f = 0; f < 2; ++f) {
+  for (int f = 0; f < XF; ++f) {
     const int x = x0 + 8 * f + g;
     vx[f] = x < nx;
     flx[f] = vx[f] ? lx[x] : 0.0;
@@ -859,7 +873,9 @@ __global__ void __launch_bounds__(32 * CC_NW) k_cauchy_mma(int nx, const double*
       fa[f][ks] = (vx[f] && col < S) ? ax[(int64_t)x * 8 + col] : 0.0;
     }
   }
-  double m[2][2] = {{0.0, 0.0}, {0.0, 0.0}};   // M[x0 + 8f + g][2t + j]
+  double m[XF][2];   // M[x0 + 8f + g][2t + j]
+#pragma unroll
+  for (int f = 0; f < XF; ++f) m[f][0] = m[f][1] = 0.0;
   const int nyt = (ny + 7) >> 3;
   const int ystep = CC_NW * YS;
   int yt = warp + CC_NW * split;
@@ -870,7 +886,7 @@ __global__ void __launch_bounds__(32 * CC_NW) k_cauchy_mma(int nx, const double*
     const int yn = yt + ystep;
     if (yn < nyt) load_y<S, KS>(nxt_ops, yn * 8, g, t, ny, ly, by, cy);
 #pragma unroll
-    for (int f = 0; f < 2; ++f) {
+    for (int f = 0; f < XF; ++f) {
       double p0 = 0.0, p1 = 0.0;   // P[g][2t], P[g][2t+1]
 #pragma unroll
       for (int ks = 0; ks < KS; ++ks) dmma884(p0, p1, fa[f][ks], cur.b[ks]);
@@ -887,7 +903,7 @@ __global__ void __launch_bounds__(32 * CC_NW) k_cauchy_mma(int nx, const double*
   __shared__ double s_min[CC_XR];
   __shared__ unsigned s_last;
 #pragma unroll
-  for (int f = 0; f < 2; ++f) {
+  for (int f = 0; f < XF; ++f) {
     sm[warp][8 * f + g][2 * t] = m[f][0];
     sm[warp][8 * f + g][2 * t + 1] = m[f][1];
   }
@@ -1039,8 +1055,8 @@ int EigEngine::init(int s_, int kmax_, int device) {
   KRY_CUDA(cudaMemset(cnt, 0, cnt_cap * sizeof(unsigned)));
   if (const char* st = getenv("KRY_SECULAR_STATS")) {
     if (st[0] == '1') {
-      KRY_CHECK(dalloc(&stats, 128));
-      KRY_CUDA(cudaMemset(stats, 0, 128 * sizeof(unsigned)));
+      KRY_CHECK(dalloc(&stats, 160));
+      KRY_CUDA(cudaMemset(stats, 0, 160 * sizeof(unsigned)));
     }
   }
   return KRY_OK;
@@ -1048,7 +1064,7 @@ int EigEngine::init(int s_, int kmax_, int device) {
 
 void EigEngine::release() {
   if (stats) {
-    unsigned h[128];
+    unsigned h[160];
     if (cudaMemcpy(h, stats, sizeof(h), cudaMemcpyDeviceToHost) == cudaSuccess) {
       fprintf(stderr, "[kry] secular iterations:");
       for (int i = 0; i <= 80; ++i)
@@ -1056,7 +1072,8 @@ void EigEngine::release() {
       fprintf(stderr, "\n[kry] secular bisection steps:");
       for (int i = 0; i < 32; ++i)
         if (h[96 + i]) fprintf(stderr, " %d:%u", i, h[96 + i]);
-      fprintf(stderr, "\n");
+      fprintf(stderr, "\n[kry] deflate: calls %u runs %u rotated %u longest %u re-sorts %u "
+              "deflated %u candidates %u\n", h[133], h[130], h[131], h[132], h[134], h[135], h[136]);
     }
     dfree(stats);
     stats = nullptr;

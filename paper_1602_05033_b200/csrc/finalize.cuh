@@ -17,8 +17,11 @@ int launch_chunk_coef(cudaStream_t st, const double* S, const double* qy, int s,
                       int blk0, int nblk, double* Qc);
 // pass-2 / stored factor accumulation on DMMA (zacc.cu):
 // Z[i][:] (+)= sum_b V_b[i][:] Q[b s .. b s + s)[:], V_b = vbase + b vstride
+// max_ctas > 0: a grid of at most that many CTAs looping over the tiles
 int launch_zacc(cudaStream_t st, int s, const double* vbase, int64_t vstride, int nb,
-                const double* Q, int ldq, int r, double* Z, int64_t n, int accumulate);
+                const double* Q, int ldq, int r, double* Z, int64_t n, int accumulate,
+                int max_ctas = 0);
+void zacc_footprint(int s, int r, int* regs, size_t* smem);
 int launch_chunk_coef_ld(cudaStream_t st, const double* S, const double* qy, int s, int rank,
                          int blk0, int nblk, int ldq, double* Qc);
 int zacc_ldq(int r);   // padded leading dimension of the Q panel

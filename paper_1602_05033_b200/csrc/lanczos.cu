@@ -328,6 +328,27 @@ __device__ void set_status(DevState* st, int code) {
   if (tid() == 0 && st->status == KRY_OK) st->status = code;
 }
 
+// The new block V_{j+1} = W R1^-1 leaves the combine with one Cholesky-QR
+// stage; its Gram Gcc (just reduced) gives the second stage R2 = chol(Gcc),
+// which the next coefficient solve applies lazily.  The coupling the
+// residual check of step j reads (T.tau1[j-1]) is finalised here to R2 R1
+// -- the same product, bit for bit, that the next solve stores in T.sub --
+// so the check uses the reference's final QR factor (basis.py:241-249)
+// instead of the first stage (which differs by ~eps ||AV||^2 / ||W||^2).
+__device__ void finalize_tau(DevState* st, const TStore& T, double (*sm)[64], const double* Gcc) {
+  const int j = st->step;   // the step whose combine produced the block
+  if (j < 1 || j > T.cap) return;
+  __syncthreads();
+  double mr;
+  // scratch slots 3..5: the callers (POST_P / POST_FUSED) hold Gram blocks
+  // in slots 0..2 only (the smallest post scratch has 14 slots)
+  const int bad = chol_inv_par(Gcc, sm[3], sm[4], st->s, &mr);
+  if (bad) return;   // the next solve takes the fallback; keep R1
+  mm(sm[5], sm[3], 0, st->R1prev, 0, st->s);
+  if (tid() < 64) T.tau1[(int64_t)(j - 1) * 64 + tid()] = sm[5][tid()];
+  __syncthreads();
+}
+
 // total: MP x 8 reduced Gram (row = X column, col = Y column)
 __device__ void extract_block(const double* total, int row0, int s, double* dst) {
   __syncthreads();
@@ -556,7 +577,7 @@ __device__ __noinline__ void run_post(int post, const double* total, DevState* s
         st->GoW[tid()] = sm[1][tid()];
         st->Gcc[tid()] = sm[2][tid()];
       }
-      __syncthreads();
+      finalize_tau(st, T, sm, sm[2]);
       break;
     case POST_STEP:
       coef_solve(total, st, T, sm, 0, s, 0);
@@ -575,7 +596,7 @@ __device__ __noinline__ void run_post(int post, const double* total, DevState* s
         st->GoW[tid()] = sm[1][tid()];
         st->Gcc[tid()] = sm[2][tid()];
       }
-      __syncthreads();
+      finalize_tau(st, T, sm, sm[2]);
       coef_solve(total, st, T, sm, 24, 32, 1);
       break;
     case POST_INIT: {
@@ -1398,15 +1419,16 @@ int launch_combine(cudaStream_t st, int s, const OpDev& op, const CombineCall& c
   if (prof_ms && ev) cudaEventRecord(ev[0], st);
   const bool coop = (s % 2 == 0) && op.kind == KRY_OP_STENCIL && (c.ldc % 2 == 0) &&
                     (!c.has_old || c.ldo % 2 == 0);
+  auto capped = [&](int gr) { return c.grid_cap > 0 ? std::min(gr, c.grid_cap) : gr; };
   if (coop) {
 #define L(S)                                                                 \
-  k_combine<S, true><<<resident_grid(k_combine<S, true>, c.n, KRY_COMB_CAP), TP, 0, st>>>( \
+  k_combine<S, true><<<capped(resident_grid(k_combine<S, true>, c.n, KRY_COMB_CAP)), TP, 0, st>>>( \
       op, c, dst, T, g.partials, g.ticket + 0)
     KRY_DISPATCH_S(s, L);
 #undef L
   } else {
 #define L(S)                                                                   \
-  k_combine<S, false><<<resident_grid(k_combine<S, false>, c.n), TP, 0, st>>>( \
+  k_combine<S, false><<<capped(resident_grid(k_combine<S, false>, c.n)), TP, 0, st>>>( \
       op, c, dst, T, g.partials, g.ticket + 0)
     KRY_DISPATCH_S(s, L);
 #undef L
@@ -1421,8 +1443,9 @@ int launch_apply_gram(cudaStream_t st, int s, const OpDev& op, const ApplyGramCa
                       DevState* dst, const TStore& T, GramScratch& g, int grid) {
   (void)grid;
   const bool coop = (s % 2 == 0) && (op.kind == KRY_OP_STENCIL || !c.use_op) && (c.ldv % 2 == 0);
+  auto capped = [&](int gr) { return c.grid_cap > 0 ? std::min(gr, c.grid_cap) : gr; };
 #define LA(S, U, C)                                                                    \
-  k_apply_gram<S, U, C><<<resident_grid(k_apply_gram<S, U, C>, c.n), TP, 0, st>>>( \
+  k_apply_gram<S, U, C><<<capped(resident_grid(k_apply_gram<S, U, C>, c.n)), TP, 0, st>>>( \
       op, c, dst, T, g.partials, g.ticket + 1 * KRY_TICKET_STRIDE)
   if (c.use_op && coop) {
 #define L(S) LA(S, 1, true)
@@ -1520,5 +1543,57 @@ int launch_explicit_finish(cudaStream_t st, DevState* dst, const TStore& T, int 
 }
 
 #include "step.cuh"
+
+namespace kry {
+// CTAs of a kernel that fit on one SM next to a resident CTA that holds
+// z_regs registers and z_smem shared bytes (allocation granularities of
+// sm_100: 256 registers per warp, 1 KB reserved shared memory per CTA)
+static int fit_next_to(const void* fn, int threads, size_t dyn_smem, int z_regs, size_t z_smem) {
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  int dev = 0, regs_sm = 65536, smem_sm = 228 * 1024, thr_sm = 2048;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&thr_sm, cudaDevAttrMaxThreadsPerMultiProcessor, dev);
+  const int warps = (threads + 31) / 32;
+  const int regs = ((fa.numRegs * 32 + 255) / 256) * 256 * warps;
+  const size_t smem = fa.sharedSizeBytes + dyn_smem + 1024;
+  const int by_regs = (regs_sm - z_regs) / std::max(regs, 1);
+  const int by_smem = (int)(((size_t)smem_sm - z_smem - 1024) / smem);
+  const int by_thr = (thr_sm - 256) / threads;
+  return std::max(1, std::min(std::min(by_regs, by_smem), by_thr));
+}
+
+void pass2_caps(const OpDev& op, int s, int z_regs, size_t z_smem, int* cap_apply,
+                int* cap_combine) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const void* comb = nullptr;
+  const void* app = nullptr;
+  size_t app_smem = 0;
+  int app_threads = TP;
+  const int mode = apply_mode(op, s);
+#define C(S)                                      \
+  case S:                                         \
+    comb = (const void*)k_combine<S, true>;       \
+    if (mode == 2 && S % 2 == 0) {                \
+      app = (const void*)k_apply_tma<(S % 2 == 0 ? S : 2)>; \
+      app_smem = apt_smem_bytes(S);               \
+      app_threads = APT_NW * 32 + 32;             \
+    } else {                                      \
+      app = (const void*)k_apply_gram<S, 1, true>; \
+    }                                             \
+    break;
+  switch (s) { C(1) C(2) C(3) C(4) C(5) C(6) C(7) C(8) default: break; }
+#undef C
+  *cap_combine = comb ? fit_next_to(comb, TP, 0, z_regs, z_smem) * sms : 0;
+  *cap_apply = app ? fit_next_to(app, app_threads, app_smem, z_regs, z_smem) * sms : 0;
+}
+}  // namespace kry
 
 }  // namespace kry

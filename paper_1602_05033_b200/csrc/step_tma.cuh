@@ -508,7 +508,8 @@ int launch_apply_tma(cudaStream_t st, int s, const OpDev& op, const ApplyGramCal
       per = std::max(1, nb);                                                               \
     }                                                                                      \
     const int64_t ntiles = (c.n + TMA_CH - 1) / TMA_CH;                                     \
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)per * sms)); \
+    int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)per * sms));  \
+    if (c.grid_cap > 0) grid = std::min(grid, c.grid_cap);                                 \
     k_apply_tma<S><<<grid, threads, sm, st>>>(op, cc, dst, T, g.partials, g.ticket + 1 * KRY_TICKET_STRIDE);   \
   }
   switch (s) {

@@ -66,7 +66,8 @@ __global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__
                                                       int64_t vstride, int nb,
                                                       const double* __restrict__ Q, int ldq,
                                                       int r, double* __restrict__ Z, int64_t n,
-                                                      int accumulate, int npanels) {
+                                                      int accumulate, int npanels,
+                                                      int64_t ntiles) {
   constexpr int KS = (S + 3) / 4;      // k4-steps per block
   constexpr int AST = zast<S>();
   constexpr int KP = 4 * KS;           // padded k rows of a B stage
@@ -79,13 +80,16 @@ __global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp >> 2, wn = warp & 3;
-  const int panel = blockIdx.x % npanels;
-  const int64_t i0 = (int64_t)(blockIdx.x / npanels) * ZBM;
-  const int j0 = panel * ZBN;
   // zero the padding once (k columns >= s of A, k rows >= s of B)
   for (int e = tid; e < ZST * BPS * ASZ; e += blockDim.x) sA[e] = 0.0;
   for (int e = tid; e < ZST * BPS * BSZ; e += blockDim.x) sB[e] = 0.0;
   __syncthreads();
+  // tiles in a grid-stride loop: one wave of CTAs (pass 2, sharing the SMs
+  // with the regeneration kernels) or one tile per CTA
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const int panel = (int)(tile % npanels);
+  const int64_t i0 = (tile / npanels) * ZBM;
+  const int j0 = panel * ZBN;
   // stage `st` <- blocks grp*BPS .. grp*BPS+BPS-1 (zero-filled past nb)
   auto load_stage = [&](int grp, int st) {
 #pragma unroll
@@ -156,6 +160,7 @@ __global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__
     }
   }
   cp_wait<0>();
+  __syncthreads();   // the next tile's prologue overwrites the stages
   // epilogue: Z (+)= acc; lane (g, t) holds rows ..+g, columns ..+2t, +2t+1
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt) {
@@ -174,6 +179,7 @@ __global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__
       }
     }
   }
+  }   // tile loop
 }
 
 // panel width 32 NT: NT = 8 (one panel for r <= 256) measured slower on c4
@@ -187,12 +193,15 @@ static int zacc_nt(int r) {
 
 template <int S, int NT>
 static int zacc_go(cudaStream_t st, const double* vbase, int64_t vstride, int nb,
-                   const double* Q, int ldq, int r, double* Z, int64_t n, int accumulate) {
+                   const double* Q, int ldq, int r, double* Z, int64_t n, int accumulate,
+                   int max_ctas) {
   constexpr int KP = 4 * ((S + 3) / 4);
   constexpr int BN = 32 * NT;
   constexpr int BPS = zbps(S);
   const int npanels = (r + BN - 1) / BN;
-  const int64_t grid = ((n + ZBM - 1) / ZBM) * npanels;
+  const int64_t ntiles = ((n + ZBM - 1) / ZBM) * npanels;
+  int64_t grid = ntiles;
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   if (grid > 0x7fffffffLL) return fail(KRY_ERR_DIMENSION, "pass-2 factor too large");
   const size_t smem = (size_t)ZST * BPS * (ZBM * zast<S>() + KP * zbst(BN)) * sizeof(double);
   static bool attr[64] = {false};   // per device
@@ -204,23 +213,48 @@ static int zacc_go(cudaStream_t st, const double* vbase, int64_t vstride, int nb
     attr[dev & 63] = true;
   }
   k_zacc<S, NT><<<(unsigned)grid, 32 * ZWARPS, smem, st>>>(vbase, vstride, nb, Q, ldq, r, Z, n,
-                                                            accumulate, npanels);
+                                                            accumulate, npanels, ntiles);
   return KRY_OK;
 }
 
 template <int S>
 static int zacc_s(cudaStream_t st, const double* vbase, int64_t vstride, int nb, const double* Q,
-                  int ldq, int r, double* Z, int64_t n, int accumulate) {
+                  int ldq, int r, double* Z, int64_t n, int accumulate, int max_ctas) {
   switch (zacc_nt(r)) {
-    case 2: return zacc_go<S, 2>(st, vbase, vstride, nb, Q, ldq, r, Z, n, accumulate);
-    default: return zacc_go<S, 4>(st, vbase, vstride, nb, Q, ldq, r, Z, n, accumulate);
+    case 2: return zacc_go<S, 2>(st, vbase, vstride, nb, Q, ldq, r, Z, n, accumulate, max_ctas);
+    default: return zacc_go<S, 4>(st, vbase, vstride, nb, Q, ldq, r, Z, n, accumulate, max_ctas);
+  }
+}
+
+// registers and shared bytes of one k_zacc CTA for (s, r), for the pass-2
+// co-residency caps of the regeneration kernels
+template <int S>
+static void zacc_fp(int r, int* regs, size_t* smem) {
+  constexpr int KP = 4 * ((S + 3) / 4);
+  constexpr int BPS = zbps(S);
+  const int nt = zacc_nt(r);
+  cudaFuncAttributes fa;
+  cudaError_t e = nt == 2 ? cudaFuncGetAttributes(&fa, k_zacc<S, 2>)
+                          : cudaFuncGetAttributes(&fa, k_zacc<S, 4>);
+  if (e != cudaSuccess) { cudaGetLastError(); fa.numRegs = 128; fa.sharedSizeBytes = 0; }
+  *regs = ((fa.numRegs * 32 + 255) / 256) * 256 * ZWARPS;
+  *smem = fa.sharedSizeBytes + 1024 +
+          (size_t)ZST * BPS * (ZBM * zast<S>() + KP * zbst(32 * nt)) * sizeof(double);
+}
+void zacc_footprint(int s, int r, int* regs, size_t* smem) {
+  switch (s) {
+    case 1: zacc_fp<1>(r, regs, smem); break; case 2: zacc_fp<2>(r, regs, smem); break;
+    case 3: zacc_fp<3>(r, regs, smem); break; case 4: zacc_fp<4>(r, regs, smem); break;
+    case 5: zacc_fp<5>(r, regs, smem); break; case 6: zacc_fp<6>(r, regs, smem); break;
+    case 7: zacc_fp<7>(r, regs, smem); break; default: zacc_fp<8>(r, regs, smem); break;
   }
 }
 
 int launch_zacc(cudaStream_t st, int s, const double* vbase, int64_t vstride, int nb,
-                const double* Q, int ldq, int r, double* Z, int64_t n, int accumulate) {
+                const double* Q, int ldq, int r, double* Z, int64_t n, int accumulate,
+                int max_ctas) {
   if (nb < 1 || r < 1) return KRY_OK;
-#define L(S) KRY_CHECK(zacc_s<S>(st, vbase, vstride, nb, Q, ldq, r, Z, n, accumulate))
+#define L(S) KRY_CHECK(zacc_s<S>(st, vbase, vstride, nb, Q, ldq, r, Z, n, accumulate, max_ctas))
   switch (s) {
     case 1: L(1); break; case 2: L(2); break; case 3: L(3); break; case 4: L(4); break;
     case 5: L(5); break; case 6: L(6); break; case 7: L(7); break; case 8: L(8); break;
