@@ -2528,42 +2528,35 @@ int kry_recover(kry_ctx* c, double* zhost) {
   };
   const int64_t ld = s;
   bool gemm_used[2] = {false, false};
-  // SM sharing: while the accumulation of chunk q-1 runs (one persistent CTA
-  // per SM, a DMMA-bound grid-stride GEMM) the regeneration of chunk q runs
-  // with grids capped to what fits next to it on every SM, so both kernels
-  // are resident at once instead of taking turns (KRY_P2_SHARE=0 disables)
-  int sms = 148, cap_apply = 0, cap_comb = 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->dev);
-  bool share = nbuf == 2 && !dist(c);
-  if (const char* e = getenv("KRY_P2_SHARE")) share = share && e[0] != '0';
-  if (share) {
-    int zr = 0;
-    size_t zs = 0;
-    zacc_footprint(s, r, &zr, &zs);
-    pass2_caps(c->op, s, zr, zs, &cap_apply, &cap_comb);
-  }
-  const int nchunks = (int)((m + G - 1) / G);
+  // (Sharing the SMs between the accumulation and the regeneration -- one
+  // persistent accumulation CTA per SM, regeneration grids capped to fit
+  // beside it -- measured slower on c4 (pass 2 0.69 s vs 0.49 s) and, since
+  // the capped grids change the order of the Gram reductions, it broke the
+  // bitwise replay on the chaotic config 3.  The two kernels therefore keep
+  // their full grids and overlap only across stream boundaries.)
   // fold chunk q (blocks q*G+1 .. q*G+nblk) into Z on the second stream
+  // KRY_P2_SERIAL=1: the folds run on the Lanczos stream between chunks
+  // (no concurrency with the regeneration), for A/B measurements
+  const char* ser = getenv("KRY_P2_SERIAL");
+  cudaStream_t fst = (ser && ser[0] == '1') ? c->stream : c->estream;
   auto gemm_chunk = [&](int64_t q, int nblk) -> int {
     const int b = (int)(q % nbuf);
     KRY_CUDA(cudaEventRecord(ev_full[b], c->stream));
-    KRY_CUDA(cudaStreamWaitEvent(c->estream, ev_full[b], 0));
-    KRY_CHECK(launch_chunk_coef_ld(c->estream, c->T.S, c->qy, s, r, (int)(q * G), nblk, ldq, Qc[b]));
+    KRY_CUDA(cudaStreamWaitEvent(fst, ev_full[b], 0));
+    KRY_CHECK(launch_chunk_coef_ld(fst, c->T.S, c->qy, s, r, (int)(q * G), nblk, ldq, Qc[b]));
     cudaEvent_t pe[2] = {nullptr, nullptr};
     if (c->prof) {
       cudaEventCreate(&pe[0]);
       cudaEventCreate(&pe[1]);
-      cudaEventRecord(pe[0], c->estream);
+      cudaEventRecord(pe[0], fst);
     }
-    const bool last = q == nchunks - 1;   // nothing left to overlap: the full grid
-    KRY_CHECK(launch_zacc(c->estream, s, buf[b] + lo_d, slot_d, nblk, Qc[b], ldq, r, c->Z, n,
-                          q > 0, (share && !last) ? sms : 0));
+    KRY_CHECK(launch_zacc(fst, s, buf[b] + lo_d, slot_d, nblk, Qc[b], ldq, r, c->Z, n, q > 0));
     if (c->prof) {
-      cudaEventRecord(pe[1], c->estream);
+      cudaEventRecord(pe[1], fst);
       c->ev_zacc.push_back({pe[0], pe[1]});
       c->zacc_flops += 2.0 * (double)n * nblk * s * r;
     }
-    KRY_CUDA(cudaEventRecord(ev_free[b], c->estream));
+    KRY_CUDA(cudaEventRecord(ev_free[b], fst));
     gemm_used[b] = true;
     return KRY_OK;
   };
@@ -2574,13 +2567,10 @@ int kry_recover(kry_ctx* c, double* zhost) {
     // coefficient solve j on V_j (replay) -- already done by the previous
     // fused launch when coef_ready
     const bool fused = step_on(c) && c->coef_ready;
-    // regeneration of chunk >= 1 shares the SMs with the previous chunk's fold
-    const bool shared = share && j >= G;
     if (!fused) {
       c->coef_ready = false;
       ApplyGramCall ag{blk(j), ld, n, 1, POST_STEP, 0};
       ag.wout = speculate ? wbuf_of(c) : nullptr;
-      ag.grid_cap = shared ? cap_apply : 0;
       rc = run_apply_gram(c, ag);
       if (rc) break;
       if (!speculate) {
@@ -2607,7 +2597,6 @@ int kry_recover(kry_ctx* c, double* zhost) {
     if (speculate) {
       CombineCall cc{vold, ld, blk(j), ld, blk(j + 1), ld, n, j > 1 ? 1 : 0, 1, 1, 1};
       cc.win = wbuf_of(c);
-      cc.grid_cap = shared ? cap_comb : 0;
       rc = run_combine(c, cc, nullptr, nullptr);
       if (rc == KRY_OK) rc = sync_status(c);
       if (rc == KRY_OK) rc = map_status(c, ("second pass step " + std::to_string(j)).c_str());

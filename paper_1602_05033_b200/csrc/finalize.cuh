@@ -21,7 +21,6 @@ int launch_chunk_coef(cudaStream_t st, const double* S, const double* qy, int s,
 int launch_zacc(cudaStream_t st, int s, const double* vbase, int64_t vstride, int nb,
                 const double* Q, int ldq, int r, double* Z, int64_t n, int accumulate,
                 int max_ctas = 0);
-void zacc_footprint(int s, int r, int* regs, size_t* smem);
 int launch_chunk_coef_ld(cudaStream_t st, const double* S, const double* qy, int s, int rank,
                          int blk0, int nblk, int ldq, double* Qc);
 int zacc_ldq(int r);   // padded leading dimension of the Q panel

@@ -184,7 +184,7 @@ struct CombineCall {
   double* vn2 = nullptr;   // optional second copy of V_{m+1} (pass-2 chunk buffer)
   int64_t ldn2 = 0;
   const double* win = nullptr;   // A V_m stored by the apply kernel (n x s, ld s)
-  int grid_cap = 0;              // > 0: at most this many CTAs (co-residency, pass 2)
+  int grid_cap = 0;              // > 0: at most this many CTAs
 };
 int launch_combine(cudaStream_t st, int s, const OpDev& op, const CombineCall& c,
                    DevState* dst, const TStore& T, GramScratch& g, int grid,
@@ -196,7 +196,7 @@ struct ApplyGramCall {
   int post;          // PostMode
   int reverse;
   double* wout = nullptr;   // also store A V (n x s, ld s) for the combine kernel
-  int grid_cap = 0;         // > 0: at most this many CTAs (co-residency, pass 2)
+  int grid_cap = 0;         // > 0: at most this many CTAs
 };
 int launch_apply_gram(cudaStream_t st, int s, const OpDev& op,
                       const ApplyGramCall& c, DevState* dst, const TStore& T,
@@ -220,12 +220,7 @@ int launch_post(cudaStream_t st, int post, DevState* dst, const TStore& T);
 
 int gram_grid_for(int64_t n);
 
-// Pass-2 co-residency: grid caps of the recurrence kernels (apply, combine)
-// such that every SM can host them next to one CTA of the factor
-// accumulation kernel (regs / shared bytes per CTA given), so the memory-
-// bound regeneration and the DMMA-bound accumulation share the SMs
-void pass2_caps(const OpDev& op, int s, int z_regs, size_t z_smem, int* cap_apply,
-                int* cap_combine);
+
 
 // ---------------------------------------------------------------- fused single-pass step
 // One kernel per block-Lanczos step (stencil operators): produces

@@ -1544,56 +1544,6 @@ int launch_explicit_finish(cudaStream_t st, DevState* dst, const TStore& T, int 
 
 #include "step.cuh"
 
-namespace kry {
-// CTAs of a kernel that fit on one SM next to a resident CTA that holds
-// z_regs registers and z_smem shared bytes (allocation granularities of
-// sm_100: 256 registers per warp, 1 KB reserved shared memory per CTA)
-static int fit_next_to(const void* fn, int threads, size_t dyn_smem, int z_regs, size_t z_smem) {
-  cudaFuncAttributes fa;
-  if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess) {
-    cudaGetLastError();
-    return 1;
-  }
-  int dev = 0, regs_sm = 65536, smem_sm = 228 * 1024, thr_sm = 2048;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
-  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-  cudaDeviceGetAttribute(&thr_sm, cudaDevAttrMaxThreadsPerMultiProcessor, dev);
-  const int warps = (threads + 31) / 32;
-  const int regs = ((fa.numRegs * 32 + 255) / 256) * 256 * warps;
-  const size_t smem = fa.sharedSizeBytes + dyn_smem + 1024;
-  const int by_regs = (regs_sm - z_regs) / std::max(regs, 1);
-  const int by_smem = (int)(((size_t)smem_sm - z_smem - 1024) / smem);
-  const int by_thr = (thr_sm - 256) / threads;
-  return std::max(1, std::min(std::min(by_regs, by_smem), by_thr));
-}
 
-void pass2_caps(const OpDev& op, int s, int z_regs, size_t z_smem, int* cap_apply,
-                int* cap_combine) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const void* comb = nullptr;
-  const void* app = nullptr;
-  size_t app_smem = 0;
-  int app_threads = TP;
-  const int mode = apply_mode(op, s);
-#define C(S)                                      \
-  case S:                                         \
-    comb = (const void*)k_combine<S, true>;       \
-    if (mode == 2 && S % 2 == 0) {                \
-      app = (const void*)k_apply_tma<(S % 2 == 0 ? S : 2)>; \
-      app_smem = apt_smem_bytes(S);               \
-      app_threads = APT_NW * 32 + 32;             \
-    } else {                                      \
-      app = (const void*)k_apply_gram<S, 1, true>; \
-    }                                             \
-    break;
-  switch (s) { C(1) C(2) C(3) C(4) C(5) C(6) C(7) C(8) default: break; }
-#undef C
-  *cap_combine = comb ? fit_next_to(comb, TP, 0, z_regs, z_smem) * sms : 0;
-  *cap_apply = app ? fit_next_to(app, app_threads, app_smem, z_regs, z_smem) * sms : 0;
-}
-}  // namespace kry
 
 }  // namespace kry

@@ -226,29 +226,7 @@ static int zacc_s(cudaStream_t st, const double* vbase, int64_t vstride, int nb,
   }
 }
 
-// registers and shared bytes of one k_zacc CTA for (s, r), for the pass-2
-// co-residency caps of the regeneration kernels
-template <int S>
-static void zacc_fp(int r, int* regs, size_t* smem) {
-  constexpr int KP = 4 * ((S + 3) / 4);
-  constexpr int BPS = zbps(S);
-  const int nt = zacc_nt(r);
-  cudaFuncAttributes fa;
-  cudaError_t e = nt == 2 ? cudaFuncGetAttributes(&fa, k_zacc<S, 2>)
-                          : cudaFuncGetAttributes(&fa, k_zacc<S, 4>);
-  if (e != cudaSuccess) { cudaGetLastError(); fa.numRegs = 128; fa.sharedSizeBytes = 0; }
-  *regs = ((fa.numRegs * 32 + 255) / 256) * 256 * ZWARPS;
-  *smem = fa.sharedSizeBytes + 1024 +
-          (size_t)ZST * BPS * (ZBM * zast<S>() + KP * zbst(32 * nt)) * sizeof(double);
-}
-void zacc_footprint(int s, int r, int* regs, size_t* smem) {
-  switch (s) {
-    case 1: zacc_fp<1>(r, regs, smem); break; case 2: zacc_fp<2>(r, regs, smem); break;
-    case 3: zacc_fp<3>(r, regs, smem); break; case 4: zacc_fp<4>(r, regs, smem); break;
-    case 5: zacc_fp<5>(r, regs, smem); break; case 6: zacc_fp<6>(r, regs, smem); break;
-    case 7: zacc_fp<7>(r, regs, smem); break; default: zacc_fp<8>(r, regs, smem); break;
-  }
-}
+
 
 int launch_zacc(cudaStream_t st, int s, const double* vbase, int64_t vstride, int nb,
                 const double* Q, int ldq, int r, double* Z, int64_t n, int accumulate,
