@@ -51,16 +51,16 @@ def step_traffic(config):
     """DRAM bytes of one pass-1 step (k_apply_tma + k_combine launches) from
     the committed ncu --set full captures (profiles/), or None."""
     try:
-        return (_ncu_bytes(os.path.join(ROOT, "profiles", "r1_k_apply_tma_%s_ncu.json" % config))
-                + _ncu_bytes(os.path.join(ROOT, "profiles", "r1_k_combine_%s_ncu.json" % config)))
+        return (_ncu_bytes(os.path.join(ROOT, "profiles", "r2_k_apply_tma_%s_ncu.json" % config))
+                + _ncu_bytes(os.path.join(ROOT, "profiles", "r2_k_combine_%s_ncu.json" % config)))
     except Exception:
         return None
 
 
 def captured_traffic(config):
     """DRAM bytes per k_combine launch from the committed ncu --set full
-    capture of this config (profiles/r1_k_combine_<config>_ncu.json), or None."""
-    path = os.path.join(ROOT, "profiles", "r1_k_combine_%s_ncu.json" % config)
+    capture of this config (profiles/r2_k_combine_<config>_ncu.json), or None."""
+    path = os.path.join(ROOT, "profiles", "r2_k_combine_%s_ncu.json" % config)
     try:
         d = json.load(open(path))
         scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
@@ -519,14 +519,22 @@ def main():
         "phases_s": {"init": r0["init_s"], "pass1": r0["pass1_s"],
                      "checks_in_pass1": r0["check_s"],
                      "finalize": r0["finalize_s"], "pass2": r0["pass2_s"]},
-        "roofline": {"bound": "hbm", "kernel": "pass-1 block-Lanczos step (k_apply_tma + "
-                     "k_combine)", "unit_bytes": b_iter,
-                     "definition": "SURVEY 8(d): B_iter = 24 n s bytes per step / device time "
-                     "per step on the Lanczos stream (CUDA events)",
-                     "achieved": achieved, "peak": hbm, "peak_kind": hbm_kind, "unit": "GB/s",
-                     "frac": achieved / hbm if hbm else None,
-                     "traffic": step_traffic(args.config),
-                     "step_ms": 1000.0 * t_step,
+        "roofline": {"bound": "hbm",
+                     "kernel": "k_combine: pass-1 recurrence, one launch per block-Lanczos "
+                     "iteration (the north star's fused SpMM/recurrence target)",
+                     "definition": "SURVEY 8(d) unit: one iteration, B_iter = 24 n s bytes "
+                     "(read V_{m-1}, V_m, write V_{m+1}; constant stencil, no operator "
+                     "bytes) per launch / average CUDA-event launch time",
+                     "unit_bytes": b_iter, "achieved": b_iter / (comb_avg_ms / 1000.0) / 1e9
+                     if comb_avg_ms > 0 else 0.0, "peak": hbm, "peak_kind": hbm_kind,
+                     "unit": "GB/s",
+                     "frac": (b_iter / (comb_avg_ms / 1000.0) / 1e9 / hbm)
+                     if comb_avg_ms > 0 and hbm else None,
+                     "traffic": captured_traffic(args.config),
+                     "step": {"achieved": achieved, "frac": achieved / hbm if hbm else None,
+                              "step_ms": 1000.0 * t_step, "traffic": step_traffic(args.config),
+                              "note": "B_iter / device time per iteration on the Lanczos "
+                              "stream (apply + combine, 48 n s bytes moved)"},
                      "pass1_loop_frac": (b_iter * r_last["iterations"] / r_last["pass1_s"] / 1e9
                                          / hbm) if r_last["pass1_s"] > 0 else None,
                      "fp64_peak_tflops": {"dmma": dmma.value, "dfma": dfma.value,

@@ -1275,10 +1275,12 @@ static int ctx_create_body(kry_ctx* c, int device, const kry_operator_desc* od, 
   {
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    const char* e = getenv("KRY_STREAM_PRIO");
-    if (e && e[0] == '0') least = greatest = 0;
-    KRY_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamDefault, greatest));
-    KRY_CUDA(cudaStreamCreateWithPriority(&c->estream, cudaStreamDefault, least));
+    const char* e = getenv("KRY_STREAM_PRIO");   // 0: equal, 2: second stream first
+    int pm = greatest, pe = least;
+    if (e && e[0] == '0') pm = pe = 0;
+    if (e && e[0] == '2') { pm = least; pe = greatest; }
+    KRY_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamDefault, pm));
+    KRY_CUDA(cudaStreamCreateWithPriority(&c->estream, cudaStreamDefault, pe));
   }
   KRY_CUDA(cudaEventCreateWithFlags(&c->ev_t, cudaEventDisableTiming));
   KRY_CUDA(cudaEventCreateWithFlags(&c->ev_res[0], cudaEventDisableTiming));

@@ -32,6 +32,7 @@ namespace kry {
 
 namespace {
 constexpr int ZBM = 64, ZST = 3, ZWARPS = 8, ZNTMAX = 8;
+constexpr int ZTPC = 1;   // tiles per CTA (4 and a resident persistent grid measured slower)
 // B row stride (doubles) for a panel of BN columns: conflict-free B fragments
 __host__ __device__ constexpr int zbst(int bn) { return bn + 4; }
 
@@ -84,14 +85,9 @@ __global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__
   for (int e = tid; e < ZST * BPS * ASZ; e += blockDim.x) sA[e] = 0.0;
   for (int e = tid; e < ZST * BPS * BSZ; e += blockDim.x) sB[e] = 0.0;
   __syncthreads();
-  // tiles in a grid-stride loop: one wave of CTAs (pass 2, sharing the SMs
-  // with the regeneration kernels) or one tile per CTA
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-  const int panel = (int)(tile % npanels);
-  const int64_t i0 = (tile / npanels) * ZBM;
-  const int j0 = panel * ZBN;
-  // stage `st` <- blocks grp*BPS .. grp*BPS+BPS-1 (zero-filled past nb)
-  auto load_stage = [&](int grp, int st) {
+  // stage `st` <- blocks grp*BPS .. grp*BPS+BPS-1 of tile (i0, j0), zero-
+  // filled past nb
+  auto load_stage = [&](int64_t i0, int j0, int grp, int st) {
 #pragma unroll
     for (int bb = 0; bb < BPS; ++bb) {
       const int b = grp * BPS + bb;
@@ -122,64 +118,80 @@ __global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__
       }
     }
   };
-  double acc[4][NT][2];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   const int ng = (nb + BPS - 1) / BPS;
+  auto prologue = [&](int64_t tl) {
+    const int64_t i0 = (tl / npanels) * ZBM;
+    const int j0 = (int)(tl % npanels) * ZBN;
 #pragma unroll
-  for (int st = 0; st < ZST - 1; ++st) {
-    if (st < ng) load_stage(st, st);
-    cp_commit();
-  }
-  for (int gi = 0; gi < ng; ++gi) {
-    cp_wait<ZST - 2>();
-    __syncthreads();
-    {   // prefetch group gi + ZST - 1 into the stage freed by group gi - 1
-      const int gn = gi + ZST - 1;
-      if (gn < ng) load_stage(gn, gn % ZST);
+    for (int st = 0; st < ZST - 1; ++st) {
+      if (st < ng) load_stage(i0, j0, st, st);
       cp_commit();
     }
+  };
+  // Tiles in a grid-stride loop.  The next tile's first stages are issued
+  // (cp.async) BEFORE this tile's epilogue, so the Z read-modify-write -- a
+  // latency-bound strided access, 25 % of the stall samples when it ran
+  // alone -- overlaps the copies of the next tile.
+  int64_t tile = blockIdx.x;
+  if (tile < ntiles) prologue(tile);
+  while (tile < ntiles) {
+    const int64_t i0 = (tile / npanels) * ZBM;
+    const int j0 = (int)(tile % npanels) * ZBN;
+    double acc[4][NT][2];
 #pragma unroll
-    for (int bb = 0; bb < BPS; ++bb) {
-      const double* A = sA + ((int64_t)(gi % ZST) * BPS + bb) * ASZ;
-      const double* B = sB + ((int64_t)(gi % ZST) * BPS + bb) * BSZ;
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        double fa[4], fb[NT];
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) fa[mt] = A[(wm * 32 + mt * 8 + g) * AST + 4 * ks + t];
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) fb[nt] = B[(4 * ks + t) * ZBST + wn * 8 * NT + nt * 8 + g];
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) zdmma(acc[mt][nt][0], acc[mt][nt][1], fa[mt], fb[nt]);
+      for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int gi = 0; gi < ng; ++gi) {
+      cp_wait<ZST - 2>();
+      __syncthreads();
+      {   // prefetch group gi + ZST - 1 into the stage freed by group gi - 1
+        const int gn = gi + ZST - 1;
+        if (gn < ng) load_stage(i0, j0, gn, gn % ZST);
+        cp_commit();
       }
-    }
-  }
-  cp_wait<0>();
-  __syncthreads();   // the next tile's prologue overwrites the stages
-  // epilogue: Z (+)= acc; lane (g, t) holds rows ..+g, columns ..+2t, +2t+1
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt) {
-    const int64_t i = i0 + wm * 32 + mt * 8 + g;
-    if (i >= n) continue;
-    double* zr = Z + i * r;
+      for (int bb = 0; bb < BPS; ++bb) {
+        const double* A = sA + ((int64_t)(gi % ZST) * BPS + bb) * ASZ;
+        const double* B = sB + ((int64_t)(gi % ZST) * BPS + bb) * BSZ;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const int j = j0 + wn * 8 * NT + nt * 8 + 2 * t;
+        for (int ks = 0; ks < KS; ++ks) {
+          double fa[4], fb[NT];
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        if (j + e < r) {
-          const double v = acc[mt][nt][e];
-          zr[j + e] = accumulate ? zr[j + e] + v : v;
+          for (int mt = 0; mt < 4; ++mt) fa[mt] = A[(wm * 32 + mt * 8 + g) * AST + 4 * ks + t];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) fb[nt] = B[(4 * ks + t) * ZBST + wn * 8 * NT + nt * 8 + g];
+#pragma unroll
+          for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) zdmma(acc[mt][nt][0], acc[mt][nt][1], fa[mt], fb[nt]);
         }
       }
     }
+    cp_wait<0>();
+    __syncthreads();   // every warp is done with the stages
+    const int64_t next = tile + gridDim.x;
+    if (next < ntiles) prologue(next);
+    // epilogue: Z (+)= acc; lane (g, t) holds rows ..+g, columns ..+2t, +2t+1
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int64_t i = i0 + wm * 32 + mt * 8 + g;
+      if (i >= n) continue;
+      double* zr = Z + i * r;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int j = j0 + wn * 8 * NT + nt * 8 + 2 * t;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (j + e < r) {
+            const double v = acc[mt][nt][e];
+            zr[j + e] = accumulate ? zr[j + e] + v : v;
+          }
+        }
+      }
+    }
+    tile = next;
   }
-  }   // tile loop
 }
 
 // panel width 32 NT: NT = 8 (one panel for r <= 256) measured slower on c4
@@ -201,6 +213,11 @@ static int zacc_go(cudaStream_t st, const double* vbase, int64_t vstride, int nb
   const int npanels = (r + BN - 1) / BN;
   const int64_t ntiles = ((n + ZBM - 1) / ZBM) * npanels;
   int64_t grid = ntiles;
+  // a few tiles per CTA (not one resident wave): the epilogue of one tile
+  // overlaps the copies of the next, and the CTAs stay short enough for the
+  // regeneration kernels on the other stream to be scheduled between them
+  // (a resident persistent grid measured 22 TF/s and serialised pass 2)
+  if (max_ctas == 0) max_ctas = (int)std::min<int64_t>((ntiles + ZTPC - 1) / ZTPC, 0x7fffffff);
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   if (grid > 0x7fffffffLL) return fail(KRY_ERR_DIMENSION, "pass-2 factor too large");
   const size_t smem = (size_t)ZST * BPS * (ZBM * zast<S>() + KP * zbst(BN)) * sizeof(double);

@@ -17,6 +17,8 @@ envelope underestimates the spread of a chaotic deviation; the factor 2 is
 that allowance).  Test infrastructure only (build container).
 
     python tests/golden/make_noise_fixtures.py c3 /tmp/gt upd ldu dlu lud rev cholqr cholqr-upd cholqr-dlu
+    python tests/golden/make_noise_fixtures.py --golden-base=/tmp/gt/lapack/c5_blocks_csr_hist.npz \
+        c5 /tmp/gt upd ldu dlu cholqr cholqr-upd
 """
 import os
 import sys
@@ -26,7 +28,10 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def main(cfg, src, variants):
+def main(cfg, src, variants, golden_base=None):
+    """``golden_base``: the plain run's history evaluated with LAPACK (stored
+    as the golden "surrogate"); the ensemble deviations are always taken
+    between runs evaluated the same way (files in ``src``)."""
     base = np.load(os.path.join(src, "%s_blocks_csr_hist.npz" % cfg))["surrogate_history"]
     tol = float(np.load(os.path.join(src, "%s_blocks_csr.npz" % cfg))["tol"])
     devs, iters = [], []
@@ -48,10 +53,16 @@ def main(cfg, src, variants):
     n = min(len(d) for d in devs)
     env = np.max([d[:n] for d in devs], axis=0)
     out = os.path.join(HERE, "%s_noise.npz" % cfg)
-    np.savez_compressed(out, surrogate=base, env=env, variants=np.array(variants),
+    gold = base if golden_base is None else np.load(golden_base)["surrogate_history"]
+    np.savez_compressed(out, surrogate=gold, env=env, variants=np.array(variants),
                         variant_iters=np.array(iters))
     print("wrote", out, "max rel env", float(np.max(env / base[:n])), "iters", iters)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], sys.argv[3:])
+    args = sys.argv[1:]
+    gb = None
+    if args and args[0].startswith("--golden-base="):
+        gb = args[0].split("=", 1)[1]
+        args = args[1:]
+    main(args[0], args[1], args[2:], gb)
