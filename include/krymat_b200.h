@@ -21,6 +21,9 @@
  *   kry_finalize_sylv     finalisation + truncated_svd      solvers.py:349-358, kernels.py:334-345
  *   kry_recover           two_pass_recover (standard)       solvers.py:130-169
  *   kry_partial_eig       partial_eig_blocktridiag          kernels.py:296-306
+ *   kry_band_eigh         np.linalg.eigh(T_m.to_dense())       solvers.py:256, :350-351
+ *   kry_dense_eigh        np.linalg.eigh (dense symmetric)     kernels.py:316, solvers.py:420
+ *   kry_dense_svd         np.linalg.svd (truncated_svd_factor) kernels.py:337
  *   kry_ctri_lyap_blocks  ctri_lyapunov on given blocks     residual.py:40-59
  *   kry_ctri_sylv_blocks  ctri_sylvester on given blocks    residual.py:62-84
  *   kry_true_lyap_residual true_lyapunov_residual          solvers.py:104-115
@@ -195,6 +198,20 @@ int kry_get_factor(kry_ctx *ctx, double *z);   /* copy device Z to host */
 int kry_partial_eig(int device, int s, int m, const double *diag,
                     const double *sub, double *lam, double *first_rows,
                     double *last_rows);
+/* the finalisation's dense LAPACK calls on the repo's own block Jacobi
+ * kernels (host buffers, column-major): eigh of a symmetric k x k matrix
+ * (a: matrix in, eigenvectors out; w ascending) and the thin SVD of an
+ * m x n matrix (u: m x n, sig descending, vt: n x n); sweeps may be NULL;
+ * semidefinite != 0: the caller knows the spectrum has one sign (no shift) */
+int kry_dense_eigh(int device, int k, double *a, double *w, int *sweeps,
+                   int semidefinite);
+/* eigh of a block-tridiagonal matrix given by its blocks (diag: m s x s,
+ * sub: m-1 s x s, T[b+1,b] = sub[b]) by divide and conquer on the band:
+ * lam ascending (s m), q column-major (s m) x (s m) eigenvectors */
+int kry_band_eigh(int device, int s, int m, const double *diag,
+                  const double *sub, double *lam, double *q);
+int kry_dense_svd(int device, int m, int n, const double *a, double *u,
+                  double *sig, double *vt, int *sweeps);
 int kry_ctri_lyap_blocks(int device, int s, int m, const double *diag,
                          const double *sub, const double *gamma,
                          const double *tau, double *res);

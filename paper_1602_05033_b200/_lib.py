@@ -128,6 +128,11 @@ SIGNATURES = {
     "kry_get_factor": (ctypes.c_int, [_P, dptr]),
     "kry_partial_eig": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, dptr, dptr,
                                        dptr, dptr, dptr]),
+    "kry_band_eigh": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, dptr, dptr, dptr,
+                                     dptr]),
+    "kry_dense_eigh": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, dptr, dptr, iptr, ctypes.c_int]),
+    "kry_dense_svd": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, dptr, dptr, dptr,
+                                     dptr, iptr]),
     "kry_ctri_lyap_blocks": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, dptr,
                                             dptr, dptr, dptr, dptr]),
     "kry_ctri_sylv_blocks": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, dptr,

@@ -5,8 +5,7 @@
 #include "kry_internal.cuh"
 #include "eigen.cuh"
 #include "finalize.cuh"
-#include <cublas_v2.h>
-#include <cusolverDn.h>
+#include "dense.cuh"
 #include <nccl.h>
 #include <atomic>
 #include <chrono>
@@ -257,8 +256,6 @@ using namespace kry;
 struct kry_ctx {
   int dev = 0;
   cudaStream_t stream = nullptr;
-  cublasHandle_t cublas = nullptr;
-  cusolverDnHandle_t solver = nullptr;
   OpDev op{};
   std::vector<void*> op_mem;
   int64_t n = 0;
@@ -1010,75 +1007,74 @@ struct StageTimer {
 };
 
 
-// cuBLAS / cuSOLVER handles are pooled per device: creating them costs
-// ~0.1-0.5 s (it dominated a whole small solve), so a context checks a pair
-// out on first use and returns it on destroy (a handle is never shared by
-// two live contexts, so concurrent solves stay safe).
-struct HandlePair {
-  cublasHandle_t blas;
-  cusolverDnHandle_t solver;
-};
-static std::mutex g_handle_mu;
-static std::vector<HandlePair> g_handle_pool[64];
+// dense symmetric eigendecomposition in place (A k x k -> eigenvectors), w
+// ascending: the repo's block Jacobi kernels (dense.cu)
+int syevd(kry_ctx* c, double* A, int k, double* w, bool semidefinite = false) {
+  return dense_syev(c->stream, A, k, w, nullptr, semidefinite);
+}
 
-int ensure_handles(kry_ctx* c) {
-  if (c->cublas && c->solver) return KRY_OK;
-  HandlePair h{nullptr, nullptr};
-  {
-    std::lock_guard<std::mutex> lock(g_handle_mu);
-    auto& pool = g_handle_pool[c->dev & 63];
-    if (!pool.empty()) {
-      h = pool.back();
-      pool.pop_back();
+// VT[i + j N] = right[j + i N] for i < p (rows beyond p stay zero)
+__global__ void k_right_to_vt(const double* right, int N, int p, double* VT) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)N * p;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e % N), i = (int)(e / N);
+    VT[i + (int64_t)j * N] = right[e];
+  }
+}
+
+// The reduced Sylvester solution is numerically of low rank: cross
+// factorisation Y ~ Lf Uf at the rounding level (dense.cu), then the SVD of
+// the thin product by two one-sided Jacobi iterations.  The singular
+// values beyond the cross rank are below eps sigma_1 and are returned as 0.
+// done = false: rank too large for the thin route (caller: dense Jacobi SVD).
+int svd_lowrank(kry_ctx* a, const double* Y, int M, int N, double* sig, double* U, double* VT,
+                bool* done) {
+  *done = false;
+  const int pmax = std::min(N, 768);
+  double *R = nullptr, *Lf = nullptr, *Uf = nullptr, *left = nullptr, *right = nullptr;
+  auto cleanup = [&]() {
+    for (double* q : {R, Lf, Uf, left, right})
+      if (q) dfree(q);
+  };
+  int rc;
+  if ((rc = dalloc(&R, (size_t)M * N)) || (rc = dalloc(&Lf, (size_t)M * pmax)) ||
+      (rc = dalloc(&Uf, (size_t)pmax * N))) {
+    cleanup();
+    return rc;
+  }
+  StageTimer tm(a->stream);
+  KRY_CUDA(cudaMemcpyAsync(R, Y, (size_t)M * N * sizeof(double), cudaMemcpyDeviceToDevice, a->stream));
+  int p = 0;
+  if ((rc = dense_gecp(a->stream, R, M, N, Lf, Uf, pmax, &p))) { cleanup(); return rc; }
+  tm.mark("finalize: cross factorisation");
+  if (p >= pmax && pmax < N) { cleanup(); return KRY_OK; }
+  cudaMemsetAsync(sig, 0, (size_t)N * sizeof(double), a->stream);
+  cudaMemsetAsync(U, 0, (size_t)M * N * sizeof(double), a->stream);
+  cudaMemsetAsync(VT, 0, (size_t)N * N * sizeof(double), a->stream);
+  if (p > 0) {
+    if ((rc = dalloc(&left, (size_t)M * p)) || (rc = dalloc(&right, (size_t)N * p))) {
+      cleanup();
+      return rc;
     }
+    if ((rc = dense_svd_product(a->stream, Lf, M, Uf, N, p, sig, left, right))) { cleanup(); return rc; }
+    KRY_CUDA(cudaMemcpyAsync(U, left, (size_t)M * p * sizeof(double), cudaMemcpyDeviceToDevice, a->stream));
+    k_right_to_vt<<<(int)std::min<int64_t>(((int64_t)N * p + 255) / 256, 148 * 8), 256, 0, a->stream>>>(
+        right, N, p, VT);
+    count_launch();
+    KRY_CUDA(cudaStreamSynchronize(a->stream));
   }
-  if (!h.blas && cublasCreate(&h.blas) != CUBLAS_STATUS_SUCCESS)
-    return fail(KRY_ERR_CUDA, "cublasCreate failed");
-  if (!h.solver && cusolverDnCreate(&h.solver) != CUSOLVER_STATUS_SUCCESS) {
-    cublasDestroy(h.blas);
-    return fail(KRY_ERR_CUDA, "cusolverDnCreate failed");
-  }
-  c->cublas = h.blas;
-  c->solver = h.solver;
-  cublasSetStream(c->cublas, c->stream);
-  cusolverDnSetStream(c->solver, c->stream);
+  tm.mark("finalize: thin SVD");
+  cleanup();
+  *done = true;
   return KRY_OK;
 }
 
-static void release_handles(kry_ctx* c) {
-  if (!c->cublas || !c->solver) {
-    if (c->cublas) cublasDestroy(c->cublas);
-    if (c->solver) cusolverDnDestroy(c->solver);
-  } else {
-    cublasSetStream(c->cublas, 0);
-    cusolverDnSetStream(c->solver, 0);
-    std::lock_guard<std::mutex> lock(g_handle_mu);
-    g_handle_pool[c->dev & 63].push_back(HandlePair{c->cublas, c->solver});
-  }
-  c->cublas = nullptr;
-  c->solver = nullptr;
-}
-
-// dense symmetric eigendecomposition in place (A k x k -> eigenvectors), w ascending
-int syevd(kry_ctx* c, double* A, int k, double* w) {
-  int lwork = 0;
-  if (cusolverDnDsyevd_bufferSize(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, k,
-                                  A, k, w, &lwork) != CUSOLVER_STATUS_SUCCESS)
-    return fail(KRY_ERR_FACTORIZATION, "syevd buffer query failed");
-  double* work = nullptr;
-  int* info = nullptr;
-  KRY_CHECK(dalloc(&work, (size_t)lwork + 1));
-  KRY_CHECK(dalloc(&info, 1));
-  auto stt = cusolverDnDsyevd(c->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, k, A, k,
-                              w, work, lwork, info);
-  int hinfo = 0;
-  cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
-  cudaStreamSynchronize(c->stream);
-  dfree(work);
-  dfree(info);
-  if (stt != CUSOLVER_STATUS_SUCCESS || hinfo != 0)
-    return fail(KRY_ERR_FACTORIZATION, "dense symmetric eigensolver did not converge");
-  return KRY_OK;
+// thin SVD of Y (M x N column-major, M >= N): sig descending, U (M x N), VT (N x N)
+int svd_thin(kry_ctx* a, double* Y, int M, int N, double* sig, double* U, double* VT) {
+  bool done = false;
+  KRY_CHECK(svd_lowrank(a, Y, M, N, sig, U, VT, &done));
+  if (done) return KRY_OK;
+  return dense_gesvd(a->stream, Y, M, N, sig, U, VT);
 }
 
 struct FinalBufs {
@@ -1100,9 +1096,14 @@ int final_eig(kry_ctx* c, FinalBufs& b, int* k_out) {
   KRY_CHECK(dalloc(&b.lam, (size_t)k));
   KRY_CHECK(dalloc(&b.u, (size_t)k * 8));
   StageTimer tm(c->stream);
-  KRY_CHECK(launch_assemble_T(c->stream, c->T.dsym, c->T.sub, s, m, b.Td));
-  KRY_CHECK(syevd(c, b.Td, k, b.lam));
-  tm.mark("finalize: syevd(T)");
+  if (!getenv("KRY_T_JACOBI")) {
+    KRY_CHECK(dc_band_eigh(c->stream, c->T.dsym, c->T.sub, s, m, b.lam, b.Td));
+    tm.mark("finalize: band D&C eigh(T)");
+  } else {   // A/B: dense block Jacobi on the assembled T
+    KRY_CHECK(launch_assemble_T(c->stream, c->T.dsym, c->T.sub, s, m, b.Td));
+    KRY_CHECK(syevd(c, b.Td, k, b.lam, true));
+    tm.mark("finalize: Jacobi eigh(T)");
+  }
   KRY_CHECK(launch_first_rows_times(c->stream, b.Td, k, s, c->gamma_d, b.u));
   *k_out = k;
   return KRY_OK;
@@ -1447,7 +1448,6 @@ void kry_ctx_destroy(kry_ctx* c) {
   for (auto& e : c->ev_comb) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   for (auto& e : c->ev_zacc) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   cudaStreamSynchronize(c->stream);
-  release_handles(c);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->loop) {
     kry_loop* g = c->loop;
@@ -2051,11 +2051,95 @@ int kry_solve_sylv_pass1(kry_ctx* a, kry_ctx* b, double tol, int max_m, int chec
   return fail(KRY_ERR_CONVERGENCE, *reason == 2 ? "invariant" : "max_m");
 }
 
+// Bm[j][c] = W[j + (p - 1 - c) p] for c < r (eigenvectors of the r largest
+// eigenvalues, W column-major with ascending eigenvalues), 0 for r <= c < ld
+__global__ void k_top_cols_rows(const double* W, int p, int r, int ld, double* Bm) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)p * ld;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % ld), j = (int)(e / ld);
+    Bm[e] = c < r ? W[j + (int64_t)(p - 1 - c) * p] : 0.0;
+  }
+}
+
+// Truncated factor of the reduced Lyapunov solution without forming it
+// (solvers.py:259-263, truncated_spd_factor kernels.py:309-331):
+//   Ytilde = M, M_ij = (u_i . u_j) / |lam_i + lam_j|  (PSD, low numerical rank)
+//   M ~ L L^T            pivoted Cholesky, p columns (dense.cu)
+//   S = L^T L = W D W^T   p x p: the nonzero eigenvalues of M are those of S,
+//                         the eigenvectors L W D^{-1/2}
+//   factor = (L W_r D_r^{-1/2}) D_r^{1/2} = L W_r,   qy = Q L W_r
+// Returns 1 (not an error) when the factorisation did not reach the rounding
+// level within pmax columns: the caller takes the dense route.
+static int finalize_lyap_lowrank(kry_ctx* c, FinalBufs& b, int k, double eps, double lmax,
+                                 double* hout, bool* done) {
+  *done = false;
+  const int pmax = std::min(k, 1024);
+  const int ldl = (pmax + 1) & ~1;
+  double *L = nullptr, *S = nullptr, *w = nullptr, *mind = nullptr, *work = nullptr,
+         *outd = nullptr, *Bm = nullptr, *fr = nullptr;
+  auto cleanup = [&]() {
+    for (double* q : {L, S, w, mind, work, outd, Bm, fr})
+      if (q) dfree(q);
+  };
+  int rc;
+  if ((rc = dalloc(&L, (size_t)k * ldl)) || (rc = dalloc(&mind, 8)) || (rc = dalloc(&outd, 8))) {
+    cleanup();
+    return rc;
+  }
+  StageTimer tm(c->stream);
+  int p = 0;
+  if ((rc = dense_pchol_cauchy(c->stream, b.u, b.lam, k, c->s, L, ldl, pmax, &p))) {
+    cleanup();
+    return rc;
+  }
+  tm.mark("finalize: pivoted Cholesky");
+  if (p >= pmax && pmax < k) { cleanup(); return KRY_OK; }
+  if (p < 1) p = 1;
+  if ((rc = dalloc(&S, (size_t)p * p)) || (rc = dalloc(&w, (size_t)p)) ||
+      (rc = dalloc(&work, (size_t)p + 8))) {
+    cleanup();
+    return rc;
+  }
+  rc = dense_gemm(c->stream, p, p, k, L, ldl, 1, L, ldl, nullptr, S, p, nullptr);
+  if (rc == KRY_OK) rc = dense_syev(c->stream, S, p, w, nullptr, true);
+  tm.mark("finalize: eig(L^T L)");
+  const double md = 2.0 * fabs(lmax);   // min |lam_i + lam_j| of a negative spectrum
+  if (rc == KRY_OK)
+    rc = cudaMemcpyAsync(mind, &md, sizeof(double), cudaMemcpyHostToDevice, c->stream) == cudaSuccess
+             ? KRY_OK : fail(KRY_ERR_CUDA, "finalize copy failed");
+  if (rc == KRY_OK) rc = launch_truncate(c->stream, w, p, 0, eps, mind, 1, work, outd);
+  if (rc != KRY_OK) { cleanup(); return rc; }
+  KRY_CUDA(cudaMemcpyAsync(hout, outd, 5 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  KRY_CUDA(cudaStreamSynchronize(c->stream));
+  const int r = (int)hout[0];
+  if (c->qy) dfree(c->qy);
+  c->qy = nullptr;
+  c->rank = r;
+  if (r > 0) {
+    const int ld = (r + 1) & ~1;
+    if ((rc = dalloc(&Bm, (size_t)p * ld)) || (rc = dalloc(&fr, (size_t)k * ld)) ||
+        (rc = dalloc(&c->qy, (size_t)k * r))) {
+      cleanup();
+      return rc;
+    }
+    k_top_cols_rows<<<(int)std::min<int64_t>(((int64_t)p * ld + 255) / 256, 148 * 8), 256, 0,
+                      c->stream>>>(S, p, r, ld, Bm);
+    count_launch();
+    rc = dense_gemm(c->stream, k, ld, p, L, ldl, 0, Bm, ld, nullptr, fr, ld, nullptr);
+    // qy (row-major k x r) = Q fr, Q column-major (eigenvectors in columns)
+    if (rc == KRY_OK) rc = dense_gemm(c->stream, k, r, k, b.Td, k, 1, fr, ld, nullptr, c->qy, r, nullptr);
+    if (rc == KRY_OK) KRY_CUDA(cudaStreamSynchronize(c->stream));
+    tm.mark("finalize: qy = Q L W_r");
+  }
+  cleanup();
+  if (rc == KRY_OK) *done = true;
+  return rc;
+}
+
 int kry_finalize_lyap(kry_ctx* c, double eps, int* rank, double* discarded) {
   KRY_CUDA(cudaSetDevice(c->dev));
   if (c->m_final < 1) c->m_final = c->m;
   if (c->m_final < 1) return fail(KRY_ERR_STATE, "nothing to finalise");
-  KRY_CHECK(ensure_handles(c));
   FinalBufs b;
   int k = 0;
   int rc = final_eig(c, b, &k);
@@ -2074,19 +2158,24 @@ int kry_finalize_lyap(kry_ctx* c, double eps, int* rank, double* discarded) {
     cleanup();
     return fail(KRY_ERR_INDEFINITE, "projected matrix is not negative definite");
   }
-  if ((rc = dalloc(&Y, (size_t)k * k)) || (rc = dalloc(&mu, (size_t)k)) ||
-      (rc = dalloc(&mind, 1024)) || (rc = dalloc(&work, (size_t)k)) || (rc = dalloc(&outd, 8))) {
-    cleanup();
-    return rc;
-  }
-  int nparts = 0;
-  StageTimer tm(c->stream);
-  rc = launch_ytilde(c->stream, b.u, b.lam, k, b.u, b.lam, k, c->s, Y, k, mind, &nparts);
-  if (rc == KRY_OK) rc = syevd(c, Y, k, mu);
-  tm.mark("finalize: syevd(Ytilde)");
-  if (rc == KRY_OK) rc = launch_truncate(c->stream, mu, k, 0, eps, mind, nparts, work, outd);
+  bool lowrank_done = false;
+  rc = finalize_lyap_lowrank(c, b, k, eps, lmax, hout, &lowrank_done);
   if (rc != KRY_OK) { cleanup(); return rc; }
-  KRY_CUDA(cudaMemcpy(hout, outd, 5 * sizeof(double), cudaMemcpyDeviceToHost));
+  if (!lowrank_done) {
+    if ((rc = dalloc(&Y, (size_t)k * k)) || (rc = dalloc(&mu, (size_t)k)) ||
+        (rc = dalloc(&mind, 1024)) || (rc = dalloc(&work, (size_t)k)) || (rc = dalloc(&outd, 8))) {
+      cleanup();
+      return rc;
+    }
+    int nparts = 0;
+    StageTimer tm(c->stream);
+    rc = launch_ytilde(c->stream, b.u, b.lam, k, b.u, b.lam, k, c->s, Y, k, mind, &nparts);
+    if (rc == KRY_OK) rc = syevd(c, Y, k, mu, true);
+    tm.mark("finalize: syevd(Ytilde)");
+    if (rc == KRY_OK) rc = launch_truncate(c->stream, mu, k, 0, eps, mind, nparts, work, outd);
+    if (rc != KRY_OK) { cleanup(); return rc; }
+    KRY_CUDA(cudaMemcpy(hout, outd, 5 * sizeof(double), cudaMemcpyDeviceToHost));
+  }
   double lmin_abs = 0.0;
   {
     double l0;
@@ -2107,7 +2196,9 @@ int kry_finalize_lyap(kry_ctx* c, double eps, int* rank, double* discarded) {
   }
   const int r = (int)hout[0];
   c->discarded = hout[1];
-  if (r > 0) {
+  if (lowrank_done) {
+    // qy is set
+  } else if (r > 0) {
     if ((rc = dalloc(&factor, (size_t)k * r))) { cleanup(); return rc; }
     rc = launch_scale_factor(c->stream, Y, k, mu, k, r, 0, 0, factor);
     if (rc == KRY_OK) rc = set_qy(c, b.Td, k, factor, r);
@@ -2126,8 +2217,6 @@ int kry_finalize_sylv(kry_ctx* a, kry_ctx* bb, double eps, int* rank, double* di
   KRY_CUDA(cudaSetDevice(a->dev));
   if (a->m_final < 1) a->m_final = a->m;
   if (bb->m_final < 1) bb->m_final = bb->m;
-  KRY_CHECK(ensure_handles(a));
-  KRY_CHECK(ensure_handles(bb));
   KRY_CUDA(cudaStreamSynchronize(bb->stream));
   FinalBufs fa, fb;
   int kA = 0, kB = 0;
@@ -2170,21 +2259,7 @@ int kry_finalize_sylv(kry_ctx* a, kry_ctx* bb, double eps, int* rank, double* di
   else
     rc = launch_ytilde(a->stream, fb.u, fb.lam, kB, fa.u, fa.lam, kA, a->s, Y, kB, mind, &nparts);
   if (rc != KRY_OK) { cleanup(); return rc; }
-  int lwork = 0;
-  if (cusolverDnDgesvd_bufferSize(a->solver, M, N, &lwork) != CUSOLVER_STATUS_SUCCESS) {
-    cleanup();
-    return fail(KRY_ERR_FACTORIZATION, "gesvd buffer query failed");
-  }
-  if ((rc = dalloc(&gw, (size_t)lwork + 1))) { cleanup(); return rc; }
-  signed char jobu = 'S', jobvt = 'S';
-  auto sst = cusolverDnDgesvd(a->solver, jobu, jobvt, M, N, Y, M, sig, U, M, VT, N, gw, lwork,
-                              nullptr, info);
-  int hinfo = 0;
-  KRY_CUDA(cudaMemcpy(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost));
-  if (sst != CUSOLVER_STATUS_SUCCESS || hinfo != 0) {
-    cleanup();
-    return fail(KRY_ERR_FACTORIZATION, "SVD did not converge");
-  }
+  if ((rc = svd_thin(a, Y, M, N, sig, U, VT)) != KRY_OK) { cleanup(); return rc; }
   rc = launch_truncate(a->stream, sig, N, 1, eps, mind, nparts, work, outd);
   double hout[8];
   KRY_CUDA(cudaMemcpy(hout, outd, 5 * sizeof(double), cudaMemcpyDeviceToHost));
@@ -2238,7 +2313,6 @@ int kry_finalize_sylv(kry_ctx* a, kry_ctx* bb, double eps, int* rank, double* di
 int kry_sylv1_setup(kry_ctx* c, int n2, const double* b, const double* c2, double* ups) {
   KRY_CUDA(cudaSetDevice(c->dev));
   if (n2 < 1) return fail(KRY_ERR_DIMENSION, "B must be a non-empty square matrix");
-  KRY_CHECK(ensure_handles(c));
   for (double* p : {c->d1_ups, c->d1_P, c->d1_v, c->d1_in, c->d1_eye, c->d1_z2}) dfree(p);
   c->d1_ups = c->d1_P = c->d1_v = c->d1_in = c->d1_eye = c->d1_z2 = nullptr;
   c->d1_n2 = n2;
@@ -2313,7 +2387,6 @@ int kry_finalize_sylv1(kry_ctx* a, double eps, int* rank, double* discarded, dou
     return KRY_OK;
   }
   if (a->m_final < 1) a->m_final = a->m;
-  KRY_CHECK(ensure_handles(a));
   const int n2 = a->d1_n2;
   FinalBufs fa;
   int kA = 0;
@@ -2355,21 +2428,7 @@ int kry_finalize_sylv1(kry_ctx* a, double eps, int* rank, double* discarded, dou
     rc = launch_ytilde(a->stream, a->d1_v, a->d1_ups, n2, fa.u, fa.lam, kA, a->s, Y, n2, mind,
                        &nparts);
   if (rc != KRY_OK) { cleanup(); return rc; }
-  int lwork = 0;
-  if (cusolverDnDgesvd_bufferSize(a->solver, M, N, &lwork) != CUSOLVER_STATUS_SUCCESS) {
-    cleanup();
-    return fail(KRY_ERR_FACTORIZATION, "gesvd buffer query failed");
-  }
-  if ((rc = dalloc(&gw, (size_t)lwork + 1))) { cleanup(); return rc; }
-  signed char jobu = 'S', jobvt = 'S';
-  auto sst = cusolverDnDgesvd(a->solver, jobu, jobvt, M, N, Y, M, sig, U, M, VT, N, gw, lwork,
-                              nullptr, info);
-  int hinfo = 0;
-  KRY_CUDA(cudaMemcpy(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost));
-  if (sst != CUSOLVER_STATUS_SUCCESS || hinfo != 0) {
-    cleanup();
-    return fail(KRY_ERR_FACTORIZATION, "SVD did not converge");
-  }
+  if ((rc = svd_thin(a, Y, M, N, sig, U, VT)) != KRY_OK) { cleanup(); return rc; }
   rc = launch_truncate(a->stream, sig, N, 1, eps, mind, nparts, work, outd);
   double hout[8];
   KRY_CUDA(cudaMemcpy(hout, outd, 5 * sizeof(double), cudaMemcpyDeviceToHost));
@@ -2396,11 +2455,19 @@ int kry_finalize_sylv1(kry_ctx* a, double eps, int* rank, double* discarded, dou
     }
     rc = set_qy(a, fa.Td, kA, f1, r);
     // z2 (row-major n2 x r) = col-major (r x n2) = f2^T P^T
-    const double one = 1.0, zero = 0.0;
-    if (rc == KRY_OK &&
-        cublasDgemm(a->cublas, CUBLAS_OP_T, CUBLAS_OP_T, r, n2, n2, &one, f2, n2, a->d1_P, n2,
-                    &zero, a->d1_z2, r) != CUBLAS_STATUS_SUCCESS)
-      rc = fail(KRY_ERR_CUDA, "cublasDgemm (z2) failed");
+    if (rc == KRY_OK) {
+      double* f2r = nullptr;
+      const int ld = (r + 1) & ~1;
+      if ((rc = dalloc(&f2r, (size_t)n2 * ld)) == KRY_OK) {
+        const int64_t tot = (int64_t)n2 * ld;
+        k_cols_to_rows<<<(int)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, a->stream>>>(
+            f2, n2, r, ld, f2r);
+        count_launch();
+        // z2 = P f2 (P column-major eigenvectors of B)
+        rc = dense_gemm(a->stream, n2, r, n2, a->d1_P, n2, 1, f2r, ld, nullptr, a->d1_z2, r, nullptr);
+        dfree(f2r);
+      }
+    }
   } else {
     set_qy(a, fa.Td, kA, nullptr, 0);
   }
@@ -2653,7 +2720,6 @@ int kry_set_qy(kry_ctx* c, int m, int t, const double* qy) {
   KRY_CUDA(cudaSetDevice(c->dev));
   if (m < 1 || m > c->m) return fail(KRY_ERR_DIMENSION, "qy covers more blocks than generated");
   if (t < 0) return fail(KRY_ERR_DIMENSION, "negative factor rank");
-  KRY_CHECK(ensure_handles(c));
   if (c->qy) dfree(c->qy);
   c->qy = nullptr;
   c->m_final = m;
@@ -2718,6 +2784,40 @@ struct Standalone {
 };
 }  // namespace
 
+// np.linalg.eigh(BlockTridiagonal.to_dense()) on the band divide-and-conquer
+// solver of the finalisation: lam ascending (k), q column-major k x k (host)
+int kry_band_eigh(int device, int s, int m, const double* diag, const double* sub, double* lam,
+                  double* q) {
+  if (s < 1 || s > KRY_SMAX || m < 1) return fail(KRY_ERR_ARGUMENT, "bad block sizes");
+  KRY_CUDA(cudaSetDevice(device));
+  const int k = s * m;
+  std::vector<double> hd((size_t)(m + 1) * 64, 0.0), hs((size_t)(m + 1) * 64, 0.0);
+  for (int b = 0; b < m; ++b)
+    for (int r = 0; r < s; ++r)
+      for (int c = 0; c < s; ++c) hd[(size_t)b * 64 + r * 8 + c] = diag[((size_t)b * s + r) * s + c];
+  for (int b = 0; b + 1 < m; ++b)
+    for (int r = 0; r < s; ++r)
+      for (int c = 0; c < s; ++c) hs[(size_t)b * 64 + r * 8 + c] = sub[((size_t)b * s + r) * s + c];
+  double *dd = nullptr, *ds = nullptr, *dl = nullptr, *dq = nullptr;
+  int rc;
+  if ((rc = dalloc(&dd, hd.size())) || (rc = dalloc(&ds, hs.size())) || (rc = dalloc(&dl, (size_t)k)) ||
+      (rc = dalloc(&dq, (size_t)k * k))) {
+    dfree(dd); dfree(ds); dfree(dl); dfree(dq);
+    return rc;
+  }
+  cudaStream_t st = 0;
+  cudaMemcpy(dd, hd.data(), hd.size() * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemcpy(ds, hs.data(), hs.size() * sizeof(double), cudaMemcpyHostToDevice);
+  rc = dc_band_eigh(st, dd, ds, s, m, dl, dq);
+  if (rc == KRY_OK) {
+    cudaMemcpy(lam, dl, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost);
+    if (cudaMemcpy(q, dq, (size_t)k * k * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+      rc = fail(KRY_ERR_CUDA, "band eigh copy failed");
+  }
+  dfree(dd); dfree(ds); dfree(dl); dfree(dq);
+  return rc;
+}
+
 int kry_partial_eig(int device, int s, int m, const double* diag, const double* sub, double* lam,
                     double* first_rows, double* last_rows) {
   if (s < 1 || s > KRY_SMAX || m < 1) return fail(KRY_ERR_ARGUMENT, "bad block sizes");
@@ -2737,6 +2837,53 @@ int kry_partial_eig(int device, int s, int m, const double* diag, const double* 
   KRY_CUDA(cudaStreamSynchronize(S.st));
   dfree(lastd);
   return KRY_OK;
+}
+
+// np.linalg.eigh / np.linalg.svd of the finalisation on the repo's block
+// Jacobi kernels (dense.cu), host buffers in and out
+int kry_dense_eigh(int device, int k, double* a, double* w, int* sweeps, int semidefinite) {
+  if (k < 1) return fail(KRY_ERR_ARGUMENT, "bad matrix order");
+  KRY_CUDA(cudaSetDevice(device));
+  double *A = nullptr, *W = nullptr;
+  int rc;
+  if ((rc = dalloc(&A, (size_t)k * k)) || (rc = dalloc(&W, (size_t)k))) {
+    dfree(A); dfree(W);
+    return rc;
+  }
+  cudaStream_t st = 0;
+  cudaMemcpyAsync(A, a, (size_t)k * k * sizeof(double), cudaMemcpyHostToDevice, st);
+  rc = dense_syev(st, A, k, W, sweeps, semidefinite != 0);
+  if (rc == KRY_OK) {
+    cudaMemcpyAsync(a, A, (size_t)k * k * sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(w, W, (size_t)k * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) rc = fail(KRY_ERR_CUDA, "dense eigh copy failed");
+  }
+  dfree(A); dfree(W);
+  return rc;
+}
+
+int kry_dense_svd(int device, int m, int n, const double* a, double* u, double* sig, double* vt,
+                  int* sweeps) {
+  if (m < 1 || n < 1) return fail(KRY_ERR_ARGUMENT, "bad matrix shape");
+  KRY_CUDA(cudaSetDevice(device));
+  double *A = nullptr, *U = nullptr, *S = nullptr, *VT = nullptr;
+  int rc;
+  if ((rc = dalloc(&A, (size_t)m * n)) || (rc = dalloc(&U, (size_t)m * n)) ||
+      (rc = dalloc(&S, (size_t)n)) || (rc = dalloc(&VT, (size_t)n * n))) {
+    dfree(A); dfree(U); dfree(S); dfree(VT);
+    return rc;
+  }
+  cudaStream_t st = 0;
+  cudaMemcpyAsync(A, a, (size_t)m * n * sizeof(double), cudaMemcpyHostToDevice, st);
+  rc = dense_gesvd(st, A, m, n, S, U, VT, sweeps);
+  if (rc == KRY_OK) {
+    cudaMemcpyAsync(u, U, (size_t)m * n * sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(sig, S, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(vt, VT, (size_t)n * n * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) rc = fail(KRY_ERR_CUDA, "dense svd copy failed");
+  }
+  dfree(A); dfree(U); dfree(S); dfree(VT);
+  return rc;
 }
 
 static int upload88(cudaStream_t st, double* dst, const double* h, int s) {
@@ -2814,7 +2961,6 @@ int kry_ctri_sylv_blocks(int device, int s, int m1, const double* diag1, const d
 
 int kry_true_lyap_residual(kry_ctx* c, const double* z, int t, const double* ch, double* res) {
   KRY_CUDA(cudaSetDevice(c->dev));
-  KRY_CHECK(ensure_handles(c));
   const int s = c->s;
   const int64_t n = c->n;
   const int p = 2 * t + s;
@@ -2838,11 +2984,8 @@ int kry_true_lyap_residual(kry_ctx* c, const double* z, int t, const double* ch,
                              t * sizeof(double), n, cudaMemcpyDeviceToDevice, c->stream));
   KRY_CUDA(cudaMemcpy2DAsync(M + 2 * t, ldm * sizeof(double), ch, s * sizeof(double),
                              s * sizeof(double), n, cudaMemcpyHostToDevice, c->stream));
-  const double one = 1.0, zero = 0.0;
-  // G = M^T M : col-major view of M is p x n (ld ldm)
-  if (cublasDgemm(c->cublas, CUBLAS_OP_N, CUBLAS_OP_T, p, p, (int)n, &one, M, ldm, M, ldm, &zero,
-                  G, p) != CUBLAS_STATUS_SUCCESS)
-    return fail(KRY_ERR_CUDA, "cublasDgemm (verify) failed");
+  // G = M^T M (M row-major n x p, stride ldm) on the repo's DMMA GEMM
+  KRY_CHECK(dense_gemm(c->stream, p, p, (int)n, M, ldm, 1, M, ldm, nullptr, G, p, nullptr));
   std::vector<double> h((size_t)p * p);
   KRY_CUDA(cudaMemcpyAsync(h.data(), G, h.size() * sizeof(double), cudaMemcpyDeviceToHost,
                            c->stream));

@@ -1,0 +1,1051 @@
+// Dense symmetric eigensolver and SVD for the finalisation (sm_100a, fp64).
+//
+// Reference: np.linalg.eigh(t_dense) (solvers.py:256, :350-351),
+// eigh(Ytilde) in truncated_spd_factor (kernels.py:316), np.linalg.svd in
+// truncated_svd_factor (kernels.py:337) and the eigh of the dense side B of
+// the one-sided Sylvester solver (solvers.py:420).
+//
+// B200 design: a one-sided BLOCK JACOBI method (Hestenes) on DMMA.  The
+// matrix A (M x N, column-major) is orthogonalised from the right,
+// A V = U Sigma, by sweeps over all pairs of column blocks (width 16; round-
+// robin tournament, N/32 independent pairs per round = one CTA each).  A CTA
+//   1. streams its M x 32 panel once and forms the 32 x 32 Gram matrix
+//      G = P^T P on the fp64 tensor cores (m8n8k4 DMMA),
+//   2. diagonalises G in shared memory by a parallel cyclic two-sided Jacobi
+//      iteration (16 disjoint rotations per step), accumulating R,
+//   3. streams the panel again, P <- P R (and the matching panel of V),
+//      again on DMMA.
+// The Gram entries carry a relative error of eps ||a_i|| ||a_j||, so the
+// stopping rule |a_i . a_j| <= tol ||a_i|| ||a_j|| for EVERY pair gives the
+// singular values (column norms) to high relative accuracy, and V is a
+// product of plane rotations (orthogonal to roundoff).  For a symmetric A
+// the columns of V are its eigenvectors and lambda_i = v_i . (A v_i) comes
+// with its sign from the final columns.  Everything runs on one stream; the
+// host reads one convergence word per sweep.
+#include "dense.cuh"
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+namespace kry {
+
+namespace {
+
+constexpr double DEPS = 2.220446049250313e-16;
+constexpr int JCH = 64;    // rows per streamed chunk
+constexpr int JPS = 72;    // chunk column stride in shared memory (== 8 mod 32)
+
+__device__ __forceinline__ void jdmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+// pair p of round r of the circle-method tournament on n (even) players
+__host__ __device__ __forceinline__ void tournament_pair(int n, int r, int p, int* a, int* b) {
+  if (p == 0) {
+    *a = n - 1;
+    *b = r;
+  } else {
+    *a = (r + p) % (n - 1);
+    *b = (r - p + (n - 1)) % (n - 1);
+  }
+}
+
+// One round of the block tournament: CTA = one pair of column blocks.
+template <int BW>
+__global__ void __launch_bounds__(256) k_jac_round(double* __restrict__ A, int64_t lda, int M,
+                                                   int N, double* __restrict__ V, int64_t ldv,
+                                                   int NB, int round, double tol,
+                                                   const double* __restrict__ floor2p,
+                                                   int inner_sweeps, int* __restrict__ flag) {
+  constexpr int PW = 2 * BW;          // panel width
+  constexpr int GS = PW + 1;          // G row stride
+  constexpr int RS = PW + 8;          // R row stride (== 8 mod 32 for PW = 32)
+  constexpr int NPAIR = PW / 2;
+  constexpr int PER = PW * JCH / 256; // chunk elements per thread
+  constexpr int TPW = (PW / 8) * (PW / 8) / 8;   // Gram tiles per warp
+  static_assert(PW == 32, "panel of 32 columns");
+  __shared__ double sP[PW * JPS];
+  __shared__ double sG[PW * GS];
+  __shared__ double sR[PW * RS];
+  __shared__ double s_c[NPAIR], s_s[NPAIR];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  int bi, bj;
+  tournament_pair(NB, round, blockIdx.x, &bi, &bj);
+  if (bi > bj) { const int x = bi; bi = bj; bj = x; }
+  if ((int64_t)bi * BW >= N) return;   // phantom pair
+  const double floor2 = *floor2p;
+  auto gcol = [&](int c) -> int { return (c < BW) ? bi * BW + c : bj * BW + (c - BW); };
+  // chunk element q of this thread: column q-th slice, row tid % 64
+  const int er = tid & (JCH - 1);
+  const int ec0 = tid >> 6;            // + 4 q
+  double pre[PER];
+  auto gload = [&](const double* X, int64_t ldx, int rows, int row0) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int c = ec0 + 4 * q;
+      const int gc = gcol(c);
+      const int r = row0 + er;
+      pre[q] = (gc < N && r < rows) ? X[(int64_t)gc * ldx + r] : 0.0;
+    }
+  };
+  auto sstore = [&]() {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) sP[(ec0 + 4 * q) * JPS + er] = pre[q];
+  };
+  // ---- phase 1: G = P^T P
+  {
+    double acc[TPW][2];
+#pragma unroll
+    for (int e = 0; e < TPW; ++e) acc[e][0] = acc[e][1] = 0.0;
+    const int nch = (M + JCH - 1) / JCH;
+    gload(A, lda, M, 0);
+    for (int ch = 0; ch < nch; ++ch) {
+      __syncthreads();
+      sstore();
+      __syncthreads();
+      if (ch + 1 < nch) gload(A, lda, M, (ch + 1) * JCH);
+#pragma unroll
+      for (int ks = 0; ks < JCH / 4; ++ks) {
+#pragma unroll
+        for (int e = 0; e < TPW; ++e) {
+          const int idx = warp * TPW + e, ti = idx / (PW / 8), tj = idx % (PW / 8);
+          const double a = sP[(ti * 8 + g) * JPS + ks * 4 + t];
+          const double b = sP[(tj * 8 + g) * JPS + ks * 4 + t];
+          jdmma(acc[e][0], acc[e][1], a, b);
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < TPW; ++e) {
+      const int idx = warp * TPW + e, ti = idx / (PW / 8), tj = idx % (PW / 8);
+      sG[(ti * 8 + g) * GS + tj * 8 + 2 * t] = acc[e][0];
+      sG[(ti * 8 + g) * GS + tj * 8 + 2 * t + 1] = acc[e][1];
+    }
+  }
+  __syncthreads();
+  // ---- phase 2: G -> diagonal by a parallel cyclic two-sided Jacobi iteration,
+  // rotations accumulated in R.  A pair (i, j) rotates when
+  //   |g_ij| > tol sqrt(g_ii g_jj)  and  min(g_ii, g_jj) > floor2
+  // (floor2 = (tiny ||A||)^2: columns at the rounding-noise level of a rank-
+  // deficient matrix are left alone; their norms are below every singular
+  // value that matters and V stays orthogonal).  Before every inner sweep the
+  // whole block scans G: nothing to rotate -> done; only cross pairs (one
+  // column from each block, the usual case after the first outer sweeps) ->
+  // the 16 rounds of the bipartite schedule instead of the full 31.
+  bool first = true;
+  for (int isw = 0; isw < inner_sweeps; ++isw) {
+    int need = 0;   // bit 0: a cross pair, bit 1: a pair inside a block
+    for (int e = tid; e < PW * PW; e += 256) {
+      const int i = e / PW, j = e % PW;
+      if (i < j) {
+        const double gi = sG[i * GS + i], gj = sG[j * GS + j];
+        const double o = fabs(sG[i * GS + j]);
+        if (fmin(gi, gj) > floor2 && o * o > tol * tol * gi * gj) need |= ((i < BW) == (j < BW)) ? 2 : 1;
+      }
+    }
+    {   // (__syncthreads_or returns a truth value, not the bitwise OR)
+      const int in_block = __syncthreads_or(need & 2), cross = __syncthreads_or(need & 1);
+      need = (in_block ? 2 : 0) | (cross ? 1 : 0);
+    }
+    if (!need) break;
+    if (first) {
+      first = false;
+      if (tid == 0) *flag = 1;
+      for (int e = tid; e < PW * RS; e += 256) sR[e] = 0.0;
+      __syncthreads();
+      if (tid < PW) sR[tid * RS + tid] = 1.0;
+      __syncthreads();
+    }
+    const bool bip = !(need & 2);
+    const int nrounds = bip ? BW : PW - 1;
+    for (int rr = 0; rr < nrounds; ++rr) {
+      // pair j = (pj, qj); this thread also owns the 2 x 2 block of G at
+      // rows (pair tid / 16) x columns (pair tid % 16)
+      auto pair_of = [&](int j, int* p, int* q) {
+        if (bip) { *p = j; *q = BW + ((j + rr) % BW); }
+        else tournament_pair(PW, rr, j, p, q);
+      };
+      int pc, qc, pr, qr;
+      pair_of(tid % NPAIR, &pc, &qc);
+      pair_of(tid / NPAIR, &pr, &qr);
+      if (tid < NPAIR) {
+        const double gpp = sG[pc * GS + pc], gqq = sG[qc * GS + qc], gpq = sG[pc * GS + qc];
+        double c = 1.0, s = 0.0;
+        if (fmin(gpp, gqq) > floor2 && gpq * gpq > tol * tol * gpp * gqq) {
+          // t^2 + 2 tau t - 1 = 0, tau = (gqq - gpp) / (2 gpq): the smaller root
+          const double d = gqq - gpp, b2 = 2.0 * gpq;
+          const double tt = (d >= 0.0 ? b2 : -b2) / (fabs(d) + sqrt(fma(d, d, b2 * b2)));
+          c = rsqrt(fma(tt, tt, 1.0));
+          s = tt * c;
+        }
+        s_c[tid] = c;
+        s_s[tid] = s;
+      }
+      __syncthreads();
+      {   // G <- J^T G J on this thread's 2 x 2 block
+        const double cc = s_c[tid % NPAIR], sc = s_s[tid % NPAIR];
+        const double cr = s_c[tid / NPAIR], sr = s_s[tid / NPAIR];
+        if (sc != 0.0 || sr != 0.0) {
+          const double a = sG[pr * GS + pc], b = sG[pr * GS + qc];
+          const double c = sG[qr * GS + pc], d = sG[qr * GS + qc];
+          const double a1 = cc * a - sc * b, b1 = sc * a + cc * b;
+          const double c1 = cc * c - sc * d, d1 = sc * c + cc * d;
+          sG[pr * GS + pc] = cr * a1 - sr * c1;
+          sG[qr * GS + pc] = sr * a1 + cr * c1;
+          sG[pr * GS + qc] = cr * b1 - sr * d1;
+          sG[qr * GS + qc] = sr * b1 + cr * d1;
+        }
+        // R <- R J  (item = (row, pair tid % 16))
+        if (sc != 0.0) {
+#pragma unroll
+          for (int h = 0; h < PW * NPAIR / 256; ++h) {
+            const int r = (tid + 256 * h) / NPAIR;
+            const double u = sR[r * RS + pc], v = sR[r * RS + qc];
+            sR[r * RS + pc] = cc * u - sc * v;
+            sR[r * RS + qc] = sc * u + cc * v;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (first) return;   // the panel is orthogonal already
+  // ---- phase 3: P <- P R for the panels of A and of V
+  for (int which = 0; which < 2; ++which) {
+    double* X = which == 0 ? A : V;
+    if (!X) continue;
+    const int64_t ldx = which == 0 ? lda : ldv;
+    const int rows = which == 0 ? M : N;
+    const int nch = (rows + JCH - 1) / JCH;
+    gload(X, ldx, rows, 0);
+    for (int ch = 0; ch < nch; ++ch) {
+      __syncthreads();   // the previous chunk has been stored to global memory
+      sstore();
+      __syncthreads();
+      if (ch + 1 < nch) gload(X, ldx, rows, (ch + 1) * JCH);
+      double acc[PW / 8][2];
+#pragma unroll
+      for (int nt = 0; nt < PW / 8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+      const int r0 = warp * 8;
+#pragma unroll
+      for (int ks = 0; ks < PW / 4; ++ks) {
+        const double a = sP[(ks * 4 + t) * JPS + r0 + g];
+#pragma unroll
+        for (int nt = 0; nt < PW / 8; ++nt) {
+          const double b = sR[(ks * 4 + t) * RS + nt * 8 + g];
+          jdmma(acc[nt][0], acc[nt][1], a, b);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int nt = 0; nt < PW / 8; ++nt) {
+        sP[(nt * 8 + 2 * t) * JPS + r0 + g] = acc[nt][0];
+        sP[(nt * 8 + 2 * t + 1) * JPS + r0 + g] = acc[nt][1];
+      }
+      __syncthreads();
+      const int row0 = ch * JCH;
+#pragma unroll
+      for (int q = 0; q < PER; ++q) {
+        const int c = ec0 + 4 * q;
+        const int gc = gcol(c);
+        const int r = row0 + er;
+        if (gc < N && r < rows) X[(int64_t)gc * ldx + r] = sP[c * JPS + er];
+      }
+    }
+  }
+}
+
+// out[0] = max_i ||a_i||^2 (positive doubles order like their bit patterns)
+__global__ void k_colnorm2_max(const double* A, int64_t lda, int M, int N, double* out) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= N) return;
+  double acc = 0.0;
+  for (int r = lane; r < M; r += 32) {
+    const double a = A[(int64_t)i * lda + r];
+    acc = fma(a, a, acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(out), (unsigned long long)__double_as_longlong(acc));
+}
+__global__ void k_floor2(double* v, double f) { v[0] *= f; }
+
+__global__ void k_set_identity(double* V, int64_t ldv, int n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)n * n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e % n), c = (int)(e / n);
+    V[(int64_t)c * ldv + r] = (r == c) ? 1.0 : 0.0;
+  }
+}
+
+// per column i: val[i] = v_i . a_i (mode 0: eigenvalue of a symmetric matrix)
+// or ||a_i|| (mode 1: singular value); one warp per column
+__global__ void k_col_values(const double* A, int64_t lda, const double* V, int64_t ldv, int M,
+                             int N, int mode, double* val) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= N) return;
+  double acc = 0.0;
+  // scaled two-pass norm is not needed: entries are O(||A||), squares cannot overflow here
+  for (int r = lane; r < M; r += 32) {
+    const double a = A[(int64_t)i * lda + r];
+    acc = fma(a, mode == 0 ? V[(int64_t)i * ldv + r] : a, acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) val[i] = mode == 0 ? acc : sqrt(acc);
+}
+
+// pos[i] = rank of val[i] (ascending, or descending with desc), ties by index
+__global__ void k_rank(const double* val, int n, int desc, int* pos, double* sorted) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double v = val[i];
+  int r = 0;
+  for (int j = 0; j < n; ++j) {
+    const double u = val[j];
+    const bool before = desc ? (u > v || (u == v && j < i)) : (u < v || (u == v && j < i));
+    r += before ? 1 : 0;
+  }
+  pos[i] = r;
+  sorted[r] = v;
+}
+
+// dst[:, pos[i]] = src[:, i] * (scale ? 1 / val[i] : 1)   (column-major, rows x n)
+__global__ void k_scatter_cols(const double* src, int64_t lds, int rows, int n, const int* pos,
+                               const double* val, int scale, double* dst, int64_t ldd) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)rows * n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e % rows), i = (int)(e / rows);
+    double x = src[(int64_t)i * lds + r];
+    if (scale) x = val[i] > 0.0 ? x / val[i] : 0.0;
+    dst[(int64_t)pos[i] * ldd + r] = x;
+  }
+}
+
+// VT[pos[i] + j ldvt] = V[j + i ldv]
+__global__ void k_scatter_rows_t(const double* V, int64_t ldv, int n, const int* pos, double* VT,
+                                 int64_t ldvt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)n * n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e % n), i = (int)(e / n);
+    VT[pos[i] + (int64_t)j * ldvt] = V[(int64_t)i * ldv + j];
+  }
+}
+
+// out[i][j] (row-major, ld) = V[j + i n] * (scale ? sc[i] : 1): rows = columns of V
+__global__ void k_scale_rows(const double* V, int n, int ldv, const double* sc, int unused,
+                             double* out, int ld) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)n * n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e % n), i = (int)(e / n);
+    out[(int64_t)i * ld + j] = V[(int64_t)i * ldv + j] * sc[i];
+  }
+}
+// Bm[j][pos[i]] = VB[j + i p] / sL[j]
+__global__ void k_left_coef(const double* VB, int p, const double* sL, const int* pos, double* Bm,
+                            int ld) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)p * p;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e % p), i = (int)(e / p);
+    const double sl = sL[j];
+    Bm[(int64_t)j * ld + pos[i]] = sl > 0.0 ? VB[(int64_t)i * p + j] / sl : 0.0;
+  }
+}
+// dst (column-major rows x n) = src (row-major, ld)
+__global__ void k_rows_to_cols(const double* src, int ld, int rows, int n, double* dst) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)rows * n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e % rows), c = (int)(e / rows);
+    dst[e] = src[(int64_t)r * ld + c];
+  }
+}
+
+int grid1(int64_t n, int bs = 256) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + bs - 1) / bs, 148 * 8));
+}
+
+// sweeps of the block tournament until no pair rotates
+int jacobi_sweeps(cudaStream_t st, double* A, int64_t lda, int M, int N, double* V, int64_t ldv,
+                  int* sweeps_out) {
+  constexpr int BW = 16;
+  int NB = (N + BW - 1) / BW;
+  if (NB < 2) NB = 2;
+  if (NB & 1) ++NB;
+  // the Gram entries are M-term sums: their rounding noise relative to
+  // ||a_i|| ||a_j|| is ~ sqrt(M) eps, the threshold LAPACK's dgesvj uses
+  const double tol = std::max(4.0, sqrt((double)M)) * DEPS;
+  int* flag = nullptr;
+  KRY_CHECK(dalloc(&flag, 64));
+  // columns below eps x the largest column norm are rounding noise
+  double* floor2 = reinterpret_cast<double*>(flag + 2);
+  cudaMemsetAsync(flag, 0, 64 * sizeof(int), st);
+  k_colnorm2_max<<<(N * 32 + 255) / 256, 256, 0, st>>>(A, lda, M, N, floor2);
+  k_floor2<<<1, 1, 0, st>>>(floor2, DEPS * DEPS);
+  count_launch(2);
+  const int max_sweeps = 60;
+  // one cyclic sweep over the 32 x 32 Gram block per visit (the block
+  // ordering is then one particular cyclic ordering of the scalar method);
+  // KRY_JACOBI_INNER: more inner sweeps per visit (measured slower)
+  int inner = 1;
+  if (const char* e = getenv("KRY_JACOBI_INNER")) inner = std::max(1, atoi(e));
+  int sweep = 0, rc = KRY_OK;
+  for (; sweep < max_sweeps; ++sweep) {
+    cudaMemsetAsync(flag, 0, sizeof(int), st);
+    for (int r = 0; r < NB - 1; ++r)
+      k_jac_round<BW><<<NB / 2, 256, 0, st>>>(A, lda, M, N, V, ldv, NB, r, tol, floor2, inner, flag);
+    count_launch(NB - 1);
+    int h = 0;
+    cudaError_t e = cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      rc = fail(KRY_ERR_CUDA, std::string("Jacobi sweep failed: ") + cudaGetErrorString(e));
+      break;
+    }
+    if (!h) break;
+  }
+  dfree(flag);
+  if (rc != KRY_OK) return rc;
+  if (sweep >= max_sweeps)
+    return fail(KRY_ERR_FACTORIZATION, "dense Jacobi iteration did not converge");
+  if (sweeps_out) *sweeps_out = sweep + 1;
+  return KRY_OK;
+}
+
+}  // namespace
+
+// ================================================================ GEMM (DMMA)
+// C = A B, 64 x 128 tiles, 8 warps of 32 x 32 (4 x 4 m8n8k4 tiles, 32
+// accumulator doubles per lane), K in steps of 16 through a 3-stage cp.async
+// ring; strides padded so both fragment reads are conflict-free.
+namespace {
+constexpr int GBM = 64, GBN = 128, GBK = 16, GST = 3;
+constexpr int GAS = GBK + 4;   // A tile, row-major: [GBM][GAS]
+constexpr int GAT = GBM + 8;   // A tile, column-major source: [GBK][GAT]
+constexpr int GBS = GBN + 8;   // B tile: [GBK][GBS]
+
+__device__ __forceinline__ void gcp16(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void gcp8(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+// two consecutive doubles (x, x + 1 along the contiguous direction, `lim` =
+// extent in that direction); wide = 16-byte aligned source rows
+__device__ __forceinline__ void gcp_pair(double* dst, const double* src, const double* safe,
+                                         bool row_ok, int x, int lim, bool wide) {
+  if (wide && row_ok && x + 1 < lim) {
+    gcp16(dst, src, true);
+  } else {
+    const bool v0 = row_ok && x < lim, v1 = row_ok && x + 1 < lim;
+    gcp8(dst, v0 ? src : safe, v0);
+    gcp8(dst + 1, v1 ? src + 1 : safe, v1);
+  }
+}
+
+template <bool ACOL>
+__global__ void __launch_bounds__(256) k_dgemm(int M, int N, int K, const double* __restrict__ A,
+                                               int64_t lda, const double* __restrict__ B,
+                                               int64_t ldb, const int* __restrict__ brow,
+                                               double* __restrict__ C, int64_t ldc,
+                                               const int* __restrict__ crow, int awide,
+                                               int bwide, const int* __restrict__ dyn) {
+  if (dyn) {   // device-side sizes: K = dyn[0], M = dyn[0] + 1 (bordered update)
+    K = dyn[0];
+    M = min(M, K + 1);
+  }
+  if ((int)blockIdx.y * GBM >= M) return;
+  constexpr int ASZ = ACOL ? GBK * GAT : GBM * GAS;
+  constexpr int BSZ = GBK * GBS;
+  extern __shared__ __align__(16) double gsm[];
+  double* sA = gsm;
+  double* sB = gsm + GST * ASZ;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp >> 2, wn = warp & 3;
+  const int i0 = blockIdx.y * GBM, j0 = blockIdx.x * GBN;
+  auto load_stage = [&](int kt, int st) {
+    const int k0 = kt * GBK;
+    double* dA = sA + st * ASZ;
+    double* dB = sB + st * BSZ;
+    if (!ACOL) {
+      for (int q = tid; q < GBM * (GBK / 2); q += 256) {
+        const int row = q / (GBK / 2), pc = q % (GBK / 2);
+        const int i = i0 + row, kk = k0 + 2 * pc;
+        gcp_pair(dA + row * GAS + 2 * pc, A + (int64_t)i * lda + kk, A, i < M, kk, K, awide);
+      }
+    } else {
+      for (int q = tid; q < GBK * (GBM / 2); q += 256) {
+        const int kr = q / (GBM / 2), pc = q % (GBM / 2);
+        const int kk = k0 + kr, i = i0 + 2 * pc;
+        gcp_pair(dA + kr * GAT + 2 * pc, A + (int64_t)kk * lda + i, A, kk < K, i, M, awide);
+      }
+    }
+    for (int q = tid; q < GBK * (GBN / 2); q += 256) {
+      const int kr = q / (GBN / 2), pc = q % (GBN / 2);
+      const int kk = k0 + kr, j = j0 + 2 * pc;
+      const bool ok = kk < K;
+      const int64_t br = ok ? (brow ? brow[kk] : kk) : 0;
+      gcp_pair(dB + kr * GBS + 2 * pc, B + br * ldb + j, B, ok, j, N, bwide);
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int nk = (K + GBK - 1) / GBK;
+#pragma unroll
+  for (int st = 0; st < GST - 1; ++st) {
+    if (st < nk) load_stage(st, st);
+    asm volatile("cp.async.commit_group;");
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(GST - 2));
+    __syncthreads();
+    {
+      const int kn = kt + GST - 1;
+      if (kn < nk) load_stage(kn, kn % GST);
+      asm volatile("cp.async.commit_group;");
+    }
+    const double* tA = sA + (kt % GST) * ASZ;
+    const double* tB = sB + (kt % GST) * BSZ;
+#pragma unroll
+    for (int ks = 0; ks < GBK / 4; ++ks) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+        fa[mt] = ACOL ? tA[(4 * ks + t) * GAT + wm * 32 + mt * 8 + g]
+                      : tA[(wm * 32 + mt * 8 + g) * GAS + 4 * ks + t];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) fb[nt] = tB[(4 * ks + t) * GBS + wn * 32 + nt * 8 + g];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) jdmma(acc[mt][nt][0], acc[mt][nt][1], fa[mt], fb[nt]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;");
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+    const int i = i0 + wm * 32 + mt * 8 + g;
+    if (i >= M) continue;
+    double* cr = C + (int64_t)(crow ? crow[i] : i) * ldc;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const int j = j0 + wn * 32 + nt * 8 + 2 * t;
+      if (j < N) cr[j] = acc[mt][nt][0];
+      if (j + 1 < N) cr[j + 1] = acc[mt][nt][1];
+    }
+  }
+}
+}  // namespace
+
+int dense_gemm(cudaStream_t st, int M, int N, int K, const double* A, int64_t lda, int a_colmajor,
+               const double* B, int64_t ldb, const int* brow, double* C, int64_t ldc,
+               const int* crow, const int* dyn) {
+  if (M < 1 || N < 1) return KRY_OK;
+  const size_t smem = (size_t)GST * ((a_colmajor ? GBK * GAT : GBM * GAS) + GBK * GBS) * sizeof(double);
+  static bool attr[64][2] = {{false}};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr[dev & 63][a_colmajor ? 1 : 0]) {
+    if (a_colmajor)
+      KRY_CUDA(cudaFuncSetAttribute(k_dgemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    else
+      KRY_CUDA(cudaFuncSetAttribute(k_dgemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr[dev & 63][a_colmajor ? 1 : 0] = true;
+  }
+  const int awide = ((lda & 1) == 0 && ((uintptr_t)A & 15) == 0) ? 1 : 0;
+  const int bwide = ((ldb & 1) == 0 && ((uintptr_t)B & 15) == 0) ? 1 : 0;
+  dim3 grid((N + GBN - 1) / GBN, (M + GBM - 1) / GBM);
+  if (a_colmajor)
+    k_dgemm<true><<<grid, 256, smem, st>>>(M, N, K, A, lda, B, ldb, brow, C, ldc, crow, awide, bwide, dyn);
+  else
+    k_dgemm<false><<<grid, 256, smem, st>>>(M, N, K, A, lda, B, ldb, brow, C, ldc, crow, awide, bwide, dyn);
+  count_launch();
+  KRY_CUDA(cudaGetLastError());
+  return KRY_OK;
+}
+
+// ================================================================ pivoted Cholesky
+// M_ij = (a_i . a_j) / |l_i + l_j|  (the reduced Lyapunov solution in the
+// eigenbasis of T_m, solvers.py:259-261: symmetric positive semidefinite and
+// numerically of low rank) is never formed: a right-looking pivoted
+// Cholesky factorisation M ~ L L^T evaluates one column per step from a and
+// l.  One persistent grid (<= one CTA per SM, all resident): per step every
+// CTA posts the largest residual diagonal entry of its rows, a grid barrier
+// (monotone counter), then every CTA picks the same pivot from the posted
+// slots and updates its rows (one warp per row, lanes over the previous
+// columns, fixed-order shuffle sum).  Stops when the largest residual
+// diagonal entry is at the rounding level of the largest original one.
+namespace {
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void __launch_bounds__(256) k_pchol(const double* __restrict__ a,
+                                               const double* __restrict__ lam, int k, int s,
+                                               double* L, int ldl, int pmax, double reltol,
+                                               double* d, double* slots, unsigned* bar,
+                                               int* p_out) {
+  __shared__ double s_rv[8];
+  __shared__ int s_ri[8];
+  __shared__ double s_best, s_d0, s_api[8], s_lpi;
+  __shared__ int s_pi;
+  extern __shared__ double s_row[];   // row pi of L (pmax)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x, b = blockIdx.x;
+  const int R = (k + G - 1) / G;
+  const int lo = min(k, b * R), hi = min(k, lo + R);
+  for (int i = lo + tid; i < hi; i += 256) {
+    double dot = 0.0;
+    for (int c = 0; c < s; ++c) dot = fma(a[(int64_t)i * 8 + c], a[(int64_t)i * 8 + c], dot);
+    d[i] = dot / fabs(2.0 * lam[i]);
+  }
+  __syncthreads();
+  int t = 0;
+  for (; t < pmax; ++t) {
+    // largest residual diagonal of this CTA's rows (ties: smallest index)
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    for (int i = lo + tid; i < hi; i += 256) {
+      const double v = d[i];
+      if (v > bv) { bv = v; bi = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { s_rv[warp] = bv; s_ri[warp] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < 8; ++w)
+        if (s_rv[w] > bv || (s_rv[w] == bv && s_ri[w] < bi)) { bv = s_rv[w]; bi = s_ri[w]; }
+      double* mine = slots + ((int64_t)(t & 1) * G + b) * 2;
+      mine[0] = bv;
+      mine[1] = (double)bi;
+      __threadfence();
+      atomicAdd(bar, 1u);
+      const unsigned target = (unsigned)(t + 1) * (unsigned)G;
+      while (ld_acquire_u32(bar) < target) { }
+      __threadfence();
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double gv = -1.0;
+      int gi = 0x7fffffff;
+      for (int q = lane; q < G; q += 32) {
+        const double v = __ldcg(slots + ((int64_t)(t & 1) * G + q) * 2);
+        const int ix = (int)__ldcg(slots + ((int64_t)(t & 1) * G + q) * 2 + 1);
+        if (v > gv || (v == gv && ix < gi)) { gv = v; gi = ix; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, gv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, gi, o);
+        if (ov > gv || (ov == gv && oi < gi)) { gv = ov; gi = oi; }
+      }
+      if (lane == 0) {
+        s_best = gv;
+        s_pi = gi;
+        if (t == 0) s_d0 = gv;
+      }
+    }
+    __syncthreads();
+    const double dpi = s_best;
+    if (!(dpi > reltol * s_d0) || !(dpi > 0.0)) break;
+    const int pi = s_pi;
+    for (int q = tid; q < t; q += 256) s_row[q] = __ldcg(L + (int64_t)pi * ldl + q);
+    if (tid < 8) s_api[tid] = tid < s ? a[(int64_t)pi * 8 + tid] : 0.0;
+    if (tid == 8) s_lpi = lam[pi];
+    __syncthreads();
+    const double root = sqrt(dpi), inv = 1.0 / root;
+    for (int i = lo + warp; i < hi; i += 8) {
+      double dot = 0.0;
+      const double* li = L + (int64_t)i * ldl;
+      for (int q = lane; q < t; q += 32) dot = fma(li[q], s_row[q], dot);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      if (lane == 0) {
+        double num = 0.0;
+        for (int c = 0; c < s; ++c) num = fma(a[(int64_t)i * 8 + c], s_api[c], num);
+        double v = (num / fabs(lam[i] + s_lpi) - dot) * inv;
+        const double di = d[i];
+        if (i == pi) { v = root; d[i] = -1.0; }
+        else if (di >= 0.0) d[i] = fmax(di - v * v, 0.0);
+        L[(int64_t)i * ldl + t] = v;
+        __threadfence();   // row pi of a later step is read by every CTA
+      }
+    }
+    __syncthreads();
+  }
+  if (b == 0 && tid == 0) *p_out = t;
+}
+}  // namespace
+
+int dense_pchol_cauchy(cudaStream_t st, const double* a, const double* lam, int k, int s,
+                       double* L, int ldl, int pmax, int* p_host) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int G = std::max(1, std::min(sms, (k + 63) / 64));
+  double *d = nullptr, *slots = nullptr;
+  unsigned* bar = nullptr;
+  int rc;
+  if ((rc = dalloc(&d, (size_t)k)) || (rc = dalloc(&slots, (size_t)4 * G + 8)) ||
+      (rc = dalloc(&bar, 4))) {
+    dfree(d); dfree(slots); dfree(bar);
+    return rc;
+  }
+  cudaMemsetAsync(bar, 0, 4 * sizeof(unsigned), st);
+  int* pdev = reinterpret_cast<int*>(bar + 2);
+  const size_t smem = (size_t)pmax * sizeof(double);
+  static bool attr[64] = {false};
+  if (smem > 40 * 1024 && !attr[dev & 63]) {
+    cudaFuncSetAttribute(k_pchol, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr[dev & 63] = true;
+  }
+  k_pchol<<<G, 256, smem, st>>>(a, lam, k, s, L, ldl, pmax, DEPS, d, slots, bar, pdev);
+  count_launch();
+  cudaError_t e = cudaMemcpyAsync(p_host, pdev, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  dfree(d); dfree(slots); dfree(bar);
+  if (e != cudaSuccess)
+    return fail(KRY_ERR_CUDA, std::string("pivoted Cholesky failed: ") + cudaGetErrorString(e));
+  return KRY_OK;
+}
+
+// ================================================================ low-rank cross factorisation
+// Gaussian elimination with complete pivoting, stopped at the rounding
+// level: R (ma x nb, column-major, destroyed) ~ Lf Uf with Lf ma x p
+// (column-major, unit pivots, |entries| <= 1) and Uf p x nb (row-major).
+// The reduced Sylvester solution Ytilde = -(u v^T)/(lam_i + ups_j)
+// (solvers.py:356) has rapidly decaying singular values, so p << min(ma, nb)
+// and the SVD is then taken of the thin factors.  One persistent grid, a
+// CTA owns a range of columns; per step: rank-1 update of the owned live
+// columns fused with the search for the next pivot, one grid barrier.  The
+// pivot column is read by every CTA and never touched again (its residual
+// is zero), so one barrier per step suffices.
+namespace {
+__global__ void __launch_bounds__(256) k_gecp(double* R, int ma, int nb, double* Lf, double* Uf,
+                                              int pmax, double reltol, int* dead_col,
+                                              double* slots, unsigned* bar, int* p_out) {
+  extern __shared__ double s_l[];   // pivot column / rho (ma)
+  __shared__ double s_v[8];
+  __shared__ int s_i[8], s_j[8];
+  __shared__ double s_rho, s_rho0;
+  __shared__ int s_pi, s_pj;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int G = gridDim.x, b = blockIdx.x;
+  const int W = (nb + G - 1) / G;
+  const int c0 = min(nb, b * W), c1 = min(nb, c0 + W);
+  int t = 0;
+  // step -1: plain scan
+  double bv = -1.0;
+  int bi = 0, bj = 0x7fffffff;
+  for (int j = c0; j < c1; ++j)
+    for (int i = tid; i < ma; i += 256) {
+      const double v = fabs(R[(int64_t)j * ma + i]);
+      if (v > bv) { bv = v; bi = i; bj = j; }
+    }
+  for (;; ++t) {
+    // block argmax (ties: smallest column, then row)
+    auto better = [](double v, int i, int j, double ov, int oi, int oj) {
+      return ov > v || (ov == v && (oj < j || (oj == j && oi < i)));
+    };
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (better(bv, bi, bj, ov, oi, oj)) { bv = ov; bi = oi; bj = oj; }
+    }
+    if (lane == 0) { s_v[warp] = bv; s_i[warp] = bi; s_j[warp] = bj; }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < 8; ++w)
+        if (better(bv, bi, bj, s_v[w], s_i[w], s_j[w])) { bv = s_v[w]; bi = s_i[w]; bj = s_j[w]; }
+      double* mine = slots + ((int64_t)(t & 1) * G + b) * 4;
+      mine[0] = bv; mine[1] = (double)bi; mine[2] = (double)bj;
+      __threadfence();
+      atomicAdd(bar, 1u);
+      const unsigned target = (unsigned)(t + 1) * (unsigned)G;
+      while (ld_acquire_u32(bar) < target) { }
+      __threadfence();
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double gv = -1.0;
+      int gi = 0, gj = 0x7fffffff;
+      for (int q = lane; q < G; q += 32) {
+        const double* sl = slots + ((int64_t)(t & 1) * G + q) * 4;
+        const double v = __ldcg(sl);
+        const int i = (int)__ldcg(sl + 1), j = (int)__ldcg(sl + 2);
+        if (better(gv, gi, gj, v, i, j)) { gv = v; gi = i; gj = j; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, gv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, gi, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, gj, o);
+        if (better(gv, gi, gj, ov, oi, oj)) { gv = ov; gi = oi; gj = oj; }
+      }
+      if (lane == 0) {
+        s_rho = gv; s_pi = gi; s_pj = gj;
+        if (t == 0) s_rho0 = gv;
+      }
+    }
+    __syncthreads();
+    if (t >= pmax || !(s_rho > reltol * s_rho0) || !(s_rho > 0.0)) break;
+    const int pi = s_pi, pj = s_pj;
+    const double rho = __ldcg(R + (int64_t)pj * ma + pi);
+    const double inv = 1.0 / rho;
+    for (int i = tid; i < ma; i += 256) {
+      const double l = __ldcg(R + (int64_t)pj * ma + i) * inv;
+      s_l[i] = l;
+      if (pj >= c0 && pj < c1) Lf[(int64_t)t * ma + i] = (i == pi) ? 1.0 : l;
+    }
+    if (tid == 0 && pj >= c0 && pj < c1) dead_col[pj] = 1;
+    __syncthreads();
+    bv = -1.0; bi = 0; bj = 0x7fffffff;
+    for (int j = c0; j < c1; ++j) {
+      double* col = R + (int64_t)j * ma;
+      if (j == pj || dead_col[j]) {
+        if (tid == 0) Uf[(int64_t)t * nb + j] = (j == pj) ? rho : 0.0;
+        continue;
+      }
+      const double u = col[pi];
+      __syncthreads();   // every thread has read u before row pi is updated
+      if (tid == 0) Uf[(int64_t)t * nb + j] = u;
+      for (int i = tid; i < ma; i += 256) {
+        double v = col[i];
+        if (u != 0.0) {
+          v = (i == pi) ? 0.0 : fma(-s_l[i], u, v);
+          col[i] = v;
+        }
+        const double av = fabs(v);
+        if (av > bv) { bv = av; bi = i; bj = j; }
+      }
+    }
+    __syncthreads();
+  }
+  if (b == 0 && tid == 0) *p_out = t;
+}
+}  // namespace
+
+int dense_gecp(cudaStream_t st, double* R, int ma, int nb, double* Lf, double* Uf, int pmax,
+               int* p_host) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int G = std::max(1, std::min(sms, nb));
+  double* slots = nullptr;
+  unsigned* bar = nullptr;
+  int* dead = nullptr;
+  int rc;
+  if ((rc = dalloc(&slots, (size_t)8 * G + 8)) || (rc = dalloc(&bar, 4)) ||
+      (rc = dalloc(&dead, (size_t)nb))) {
+    dfree(slots); dfree(bar); dfree(dead);
+    return rc;
+  }
+  cudaMemsetAsync(bar, 0, 4 * sizeof(unsigned), st);
+  cudaMemsetAsync(dead, 0, (size_t)nb * sizeof(int), st);
+  int* pdev = reinterpret_cast<int*>(bar + 2);
+  const size_t smem = (size_t)ma * sizeof(double);
+  if (smem > 200 * 1024) {
+    dfree(slots); dfree(bar); dfree(dead);
+    *p_host = pmax + 1;   // caller takes the dense route
+    return KRY_OK;
+  }
+  static bool attr[64] = {false};
+  if (!attr[dev & 63]) {
+    cudaFuncSetAttribute(k_gecp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr[dev & 63] = true;
+  }
+  k_gecp<<<G, 256, smem, st>>>(R, ma, nb, Lf, Uf, pmax, DEPS, dead, slots, bar, pdev);
+  count_launch();
+  cudaError_t e = cudaMemcpyAsync(p_host, pdev, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  dfree(slots); dfree(bar); dfree(dead);
+  if (e != cudaSuccess)
+    return fail(KRY_ERR_CUDA, std::string("cross factorisation failed: ") + cudaGetErrorString(e));
+  return KRY_OK;
+}
+
+// Thin SVD of a product Lf Uf (Lf ma x p column-major, Uf p x nb row-major),
+// both destroyed:  Lf = U_L S_L V_L^T (one-sided Jacobi),
+// B = S_L V_L^T Uf (p x nb), B^T = U_B S V_B^T (one-sided Jacobi)
+//   =>  Lf Uf = (U_L V_B) S U_B^T.
+// Outputs (device): sig (p, descending), left ma x p and right nb x p
+// (column-major, orthonormal columns in the order of sig).
+int dense_svd_product(cudaStream_t st, double* Lf, int ma, double* Uf, int nb, int p, double* sig,
+                      double* left, double* right) {
+  double *VL = nullptr, *sL = nullptr, *A1 = nullptr, *Bt = nullptr, *VB = nullptr, *val = nullptr,
+         *Bm = nullptr, *lrow = nullptr;
+  int* pos = nullptr;
+  auto cleanup = [&]() {
+    for (double* q : {VL, sL, A1, Bt, VB, val, Bm, lrow})
+      if (q) dfree(q);
+    if (pos) dfree(pos);
+  };
+  int rc;
+  const int ldp = (p + 1) & ~1;
+  if ((rc = dalloc(&VL, (size_t)p * p)) || (rc = dalloc(&sL, (size_t)p)) ||
+      (rc = dalloc(&A1, (size_t)p * ldp)) || (rc = dalloc(&Bt, (size_t)nb * p)) ||
+      (rc = dalloc(&VB, (size_t)p * p)) || (rc = dalloc(&val, (size_t)p)) ||
+      (rc = dalloc(&Bm, (size_t)p * ldp)) || (rc = dalloc(&lrow, (size_t)ma * ldp)) ||
+      (rc = dalloc(&pos, (size_t)p))) {
+    cleanup();
+    return rc;
+  }
+  k_set_identity<<<grid1((int64_t)p * p), 256, 0, st>>>(VL, p, p);
+  count_launch();
+  if ((rc = jacobi_sweeps(st, Lf, ma, ma, p, VL, p, nullptr))) { cleanup(); return rc; }
+  k_col_values<<<(p * 32 + 255) / 256, 256, 0, st>>>(Lf, ma, nullptr, 0, ma, p, 1, sL);
+  // A1 (row-major p x p) = diag(sL) V_L^T: row i = sL_i * column i of V_L
+  k_scale_rows<<<grid1((int64_t)p * p), 256, 0, st>>>(VL, p, p, sL, 0, A1, ldp);
+  count_launch(2);
+  // B (row-major p x nb) = A1 Uf  ==  B^T column-major nb x p
+  if ((rc = dense_gemm(st, p, nb, p, A1, ldp, 0, Uf, nb, nullptr, Bt, nb, nullptr))) { cleanup(); return rc; }
+  k_set_identity<<<grid1((int64_t)p * p), 256, 0, st>>>(VB, p, p);
+  count_launch();
+  if ((rc = jacobi_sweeps(st, Bt, nb, nb, p, VB, p, nullptr))) { cleanup(); return rc; }
+  k_col_values<<<(p * 32 + 255) / 256, 256, 0, st>>>(Bt, nb, nullptr, 0, nb, p, 1, val);
+  k_rank<<<(p + 127) / 128, 128, 0, st>>>(val, p, 1, pos, sig);
+  // right[:, pos_i] = Bt[:, i] / val_i
+  k_scatter_cols<<<grid1((int64_t)nb * p), 256, 0, st>>>(Bt, nb, nb, p, pos, val, 1, right, nb);
+  // Bm (row-major p x p): Bm[j][pos_i] = V_B[j][i] / sL_j;  left = (Lf Bm) as row-major ma x p
+  k_left_coef<<<grid1((int64_t)p * p), 256, 0, st>>>(VB, p, sL, pos, Bm, ldp);
+  count_launch(4);
+  if ((rc = dense_gemm(st, ma, p, p, Lf, ma, 1, Bm, ldp, nullptr, lrow, ldp, nullptr))) { cleanup(); return rc; }
+  // left (column-major ma x p) from the row-major product
+  k_rows_to_cols<<<grid1((int64_t)ma * p), 256, 0, st>>>(lrow, ldp, ma, p, left);
+  count_launch();
+  cudaError_t e = cudaStreamSynchronize(st);
+  cleanup();
+  if (e != cudaSuccess) return fail(KRY_ERR_CUDA, std::string("dense_svd_product: ") + cudaGetErrorString(e));
+  return KRY_OK;
+}
+
+namespace {
+// Gershgorin bounds: out[0] = max_i (a_ii + r_i), out[1] = max_i (-(a_ii - r_i))
+__global__ void k_gershgorin(const double* A, int k, double* out) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= k) return;
+  double r = 0.0;
+  for (int j = lane; j < k; j += 32)
+    if (j != i) r += fabs(A[(int64_t)j * k + i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  if (lane == 0) {
+    const double d = A[(int64_t)i * k + i];
+    // monotone integer order of doubles: flip negative values
+    auto key = [](double x) -> unsigned long long {
+      const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+      return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    };
+    atomicMax(reinterpret_cast<unsigned long long*>(out), key(d + r));
+    atomicMax(reinterpret_cast<unsigned long long*>(out) + 1, key(-(d - r)));
+  }
+}
+// one-sided Jacobi separates eigenvalues by |lambda|: an indefinite matrix
+// is shifted to a semidefinite one first (shift = the upper Gershgorin bound)
+__global__ void k_apply_shift(double* A, int k, double* gb, double* shift_out) {
+  auto unkey = [](unsigned long long u) -> double {
+    const unsigned long long b = (u >> 63) ? (u & 0x7fffffffffffffffull) : ~u;
+    return __longlong_as_double((long long)b);
+  };
+  const double hi = unkey(reinterpret_cast<unsigned long long*>(gb)[0]);
+  const double lo = -unkey(reinterpret_cast<unsigned long long*>(gb)[1]);
+  const double sh = (hi > 0.0 && lo < 0.0) ? hi : 0.0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *shift_out = sh;
+  if (sh == 0.0) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x)
+    A[(int64_t)i * k + i] -= sh;
+}
+__global__ void k_add_shift(double* w, int k, const double* shift) {
+  const double sh = *shift;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < k; i += gridDim.x * blockDim.x)
+    w[i] += sh;
+}
+}  // namespace
+
+int dense_syev(cudaStream_t st, double* A, int k, double* w, int* sweeps, bool semidefinite) {
+  if (k < 1) return KRY_OK;
+  double *V = nullptr, *val = nullptr;
+  int* pos = nullptr;
+  int rc;
+  if ((rc = dalloc(&V, (size_t)k * k)) || (rc = dalloc(&val, (size_t)k)) ||
+      (rc = dalloc(&pos, (size_t)k))) {
+    dfree(V); dfree(val); dfree(pos);
+    return rc;
+  }
+  double *gb = nullptr, *A0 = nullptr;
+  if ((rc = dalloc(&gb, 4)) || (rc = dalloc(&A0, (size_t)k * k))) {
+    dfree(V); dfree(val); dfree(pos); dfree(gb);
+    return rc;
+  }
+  cudaMemcpyAsync(A0, A, (size_t)k * k * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  cudaMemsetAsync(gb, 0, 4 * sizeof(double), st);
+  k_gershgorin<<<(k * 32 + 255) / 256, 256, 0, st>>>(A, k, gb);
+  if (!semidefinite) k_apply_shift<<<std::min(148, (k + 255) / 256), 256, 0, st>>>(A, k, gb, gb + 2);
+  k_set_identity<<<grid1((int64_t)k * k), 256, 0, st>>>(V, k, k);
+  count_launch(3);
+  rc = jacobi_sweeps(st, A, k, k, k, V, k, sweeps);
+  // Rayleigh quotients with the ORIGINAL matrix: the rotated columns carry
+  // the rounding of every sweep (~ sqrt(#rotations) eps ||A||), A0 v_i does
+  // not.  Column i of (A0 V) = row i of V^T A0 (A0 symmetric).
+  if (rc == KRY_OK) rc = dense_gemm(st, k, k, k, V, k, 0, A0, k, nullptr, A, k, nullptr);
+  if (rc == KRY_OK) {
+    k_col_values<<<(k * 32 + 255) / 256, 256, 0, st>>>(A, k, V, k, k, k, 0, val);
+    k_rank<<<(k + 127) / 128, 128, 0, st>>>(val, k, 0, pos, w);
+    k_scatter_cols<<<grid1((int64_t)k * k), 256, 0, st>>>(V, k, k, k, pos, val, 0, A, k);
+    count_launch(3);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess)
+      rc = fail(KRY_ERR_CUDA, std::string("dense_syev: ") + cudaGetErrorString(e));
+  }
+  dfree(gb); dfree(A0);
+  dfree(V); dfree(val); dfree(pos);
+  return rc;
+}
+
+int dense_gesvd(cudaStream_t st, double* A, int M, int N, double* sig, double* U, double* VT,
+                int* sweeps) {
+  if (M < 1 || N < 1) return KRY_OK;
+  double *V = nullptr, *val = nullptr;
+  int* pos = nullptr;
+  int rc;
+  if ((rc = dalloc(&V, (size_t)N * N)) || (rc = dalloc(&val, (size_t)N)) ||
+      (rc = dalloc(&pos, (size_t)N))) {
+    dfree(V); dfree(val); dfree(pos);
+    return rc;
+  }
+  k_set_identity<<<grid1((int64_t)N * N), 256, 0, st>>>(V, N, N);
+  count_launch();
+  rc = jacobi_sweeps(st, A, M, M, N, V, N, sweeps);
+  if (rc == KRY_OK) {
+    k_col_values<<<(N * 32 + 255) / 256, 256, 0, st>>>(A, M, nullptr, 0, M, N, 1, val);
+    k_rank<<<(N + 127) / 128, 128, 0, st>>>(val, N, 1, pos, sig);
+    k_scatter_cols<<<grid1((int64_t)M * N), 256, 0, st>>>(A, M, M, N, pos, val, 1, U, M);
+    k_scatter_rows_t<<<grid1((int64_t)N * N), 256, 0, st>>>(V, N, N, pos, VT, N);
+    count_launch(4);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess)
+      rc = fail(KRY_ERR_CUDA, std::string("dense_gesvd: ") + cudaGetErrorString(e));
+  }
+  dfree(V); dfree(val); dfree(pos);
+  return rc;
+}
+
+}  // namespace kry

@@ -27,6 +27,8 @@
 //   M = ((u u^T) o C) w,  C_ij = 1/(lam_i + lam_j),  u = F^T gamma, w = L^T tau^T
 #include "kry_internal.cuh"
 #include "eigen.cuh"
+#include "dense.cuh"
+#include <cstring>
 #include <cmath>
 #include <vector>
 #include <algorithm>
@@ -1223,6 +1225,564 @@ int EigEngine::compute_uw(cudaStream_t st, const double* gamma, const double* ta
 int EigEngine::residual_lyap(cudaStream_t st, const double* gamma, const double* tau_blk) {
   KRY_CHECK(compute_uw(st, gamma, tau_blk));
   return cauchy(st, K, lam[cur], u, K, lam[cur], u, w, res);
+}
+
+
+// ================================================================== full eigendecomposition
+// np.linalg.eigh(t_dense) of the finalisation (solvers.py:256, :350-351) for
+// the block-tridiagonal T_m, by DIVIDE AND CONQUER on the band itself (no
+// tridiagonalisation): a node of the tree covers a range of block rows; it
+// removes its middle block row (the separator), which decouples the two
+// halves, solves them recursively and then puts the s separator rows back
+// ONE SCALAR ROW AT A TIME -- exactly the bordered (arrowhead) update of the
+// incremental engine above (E1 deflation, E2 secular roots, E3 Gu-Eisenstat
+// zhat: the same kernels), but carrying ALL rows of the eigenvector matrix:
+//   X_new = W^T X_old   (X = Q^T, row = eigenvector; W = normalised
+//                        zhat_j / (mu_i - lam_j), one DMMA GEMM per row)
+// Leaves (<= 32 rows) are diagonalised by a two-sided Jacobi iteration in
+// shared memory.  Rows of a node are ordered [left half, right half,
+// separator], so the two halves of a parent are the diagonal blocks of its
+// X; `pos` maps a row of T to its final position.
+namespace {
+
+struct DcAppendArgs {
+  int off, K, K0, a, s, bm, nl, nr;
+  int posl[KRY_SMAX], posr[KRY_SMAX];   // local positions of the coupled rows
+};
+
+// E1 of a separator row: z = X_old[:, coupled rows] t, deflation as in
+// k_eig_deflate, but the Givens rotations of numerically equal poles are
+// recorded (giv_i, giv_c) for k_dc_givens instead of being applied to F / L.
+__global__ void __launch_bounds__(1024) k_dc_deflate(EigView e, DcAppendArgs g,
+                                                     const double* __restrict__ dsym,
+                                                     const double* __restrict__ sub,
+                                                     double* lam, const double* __restrict__ X,
+                                                     int64_t ldx, int* giv_i, double* giv_c) {
+  extern __shared__ double dyn_sm[];
+  const int K = g.K, s = g.s;
+  e.z = dyn_sm;
+  e.cand = reinterpret_cast<int*>(dyn_sm + K);
+  e.dflag = e.cand + K;
+  e.pflag = e.dflag + K;
+  __shared__ double t[3 * KRY_SMAX];
+  __shared__ int tp[3 * KRY_SMAX];
+  __shared__ int s_nc, s_ng;
+  __shared__ double s_d, s_tol;
+  if (threadIdx.x == 0) {
+    int nc = 0;
+    const double* D = dsym + (int64_t)g.bm * 64;
+    if (g.nl > 0)
+      for (int c = 0; c < s; ++c) {   // T[sep a][left last block row c] = sub[bm-1][a][c]
+        t[nc] = sub[(int64_t)(g.bm - 1) * 64 + g.a * 8 + c];
+        tp[nc++] = g.posl[c];
+      }
+    if (g.nr > 0)
+      for (int c = 0; c < s; ++c) {   // T[right first block row c][sep a] = sub[bm][c][a]
+        t[nc] = sub[(int64_t)g.bm * 64 + c * 8 + g.a];
+        tp[nc++] = g.posr[c];
+      }
+    for (int c = 0; c < g.a; ++c) {   // separator rows already appended
+      t[nc] = D[g.a * 8 + c];
+      tp[nc++] = g.K0 + c;
+    }
+    s_nc = nc;
+    s_d = D[g.a * 8 + g.a];
+    s_ng = 0;
+  }
+  __syncthreads();
+  const double d = s_d;
+  const int nc = s_nc;
+  lam += g.off;
+  const int C = (K + blockDim.x - 1) / blockDim.x;
+  const int j0 = min(K, (int)threadIdx.x * C), j1 = min(K, j0 + C);
+  double zmax = 0.0, zabs = 0.0;
+  for (int j = j0; j < j1; ++j) {
+    const double* xr = X + (int64_t)(g.off + j) * ldx + g.off;
+    double z = 0.0;
+    for (int r = 0; r < nc; ++r) z = fma(xr[tp[r]], t[r], z);
+    e.z[j] = z;
+    zmax = fmax(zmax, fabs(z));
+    zabs += fabs(z);
+  }
+  zmax = block_max(zmax);
+  zabs = block_sum(zabs);
+  if (threadIdx.x == 0) {
+    double lm = 0.0;
+    if (K > 0) lm = fmax(fabs(lam[0]), fabs(lam[K - 1]));
+    s_tol = 8.0 * EPS * fmax(fmax(lm, fabs(d)), zmax);
+    e.scal[0] = d;
+    e.scal[1] = s_tol;
+    e.scal[2] = zabs;
+  }
+  __syncthreads();
+  const double tol = s_tol;
+  int q;
+  {
+    int cnt = 0;
+    for (int j = j0; j < j1; ++j) cnt += (fabs(e.z[j]) > tol) ? 1 : 0;
+    int pos = block_excl_scan(cnt, &q);
+    for (int j = j0; j < j1; ++j) {
+      const int keep = fabs(e.z[j]) > tol;
+      if (keep) e.cand[pos++] = j;
+      e.dflag[j] = keep ? 0 : 1;
+    }
+  }
+  __syncthreads();
+  for (int i = 1 + threadIdx.x; i < q; i += blockDim.x) {
+    const int ja = e.cand[i - 1], jb = e.cand[i];
+    const double za = e.z[ja], zb = e.z[jb];
+    const double r = hypot(za, zb);
+    const double cth = zb / r, sth = za / r;
+    const double tt = lam[jb] - lam[ja];
+    e.pflag[i] = (fabs(tt * cth * sth) <= tol) ? 1 : 0;
+  }
+  if (threadIdx.x == 0 && q > 0) e.pflag[0] = 0;
+  __syncthreads();
+  // runs of flagged pairs: one thread per run, rotations recorded in run order
+  for (int i = 1 + threadIdx.x; i < q; i += blockDim.x) {
+    if (!e.pflag[i] || e.pflag[i - 1]) continue;
+    int len = 0;
+    for (int k = i; k < q && e.pflag[k]; ++k) ++len;
+    int slot = atomicAdd(&s_ng, len);
+    int prev = e.cand[i - 1];
+    for (int k = i; k < q && e.pflag[k]; ++k) {
+      const int cur = e.cand[k];
+      const double za = e.z[prev], zb = e.z[cur];
+      const double r = hypot(za, zb);
+      const double cth = zb / r, sth = za / r;
+      const double tt = lam[cur] - lam[prev];
+      int gp = -1, gc = -1;
+      double oc = 1.0, os = 0.0;
+      if (fabs(tt * cth * sth) <= tol) {
+        const double l1 = lam[prev], l2 = lam[cur];
+        lam[prev] = cth * cth * l1 + sth * sth * l2;
+        lam[cur] = sth * sth * l1 + cth * cth * l2;
+        e.z[prev] = 0.0;
+        e.z[cur] = r;
+        e.dflag[prev] = 1;
+        gp = prev; gc = cur; oc = cth; os = sth;
+      }
+      giv_i[2 * slot] = gp;
+      giv_i[2 * slot + 1] = gc;
+      giv_c[2 * slot] = oc;
+      giv_c[2 * slot + 1] = os;
+      ++slot;
+      prev = cur;
+    }
+  }
+  __syncthreads();
+  int pb, db;
+  {
+    int np = 0, nd = 0;
+    for (int j = j0; j < j1; ++j) {
+      if (e.dflag[j]) ++nd; else ++np;
+    }
+    int pp = block_excl_scan(np, &pb);
+    int pd = block_excl_scan(nd, &db);
+    for (int j = j0; j < j1; ++j) {
+      if (e.dflag[j]) {
+        e.def_idx[pd] = j;
+        e.def_lam[pd] = lam[j];
+        ++pd;
+      } else {
+        e.poles[pp] = lam[j];
+        e.zz[pp] = e.z[j];
+        e.pmap[pp] = j;
+        ++pp;
+      }
+    }
+  }
+  __syncthreads();
+  int unsorted = 0;
+  for (int i = 1 + threadIdx.x; i < db; i += blockDim.x)
+    unsorted |= (e.def_lam[i] < e.def_lam[i - 1]) ? 1 : 0;
+  unsorted = __syncthreads_or(unsorted);
+  if (threadIdx.x == 0) {
+    e.counts[0] = pb;
+    e.counts[1] = db;
+    e.counts[2] = s_ng;
+    for (int i = 1; unsorted && i < db; ++i) {
+      double v = e.def_lam[i];
+      if (v >= e.def_lam[i - 1]) continue;
+      int ix = e.def_idx[i];
+      int k = i - 1;
+      while (k >= 0 && e.def_lam[k] > v) {
+        e.def_lam[k + 1] = e.def_lam[k];
+        e.def_idx[k + 1] = e.def_idx[k];
+        --k;
+      }
+      e.def_lam[k + 1] = v;
+      e.def_idx[k + 1] = ix;
+    }
+  }
+}
+
+// the recorded rotations on the rows of X (thread per column; the rotations
+// of a run chain through shared rows, so they are applied in list order --
+// different runs touch disjoint rows)
+__global__ void k_dc_givens(const int* __restrict__ counts, const int* __restrict__ giv_i,
+                            const double* __restrict__ giv_c, double* X, int64_t ldx, int off,
+                            int K) {
+  const int ng = counts[2];
+  if (ng == 0) return;
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= K) return;
+  double* xc = X + (int64_t)off * ldx + off + col;
+  for (int r = 0; r < ng; ++r) {
+    const int prev = giv_i[2 * r], cur = giv_i[2 * r + 1];
+    if (prev < 0) continue;
+    const double c = giv_c[2 * r], sn = giv_c[2 * r + 1];
+    const double a = xc[(int64_t)prev * ldx], b = xc[(int64_t)cur * ldx];
+    xc[(int64_t)prev * ldx] = c * a - sn * b;
+    xc[(int64_t)cur * ldx] = sn * a + c * b;
+  }
+}
+
+// rows of W^T (root i: zhat_j / (mu_i - lam_j), normalised), the sorted
+// positions of the new eigenpairs, the new coordinate, and the deflated
+// eigenpairs copied through.  grid = 2 K + 1 CTAs: [0, K] roots, then deflated.
+__global__ void __launch_bounds__(128) k_dc_wbuild(EigView e, int off, int K, double* Wt,
+                                                   int64_t ldw, int* crow, int* brow,
+                                                   const double* __restrict__ lam_old_unused,
+                                                   double* lam_new, const double* __restrict__ Xo,
+                                                   double* Xn, int64_t ldx) {
+  const int p = e.counts[0], nd = e.counts[1];
+  const int tid = threadIdx.x;
+  __shared__ double red[4];
+  if ((int)blockIdx.x <= K) {
+    const int i = blockIdx.x;
+    if (i > p) return;
+    const double org = e.org[i], tau = e.tau[i];
+    double nrm2 = 0.0;
+    double* wr = Wt + (int64_t)i * ldw;
+    for (int j = tid; j < p; j += 128) {
+      const double v = e.zhat[j] * frcp(tau - (e.poles[j] - org));
+      wr[j] = v;
+      nrm2 = fma(v, v, nrm2);
+    }
+    nrm2 = warp_sum(nrm2);
+    if ((tid & 31) == 0) red[tid >> 5] = nrm2;
+    __syncthreads();
+    const double inv = 1.0 / sqrt(1.0 + ((red[0] + red[1]) + (red[2] + red[3])));
+    for (int j = tid; j < p; j += 128) wr[j] *= inv;
+    if (i < p && tid == 32) brow[i] = off + e.pmap[i];
+    if (tid == 0) {
+      const double mu = e.mu[i];
+      const int pos = i + count_le(e.def_lam, nd, mu);
+      lam_new[off + pos] = mu;
+      crow[i] = off + pos;
+      Xn[(int64_t)(off + pos) * ldx + off + K] = inv;
+    }
+    return;
+  }
+  const int k = blockIdx.x - (K + 1);
+  if (k >= nd) return;
+  const int src = e.def_idx[k];
+  const double lv = e.def_lam[k];
+  const int pos = k + count_lt(e.mu, p + 1, lv);
+  if (tid == 0) lam_new[off + pos] = lv;
+  const double* xs = Xo + (int64_t)(off + src) * ldx + off;
+  double* xd = Xn + (int64_t)(off + pos) * ldx + off;
+  for (int c = tid; c < K; c += 128) xd[c] = xs[c];
+  if (tid == 0) xd[K] = 0.0;
+}
+
+// leaves: two-sided cyclic Jacobi on the n <= 32 rows of one leaf (CTA each)
+struct DcLeaf { int b0, nb, off; };
+__global__ void __launch_bounds__(256) k_dc_leaf(const DcLeaf* __restrict__ leaves, int s,
+                                                 const double* __restrict__ dsym,
+                                                 const double* __restrict__ sub, double* lam,
+                                                 double* X, int64_t ldx) {
+  constexpr int PW = 32, GS = 33, NPAIR = 16;
+  __shared__ double sG[PW * GS], sR[PW * GS];
+  __shared__ double s_c[NPAIR], s_s[NPAIR], s_ev[PW];
+  __shared__ int s_rank[PW];
+  const DcLeaf lf = leaves[blockIdx.x];
+  const int n = lf.nb * s, tid = threadIdx.x;
+  for (int e = tid; e < PW * GS; e += 256) { sG[e] = 0.0; sR[e] = 0.0; }
+  __syncthreads();
+  for (int e = tid; e < n * n; e += 256) {
+    const int r = e / n, c = e % n;
+    const int br = r / s, bc = c / s, ir = r % s, ic = c % s;
+    double v = 0.0;
+    if (br == bc) v = dsym[(int64_t)(lf.b0 + br) * 64 + ir * 8 + ic];
+    else if (br == bc + 1) v = sub[(int64_t)(lf.b0 + bc) * 64 + ir * 8 + ic];
+    else if (bc == br + 1) v = sub[(int64_t)(lf.b0 + br) * 64 + ic * 8 + ir];
+    sG[r * GS + c] = v;
+  }
+  if (tid < PW) sR[tid * GS + tid] = 1.0;
+  __syncthreads();
+  const double tol = 2.0 * EPS;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    int need = 0;
+    for (int e = tid; e < PW * PW; e += 256) {
+      const int i = e / PW, j = e % PW;
+      if (i < j) {
+        const double o = sG[i * GS + j];
+        if (o * o > tol * tol * fabs(sG[i * GS + i] * sG[j * GS + j]) && o != 0.0) need = 1;
+      }
+    }
+    if (!__syncthreads_or(need)) break;
+    for (int rr = 0; rr < PW - 1; ++rr) {
+      int pc, qc, pr, qr;
+      {
+        const int j = tid % NPAIR, i = tid / NPAIR;
+        if (j == 0) { pc = PW - 1; qc = rr; } else { pc = (rr + j) % (PW - 1); qc = (rr - j + (PW - 1)) % (PW - 1); }
+        if (i == 0) { pr = PW - 1; qr = rr; } else { pr = (rr + i) % (PW - 1); qr = (rr - i + (PW - 1)) % (PW - 1); }
+      }
+      if (tid < NPAIR) {
+        const double gpp = sG[pc * GS + pc], gqq = sG[qc * GS + qc], gpq = sG[pc * GS + qc];
+        double c = 1.0, sn = 0.0;
+        if (gpq != 0.0 && gpq * gpq > tol * tol * fabs(gpp * gqq)) {
+          const double d = gqq - gpp, b2 = 2.0 * gpq;
+          const double tt = (d >= 0.0 ? b2 : -b2) / (fabs(d) + sqrt(fma(d, d, b2 * b2)));
+          c = rsqrt(fma(tt, tt, 1.0));
+          sn = tt * c;
+        }
+        s_c[tid] = c;
+        s_s[tid] = sn;
+      }
+      __syncthreads();
+      {
+        const double cc = s_c[tid % NPAIR], sc = s_s[tid % NPAIR];
+        const double cr = s_c[tid / NPAIR], sr = s_s[tid / NPAIR];
+        if (sc != 0.0 || sr != 0.0) {
+          const double a = sG[pr * GS + pc], b = sG[pr * GS + qc];
+          const double c = sG[qr * GS + pc], d = sG[qr * GS + qc];
+          const double a1 = cc * a - sc * b, b1 = sc * a + cc * b;
+          const double c1 = cc * c - sc * d, d1 = sc * c + cc * d;
+          sG[pr * GS + pc] = cr * a1 - sr * c1;
+          sG[qr * GS + pc] = sr * a1 + cr * c1;
+          sG[pr * GS + qc] = cr * b1 - sr * d1;
+          sG[qr * GS + qc] = sr * b1 + cr * d1;
+        }
+        if (sc != 0.0) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = (tid + 256 * h) / NPAIR;
+            const double u = sR[r * GS + pc], v = sR[r * GS + qc];
+            sR[r * GS + pc] = cc * u - sc * v;
+            sR[r * GS + qc] = sc * u + cc * v;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // eigenvalues = diag(G) of the first n indices (the padding never rotates),
+  // ascending; eigenvector j = column j of R
+  if (tid < n) s_ev[tid] = sG[tid * GS + tid];
+  __syncthreads();
+  if (tid < n) {
+    const double v = s_ev[tid];
+    int r = 0;
+    for (int j = 0; j < n; ++j) r += (s_ev[j] < v || (s_ev[j] == v && j < tid)) ? 1 : 0;
+    s_rank[tid] = r;
+    lam[lf.off + r] = v;
+  }
+  __syncthreads();
+  for (int e = tid; e < n * n; e += 256) {
+    const int j = e / n, i = e % n;   // eigenvector j, row i
+    X[(int64_t)(lf.off + s_rank[j]) * ldx + lf.off + i] = sR[i * GS + j];
+  }
+}
+
+// sorted union of the two halves of a node: eigenvalues merged (ties: left
+// first), rows of X copied into place with the other half's columns zeroed
+__global__ void __launch_bounds__(128) k_dc_merge(int off, int nl, int nr, const double* lam_src,
+                                                  double* lam_dst, const double* Xs, double* Xd,
+                                                  int64_t ldx) {
+  const int j = blockIdx.x, n = nl + nr;
+  if (j >= n) return;
+  const bool left = j < nl;
+  const double v = lam_src[off + j];
+  int pos;
+  if (left) pos = j + count_lt(lam_src + off + nl, nr, v);
+  else pos = (j - nl) + count_le(lam_src + off, nl, v);
+  if (threadIdx.x == 0) lam_dst[off + pos] = v;
+  const double* xs = Xs + (int64_t)(off + j) * ldx + off;
+  double* xd = Xd + (int64_t)(off + pos) * ldx + off;
+  for (int c = threadIdx.x; c < n; c += 128) {
+    const bool mine = left ? (c < nl) : (c >= nl);
+    xd[c] = mine ? xs[c] : 0.0;
+  }
+}
+
+__global__ void k_dc_copy(int off, int n, const double* lam_src, double* lam_dst, const double* Xs,
+                          double* Xd, int64_t ldx) {
+  const int j = blockIdx.x;
+  if (threadIdx.x == 0) lam_dst[off + j] = lam_src[off + j];
+  for (int c = threadIdx.x; c < n; c += blockDim.x)
+    Xd[(int64_t)(off + j) * ldx + off + c] = Xs[(int64_t)(off + j) * ldx + off + c];
+}
+
+// Q[row + j k] = X[j][pos[row]]
+__global__ void k_dc_output(const double* X, int64_t ldx, const int* pos, int k, double* Q) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)k * k;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(e % k), j = (int)(e / k);
+    Q[e] = X[(int64_t)j * ldx + pos[row]];
+  }
+}
+
+struct DcNode { int b0, b1, left, right, bm, off, n, nl, nr, buf; };
+
+int dc_build(std::vector<DcNode>& nodes, std::vector<int>& pos, int b0, int b1, int off, int s,
+             int leaf_blocks) {
+  DcNode nd;
+  nd.b0 = b0; nd.b1 = b1; nd.off = off; nd.n = (b1 - b0) * s;
+  nd.left = nd.right = -1; nd.bm = -1; nd.nl = nd.nr = 0; nd.buf = 0;
+  if (b1 - b0 <= leaf_blocks) {
+    for (int r = 0; r < nd.n; ++r) pos[b0 * s + r] = off + r;
+    nodes.push_back(nd);
+    return (int)nodes.size() - 1;
+  }
+  const int bm = (b0 + b1) / 2;
+  nd.bm = bm;
+  nd.nl = (bm - b0) * s;
+  nd.nr = (b1 - bm - 1) * s;
+  if (nd.nl > 0) nd.left = dc_build(nodes, pos, b0, bm, off, s, leaf_blocks);
+  if (nd.nr > 0) nd.right = dc_build(nodes, pos, bm + 1, b1, off + nd.nl, s, leaf_blocks);
+  for (int a = 0; a < s; ++a) pos[bm * s + a] = off + nd.nl + nd.nr + a;
+  nodes.push_back(nd);
+  return (int)nodes.size() - 1;
+}
+
+}  // namespace
+
+int dc_band_eigh(cudaStream_t st, const double* dsym, const double* sub, int s, int m, double* lam_out,
+                 double* Q) {
+  const int k = s * m;
+  if (k < 1) return KRY_OK;
+  const int leaf_blocks = std::max(1, 32 / s);
+  std::vector<DcNode> nodes;
+  std::vector<int> pos(k);
+  const int root = dc_build(nodes, pos, 0, m, 0, s, leaf_blocks);
+  const int64_t ldx = (k + 2) & ~1;
+  const int64_t ldw = ldx;
+  // workspace
+  double *X[2] = {nullptr, nullptr}, *lam[2] = {nullptr, nullptr}, *Wt = nullptr, *dws = nullptr,
+         *giv_c = nullptr;
+  int *iws = nullptr, *giv_i = nullptr, *pos_d = nullptr;
+  DcLeaf* leaves_d = nullptr;
+  const size_t nk = (size_t)k + 16;
+  auto cleanup = [&]() {
+    for (double* q : {X[0], X[1], lam[0], lam[1], Wt, dws, giv_c})
+      if (q) dfree(q);
+    for (int* q : {iws, giv_i, pos_d})
+      if (q) dfree(q);
+    if (leaves_d) dfree(leaves_d);
+  };
+  int rc;
+  if ((rc = dalloc(&X[0], (size_t)k * ldx)) || (rc = dalloc(&X[1], (size_t)k * ldx)) ||
+      (rc = dalloc(&lam[0], nk)) || (rc = dalloc(&lam[1], nk)) ||
+      (rc = dalloc(&Wt, (size_t)(k + 1) * ldw)) || (rc = dalloc(&dws, 8 * nk + 64)) ||
+      (rc = dalloc(&giv_c, 2 * nk)) || (rc = dalloc(&iws, 4 * nk + 16)) ||
+      (rc = dalloc(&giv_i, 2 * nk)) || (rc = dalloc(&pos_d, nk))) {
+    cleanup();
+    return rc;
+  }
+  cudaMemsetAsync(Wt, 0, (size_t)(k + 1) * ldw * sizeof(double), st);
+  cudaMemsetAsync(X[0], 0, (size_t)k * ldx * sizeof(double), st);
+  cudaMemsetAsync(X[1], 0, (size_t)k * ldx * sizeof(double), st);
+  EigView v;
+  memset(&v, 0, sizeof(v));
+  v.s = s;
+  v.kmax = k;
+  {
+    double* p = dws;
+    v.poles = p; p += nk; v.zz = p; p += nk; v.zhat = p; p += nk; v.def_lam = p; p += nk;
+    v.mu = p; p += nk; v.org = p; p += nk; v.tau = p; p += nk; v.scal = p; p += 16;
+    int* q = iws;
+    v.pmap = q; q += nk; v.def_idx = q; q += nk; v.counts = q; q += 16;
+  }
+  int* crow = iws + 2 * nk + 16;
+  int* brow = crow + nk;
+  cudaMemcpyAsync(pos_d, pos.data(), (size_t)k * sizeof(int), cudaMemcpyHostToDevice, st);
+  // leaves
+  std::vector<DcLeaf> leaves;
+  for (const DcNode& nd : nodes)
+    if (nd.bm < 0) leaves.push_back(DcLeaf{nd.b0, nd.b1 - nd.b0, nd.off});
+  if ((rc = dalloc(&leaves_d, leaves.size()))) { cleanup(); return rc; }
+  cudaMemcpyAsync(leaves_d, leaves.data(), leaves.size() * sizeof(DcLeaf), cudaMemcpyHostToDevice, st);
+  cudaStreamSynchronize(st);   // host vectors are read by the copies above
+  k_dc_leaf<<<(unsigned)leaves.size(), 256, 0, st>>>(leaves_d, s, dsym, sub, lam[0], X[0], ldx);
+  count_launch();
+  static bool attr[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr[dev & 63]) {
+    cudaFuncSetAttribute(k_dc_deflate, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr[dev & 63] = true;
+  }
+  // internal nodes in post-order (dc_build pushes children first)
+  for (size_t ni = 0; ni < nodes.size(); ++ni) {
+    DcNode& nd = nodes[ni];
+    if (nd.bm < 0) continue;
+    const int K0 = nd.nl + nd.nr;
+    // both halves in one buffer
+    int src = 0;
+    if (nd.left >= 0) src = nodes[nd.left].buf;
+    else if (nd.right >= 0) src = nodes[nd.right].buf;
+    for (int ch : {nd.left, nd.right}) {
+      if (ch < 0 || nodes[ch].buf == src) continue;
+      k_dc_copy<<<nodes[ch].n, 128, 0, st>>>(nodes[ch].off, nodes[ch].n, lam[1 - src], lam[src],
+                                             X[1 - src], X[src], ldx);
+      count_launch();
+    }
+    int cur = 1 - src;
+    if (K0 > 0) {
+      k_dc_merge<<<K0, 128, 0, st>>>(nd.off, nd.nl, nd.nr, lam[src], lam[cur], X[src], X[cur], ldx);
+      count_launch();
+    }
+    for (int a = 0; a < s; ++a) {
+      const int K = K0 + a;
+      DcAppendArgs g;
+      g.off = nd.off; g.K = K; g.K0 = K0; g.a = a; g.s = s; g.bm = nd.bm; g.nl = nd.nl; g.nr = nd.nr;
+      for (int c = 0; c < s; ++c) {
+        g.posl[c] = nd.nl > 0 ? pos[(nd.bm - 1) * s + c] - nd.off : 0;
+        g.posr[c] = nd.nr > 0 ? pos[(nd.bm + 1) * s + c] - nd.off : 0;
+      }
+      const size_t dsm = (size_t)K * (sizeof(double) + 3 * sizeof(int)) + 16;
+      if (dsm > 200 * 1024) { cleanup(); return fail(KRY_ERR_DIMENSION, "projected matrix too large for the finalisation"); }
+      k_dc_deflate<<<1, 1024, dsm, st>>>(v, g, dsym, sub, lam[cur], X[cur], ldx, giv_i, giv_c);
+      if (K > 0) k_dc_givens<<<(K + 127) / 128, 128, 0, st>>>(v.counts, giv_i, giv_c, X[cur], ldx, nd.off, K);
+      if (K >= 1024) {
+        if (K <= 128 * 16) k_eig_secular<4, 16><<<K + 1, 128, 0, st>>>(v);
+        else k_eig_secular<4, 0><<<K + 1, 128, 0, st>>>(v);
+      } else if (K >= 256) {
+        k_eig_secular<2, 16><<<K + 1, 64, 0, st>>>(v);
+      } else if (K >= 64) {
+        k_eig_secular<1, 8><<<K + 1, 32, 0, st>>>(v);
+      } else {
+        k_eig_secular<1, 2><<<K + 1, 32, 0, st>>>(v);
+      }
+      if (K > 0) {
+        if (K >= 1024) k_eig_zhat<4><<<K, 128, 0, st>>>(v);
+        else if (K >= 256) k_eig_zhat<2><<<K, 64, 0, st>>>(v);
+        else k_eig_zhat<1><<<K, 32, 0, st>>>(v);
+      }
+      k_dc_wbuild<<<2 * K + 1, 128, 0, st>>>(v, nd.off, K, Wt, ldw, crow, brow, nullptr,
+                                             lam[1 - cur], X[cur], X[1 - cur], ldx);
+      count_launch(5);
+      if (K > 0) {
+        rc = dense_gemm(st, K + 1, K, K, Wt, ldw, 0, X[cur] + nd.off, ldx, brow,
+                        X[1 - cur] + nd.off, ldx, crow, v.counts);
+        if (rc != KRY_OK) { cleanup(); return rc; }
+      }
+      cur = 1 - cur;
+    }
+    nd.buf = cur;
+  }
+  const int rb = nodes[root].buf;
+  k_dc_output<<<(int)std::min<int64_t>(((int64_t)k * k + 255) / 256, 148 * 16), 256, 0, st>>>(
+      X[rb], ldx, pos_d, k, Q);
+  count_launch();
+  cudaMemcpyAsync(lam_out, lam[rb], (size_t)k * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  cleanup();
+  if (e != cudaSuccess) return fail(KRY_ERR_CUDA, std::string("dc_band_eigh: ") + cudaGetErrorString(e));
+  return KRY_OK;
 }
 
 }  // namespace kry

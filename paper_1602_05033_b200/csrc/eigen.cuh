@@ -54,4 +54,10 @@ struct EigEngine {
   const double* L_cur() const { return L[cur]; }
 };
 
+// Full eigendecomposition of the block-tridiagonal T_m (block slots dsym,
+// sub as in the engine): divide and conquer on the band, lam ascending
+// (device, k = s m), Q column-major k x k (device).
+int dc_band_eigh(cudaStream_t st, const double* dsym, const double* sub, int s, int m,
+                 double* lam, double* Q);
+
 }  // namespace kry
