@@ -2101,8 +2101,10 @@ static int finalize_lyap_lowrank(kry_ctx* c, FinalBufs& b, int k, double eps, do
     return rc;
   }
   rc = dense_gemm(c->stream, p, p, k, L, ldl, 1, L, ldl, nullptr, S, p, nullptr);
-  if (rc == KRY_OK) rc = dense_syev(c->stream, S, p, w, nullptr, true);
+  int sweeps = 0;
+  if (rc == KRY_OK) rc = dense_syev(c->stream, S, p, w, &sweeps, true);
   tm.mark("finalize: eig(L^T L)");
+  if (getenv("KRY_TIMING")) fprintf(stderr, "[kry] finalize: pivoted Cholesky rank %d of %d, Jacobi sweeps %d\n", p, k, sweeps);
   const double md = 2.0 * fabs(lmax);   // min |lam_i + lam_j| of a negative spectrum
   if (rc == KRY_OK)
     rc = cudaMemcpyAsync(mind, &md, sizeof(double), cudaMemcpyHostToDevice, c->stream) == cudaSuccess

@@ -375,7 +375,9 @@ int jacobi_sweeps(cudaStream_t st, double* A, int64_t lda, int M, int N, double*
   if (NB & 1) ++NB;
   // the Gram entries are M-term sums: their rounding noise relative to
   // ||a_i|| ||a_j|| is ~ sqrt(M) eps, the threshold LAPACK's dgesvj uses
-  const double tol = std::max(4.0, sqrt((double)M)) * DEPS;
+  double tolmul = 1.0;
+  if (const char* e = getenv("KRY_JACOBI_TOL")) tolmul = std::max(0.25, atof(e));
+  const double tol = tolmul * std::max(4.0, sqrt((double)M)) * DEPS;
   int* flag = nullptr;
   KRY_CHECK(dalloc(&flag, 64));
   // columns below eps x the largest column norm are rounding noise
@@ -673,7 +675,17 @@ __global__ void __launch_bounds__(256) k_pchol(const double* __restrict__ a,
     for (int i = lo + warp; i < hi; i += 8) {
       double dot = 0.0;
       const double* li = L + (int64_t)i * ldl;
-      for (int q = lane; q < t; q += 32) dot = fma(li[q], s_row[q], dot);
+      {   // all loads of the row in flight before the sums (fixed order)
+        int q = lane;
+        for (; q + 96 < t; q += 128) {
+          const double x0 = li[q], x1 = li[q + 32], x2 = li[q + 64], x3 = li[q + 96];
+          dot = fma(x0, s_row[q], dot);
+          dot = fma(x1, s_row[q + 32], dot);
+          dot = fma(x2, s_row[q + 64], dot);
+          dot = fma(x3, s_row[q + 96], dot);
+        }
+        for (; q < t; q += 32) dot = fma(li[q], s_row[q], dot);
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
       if (lane == 0) {
@@ -698,7 +710,7 @@ int dense_pchol_cauchy(cudaStream_t st, const double* a, const double* lam, int 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int G = std::max(1, std::min(sms, (k + 63) / 64));
+  const int G = std::max(1, std::min(sms, (k + 15) / 16));   // two rows per warp
   double *d = nullptr, *slots = nullptr;
   unsigned* bar = nullptr;
   int rc;

@@ -1487,21 +1487,30 @@ __global__ void __launch_bounds__(128) k_dc_wbuild(EigView e, int off, int K, do
   if (tid == 0) xd[K] = 0.0;
 }
 
-// leaves: two-sided cyclic Jacobi on the n <= 32 rows of one leaf (CTA each)
+// leaves: two-sided cyclic Jacobi on the n <= PW rows of one leaf (CTA each;
+// PW / 2 disjoint rotations per round, every thread applies J^T G J to whole
+// 2 x 2 blocks, so one barrier separates the rounds)
 struct DcLeaf { int b0, nb, off; };
-__global__ void __launch_bounds__(256) k_dc_leaf(const DcLeaf* __restrict__ leaves, int s,
-                                                 const double* __restrict__ dsym,
-                                                 const double* __restrict__ sub, double* lam,
-                                                 double* X, int64_t ldx) {
-  constexpr int PW = 32, GS = 33, NPAIR = 16;
-  __shared__ double sG[PW * GS], sR[PW * GS];
-  __shared__ double s_c[NPAIR], s_s[NPAIR], s_ev[PW];
-  __shared__ int s_rank[PW];
+template <int PW>
+__global__ void __launch_bounds__(PW == 32 ? 256 : 1024) k_dc_leaf(const DcLeaf* __restrict__ leaves,
+                                                                  int s,
+                                                                  const double* __restrict__ dsym,
+                                                                  const double* __restrict__ sub,
+                                                                  double* lam, double* X,
+                                                                  int64_t ldx) {
+  constexpr int GS = PW + 1, NPAIR = PW / 2;
+  extern __shared__ double leaf_sm[];
+  double* sG = leaf_sm;
+  double* sR = sG + PW * GS;
+  double* s_c = sR + PW * GS;
+  double* s_s = s_c + NPAIR;
+  double* s_ev = s_s + NPAIR;
+  int* s_rank = reinterpret_cast<int*>(s_ev + PW);
   const DcLeaf lf = leaves[blockIdx.x];
-  const int n = lf.nb * s, tid = threadIdx.x;
-  for (int e = tid; e < PW * GS; e += 256) { sG[e] = 0.0; sR[e] = 0.0; }
+  const int n = lf.nb * s, tid = threadIdx.x, NT = blockDim.x;
+  for (int e = tid; e < PW * GS; e += NT) { sG[e] = 0.0; sR[e] = 0.0; }
   __syncthreads();
-  for (int e = tid; e < n * n; e += 256) {
+  for (int e = tid; e < n * n; e += NT) {
     const int r = e / n, c = e % n;
     const int br = r / s, bc = c / s, ir = r % s, ic = c % s;
     double v = 0.0;
@@ -1513,24 +1522,24 @@ __global__ void __launch_bounds__(256) k_dc_leaf(const DcLeaf* __restrict__ leav
   if (tid < PW) sR[tid * GS + tid] = 1.0;
   __syncthreads();
   const double tol = 2.0 * EPS;
+  auto pair_of = [](int rr, int j, int* p, int* q) {
+    if (j == 0) { *p = PW - 1; *q = rr; }
+    else { *p = (rr + j) % (PW - 1); *q = (rr - j + (PW - 1)) % (PW - 1); }
+  };
   for (int sweep = 0; sweep < 40; ++sweep) {
     int need = 0;
-    for (int e = tid; e < PW * PW; e += 256) {
+    for (int e = tid; e < PW * PW; e += NT) {
       const int i = e / PW, j = e % PW;
       if (i < j) {
         const double o = sG[i * GS + j];
-        if (o * o > tol * tol * fabs(sG[i * GS + i] * sG[j * GS + j]) && o != 0.0) need = 1;
+        if (o != 0.0 && o * o > tol * tol * fabs(sG[i * GS + i] * sG[j * GS + j])) need = 1;
       }
     }
     if (!__syncthreads_or(need)) break;
     for (int rr = 0; rr < PW - 1; ++rr) {
-      int pc, qc, pr, qr;
-      {
-        const int j = tid % NPAIR, i = tid / NPAIR;
-        if (j == 0) { pc = PW - 1; qc = rr; } else { pc = (rr + j) % (PW - 1); qc = (rr - j + (PW - 1)) % (PW - 1); }
-        if (i == 0) { pr = PW - 1; qr = rr; } else { pr = (rr + i) % (PW - 1); qr = (rr - i + (PW - 1)) % (PW - 1); }
-      }
       if (tid < NPAIR) {
+        int pc, qc;
+        pair_of(rr, tid, &pc, &qc);
         const double gpp = sG[pc * GS + pc], gqq = sG[qc * GS + qc], gpq = sG[pc * GS + qc];
         double c = 1.0, sn = 0.0;
         if (gpq != 0.0 && gpq * gpq > tol * tol * fabs(gpp * gqq)) {
@@ -1543,10 +1552,14 @@ __global__ void __launch_bounds__(256) k_dc_leaf(const DcLeaf* __restrict__ leav
         s_s[tid] = sn;
       }
       __syncthreads();
-      {
-        const double cc = s_c[tid % NPAIR], sc = s_s[tid % NPAIR];
-        const double cr = s_c[tid / NPAIR], sr = s_s[tid / NPAIR];
+      for (int blk = tid; blk < NPAIR * NPAIR; blk += NT) {
+        const int jc = blk % NPAIR, jr = blk / NPAIR;
+        const double cc = s_c[jc], sc = s_s[jc];
+        const double cr = s_c[jr], sr = s_s[jr];
         if (sc != 0.0 || sr != 0.0) {
+          int pc, qc, pr, qr;
+          pair_of(rr, jc, &pc, &qc);
+          pair_of(rr, jr, &pr, &qr);
           const double a = sG[pr * GS + pc], b = sG[pr * GS + qc];
           const double c = sG[qr * GS + pc], d = sG[qr * GS + qc];
           const double a1 = cc * a - sc * b, b1 = sc * a + cc * b;
@@ -1556,14 +1569,16 @@ __global__ void __launch_bounds__(256) k_dc_leaf(const DcLeaf* __restrict__ leav
           sG[pr * GS + qc] = cr * b1 - sr * d1;
           sG[qr * GS + qc] = sr * b1 + cr * d1;
         }
+      }
+      for (int e = tid; e < PW * NPAIR; e += NT) {   // R <- R J
+        const int jc = e % NPAIR, r = e / NPAIR;
+        const double cc = s_c[jc], sc = s_s[jc];
         if (sc != 0.0) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int r = (tid + 256 * h) / NPAIR;
-            const double u = sR[r * GS + pc], v = sR[r * GS + qc];
-            sR[r * GS + pc] = cc * u - sc * v;
-            sR[r * GS + qc] = sc * u + cc * v;
-          }
+          int pc, qc;
+          pair_of(rr, jc, &pc, &qc);
+          const double u = sR[r * GS + pc], v = sR[r * GS + qc];
+          sR[r * GS + pc] = cc * u - sc * v;
+          sR[r * GS + qc] = sc * u + cc * v;
         }
       }
       __syncthreads();
@@ -1581,7 +1596,7 @@ __global__ void __launch_bounds__(256) k_dc_leaf(const DcLeaf* __restrict__ leav
     lam[lf.off + r] = v;
   }
   __syncthreads();
-  for (int e = tid; e < n * n; e += 256) {
+  for (int e = tid; e < n * n; e += NT) {
     const int j = e / n, i = e % n;   // eigenvector j, row i
     X[(int64_t)(lf.off + s_rank[j]) * ldx + lf.off + i] = sR[i * GS + j];
   }
@@ -1654,7 +1669,25 @@ int dc_band_eigh(cudaStream_t st, const double* dsym, const double* sub, int s, 
                  double* Q) {
   const int k = s * m;
   if (k < 1) return KRY_OK;
-  const int leaf_blocks = std::max(1, 32 / s);
+  // leaf width: leaves are solved in parallel (one CTA each), the
+  // merges one after the other (~35 us per separator row): pick the width
+  // with the smaller estimate
+  int PW = 32;
+  {
+    double best = 1e300;
+    for (int w : {32, 64, 96}) {
+      const int lb = std::max(1, w / s);
+      const int nleaf = (m + lb - 1) / lb;
+      const double leaf_us = w == 32 ? 250.0 : (w == 64 ? 1800.0 : 5000.0);   // measured
+      const double cost = leaf_us + (double)(nleaf - 1) * s * 35.0;
+      if (cost < best) { best = cost; PW = w; }
+    }
+    if (const char* e = getenv("KRY_DC_LEAF")) {
+      const int w = atoi(e);
+      if (w == 32 || w == 64 || w == 96) PW = w;
+    }
+  }
+  const int leaf_blocks = std::max(1, PW / s);
   std::vector<DcNode> nodes;
   std::vector<int> pos(k);
   const int root = dc_build(nodes, pos, 0, m, 0, s, leaf_blocks);
@@ -1706,14 +1739,22 @@ int dc_band_eigh(cudaStream_t st, const double* dsym, const double* sub, int s, 
   if ((rc = dalloc(&leaves_d, leaves.size()))) { cleanup(); return rc; }
   cudaMemcpyAsync(leaves_d, leaves.data(), leaves.size() * sizeof(DcLeaf), cudaMemcpyHostToDevice, st);
   cudaStreamSynchronize(st);   // host vectors are read by the copies above
-  k_dc_leaf<<<(unsigned)leaves.size(), 256, 0, st>>>(leaves_d, s, dsym, sub, lam[0], X[0], ldx);
-  count_launch();
   static bool attr[64] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr[dev & 63]) {
     cudaFuncSetAttribute(k_dc_deflate, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_dc_leaf<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_dc_leaf<96>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr[dev & 63] = true;
+  }
+  {
+    const size_t lsm = (size_t)(2 * PW * (PW + 1) + 2 * (PW / 2) + PW) * sizeof(double) + PW * sizeof(int) + 16;
+    const unsigned nl = (unsigned)leaves.size();
+    if (PW == 32) k_dc_leaf<32><<<nl, 256, lsm, st>>>(leaves_d, s, dsym, sub, lam[0], X[0], ldx);
+    else if (PW == 64) k_dc_leaf<64><<<nl, 1024, lsm, st>>>(leaves_d, s, dsym, sub, lam[0], X[0], ldx);
+    else k_dc_leaf<96><<<nl, 1024, lsm, st>>>(leaves_d, s, dsym, sub, lam[0], X[0], ldx);
+    count_launch();
   }
   // internal nodes in post-order (dc_build pushes children first)
   for (size_t ni = 0; ni < nodes.size(); ++ni) {
