@@ -359,60 +359,178 @@ __device__ void extract_block(const double* total, int row0, int s, double* dst)
   __syncthreads();
 }
 
-// The coefficient solve of one fused step (see file header).  Runs on the
-// last CTA of the apply reduction; `total` holds [V^T W0 ; W0^T W0].
+// ---- warp-synchronous small-matrix helpers: the coefficient solve runs on
+// ONE warp (lane l owns elements l and l + 32 of every 8 x 8 slot), with
+// __syncwarp instead of block barriers.  Every element is computed with the
+// same sequence of operations as mm / madd / chol_inv_par above, so the
+// results are bit-identical to the block-wide versions; the ~45 dependent
+// small products of a solve no longer cost block barriers on the last CTA
+// of every step (the serial tail of the recurrence).
+__device__ __forceinline__ void w_mm(double* C, const double* A, int ta, const double* B, int tb,
+                                     int s, double alpha = 1.0, const double* D = nullptr,
+                                     double beta = 0.0) {
+  const int l = threadIdx.x & 31;
+  double out[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int e = l + 32 * h, r = e >> 3, c = e & 7;
+    double v = 0.0;
+    if (r < s && c < s) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (k < s) {
+          const double a = ta ? A[k * 8 + r] : A[r * 8 + k];
+          const double b = tb ? B[c * 8 + k] : B[k * 8 + c];
+          v = fma(a, b, v);
+        }
+      }
+      v *= alpha;
+      if (D) v = fma(beta, D[e], v);
+    }
+    out[h] = v;
+  }
+  __syncwarp();
+  C[l] = out[0];
+  C[l + 32] = out[1];
+  __syncwarp();
+}
+__device__ __forceinline__ void w_madd(double* C, const double* A, const double* B, double beta) {
+  const int l = threadIdx.x & 31;
+  const double v0 = A[l] + beta * B[l];
+  const double v1 = A[l + 32] + beta * B[l + 32];
+  __syncwarp();
+  C[l] = v0;
+  C[l + 32] = v1;
+  __syncwarp();
+}
+__device__ __forceinline__ void w_copy(double* dst, const double* src) {
+  const int l = threadIdx.x & 31;
+  const double v0 = src[l], v1 = src[l + 32];
+  __syncwarp();
+  dst[l] = v0;
+  dst[l + 32] = v1;
+  __syncwarp();
+}
+__device__ __forceinline__ void w_zero(double* dst) {
+  const int l = threadIdx.x & 31;
+  __syncwarp();
+  dst[l] = 0.0;
+  dst[l + 32] = 0.0;
+  __syncwarp();
+}
+__device__ __forceinline__ void w_extract(const double* total, int row0, int s, double* dst) {
+  const int l = threadIdx.x & 31;
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int e = l + 32 * h, r = e >> 3, c = e & 7;
+    dst[e] = (r < s && c < s) ? total[(row0 + r) * 8 + c] : 0.0;
+  }
+  __syncwarp();
+}
+// chol_inv_par on the calling warp (W: 64 doubles of scratch)
+__device__ int w_chol_inv(const double* G, double* R, double* Ri, int s, double* min_ratio,
+                          double* W) {
+  const int l = threadIdx.x & 31;
+  __syncwarp();
+  for (int q = l; q < 64; q += 32) {
+    W[q] = G[q];
+    R[q] = 0.0;
+  }
+  __syncwarp();
+  int bad = 0;
+  for (int k = 0; k < s; ++k) {
+    const double p = W[k * 8 + k];
+    if (!(p > 1e3 * 2.220446049250313e-16 * fabs(G[k * 8 + k])) || !(p > 0.0)) {
+      bad = 1;
+      break;
+    }
+    const double rkk = sqrt(p);
+    if (l >= k && l < s) R[k * 8 + l] = (l == k) ? rkk : W[k * 8 + l] / rkk;
+    __syncwarp();
+    for (int q = l; q < 64; q += 32) {
+      const int i = q >> 3, j = q & 7;
+      if (i > k && j >= i && j < s) W[q] -= R[k * 8 + i] * R[k * 8 + j];
+    }
+    __syncwarp();
+  }
+  double mr = 1e300;
+  if (!bad) {
+    if (l < s) {
+      const int j = l;
+      for (int i = 0; i < 8; ++i) Ri[i * 8 + j] = 0.0;
+      Ri[j * 8 + j] = 1.0 / R[j * 8 + j];
+      for (int i = j - 1; i >= 0; --i) {
+        double v = 0.0;
+        for (int k = i + 1; k <= j; ++k) v += R[i * 8 + k] * Ri[k * 8 + j];
+        Ri[i * 8 + j] = -v / R[i * 8 + i];
+      }
+    } else if (l < 8) {
+      for (int i = 0; i < 8; ++i) Ri[i * 8 + l] = 0.0;
+    }
+    if (l == 0) {
+      double fro = 0.0;
+      for (int i = 0; i < 64; ++i) fro += R[i] * R[i];
+      fro = sqrt(fro);
+      for (int k = 0; k < s; ++k) mr = fmin(mr, R[k * 8 + k] / fro);
+    }
+    mr = __shfl_sync(0xffffffffu, mr, 0);
+  }
+  __syncwarp();
+  *min_ratio = mr;
+  return bad;
+}
+
+// The coefficient solve of one fused step (see file header).  Runs on warp 0
+// of the last CTA of the apply reduction; `total` holds [V^T W0 ; W0^T W0].
 // `row_cw` / `row_ww`: first rows of V_c^T W0 and W0^T W0 in `total`.  With
 // `deferred` (the fused step kernel solves step j+1 ahead of time) a failure
 // only raises KRY_FLAG_FALLBACK: the host then redoes step j+1 on the
 // two-kernel path, which repeats this (idempotent up to the failure point)
 // solve and reports the error at the step the reference reports it.
-__device__ __noinline__ void coef_solve(const double* total, DevState* st, const TStore& T, double (*sm)[64],
+__device__ __noinline__ void coef_solve_w(const double* total, DevState* st, const TStore& T, double (*sm)[64],
                                         int row_cw, int row_ww, int deferred) {
   const int s = st->s;
   double* Gcc = sm[0]; double* Goc = sm[1]; double* GoW = sm[2]; double* Goo = sm[3];
   double* GcW = sm[4]; double* GWW = sm[5]; double* Sc = sm[6]; double* So = sm[7];
   double* A = sm[8]; double* B = sm[9]; double* X = sm[10]; double* Y = sm[11];
   double* Z = sm[12]; double* U = sm[13];
-  __shared__ int s_flag;
-  __shared__ double s_val[4];
+  const int lane = threadIdx.x & 31;
   // the five carried 8x8 blocks in one batch of loads (all in flight)
-  __syncthreads();
-  for (int q = tid(); q < 5 * 64; q += blockDim.x) {
+  __syncwarp();
+  for (int q = lane; q < 5 * 64; q += 32) {
     const int b = q >> 6, e = q & 63;
     const double* src = b == 0 ? st->Gcc : b == 1 ? st->Goc : b == 2 ? st->GoW : b == 3 ? st->Goo : st->So;
     double* dst = b == 0 ? Gcc : b == 1 ? Goc : b == 2 ? GoW : b == 3 ? Goo : So;
     dst[e] = src[e];
   }
-  extract_block(total, row_cw, s, GcW);
-  extract_block(total, row_ww, s, GWW);
+  w_extract(total, row_cw, s, GcW);
+  w_extract(total, row_ww, s, GWW);
   const int j = st->step + 1;        // 1-based step being solved
   const int has_old = st->has_old;
   // 1. lazy CholQR2 correction of the current block: Gcc = R2^T R2, Sc = R2^-1
   {
     double mr;
-    if (tid() == 0) s_flag = 0;
-    const int bad = chol_inv_par(Gcc, X, Sc, s, &mr);
-    if (tid() == 0) s_flag = bad;
-  }
-  __syncthreads();
-  if (s_flag) {  // the stored block is not numerically full rank
-    if (deferred) {
-      if (tid() == 0) st->flags |= KRY_FLAG_FALLBACK;
-    } else {
-      set_status(st, KRY_ERR_DEFLATION);
+    const int bad = w_chol_inv(Gcc, X, Sc, s, &mr, U);
+    if (bad) {  // the stored block is not numerically full rank
+      if (deferred) {
+        if (lane == 0) st->flags |= KRY_FLAG_FALLBACK;
+      } else {
+        if (lane == 0 && st->status == KRY_OK) st->status = KRY_ERR_DEFLATION;
+      }
+      __syncwarp();
+      return;
     }
-    __syncthreads();
-    return;
   }
   // 2. finalise the previous coupling block (or gamma): R_hat = R2 * R1prev
-  m_copy(Y, st->R1prev);
-  mm(Z, X, 0, Y, 0, s);
+  w_copy(Y, st->R1prev);
+  w_mm(Z, X, 0, Y, 0, s);
   if (j == 1) {
-    if (tid() < 64 && !st->replay) st->gamma[tid()] = Z[tid()];
+    if (!st->replay) { st->gamma[lane] = Z[lane]; st->gamma[lane + 32] = Z[lane + 32]; }
   } else {
     double* dst = T.sub + (int64_t)(j - 2) * 64;
     if (st->replay) {
-      if (tid() == 0) {
+      if (lane == 0) {
         double num = 0.0, den = 0.0;
         for (int q = 0; q < 64; ++q) {
           double d = Z[q] - dst[q];
@@ -422,140 +540,138 @@ __device__ __noinline__ void coef_solve(const double* total, DevState* st, const
         double rel = sqrt(num) / fmax(sqrt(den), 1e-300);
         st->replay_err = fmax(st->replay_err, rel);
       }
-    } else if (tid() < 64) {
-      dst[tid()] = Z[tid()];
+    } else {
+      dst[lane] = Z[lane];
+      dst[lane + 32] = Z[lane + 32];
     }
   }
-  if (tid() < 64) {
-    st->Sc[tid()] = Sc[tid()];
-    T.S[(int64_t)(j - 1) * 64 + tid()] = Sc[tid()];
+  for (int e = lane; e < 64; e += 32) {
+    st->Sc[e] = Sc[e];
+    T.S[(int64_t)(j - 1) * 64 + e] = Sc[e];
   }
-  if (tid() == 0) st->flags &= ~KRY_FLAG_FALLBACK;
-  __syncthreads();
+  if (lane == 0) st->flags &= ~KRY_FLAG_FALLBACK;
+  __syncwarp();
   // 3. Gram blocks in the orthonormal (true) basis
-  mm(A, Sc, 1, Gcc, 0, s); mm(Gcc, A, 0, Sc, 0, s);    // Gcc^ = Sc^T Gcc Sc
-  mm(A, Sc, 1, GcW, 0, s); mm(GcW, A, 0, Sc, 0, s);    // GcW^
-  mm(A, Sc, 1, GWW, 0, s); mm(GWW, A, 0, Sc, 0, s);    // GWW^
+  w_mm(A, Sc, 1, Gcc, 0, s); w_mm(Gcc, A, 0, Sc, 0, s);    // Gcc^ = Sc^T Gcc Sc
+  w_mm(A, Sc, 1, GcW, 0, s); w_mm(GcW, A, 0, Sc, 0, s);    // GcW^
+  w_mm(A, Sc, 1, GWW, 0, s); w_mm(GWW, A, 0, Sc, 0, s);    // GWW^
   if (has_old) {
-    mm(A, So, 1, Goo, 0, s); mm(Goo, A, 0, So, 0, s);  // Goo^
-    mm(A, So, 1, Goc, 0, s); mm(Goc, A, 0, Sc, 0, s);  // Goc^
-    mm(A, So, 1, GoW, 0, s); mm(GoW, A, 0, Sc, 0, s);  // GoW^
+    w_mm(A, So, 1, Goo, 0, s); w_mm(Goo, A, 0, So, 0, s);  // Goo^
+    w_mm(A, So, 1, Goc, 0, s); w_mm(Goc, A, 0, Sc, 0, s);  // Goc^
+    w_mm(A, So, 1, GoW, 0, s); w_mm(GoW, A, 0, Sc, 0, s);  // GoW^
   }
   // 4. MGS performed twice on W = W0 - Vo a - Vc b  (basis.py:164-180)
-  m_zero(A);  // a (off sum)
-  m_zero(B);  // b (diag sum)
+  w_zero(A);  // a (off sum)
+  w_zero(B);  // b (diag sum)
   for (int sweep = 0; sweep < 2; ++sweep) {
     if (has_old) {
       // alpha = GoW - Goo a - Goc b
-      mm(X, Goo, 0, A, 0, s, -1.0, GoW, 1.0);
-      mm(X, Goc, 0, B, 0, s, -1.0, X, 1.0);
-      madd(A, A, X, 1.0);
+      w_mm(X, Goo, 0, A, 0, s, -1.0, GoW, 1.0);
+      w_mm(X, Goc, 0, B, 0, s, -1.0, X, 1.0);
+      w_madd(A, A, X, 1.0);
     }
     // beta = GcW - Goc^T a - Gcc b
     if (has_old) {
-      mm(X, Goc, 1, A, 0, s, -1.0, GcW, 1.0);
+      w_mm(X, Goc, 1, A, 0, s, -1.0, GcW, 1.0);
     } else {
-      m_copy(X, GcW);
+      w_copy(X, GcW);
     }
-    mm(X, Gcc, 0, B, 0, s, -1.0, X, 1.0);
-    madd(B, B, X, 1.0);
+    w_mm(X, Gcc, 0, B, 0, s, -1.0, X, 1.0);
+    w_madd(B, B, X, 1.0);
   }
   // 5. W^T W = GWW - GcW^T b - b^T GcW + b^T Gcc b  (+ the old-block terms)
-  mm(X, GcW, 1, B, 0, s);                 // X = GcW^T b ; Z = GWW - X - X^T
-  __syncthreads();
-  if (tid() < 64) {
-    int r = tid() >> 3, c = tid() & 7;
-    Z[tid()] = GWW[tid()] - X[r * 8 + c] - X[c * 8 + r];
+  w_mm(X, GcW, 1, B, 0, s);                 // X = GcW^T b ; Z = GWW - X - X^T
+  __syncwarp();
+  for (int e = lane; e < 64; e += 32) {
+    int r = e >> 3, c = e & 7;
+    Z[e] = GWW[e] - X[r * 8 + c] - X[c * 8 + r];
   }
-  __syncthreads();
-  mm(U, Gcc, 0, B, 0, s);                 // Gcc b
-  mm(Z, B, 1, U, 0, s, 1.0, Z, 1.0);      // + b^T Gcc b
+  __syncwarp();
+  w_mm(U, Gcc, 0, B, 0, s);                 // Gcc b
+  w_mm(Z, B, 1, U, 0, s, 1.0, Z, 1.0);      // + b^T Gcc b
   if (has_old) {
-    mm(X, GoW, 1, A, 0, s);               // GoW^T a
-    __syncthreads();
-    if (tid() < 64) {
-      int r = tid() >> 3, c = tid() & 7;
-      Z[tid()] = Z[tid()] - X[r * 8 + c] - X[c * 8 + r];
+    w_mm(X, GoW, 1, A, 0, s);               // GoW^T a
+    __syncwarp();
+    for (int e = lane; e < 64; e += 32) {
+      int r = e >> 3, c = e & 7;
+      Z[e] = Z[e] - X[r * 8 + c] - X[c * 8 + r];
     }
-    __syncthreads();
-    mm(U, Goo, 0, A, 0, s);               // Goo a
-    mm(Z, A, 1, U, 0, s, 1.0, Z, 1.0);    // + a^T Goo a
-    mm(U, Goc, 0, B, 0, s);               // Goc b
-    mm(X, A, 1, U, 0, s);                 // a^T Goc b
-    __syncthreads();
-    if (tid() < 64) {
-      int r = tid() >> 3, c = tid() & 7;
-      Z[tid()] = Z[tid()] + X[r * 8 + c] + X[c * 8 + r];
+    __syncwarp();
+    w_mm(U, Goo, 0, A, 0, s);               // Goo a
+    w_mm(Z, A, 1, U, 0, s, 1.0, Z, 1.0);    // + a^T Goo a
+    w_mm(U, Goc, 0, B, 0, s);               // Goc b
+    w_mm(X, A, 1, U, 0, s);                 // a^T Goc b
+    __syncwarp();
+    for (int e = lane; e < 64; e += 32) {
+      int r = e >> 3, c = e & 7;
+      Z[e] = Z[e] + X[r * 8 + c] + X[c * 8 + r];
     }
-    __syncthreads();
+    __syncwarp();
   }
   // symmetrise W^T W
-  __syncthreads();
-  if (tid() < 64) {
-    int r = tid() >> 3, c = tid() & 7;
-    U[tid()] = 0.5 * (Z[r * 8 + c] + Z[c * 8 + r]);
+  __syncwarp();
+  for (int e = lane; e < 64; e += 32) {
+    int r = e >> 3, c = e & 7;
+    U[e] = 0.5 * (Z[r * 8 + c] + Z[c * 8 + r]);
   }
-  __syncthreads();
-  if (tid() == 0) {
-    s_val[0] = m_trace(GWW, s);
-    s_val[1] = m_trace(U, s);
-    st->scale2 = s_val[0];
-    st->w2 = s_val[1];
+  __syncwarp();
+  const double scale2 = m_trace(GWW, s), w2 = m_trace(U, s);
+  if (lane == 0) {
+    st->scale2 = scale2;
+    st->w2 = w2;
   }
-  __syncthreads();
-  const double scale2 = s_val[0], w2 = s_val[1];
   // 6. zero / near-zero residual block: decided by the explicit path
   if (!(w2 > 1e-10 * scale2)) {
-    if (tid() == 0) st->flags |= KRY_FLAG_FALLBACK;
+    if (lane == 0) st->flags |= KRY_FLAG_FALLBACK;
     return;
   }
   // 7. Cholesky QR of the residual block
   {
     double mr = 0.0;
-    const int bad = chol_inv_par(U, X, Y, s, &mr);
+    const int bad = w_chol_inv(U, X, Y, s, &mr, Z);
     const int fail = bad || mr < 1e-5;
-    if (!fail && tid() < 64) {
-      st->R1prev[tid()] = X[tid()];
-      T.tau1[(int64_t)(j - 1) * 64 + tid()] = X[tid()];
+    if (fail) {
+      if (lane == 0) st->flags |= KRY_FLAG_FALLBACK;
+      return;
     }
-    if (tid() == 0) s_flag = fail;
-  }
-  __syncthreads();
-  if (s_flag) {
-    if (tid() == 0) st->flags |= KRY_FLAG_FALLBACK;
-    return;
+    for (int e = lane; e < 64; e += 32) {
+      st->R1prev[e] = X[e];
+      T.tau1[(int64_t)(j - 1) * 64 + e] = X[e];
+    }
   }
   // 8. combine coefficients: Vn = Vo Mo + Vc Mc + W0 Mw
-  mm(Z, Sc, 0, Y, 0, s);                   // Mw = Sc R1^-1
-  if (tid() < 64) st->M[128 + tid()] = Z[tid()];
-  mm(U, B, 0, Y, 0, s);                    // b R1^-1
-  mm(Z, Sc, 0, U, 0, s, -1.0);             // Mc = -Sc b R1^-1
-  if (tid() < 64) st->M[64 + tid()] = Z[tid()];
+  w_mm(Z, Sc, 0, Y, 0, s);                   // Mw = Sc R1^-1
+  for (int e = lane; e < 64; e += 32) st->M[128 + e] = Z[e];
+  __syncwarp();
+  w_mm(U, B, 0, Y, 0, s);                    // b R1^-1
+  w_mm(Z, Sc, 0, U, 0, s, -1.0);             // Mc = -Sc b R1^-1
+  for (int e = lane; e < 64; e += 32) st->M[64 + e] = Z[e];
+  __syncwarp();
   if (has_old) {
-    mm(U, A, 0, Y, 0, s);
-    mm(Z, So, 0, U, 0, s, -1.0);           // Mo = -So a R1^-1
+    w_mm(U, A, 0, Y, 0, s);
+    w_mm(Z, So, 0, U, 0, s, -1.0);           // Mo = -So a R1^-1
   } else {
-    m_zero(Z);
+    w_zero(Z);
   }
-  if (tid() < 64) st->M[tid()] = Z[tid()];
+  for (int e = lane; e < 64; e += 32) st->M[e] = Z[e];
   // 9. projection blocks of step j
-  if (!st->replay && tid() < 64) {
-    int r = tid() >> 3, c = tid() & 7;
+  for (int e = lane; e < 64; e += 32) {
+    int r = e >> 3, c = e & 7;
     const int64_t o = (int64_t)(j - 1) * 64;
-    T.draw[o + tid()] = B[tid()];
-    T.dsym[o + tid()] = 0.5 * (B[r * 8 + c] + B[c * 8 + r]);
-    T.off[o + tid()] = has_old ? A[tid()] : 0.0;
+    if (!st->replay) {
+      T.draw[o + e] = B[e];
+      T.dsym[o + e] = 0.5 * (B[r * 8 + c] + B[c * 8 + r]);
+      T.off[o + e] = has_old ? A[e] : 0.0;
+    }
+    st->So[e] = Sc[e];
+    st->Goo[e] = st->Gcc[e];
   }
-  if (tid() < 64) {
-    st->So[tid()] = Sc[tid()];
-    st->Goo[tid()] = st->Gcc[tid()];
-  }
-  __syncthreads();
-  if (tid() == 0) {
+  __syncwarp();
+  if (lane == 0) {
     st->step = j;
     st->has_old = 1;
   }
-  __syncthreads();
+  __syncwarp();
 }
 
 __device__ __noinline__ void run_post(int post, const double* total, DevState* st, const TStore& T,
@@ -580,10 +696,14 @@ __device__ __noinline__ void run_post(int post, const double* total, DevState* s
       finalize_tau(st, T, sm, sm[2]);
       break;
     case POST_STEP:
-      coef_solve(total, st, T, sm, 0, s, 0);
+      __syncthreads();
+      if (threadIdx.x < 32) coef_solve_w(total, st, T, sm, 0, s, 0);
+      __syncthreads();
       break;
     case POST_STEP8:   // [V^T W0 | W0^T W0] as two 8-row blocks (k_apply_gl)
-      coef_solve(total, st, T, sm, 0, 8, 0);
+      __syncthreads();
+      if (threadIdx.x < 32) coef_solve_w(total, st, T, sm, 0, 8, 0);
+      __syncthreads();
       break;
     case POST_FUSED:
       // [Goc | GoW | Gcc | GcW | GWW] as five 8x8 blocks (k_step): the
@@ -597,7 +717,9 @@ __device__ __noinline__ void run_post(int post, const double* total, DevState* s
         st->Gcc[tid()] = sm[2][tid()];
       }
       finalize_tau(st, T, sm, sm[2]);
-      coef_solve(total, st, T, sm, 24, 32, 1);
+      __syncthreads();
+      if (threadIdx.x < 32) coef_solve_w(total, st, T, sm, 24, 32, 1);
+      __syncthreads();
       break;
     case POST_INIT: {
       extract_block(total, 0, s, sm[0]);
