@@ -2173,7 +2173,7 @@ int kry_finalize_lyap(kry_ctx* c, double eps, int* rank, double* discarded) {
     StageTimer tm(c->stream);
     rc = launch_ytilde(c->stream, b.u, b.lam, k, b.u, b.lam, k, c->s, Y, k, mind, &nparts);
     if (rc == KRY_OK) rc = syevd(c, Y, k, mu, true);
-    tm.mark("finalize: syevd(Ytilde)");
+    tm.mark("finalize: Jacobi eigh(Ytilde)");
     if (rc == KRY_OK) rc = launch_truncate(c->stream, mu, k, 0, eps, mind, nparts, work, outd);
     if (rc != KRY_OK) { cleanup(); return rc; }
     KRY_CUDA(cudaMemcpy(hout, outd, 5 * sizeof(double), cudaMemcpyDeviceToHost));

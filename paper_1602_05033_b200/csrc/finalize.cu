@@ -5,9 +5,11 @@
 // eigenbasis  Ytilde = -(u u^T)/(lam_i + lam_j)  (guarded denominators,
 // kernels.py:31-45), its truncated factorisation (truncated_spd_factor,
 // kernels.py:309-331 / truncated_svd_factor, kernels.py:334-345) and
-// qy = Q * factor.  The two dense k x k eigensolves / the SVD run once per
-// solve through cuSOLVER (plain library dense LAPACK); assembly, Ytilde, the
-// exact tail-mass truncation rule and the factor scaling are kernels here.
+// qy = Q * factor.  The eigendecomposition of T_m is the band divide and
+// conquer of eigen.cu, the truncated factorisations work on low-rank factors
+// of Ytilde (pivoted Cholesky / cross factorisation + block Jacobi, dense.cu);
+// assembly, Ytilde, the exact tail-mass truncation rule and the factor
+// scaling are kernels here.  No library call anywhere.
 #include "kry_internal.cuh"
 #include "finalize.cuh"
 #include <cmath>
@@ -65,7 +67,7 @@ __global__ void k_ytilde(const double* u, const double* lx, int nx, const double
 }
 
 // truncation rule of kernels.py:322-331 / 338-341 on a spectrum `ev` of length
-// k stored ascending (desc=0: eigenvalues from syevd) or descending (desc=1:
+// k stored ascending (desc=0: eigenvalues of an eigensolver) or descending (desc=1:
 // singular values).  out[0] = rank, out[1] = discarded, out[2] = min value,
 // out[3] = max |value|, out[4] = min denominator over parts.
 template <bool SM>
@@ -124,7 +126,7 @@ __global__ void k_scale_factor(const double* W, int64_t ldw, const double* ev, i
     const int src = desc ? c : (k - 1 - c);
     const double val = ev[src];
     const double sc = sqrt(fmax(val, 0.0));
-    // transposed: W holds rows as vectors (VT from gesvd): vector c = row c
+    // transposed: W holds rows as vectors (VT of an SVD): vector c = row c
     const double x = transposed ? W[(int64_t)r * ldw + src] : W[(int64_t)src * ldw + r];
     factor[e] = x * sc;
   }

@@ -3,8 +3,8 @@
 // Data layout in HBM
 //   * block vectors: n x s row-major ("point major"): the s values of one grid
 //     point are contiguous; consecutive points are `ld` doubles apart (ld = s
-//     for the pass-1 window, ld = (G+2)*s for the interleaved pass-2 chunk
-//     buffer so that a chunk is one column-major (G*s) x n cuBLAS operand).
+//     everywhere: the pass-1 window and the pass-2 chunk slots share the
+//     ring layout, a block is written once).
 //   * s x s blocks: fixed 8 x 8 row-major slots (s <= 8), zero padded.
 //   * projected matrix T_m: per-step slots of the raw MGS sums, symmetrised
 //     diagonal blocks, coupling blocks tau (R factors) and the lazy CholQR2

@@ -1,4 +1,4 @@
-"""Time kry_finalize_lyap repeatedly after one pass 1 (syevd variance probe)."""
+"""Time kry_finalize_lyap repeatedly after one pass 1 (finalisation variance probe)."""
 import ctypes, sys, time
 sys.path.insert(0, ".")
 import numpy as np
