@@ -39,6 +39,13 @@ static constexpr double EPS = 2.220446049250313e-16;
 #ifndef KRY_SECULAR_W8
 #define KRY_SECULAR_W8 0
 #endif
+// poles of the big appends (K > 2048) cached in registers: 1 = 256 threads x
+// 24 terms, 2 = 256 x 16 / 512 x 12 (both measured SLOWER on c5: 2.0 / 1.9 s
+// against 1.32 s -- one or two CTAs per SM cannot hide the reciprocal chains),
+// 0 = streamed from global memory / L1 with 16 small CTAs per SM
+#ifndef KRY_SECULAR_BIG
+#define KRY_SECULAR_BIG 0
+#endif
 
 // ------------------------------------------------------------------ block scan helpers
 __device__ __forceinline__ int warp_incl_scan(int v) {
@@ -1127,6 +1134,12 @@ int EigEngine::append_block(cudaStream_t st, const double* dsym_blk, const doubl
       if (K <= 256 * 8) k_eig_secular<8, 8><<<K + 1, 256, 0, st>>>(v);
 #else
       if (K <= 128 * 16) k_eig_secular<4, 16><<<K + 1, 128, 0, st>>>(v);
+#endif
+#if KRY_SECULAR_BIG == 1
+      else if (K <= 256 * 24) k_eig_secular<8, 24><<<K + 1, 256, 0, st>>>(v);
+#elif KRY_SECULAR_BIG == 2
+      else if (K <= 256 * 16) k_eig_secular<8, 16><<<K + 1, 256, 0, st>>>(v);
+      else if (K <= 512 * 12) k_eig_secular<16, 12><<<K + 1, 512, 0, st>>>(v);
 #endif
       else k_eig_secular<4, 0><<<K + 1, 128, 0, st>>>(v);
     } else if (K >= 256) {
