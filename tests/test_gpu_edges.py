@@ -111,3 +111,32 @@ def test_alternative_step_kernels_match_oracle(env, s, monkeypatch):
     za, zb = sol.z, ref.z
     x, xr = za @ za.T, zb @ zb.T
     assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", [{"KRY_FINALIZE_DENSE": "1"}, {"KRY_T_JACOBI": "1"}])
+def test_finalisation_dense_fallbacks_match_oracle(env, monkeypatch):
+    # the routes taken when the reduced solution is not of low rank (dense
+    # block Jacobi eigh / SVD of Ytilde) and the A/B route of eigh(T_m) on
+    # the dense Jacobi kernel instead of the band divide and conquer
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    a = P.laplacian3d(16)
+    c = np.random.default_rng(77).standard_normal((a.shape[0], 2))
+    opts = dict(tol=1e-9, max_m=200, storage="windowed")
+    ref = ko.solve_lyapunov(ko.SparseOperator(a), c, ko.SolveOptions(**opts))
+    sol = kb.solve_lyapunov(kb.SparseOperator(a), c, kb.SolveOptions(**opts))
+    assert sol.iterations == ref.iterations and sol.rank == ref.rank
+    x, xr = sol.z @ sol.z.T, ref.z @ ref.z.T
+    assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
+    # two-sided Sylvester: dense Jacobi SVD of Ytilde
+    b = P.laplacian2d(20)
+    c1 = np.random.default_rng(78).standard_normal((a.shape[0], 2))
+    c2 = np.random.default_rng(79).standard_normal((b.shape[0], 2))
+    rs = ko.solve_sylvester(ko.SparseOperator(a), ko.SparseOperator(b), c1, c2,
+                                      ko.SolveOptions(**opts))
+    ss = kb.solve_sylvester_two_sided(kb.SparseOperator(a), kb.SparseOperator(b), c1, c2,
+                                      kb.SolveOptions(**opts))
+    assert ss.iterations == rs.iterations and ss.rank == rs.rank
+    x, xr = ss.z1 @ ss.z2.T, rs.z1 @ rs.z2.T
+    assert np.linalg.norm(x - xr) <= 1e-8 * np.linalg.norm(xr)
