@@ -1727,9 +1727,28 @@ int kry_solve_lyap_pass1(kry_ctx* c, double tol, int max_m, int check_period, do
   };
   int rc = KRY_OK;
   bool done = false;
+  // KRY_TIMING: host time of the loop's phases (wait for the step, queue the
+  // next step, queue the eigen work, collect the previous check)
+  const bool htime = getenv("KRY_TIMING") != nullptr;
+  double h_wait = 0.0, h_pre = 0.0, h_eig = 0.0, h_col = 0.0;
+  struct HT {
+    bool on; double* acc; double t0;
+    HT(bool o, double* a) : on(o), acc(a), t0(o ? now_s() : 0.0) {}
+    ~HT() { if (on) *acc += now_s() - t0; }
+  };
+  struct HReport {
+    bool on; double *a, *b, *c2, *d;
+    ~HReport() {
+      if (on) fprintf(stderr, "[kry] pass-1 host phases: wait step %.1f ms, queue step %.1f ms, queue eigen %.1f ms, collect check %.1f ms\n",
+                      *a * 1e3, *b * 1e3, *c2 * 1e3, *d * 1e3);
+    }
+  } hrep{htime, &h_wait, &h_pre, &h_eig, &h_col};
   for (int it = 1; it <= max_m && !done; ++it) {
     int ex = 0;
-    rc = step_core(c, 1, &ex);
+    {
+      HT t(htime, &h_wait);
+      rc = step_core(c, 1, &ex);
+    }
     if (rc) {
       rc = rescue(rc);
       done = true;
@@ -1741,6 +1760,7 @@ int kry_solve_lyap_pass1(kry_ctx* c, double tol, int max_m, int check_period, do
     KRY_CUDA(cudaEventRecord(c->ev_t, c->stream));
     KRY_CUDA(cudaEventRecord(c->ev_step[it], c->stream));
     if (!ex && it < max_m) {
+      HT t(htime, &h_pre);
       rc = step_prelaunch(c);
       if (rc) {
         rc = rescue(rc);
@@ -1748,16 +1768,21 @@ int kry_solve_lyap_pass1(kry_ctx* c, double tol, int max_m, int check_period, do
         break;
       }
     }
+    if (getenv("KRY_DEBUG_NO_EIG")) { last_it = it; continue; }   // measurement: recurrence only
     const bool chk = (it % check_period == 0) || ex;
     const int slot = it & 1;
-    KRY_CUDA(cudaStreamWaitEvent(c->estream, c->ev_t, 0));
-    KRY_CUDA(cudaEventRecord(c->ev_pool[it].first, c->estream));
-    rc = launch_eigen_step(c, it, chk, ex != 0, slot, true);
-    if (rc) break;
-    KRY_CUDA(cudaEventRecord(c->ev_pool[it].second, c->estream));
+    {
+      HT t(htime, &h_eig);
+      KRY_CUDA(cudaStreamWaitEvent(c->estream, c->ev_t, 0));
+      KRY_CUDA(cudaEventRecord(c->ev_pool[it].first, c->estream));
+      rc = launch_eigen_step(c, it, chk, ex != 0, slot, true);
+      if (rc) break;
+      KRY_CUDA(cudaEventRecord(c->ev_pool[it].second, c->estream));
+    }
     last_it = it;
     if (pending > 0) {   // result of the previous iteration's check
       double res = 0.0;
+      HT t(htime, &h_col);
       rc = collect_check(c, pending_slot, c->beta2, &res, &rel);
       if (rc) break;
       record(pending, rel);
