@@ -36,6 +36,45 @@
 namespace kry {
 
 static constexpr double EPS = 2.220446049250313e-16;
+
+// Programmatic dependent launch: the kernels of an append form a chain of
+// short dependent launches on one stream (5 per scalar row, ~10^4 per c4
+// solve).  Each kernel lets its successor be scheduled at once
+// (launch_dependents) and waits for its predecessor's completion and memory
+// flush before touching any data (griddepcontrol.wait), so the launch
+// latency of kernel i+1 overlaps the execution of kernel i.  Both are no-ops
+// for a launch without the attribute (the finalisation's plain launches).
+__device__ __forceinline__ void pdl_sync() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+static bool pdl_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KRY_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+template <class... KArgs, class... Args>
+static void pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  if (!pdl_on()) {
+    kern<<<grid, block, smem, st>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 #ifndef KRY_SECULAR_W8
 #define KRY_SECULAR_W8 0
 #endif
@@ -116,6 +155,7 @@ __device__ double block_sum(double v) {
 template <bool SM>
 __global__ void __launch_bounds__(1024) k_eig_deflate(EigView e, int K, const double* dsym_blk,
                                                       const double* sub_prev, int a) {
+  pdl_sync();
   extern __shared__ double dyn_sm[];
   if (SM) {
     e.z = dyn_sm;
@@ -399,6 +439,7 @@ __device__ __forceinline__ double model_step(double t, double h, double psiL, do
 // thread, MT * NT >= p); MT = 0: stream them from global memory.
 template <int W, int MT>
 __global__ void __launch_bounds__(32 * W) k_eig_secular(EigView e) {
+  pdl_sync();
   constexpr int NT = 32 * W;
   __shared__ double red[2][W][4];   // double-buffered: one barrier per reduction
   __shared__ double s_t1;
@@ -601,6 +642,7 @@ __global__ void __launch_bounds__(32 * W) k_eig_secular(EigView e) {
 // combination across lanes and warps.
 template <int W>
 __global__ void __launch_bounds__(32 * W) k_eig_zhat(EigView e) {
+  pdl_sync();
   constexpr int NT = 32 * W;
   __shared__ double red[W];
   const int p = e.counts[0];
@@ -665,6 +707,7 @@ __device__ __forceinline__ int count_lt(const double* a, int n, double v) {  // 
 
 template <int S>
 __global__ void __launch_bounds__(E4_RT) k_eig_vec_partial(EigView e, double* part, int nroot_cap) {
+  pdl_sync();
   const int p = e.counts[0];
   const int chunk = blockIdx.y;
   const int c0 = chunk * E4_CH;
@@ -715,6 +758,7 @@ __global__ void __launch_bounds__(E4_RT) k_eig_vec_partial(EigView e, double* pa
 template <int S>
 __global__ void __launch_bounds__(128) k_eig_vec_finish(EigView e, const double* part,
                                                         int nroot_cap, int K, int root_blocks) {
+  pdl_sync();
   constexpr int NV = 2 * S;
   constexpr int NVP = NV <= 2 ? 2 : NV <= 4 ? 4 : NV <= 8 ? 8 : 16;   // lanes per root (pow2)
   constexpr int RPB = 128 / NVP;
@@ -777,6 +821,7 @@ __global__ void __launch_bounds__(128) k_eig_vec_finish(EigView e, const double*
 // u[j][c] = sum_r F[r][j] gamma[r][c] ;  w[j][c] = sum_r L[r][j] tau[c][r]
 __global__ void k_uw(const double* F, const double* L, int64_t km, int k, int s,
                      const double* gamma, const double* tau, double* u, double* w) {
+  pdl_sync();
   __shared__ double g[64], tt[64];
   if (threadIdx.x < 64) {
     g[threadIdx.x] = gamma[threadIdx.x];
@@ -861,6 +906,7 @@ __global__ void __launch_bounds__(32 * CC_NW) k_cauchy_mma(int nx, const double*
                                                            const double* __restrict__ cy,
                                                            double* part, unsigned* cnt,
                                                            double* res) {
+  pdl_sync();
   constexpr int KS = (S + 3) / 4;   // k-steps of the first product
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -1122,38 +1168,38 @@ int EigEngine::append_block(cudaStream_t st, const double* dsym_blk, const doubl
                                       200 * 1024));
         deflate_attr = true;
       }
-      k_eig_deflate<true><<<1, 1024, dsm, st>>>(v, K, dsym_blk, sub_prev, a);
+      pdl_launch(k_eig_deflate<true>, dim3(1), dim3(1024), dsm, st, v, K, dsym_blk, sub_prev, a);
     } else {
-      k_eig_deflate<false><<<1, 1024, 0, st>>>(v, K, dsym_blk, sub_prev, a);
+      pdl_launch(k_eig_deflate<false>, dim3(1), dim3(1024), 0, st, v, K, dsym_blk, sub_prev, a);
     }
     // K+1 roots at most, one CTA each; threads per root grow with K
     if (K >= 1024) {
 #if KRY_SECULAR_W8 == 2
-      if (K <= 64 * 32) k_eig_secular<2, 32><<<K + 1, 64, 0, st>>>(v);
+      if (K <= 64 * 32) pdl_launch(k_eig_secular<2, 32>, dim3(K + 1), dim3(64), 0, st, v);
 #elif KRY_SECULAR_W8
-      if (K <= 256 * 8) k_eig_secular<8, 8><<<K + 1, 256, 0, st>>>(v);
+      if (K <= 256 * 8) pdl_launch(k_eig_secular<8, 8>, dim3(K + 1), dim3(256), 0, st, v);
 #else
-      if (K <= 128 * 16) k_eig_secular<4, 16><<<K + 1, 128, 0, st>>>(v);
+      if (K <= 128 * 16) pdl_launch(k_eig_secular<4, 16>, dim3(K + 1), dim3(128), 0, st, v);
 #endif
 #if KRY_SECULAR_BIG == 1
-      else if (K <= 256 * 24) k_eig_secular<8, 24><<<K + 1, 256, 0, st>>>(v);
+      else if (K <= 256 * 24) pdl_launch(k_eig_secular<8, 24>, dim3(K + 1), dim3(256), 0, st, v);
 #elif KRY_SECULAR_BIG == 2
-      else if (K <= 256 * 16) k_eig_secular<8, 16><<<K + 1, 256, 0, st>>>(v);
-      else if (K <= 512 * 12) k_eig_secular<16, 12><<<K + 1, 512, 0, st>>>(v);
+      else if (K <= 256 * 16) pdl_launch(k_eig_secular<8, 16>, dim3(K + 1), dim3(256), 0, st, v);
+      else if (K <= 512 * 12) pdl_launch(k_eig_secular<16, 12>, dim3(K + 1), dim3(512), 0, st, v);
 #endif
-      else k_eig_secular<4, 0><<<K + 1, 128, 0, st>>>(v);
+      else pdl_launch(k_eig_secular<4, 0>, dim3(K + 1), dim3(128), 0, st, v);
     } else if (K >= 256) {
-      k_eig_secular<2, 16><<<K + 1, 64, 0, st>>>(v);
+      pdl_launch(k_eig_secular<2, 16>, dim3(K + 1), dim3(64), 0, st, v);
     } else if (K >= 64) {
-      k_eig_secular<1, 8><<<K + 1, 32, 0, st>>>(v);
+      pdl_launch(k_eig_secular<1, 8>, dim3(K + 1), dim3(32), 0, st, v);
     } else {
-      k_eig_secular<1, 2><<<K + 1, 32, 0, st>>>(v);
+      pdl_launch(k_eig_secular<1, 2>, dim3(K + 1), dim3(32), 0, st, v);
     }
     int nl = 2;
     if (K > 0) {
-      if (K >= 1024) k_eig_zhat<4><<<K, 128, 0, st>>>(v);
-      else if (K >= 256) k_eig_zhat<2><<<K, 64, 0, st>>>(v);
-      else k_eig_zhat<1><<<K, 32, 0, st>>>(v);
+      if (K >= 1024) pdl_launch(k_eig_zhat<4>, dim3(K), dim3(128), 0, st, v);
+      else if (K >= 256) pdl_launch(k_eig_zhat<2>, dim3(K), dim3(64), 0, st, v);
+      else pdl_launch(k_eig_zhat<1>, dim3(K), dim3(32), 0, st, v);
       ++nl;
     }
     const int root_blocks = (K + 1 + 127) / 128;
@@ -1162,9 +1208,9 @@ int EigEngine::append_block(cudaStream_t st, const double* dsym_blk, const doubl
     dim3 g1(root_blocks, nch);
     const int ndef_blocks = (K + 127) / 128;
 #define L(S)                                                                               \
-  k_eig_vec_partial<S><<<g1, 128, 0, st>>>(v, vpart, cap);                                \
-  k_eig_vec_finish<S><<<(K + 1 + fin_rpb(S) - 1) / fin_rpb(S) + ndef_blocks, 128, 0, st>>>( \
-      v, vpart, cap, K, (K + 1 + fin_rpb(S) - 1) / fin_rpb(S))
+  pdl_launch(k_eig_vec_partial<S>, g1, dim3(128), 0, st, v, vpart, cap);                   \
+  pdl_launch(k_eig_vec_finish<S>, dim3((K + 1 + fin_rpb(S) - 1) / fin_rpb(S) + ndef_blocks), dim3(128), 0, st, \
+             v, (const double*)vpart, cap, K, (K + 1 + fin_rpb(S) - 1) / fin_rpb(S))
     switch (s) {
       case 1: L(1); break; case 2: L(2); break; case 3: L(3); break; case 4: L(4); break;
       case 5: L(5); break; case 6: L(6); break; case 7: L(7); break; case 8: L(8); break;
@@ -1213,7 +1259,7 @@ int EigEngine::cauchy(cudaStream_t st, int nx, const double* lx, const double* a
   const int gx = std::max(1, (nx + CC_XR - 1) / CC_XR);
   dim3 grid(gx, cauchy_splits(nx, ny));
 #define L(S) \
-  k_cauchy_mma<S><<<grid, 32 * CC_NW, 0, st>>>(nx, lx, ax, ny, ly, by, cy, cpart, cnt, out2)
+  pdl_launch(k_cauchy_mma<S>, grid, dim3(32 * CC_NW), 0, st, nx, lx, ax, ny, ly, by, cy, cpart, cnt, out2)
   switch (s) {
     case 1: L(1); break; case 2: L(2); break; case 3: L(3); break; case 4: L(4); break;
     case 5: L(5); break; case 6: L(6); break; case 7: L(7); break; case 8: L(8); break;
@@ -1228,7 +1274,7 @@ int EigEngine::cauchy(cudaStream_t st, int nx, const double* lx, const double* a
 int EigEngine::compute_uw(cudaStream_t st, const double* gamma, const double* tau_blk) {
   int grid = (K + 255) / 256;
   if (grid < 1) grid = 1;
-  k_uw<<<grid, 256, 0, st>>>(F[cur], L[cur], kmax, K, s, gamma, tau_blk, u, w);
+  pdl_launch(k_uw, dim3(grid), dim3(256), 0, st, (const double*)F[cur], (const double*)L[cur], (int64_t)kmax, K, s, gamma, tau_blk, u, w);
   count_launch();
   KRY_CUDA(cudaGetLastError());
   return KRY_OK;
