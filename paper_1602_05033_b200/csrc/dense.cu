@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(256) k_jac_round(double* __restrict__ A, int64
                                                    int NB, int round, double tol,
                                                    const double* __restrict__ floor2p,
                                                    int inner_sweeps, int* __restrict__ flag) {
+  pdl_sync();
   constexpr int PW = 2 * BW;          // panel width
   constexpr int GS = PW + 1;          // G row stride
   constexpr int RS = PW + 8;          // R row stride (== 8 mod 32 for PW = 32)
@@ -396,7 +397,7 @@ int jacobi_sweeps(cudaStream_t st, double* A, int64_t lda, int M, int N, double*
   for (; sweep < max_sweeps; ++sweep) {
     cudaMemsetAsync(flag, 0, sizeof(int), st);
     for (int r = 0; r < NB - 1; ++r)
-      k_jac_round<BW><<<NB / 2, 256, 0, st>>>(A, lda, M, N, V, ldv, NB, r, tol, floor2, inner, flag);
+      pdl_launch(k_jac_round<BW>, dim3(NB / 2), dim3(256), 0, st, A, lda, M, N, V, ldv, NB, r, tol, (const double*)floor2, inner, flag);
     count_launch(NB - 1);
     int h = 0;
     cudaError_t e = cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -457,6 +458,7 @@ __global__ void __launch_bounds__(256) k_dgemm(int M, int N, int K, const double
                                                double* __restrict__ C, int64_t ldc,
                                                const int* __restrict__ crow, int awide,
                                                int bwide, const int* __restrict__ dyn) {
+  pdl_sync();
   if (dyn) {   // device-side sizes: K = dyn[0], M = dyn[0] + 1 (bordered update)
     K = dyn[0];
     M = min(M, K + 1);
@@ -567,9 +569,9 @@ int dense_gemm(cudaStream_t st, int M, int N, int K, const double* A, int64_t ld
   const int bwide = ((ldb & 1) == 0 && ((uintptr_t)B & 15) == 0) ? 1 : 0;
   dim3 grid((N + GBN - 1) / GBN, (M + GBM - 1) / GBM);
   if (a_colmajor)
-    k_dgemm<true><<<grid, 256, smem, st>>>(M, N, K, A, lda, B, ldb, brow, C, ldc, crow, awide, bwide, dyn);
+    pdl_launch(k_dgemm<true>, grid, dim3(256), smem, st, M, N, K, A, lda, B, ldb, brow, C, ldc, crow, awide, bwide, dyn);
   else
-    k_dgemm<false><<<grid, 256, smem, st>>>(M, N, K, A, lda, B, ldb, brow, C, ldc, crow, awide, bwide, dyn);
+    pdl_launch(k_dgemm<false>, grid, dim3(256), smem, st, M, N, K, A, lda, B, ldb, brow, C, ldc, crow, awide, bwide, dyn);
   count_launch();
   KRY_CUDA(cudaGetLastError());
   return KRY_OK;

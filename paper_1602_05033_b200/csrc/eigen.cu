@@ -37,55 +37,6 @@ namespace kry {
 
 static constexpr double EPS = 2.220446049250313e-16;
 
-// Programmatic dependent launch: the kernels of an append form a chain of
-// short dependent launches on one stream (5 per scalar row, ~10^4 per c4
-// solve).  Each kernel lets its successor be scheduled at once
-// (launch_dependents) and waits for its predecessor's completion and memory
-// flush before touching any data (griddepcontrol.wait), so the launch
-// latency of kernel i+1 overlaps the execution of kernel i.  Both are no-ops
-// for a launch without the attribute (the finalisation's plain launches).
-__device__ __forceinline__ void pdl_sync() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-}
-static bool pdl_on() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("KRY_PDL");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-template <class... KArgs, class... Args>
-static void pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                       Args... args) {
-  if (!pdl_on()) {
-    kern<<<grid, block, smem, st>>>(args...);
-    return;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
-}
-#ifndef KRY_SECULAR_W8
-#define KRY_SECULAR_W8 0
-#endif
-// poles of the big appends (K > 2048) cached in registers: 1 = 256 threads x
-// 24 terms, 2 = 256 x 16 / 512 x 12 (both measured SLOWER on c5: 2.0 / 1.9 s
-// against 1.32 s -- one or two CTAs per SM cannot hide the reciprocal chains),
-// 0 = streamed from global memory / L1 with 16 small CTAs per SM
-#ifndef KRY_SECULAR_BIG
-#define KRY_SECULAR_BIG 0
-#endif
-
 // ------------------------------------------------------------------ block scan helpers
 __device__ __forceinline__ int warp_incl_scan(int v) {
   const int lane = threadIdx.x & 31;
@@ -1317,6 +1268,7 @@ __global__ void __launch_bounds__(1024) k_dc_deflate(EigView e, DcAppendArgs g,
                                                      const double* __restrict__ sub,
                                                      double* lam, const double* __restrict__ X,
                                                      int64_t ldx, int* giv_i, double* giv_c) {
+  pdl_sync();
   extern __shared__ double dyn_sm[];
   const int K = g.K, s = g.s;
   e.z = dyn_sm;
@@ -1482,6 +1434,7 @@ __global__ void __launch_bounds__(1024) k_dc_deflate(EigView e, DcAppendArgs g,
 __global__ void k_dc_givens(const int* __restrict__ counts, const int* __restrict__ giv_i,
                             const double* __restrict__ giv_c, double* X, int64_t ldx, int off,
                             int K) {
+  pdl_sync();
   const int ng = counts[2];
   if (ng == 0) return;
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1505,6 +1458,7 @@ __global__ void __launch_bounds__(128) k_dc_wbuild(EigView e, int off, int K, do
                                                    const double* __restrict__ lam_old_unused,
                                                    double* lam_new, const double* __restrict__ Xo,
                                                    double* Xn, int64_t ldx) {
+  pdl_sync();
   const int p = e.counts[0], nd = e.counts[1];
   const int tid = threadIdx.x;
   __shared__ double red[4];
@@ -1845,25 +1799,25 @@ int dc_band_eigh(cudaStream_t st, const double* dsym, const double* sub, int s, 
       }
       const size_t dsm = (size_t)K * (sizeof(double) + 3 * sizeof(int)) + 16;
       if (dsm > 200 * 1024) { cleanup(); return fail(KRY_ERR_DIMENSION, "projected matrix too large for the finalisation"); }
-      k_dc_deflate<<<1, 1024, dsm, st>>>(v, g, dsym, sub, lam[cur], X[cur], ldx, giv_i, giv_c);
-      if (K > 0) k_dc_givens<<<(K + 127) / 128, 128, 0, st>>>(v.counts, giv_i, giv_c, X[cur], ldx, nd.off, K);
+      pdl_launch(k_dc_deflate, dim3(1), dim3(1024), dsm, st, v, g, dsym, sub, lam[cur], (const double*)X[cur], ldx, giv_i, giv_c);
+      if (K > 0) pdl_launch(k_dc_givens, dim3((K + 127) / 128), dim3(128), 0, st, (const int*)v.counts, (const int*)giv_i, (const double*)giv_c, X[cur], ldx, nd.off, K);
       if (K >= 1024) {
-        if (K <= 128 * 16) k_eig_secular<4, 16><<<K + 1, 128, 0, st>>>(v);
-        else k_eig_secular<4, 0><<<K + 1, 128, 0, st>>>(v);
+        if (K <= 128 * 16) pdl_launch(k_eig_secular<4, 16>, dim3(K + 1), dim3(128), 0, st, v);
+        else pdl_launch(k_eig_secular<4, 0>, dim3(K + 1), dim3(128), 0, st, v);
       } else if (K >= 256) {
-        k_eig_secular<2, 16><<<K + 1, 64, 0, st>>>(v);
+        pdl_launch(k_eig_secular<2, 16>, dim3(K + 1), dim3(64), 0, st, v);
       } else if (K >= 64) {
-        k_eig_secular<1, 8><<<K + 1, 32, 0, st>>>(v);
+        pdl_launch(k_eig_secular<1, 8>, dim3(K + 1), dim3(32), 0, st, v);
       } else {
-        k_eig_secular<1, 2><<<K + 1, 32, 0, st>>>(v);
+        pdl_launch(k_eig_secular<1, 2>, dim3(K + 1), dim3(32), 0, st, v);
       }
       if (K > 0) {
-        if (K >= 1024) k_eig_zhat<4><<<K, 128, 0, st>>>(v);
-        else if (K >= 256) k_eig_zhat<2><<<K, 64, 0, st>>>(v);
-        else k_eig_zhat<1><<<K, 32, 0, st>>>(v);
+        if (K >= 1024) pdl_launch(k_eig_zhat<4>, dim3(K), dim3(128), 0, st, v);
+        else if (K >= 256) pdl_launch(k_eig_zhat<2>, dim3(K), dim3(64), 0, st, v);
+        else pdl_launch(k_eig_zhat<1>, dim3(K), dim3(32), 0, st, v);
       }
-      k_dc_wbuild<<<2 * K + 1, 128, 0, st>>>(v, nd.off, K, Wt, ldw, crow, brow, nullptr,
-                                             lam[1 - cur], X[cur], X[1 - cur], ldx);
+      pdl_launch(k_dc_wbuild, dim3(2 * K + 1), dim3(128), 0, st, v, nd.off, K, Wt, ldw, crow, brow,
+                 (const double*)nullptr, lam[1 - cur], (const double*)X[cur], X[1 - cur], ldx);
       count_launch(5);
       if (K > 0) {
         rc = dense_gemm(st, K + 1, K, K, Wt, ldw, 0, X[cur] + nd.off, ldx, brow,

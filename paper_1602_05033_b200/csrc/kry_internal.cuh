@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 #include "../../include/krymat_b200.h"
 
@@ -68,6 +69,57 @@ extern thread_local std::string g_last_error;
   } while (0)
 
 void count_launch(int k = 1);
+
+#ifdef __CUDACC__
+// Programmatic dependent launch: the kernels of an append form a chain of
+// short dependent launches on one stream (5 per scalar row, ~10^4 per c4
+// solve).  Each kernel lets its successor be scheduled at once
+// (launch_dependents) and waits for its predecessor's completion and memory
+// flush before touching any data (griddepcontrol.wait), so the launch
+// latency of kernel i+1 overlaps the execution of kernel i.  Both are no-ops
+// for a launch without the attribute (the finalisation's plain launches).
+__device__ __forceinline__ void pdl_sync() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+inline bool pdl_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("KRY_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+template <class... KArgs, class... Args>
+inline void pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  if (!pdl_on()) {
+    kern<<<grid, block, smem, st>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+#ifndef KRY_SECULAR_W8
+#define KRY_SECULAR_W8 0
+#endif
+// poles of the big appends (K > 2048) cached in registers: 1 = 256 threads x
+// 24 terms, 2 = 256 x 16 / 512 x 12 (both measured SLOWER on c5: 2.0 / 1.9 s
+// against 1.32 s -- one or two CTAs per SM cannot hide the reciprocal chains),
+// 0 = streamed from global memory / L1 with 16 small CTAs per SM
+#ifndef KRY_SECULAR_BIG
+#define KRY_SECULAR_BIG 0
+#endif
+#endif
 
 // ---------------------------------------------------------------- operator
 // division by an invariant 32-bit divisor: q = (umulhi(n, mul) + n) >> shift
