@@ -2113,6 +2113,7 @@ static int finalize_lyap_lowrank(kry_ctx* c, FinalBufs& b, int k, double eps, do
     return rc;
   }
   StageTimer tm(c->stream);
+  cudaMemsetAsync(L, 0, (size_t)k * ldl * sizeof(double), c->stream);
   int p = 0;
   if ((rc = dense_pchol_cauchy(c->stream, b.u, b.lam, k, c->s, L, ldl, pmax, &p))) {
     cleanup();

@@ -1263,6 +1263,7 @@ struct DcAppendArgs {
 // E1 of a separator row: z = X_old[:, coupled rows] t, deflation as in
 // k_eig_deflate, but the Givens rotations of numerically equal poles are
 // recorded (giv_i, giv_c) for k_dc_givens instead of being applied to F / L.
+template <bool SM>
 __global__ void __launch_bounds__(1024) k_dc_deflate(EigView e, DcAppendArgs g,
                                                      const double* __restrict__ dsym,
                                                      const double* __restrict__ sub,
@@ -1271,10 +1272,12 @@ __global__ void __launch_bounds__(1024) k_dc_deflate(EigView e, DcAppendArgs g,
   pdl_sync();
   extern __shared__ double dyn_sm[];
   const int K = g.K, s = g.s;
-  e.z = dyn_sm;
-  e.cand = reinterpret_cast<int*>(dyn_sm + K);
-  e.dflag = e.cand + K;
-  e.pflag = e.dflag + K;
+  if (SM) {   // per-pole work arrays in shared memory while they fit
+    e.z = dyn_sm;
+    e.cand = reinterpret_cast<int*>(dyn_sm + K);
+    e.dflag = e.cand + K;
+    e.pflag = e.dflag + K;
+  }
   __shared__ double t[3 * KRY_SMAX];
   __shared__ int tp[3 * KRY_SMAX];
   __shared__ int s_nc, s_ng;
@@ -1722,8 +1725,8 @@ int dc_band_eigh(cudaStream_t st, const double* dsym, const double* sub, int s, 
   int rc;
   if ((rc = dalloc(&X[0], (size_t)k * ldx)) || (rc = dalloc(&X[1], (size_t)k * ldx)) ||
       (rc = dalloc(&lam[0], nk)) || (rc = dalloc(&lam[1], nk)) ||
-      (rc = dalloc(&Wt, (size_t)(k + 1) * ldw)) || (rc = dalloc(&dws, 8 * nk + 64)) ||
-      (rc = dalloc(&giv_c, 2 * nk)) || (rc = dalloc(&iws, 4 * nk + 16)) ||
+      (rc = dalloc(&Wt, (size_t)(k + 1) * ldw)) || (rc = dalloc(&dws, 9 * nk + 64)) ||
+      (rc = dalloc(&giv_c, 2 * nk)) || (rc = dalloc(&iws, 7 * nk + 16)) ||
       (rc = dalloc(&giv_i, 2 * nk)) || (rc = dalloc(&pos_d, nk))) {
     cleanup();
     return rc;
@@ -1744,6 +1747,11 @@ int dc_band_eigh(cudaStream_t st, const double* dsym, const double* sub, int s, 
   }
   int* crow = iws + 2 * nk + 16;
   int* brow = crow + nk;
+  // global work arrays of the deflation for orders beyond the shared-memory limit
+  v.z = dws + 8 * nk + 32;
+  v.cand = brow + nk;
+  v.dflag = v.cand + nk;
+  v.pflag = v.dflag + nk;
   cudaMemcpyAsync(pos_d, pos.data(), (size_t)k * sizeof(int), cudaMemcpyHostToDevice, st);
   // leaves
   std::vector<DcLeaf> leaves;
@@ -1756,7 +1764,7 @@ int dc_band_eigh(cudaStream_t st, const double* dsym, const double* sub, int s, 
   int dev = 0;
   cudaGetDevice(&dev);
   if (!attr[dev & 63]) {
-    cudaFuncSetAttribute(k_dc_deflate, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_dc_deflate<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_dc_leaf<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_dc_leaf<96>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr[dev & 63] = true;
@@ -1798,8 +1806,10 @@ int dc_band_eigh(cudaStream_t st, const double* dsym, const double* sub, int s, 
         g.posr[c] = nd.nr > 0 ? pos[(nd.bm + 1) * s + c] - nd.off : 0;
       }
       const size_t dsm = (size_t)K * (sizeof(double) + 3 * sizeof(int)) + 16;
-      if (dsm > 200 * 1024) { cleanup(); return fail(KRY_ERR_DIMENSION, "projected matrix too large for the finalisation"); }
-      pdl_launch(k_dc_deflate, dim3(1), dim3(1024), dsm, st, v, g, dsym, sub, lam[cur], (const double*)X[cur], ldx, giv_i, giv_c);
+      if (dsm <= 200 * 1024 && !getenv("KRY_DC_NOSMEM"))   // (the variable forces the large-order path: tests)
+        pdl_launch(k_dc_deflate<true>, dim3(1), dim3(1024), dsm, st, v, g, dsym, sub, lam[cur], (const double*)X[cur], ldx, giv_i, giv_c);
+      else
+        pdl_launch(k_dc_deflate<false>, dim3(1), dim3(1024), 0, st, v, g, dsym, sub, lam[cur], (const double*)X[cur], ldx, giv_i, giv_c);
       if (K > 0) pdl_launch(k_dc_givens, dim3((K + 127) / 128), dim3(128), 0, st, (const int*)v.counts, (const int*)giv_i, (const double*)giv_c, X[cur], ldx, nd.off, K);
       if (K >= 1024) {
         if (K <= 128 * 16) pdl_launch(k_eig_secular<4, 16>, dim3(K + 1), dim3(128), 0, st, v);

@@ -191,3 +191,14 @@ def test_band_eigh_on_reference_projections(cfg):
     import os
     g = np.load(os.path.join(os.path.dirname(__file__), "golden", cfg + ".npz"))
     _check_band(g["t_diag"], g["t_off"], tol=5e-13)
+
+
+def test_band_eigh_large_order_deflation_path(monkeypatch):
+    # orders beyond ~10^4 keep the deflation's work arrays in global memory
+    monkeypatch.setenv("KRY_DC_NOSMEM", "1")
+    rng = np.random.default_rng(21)
+    s, m = 4, 120
+    diag = np.array([-(lambda d: d @ d.T)(rng.standard_normal((s, s))) - 10 * np.eye(s)
+                     for _ in range(m)])
+    sub = np.array([np.triu(rng.standard_normal((s, s))) for _ in range(m - 1)])
+    _check_band(diag, sub)
