@@ -27,6 +27,7 @@
 #include "kry_internal.cuh"
 #include "finalize.cuh"
 #include <algorithm>
+#include <cstdlib>
 
 namespace kry {
 
@@ -194,6 +195,180 @@ __global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__
   }
 }
 
+// Variant with the 8 warps stacked along M (warp = 8 rows x the whole panel,
+// up to 16 n-tiles of 8 columns, `ntp` of them used): the panel width is
+// then any multiple of 8, so the rank is padded to 8 npanels columns at most
+// instead of to a multiple of 128 (r = 231: 2 panels of 15 n-tiles = 240
+// columns against 256, 6 % fewer DMMAs).  One A fragment and ntp B fragments
+// per k4-step feed ntp DMMAs.
+constexpr int ZNTW = 16;
+template <int S>
+__global__ void __launch_bounds__(32 * ZWARPS) k_zacc8(const double* __restrict__ vbase,
+                                                       int64_t vstride, int nb,
+                                                       const double* __restrict__ Q, int ldq,
+                                                       int r, double* __restrict__ Z, int64_t n,
+                                                       int accumulate, int npanels, int ntp,
+                                                       int64_t ntiles) {
+  constexpr int KS = (S + 3) / 4;
+  constexpr int AST = zast<S>();
+  constexpr int KP = 4 * KS;
+  constexpr int BPS = zbps(S);
+  constexpr int ZBST = 8 * ZNTW + 8;   // == 8 mod 32: conflict-free B fragments
+  constexpr int ASZ = ZBM * AST, BSZ = KP * ZBST;
+  extern __shared__ __align__(16) double zsm[];
+  double* sA = zsm;
+  double* sB = zsm + ZST * BPS * ASZ;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int bnp = 8 * ntp;   // panel width
+  for (int e = tid; e < ZST * BPS * ASZ; e += blockDim.x) sA[e] = 0.0;
+  for (int e = tid; e < ZST * BPS * BSZ; e += blockDim.x) sB[e] = 0.0;
+  __syncthreads();
+  auto load_stage = [&](int64_t i0, int j0, int grp, int st) {
+#pragma unroll
+    for (int bb = 0; bb < BPS; ++bb) {
+      const int b = grp * BPS + bb;
+      const bool bok = b < nb;
+      double* dA = sA + ((int64_t)st * BPS + bb) * ASZ;
+      double* dB = sB + ((int64_t)st * BPS + bb) * BSZ;
+      const double* vb = vbase + (int64_t)(bok ? b : 0) * vstride + i0 * S;
+      if ((S & 1) == 0) {
+        constexpr int PR = (S / 2) > 0 ? S / 2 : 1;
+        for (int q = tid; q < ZBM * PR; q += blockDim.x) {
+          const int row = q / PR, pc = q % PR;
+          const bool ok = bok && i0 + row < n;
+          cp16(&dA[row * AST + 2 * pc], ok ? vb + (int64_t)row * S + 2 * pc : vbase, ok);
+        }
+      } else {
+        for (int q = tid; q < ZBM * S; q += blockDim.x) {
+          const int row = q / S, c = q % S;
+          const bool ok = bok && i0 + row < n;
+          cp8(&dA[row * AST + c], ok ? vb + (int64_t)row * S + c : vbase, ok);
+        }
+      }
+      const double* qb = Q + (int64_t)(bok ? b : 0) * S * ldq + j0;
+      const int pb = bnp / 2;   // 16-byte pieces per Q row
+      for (int q = tid; q < S * pb; q += blockDim.x) {
+        const int row = q / pb, pc = q % pb;
+        cp16(&dB[row * ZBST + 2 * pc], qb + (int64_t)row * ldq + 2 * pc, bok);
+      }
+    }
+  };
+  const int ng = (nb + BPS - 1) / BPS;
+  auto prologue = [&](int64_t tl) {
+    const int64_t i0 = (tl / npanels) * ZBM;
+    const int j0 = (int)(tl % npanels) * bnp;
+#pragma unroll
+    for (int st = 0; st < ZST - 1; ++st) {
+      if (st < ng) load_stage(i0, j0, st, st);
+      cp_commit();
+    }
+  };
+  int64_t tile = blockIdx.x;
+  if (tile < ntiles) prologue(tile);
+  while (tile < ntiles) {
+    const int64_t i0 = (tile / npanels) * ZBM;
+    const int j0 = (int)(tile % npanels) * bnp;
+    double acc[ZNTW][2];
+#pragma unroll
+    for (int b = 0; b < ZNTW; ++b) acc[b][0] = acc[b][1] = 0.0;
+    for (int gi = 0; gi < ng; ++gi) {
+      cp_wait<ZST - 2>();
+      __syncthreads();
+      {
+        const int gn = gi + ZST - 1;
+        if (gn < ng) load_stage(i0, j0, gn, gn % ZST);
+        cp_commit();
+      }
+#pragma unroll
+      for (int bb = 0; bb < BPS; ++bb) {
+        const double* A = sA + ((int64_t)(gi % ZST) * BPS + bb) * ASZ;
+        const double* B = sB + ((int64_t)(gi % ZST) * BPS + bb) * BSZ;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const double fa = A[(warp * 8 + g) * AST + 4 * ks + t];
+          const double* brow = B + (4 * ks + t) * ZBST + g;
+#pragma unroll
+          for (int nt = 0; nt < ZNTW; ++nt)
+            if (nt < ntp) zdmma(acc[nt][0], acc[nt][1], fa, brow[nt * 8]);
+        }
+      }
+    }
+    cp_wait<0>();
+    __syncthreads();
+    const int64_t next = tile + gridDim.x;
+    if (next < ntiles) prologue(next);
+    const int64_t i = i0 + warp * 8 + g;
+    if (i < n) {
+      double* zr = Z + i * r;
+#pragma unroll
+      for (int nt = 0; nt < ZNTW; ++nt) {
+        if (nt >= ntp) continue;
+        const int j = j0 + nt * 8 + 2 * t;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (j + e < r) {
+            const double v = acc[nt][e];
+            zr[j + e] = accumulate ? zr[j + e] + v : v;
+          }
+        }
+      }
+    }
+    tile = next;
+  }
+}
+
+// panels of the stacked-warp variant: the fewest panels of <= 16 n-tiles, then
+// the narrowest width that covers the rank
+static void zacc8_shape(int r, int* npanels, int* ntp) {
+  const int nt = (r + 7) / 8;
+  *npanels = (nt + ZNTW - 1) / ZNTW;
+  *ntp = (nt + *npanels - 1) / *npanels;
+}
+// KRY_ZACC8: 0 (default) 2 x 4 warps (32 x 8 NT tiles per warp), 1: 8 x 1
+// warps, -1: the stacked variant where it saves at least 4 % of the padded
+// columns.  Measured on c4 (r = 231): the stacked variant issues 6 % fewer
+// DMMAs but one B-fragment load per DMMA instead of one per two, and runs at
+// 16.0 TF/s against 17.2 (pass 2 0.521 s against 0.493 s) -- off.
+static int zacc_variant(int r) {
+  static int mode = -2;
+  if (mode == -2) {
+    const char* e = getenv("KRY_ZACC8");
+    mode = e ? atoi(e) : 0;
+  }
+  if (mode == 0 || mode == 1) return mode;
+  int np, ntp;
+  zacc8_shape(r, &np, &ntp);
+  const int cols8 = np * ntp * 8;
+  const int bn = 32 * (((r + 31) / 32) <= 2 ? 2 : 4);
+  const int cols4 = ((r + bn - 1) / bn) * bn;
+  return cols8 * 100 <= cols4 * 96 ? 1 : 0;
+}
+
+template <int S>
+static int zacc8_go(cudaStream_t st, const double* vbase, int64_t vstride, int nb, const double* Q,
+                    int ldq, int r, double* Z, int64_t n, int accumulate, int max_ctas) {
+  constexpr int KP = 4 * ((S + 3) / 4);
+  constexpr int BPS = zbps(S);
+  int npanels, ntp;
+  zacc8_shape(r, &npanels, &ntp);
+  const int64_t ntiles = ((n + ZBM - 1) / ZBM) * npanels;
+  int64_t grid = ntiles;
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  if (grid > 0x7fffffffLL) return fail(KRY_ERR_DIMENSION, "pass-2 factor too large");
+  const size_t smem = (size_t)ZST * BPS * (ZBM * zast<S>() + KP * (8 * ZNTW + 8)) * sizeof(double);
+  static bool attr[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr[dev & 63]) {
+    KRY_CUDA(cudaFuncSetAttribute(k_zacc8<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr[dev & 63] = true;
+  }
+  k_zacc8<S><<<(unsigned)grid, 32 * ZWARPS, smem, st>>>(vbase, vstride, nb, Q, ldq, r, Z, n,
+                                                         accumulate, npanels, ntp, ntiles);
+  return KRY_OK;
+}
+
 // panel width 32 NT: NT = 8 (one panel for r <= 256) measured slower on c4
 // (84 vs 65 ms per chunk: 1 CTA of 168 registers per SM, 12 % warps active),
 // so panels stop at 128 columns (2 CTAs per SM)
@@ -237,6 +412,8 @@ static int zacc_go(cudaStream_t st, const double* vbase, int64_t vstride, int nb
 template <int S>
 static int zacc_s(cudaStream_t st, const double* vbase, int64_t vstride, int nb, const double* Q,
                   int ldq, int r, double* Z, int64_t n, int accumulate, int max_ctas) {
+  if (zacc_variant(r) == 1)
+    return zacc8_go<S>(st, vbase, vstride, nb, Q, ldq, r, Z, n, accumulate, max_ctas);
   switch (zacc_nt(r)) {
     case 2: return zacc_go<S, 2>(st, vbase, vstride, nb, Q, ldq, r, Z, n, accumulate, max_ctas);
     default: return zacc_go<S, 4>(st, vbase, vstride, nb, Q, ldq, r, Z, n, accumulate, max_ctas);
@@ -293,7 +470,9 @@ int launch_chunk_coef_ld(cudaStream_t st, const double* S, const double* qy, int
 
 int zacc_ldq(int r) {
   const int bn = 32 * zacc_nt(r);
-  return ((r + bn - 1) / bn) * bn;
+  int np, ntp;
+  zacc8_shape(r, &np, &ntp);
+  return std::max(((r + bn - 1) / bn) * bn, np * ntp * 8);
 }
 
 }  // namespace kry
