@@ -143,6 +143,10 @@ __global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    // n-tiles of this warp that hold real columns (the last panel pads the
+    // rank to a multiple of 32 NT: r = 231 -> 25 of its 128 columns are
+    // padding; their DMMAs and B fragments are skipped, warp-uniformly)
+    const int ntl = min(NT, max(0, (r - (j0 + wn * 8 * NT) + 7) / 8));
     for (int gi = 0; gi < ng; ++gi) {
       cp_wait<ZST - 2>();
       __syncthreads();
@@ -161,11 +165,15 @@ __global__ void __launch_bounds__(32 * ZWARPS) k_zacc(const double* __restrict__
 #pragma unroll
           for (int mt = 0; mt < 4; ++mt) fa[mt] = A[(wm * 32 + mt * 8 + g) * AST + 4 * ks + t];
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) fb[nt] = B[(4 * ks + t) * ZBST + wn * 8 * NT + nt * 8 + g];
+          for (int nt = 0; nt < NT; ++nt)
+            if (nt < ntl) fb[nt] = B[(4 * ks + t) * ZBST + wn * 8 * NT + nt * 8 + g];
 #pragma unroll
-          for (int mt = 0; mt < 4; ++mt)
+          for (int nt = 0; nt < NT; ++nt) {
+            if (nt < ntl) {
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) zdmma(acc[mt][nt][0], acc[mt][nt][1], fa[mt], fb[nt]);
+              for (int mt = 0; mt < 4; ++mt) zdmma(acc[mt][nt][0], acc[mt][nt][1], fa[mt], fb[nt]);
+            }
+          }
         }
       }
     }
