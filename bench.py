@@ -185,6 +185,35 @@ def timed_solve_device(kb, lib, ctx, c_dev_ptr, opts, s, prof=True):
                 basis_its=int(hist[nh.value - 1, 0]) if nh.value else 0)
 
 
+def combine_alone(lib, ctx, c_dev_ptr, opts, s, its):
+    """Average k_combine launch time with the eigen stream idle: one extra,
+    untimed pass 1 of ``its`` iterations that queues the recurrence only
+    (KRY_DEBUG_NO_EIG).  In the timed region the eigen appends of the second
+    stream run beside the recurrence and take SM time from it, so the in-situ
+    launch time is longer than the kernel's own."""
+    from paper_1602_05033_b200 import _lib
+
+    gamma = np.zeros((s, s))
+    beta2 = ctypes.c_double()
+    os.environ["KRY_DEBUG_NO_EIG"] = "1"
+    try:
+        lib.kry_profile_enable(ctx.ptr, 0)
+        lib.kry_profile_enable(ctx.ptr, 1)
+        _lib.check(lib.kry_init_basis_device(ctx.ptr, ctypes.c_void_p(c_dev_ptr),
+                                             _lib.as_dptr(gamma), ctypes.byref(beta2)))
+        hist = np.zeros((its + 1, 5))
+        nh, it, reason = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        rel = ctypes.c_double()
+        lib.kry_solve_lyap_pass1(ctx.ptr, 0.0, its, 1, _lib.as_dptr(hist), ctypes.byref(nh),
+                                 ctypes.byref(it), ctypes.byref(rel), ctypes.byref(reason))
+        ms, n = ctypes.c_double(), ctypes.c_int()
+        lib.kry_profile_read(ctx.ptr, ctypes.byref(ms), ctypes.byref(n), None, None)
+        return ms.value / max(n.value, 1), n.value
+    finally:
+        os.environ.pop("KRY_DEBUG_NO_EIG", None)
+        lib.kry_profile_enable(ctx.ptr, 0)
+
+
 def cpu_model():
     try:
         out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
@@ -399,6 +428,13 @@ def main():
     chk_ok = lib.kry_profile_check(ctx.ptr, 20, ctypes.byref(chk_ms), ctypes.byref(chk_k)) == 0
     dfma, dmma = ctypes.c_double(), ctypes.c_double()
     lib.kry_fp64_peak(local, ctypes.byref(dfma), ctypes.byref(dmma))
+    alone_ms, alone_n = (0.0, 0)
+    if world == 1:
+        try:
+            alone_ms, alone_n = combine_alone(lib, ctx, c_dev.data_ptr(), opts, s,
+                                              min(runs[-1]["iterations"], opts.max_m))
+        except Exception:   # measurement only
+            alone_ms, alone_n = (0.0, 0)
     ms_total = sum(r["ms"] for r in runs)
     its_total = sum(r["iterations"] for r in runs)
     if dist:
@@ -430,6 +466,14 @@ def main():
                 "bytes_per_launch": bytes_launch, "avg_launch_ms": comb_avg_ms,
                 "achieved": comb_gbs, "unit": "GB/s", "frac": comb_gbs / hbm if hbm else None,
                 "traffic": captured_traffic(args.config), "launches": comb_n.value}]
+    if alone_ms > 0:
+        agbs = bytes_launch / (alone_ms / 1000.0) / 1e9
+        kernels[0]["alone"] = {
+            "avg_launch_ms": alone_ms, "achieved": agbs, "frac": agbs / hbm if hbm else None,
+            "frac_survey_bytes": (b_iter / (alone_ms / 1000.0) / 1e9) / hbm if hbm else None,
+            "launches": alone_n,
+            "note": "same kernel with the eigen stream idle (untimed extra pass 1): in the timed "
+                    "region the eigen appends run beside the recurrence and take SM time from it"}
     fp64_peak = dmma.value if dmma.value > 0 else None
     if zacc_n.value:
         tf = zacc_fl.value / (zacc_ms.value / 1000.0) / 1e12

@@ -1112,6 +1112,10 @@ int EigEngine::append_block(cudaStream_t st, const double* dsym_blk, const doubl
   if (K + s > kmax - 8) return fail(KRY_ERR_STATE, "eigen engine capacity exceeded");
   for (int a = 0; a < s; ++a) {
     EigView v = view();
+    // programmatic dependent launch pays where the kernels are launch-bound
+    // (K < 1024: c1-c3); for the large appends it gains nothing and the
+    // tighter packing only takes SM time from the recurrence kernels
+    PdlScope pdl_scope(K < 1024);
     const size_t dsm = (size_t)K * (sizeof(double) + 3 * sizeof(int));
     if (dsm <= 200 * 1024) {
       if (!deflate_attr) {

@@ -82,13 +82,22 @@ __device__ __forceinline__ void pdl_sync() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
+inline bool& pdl_scope_flag() {
+  static thread_local bool on = true;
+  return on;
+}
+struct PdlScope {   // restricts pdl_launch to plain launches inside a scope
+  bool prev;
+  explicit PdlScope(bool on) : prev(pdl_scope_flag()) { pdl_scope_flag() = on; }
+  ~PdlScope() { pdl_scope_flag() = prev; }
+};
 inline bool pdl_on() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("KRY_PDL");
     v = (e && e[0] == '0') ? 0 : 1;
   }
-  return v == 1;
+  return v == 1 && pdl_scope_flag();
 }
 template <class... KArgs, class... Args>
 inline void pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
