@@ -51,6 +51,105 @@ __host__ __device__ __forceinline__ void tournament_pair(int n, int r, int p, in
   }
 }
 
+// rotation test of a pair with diagonal entries gi, gj and |off-diagonal| o.
+// Gram matrix of columns (SYM = false): relative test, columns below the
+// noise floor (floor2 = squared norm) left alone.  Symmetric matrix itself
+// (SYM = true, two-sided method): relative test on |gi gj| plus an absolute
+// floor (floor2 = |entry|) far below eps ||A||.
+template <bool SYM>
+__device__ __forceinline__ bool jac_rotates(double gi, double gj, double o, double tol,
+                                            double floor2) {
+  if (SYM) return o > floor2 && o * o > tol * tol * fabs(gi * gj);
+  return fmin(gi, gj) > floor2 && o * o > tol * tol * gi * gj;
+}
+
+// Parallel cyclic two-sided Jacobi sweeps on the 2 BW x 2 BW matrix sG (all
+// 256 threads of the CTA), rotations accumulated in sR (initialised to I on
+// the first rotation).  Returns false when nothing had to rotate.
+template <int BW, bool SYM>
+__device__ bool jac_inner(double* sG, double* sR, double* s_c, double* s_s, double tol,
+                          double floor2, int inner_sweeps) {
+  constexpr int PW = 2 * BW, GS = PW + 1, RS = PW + 8, NPAIR = PW / 2;
+  const int tid = threadIdx.x;
+  bool first = true;
+  for (int isw = 0; isw < inner_sweeps; ++isw) {
+    int need = 0;   // bit 0: a cross pair, bit 1: a pair inside a block
+    for (int e = tid; e < PW * PW; e += 256) {
+      const int i = e / PW, j = e % PW;
+      if (i < j) {
+        const double gi = sG[i * GS + i], gj = sG[j * GS + j];
+        const double o = fabs(sG[i * GS + j]);
+        if (jac_rotates<SYM>(gi, gj, o, tol, floor2)) need |= ((i < BW) == (j < BW)) ? 2 : 1;
+      }
+    }
+    {   // (__syncthreads_or returns a truth value, not the bitwise OR)
+      const int in_block = __syncthreads_or(need & 2), cross = __syncthreads_or(need & 1);
+      need = (in_block ? 2 : 0) | (cross ? 1 : 0);
+    }
+    if (!need) break;
+    if (first) {
+      first = false;
+      for (int e = tid; e < PW * RS; e += 256) sR[e] = 0.0;
+      __syncthreads();
+      if (tid < PW) sR[tid * RS + tid] = 1.0;
+      __syncthreads();
+    }
+    const bool bip = !(need & 2);
+    const int nrounds = bip ? BW : PW - 1;
+    for (int rr = 0; rr < nrounds; ++rr) {
+      // pair j = (pj, qj); this thread also owns the 2 x 2 block of G at
+      // rows (pair tid / 16) x columns (pair tid % 16)
+      auto pair_of = [&](int j, int* p, int* q) {
+        if (bip) { *p = j; *q = BW + ((j + rr) % BW); }
+        else tournament_pair(PW, rr, j, p, q);
+      };
+      int pc, qc, pr, qr;
+      pair_of(tid % NPAIR, &pc, &qc);
+      pair_of(tid / NPAIR, &pr, &qr);
+      if (tid < NPAIR) {
+        const double gpp = sG[pc * GS + pc], gqq = sG[qc * GS + qc], gpq = sG[pc * GS + qc];
+        double c = 1.0, s = 0.0;
+        if (jac_rotates<SYM>(gpp, gqq, fabs(gpq), tol, floor2)) {
+          // t^2 + 2 tau t - 1 = 0, tau = (gqq - gpp) / (2 gpq): the smaller root
+          const double d = gqq - gpp, b2 = 2.0 * gpq;
+          const double tt = (d >= 0.0 ? b2 : -b2) / (fabs(d) + sqrt(fma(d, d, b2 * b2)));
+          c = rsqrt(fma(tt, tt, 1.0));
+          s = tt * c;
+        }
+        s_c[tid] = c;
+        s_s[tid] = s;
+      }
+      __syncthreads();
+      {   // G <- J^T G J on this thread's 2 x 2 block
+        const double cc = s_c[tid % NPAIR], sc = s_s[tid % NPAIR];
+        const double cr = s_c[tid / NPAIR], sr = s_s[tid / NPAIR];
+        if (sc != 0.0 || sr != 0.0) {
+          const double a = sG[pr * GS + pc], b = sG[pr * GS + qc];
+          const double c = sG[qr * GS + pc], d = sG[qr * GS + qc];
+          const double a1 = cc * a - sc * b, b1 = sc * a + cc * b;
+          const double c1 = cc * c - sc * d, d1 = sc * c + cc * d;
+          sG[pr * GS + pc] = cr * a1 - sr * c1;
+          sG[qr * GS + pc] = sr * a1 + cr * c1;
+          sG[pr * GS + qc] = cr * b1 - sr * d1;
+          sG[qr * GS + qc] = sr * b1 + cr * d1;
+        }
+        // R <- R J  (item = (row, pair tid % 16))
+        if (sc != 0.0) {
+#pragma unroll
+          for (int h = 0; h < PW * NPAIR / 256; ++h) {
+            const int r = (tid + 256 * h) / NPAIR;
+            const double u = sR[r * RS + pc], v = sR[r * RS + qc];
+            sR[r * RS + pc] = cc * u - sc * v;
+            sR[r * RS + qc] = sc * u + cc * v;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  return !first;
+}
+
 // One round of the block tournament: CTA = one pair of column blocks.
 template <int BW>
 __global__ void __launch_bounds__(256) k_jac_round(double* __restrict__ A, int64_t lda, int M,
@@ -135,84 +234,8 @@ __global__ void __launch_bounds__(256) k_jac_round(double* __restrict__ A, int64
   // whole block scans G: nothing to rotate -> done; only cross pairs (one
   // column from each block, the usual case after the first outer sweeps) ->
   // the 16 rounds of the bipartite schedule instead of the full 31.
-  bool first = true;
-  for (int isw = 0; isw < inner_sweeps; ++isw) {
-    int need = 0;   // bit 0: a cross pair, bit 1: a pair inside a block
-    for (int e = tid; e < PW * PW; e += 256) {
-      const int i = e / PW, j = e % PW;
-      if (i < j) {
-        const double gi = sG[i * GS + i], gj = sG[j * GS + j];
-        const double o = fabs(sG[i * GS + j]);
-        if (fmin(gi, gj) > floor2 && o * o > tol * tol * gi * gj) need |= ((i < BW) == (j < BW)) ? 2 : 1;
-      }
-    }
-    {   // (__syncthreads_or returns a truth value, not the bitwise OR)
-      const int in_block = __syncthreads_or(need & 2), cross = __syncthreads_or(need & 1);
-      need = (in_block ? 2 : 0) | (cross ? 1 : 0);
-    }
-    if (!need) break;
-    if (first) {
-      first = false;
-      if (tid == 0) *flag = 1;
-      for (int e = tid; e < PW * RS; e += 256) sR[e] = 0.0;
-      __syncthreads();
-      if (tid < PW) sR[tid * RS + tid] = 1.0;
-      __syncthreads();
-    }
-    const bool bip = !(need & 2);
-    const int nrounds = bip ? BW : PW - 1;
-    for (int rr = 0; rr < nrounds; ++rr) {
-      // pair j = (pj, qj); this thread also owns the 2 x 2 block of G at
-      // rows (pair tid / 16) x columns (pair tid % 16)
-      auto pair_of = [&](int j, int* p, int* q) {
-        if (bip) { *p = j; *q = BW + ((j + rr) % BW); }
-        else tournament_pair(PW, rr, j, p, q);
-      };
-      int pc, qc, pr, qr;
-      pair_of(tid % NPAIR, &pc, &qc);
-      pair_of(tid / NPAIR, &pr, &qr);
-      if (tid < NPAIR) {
-        const double gpp = sG[pc * GS + pc], gqq = sG[qc * GS + qc], gpq = sG[pc * GS + qc];
-        double c = 1.0, s = 0.0;
-        if (fmin(gpp, gqq) > floor2 && gpq * gpq > tol * tol * gpp * gqq) {
-          // t^2 + 2 tau t - 1 = 0, tau = (gqq - gpp) / (2 gpq): the smaller root
-          const double d = gqq - gpp, b2 = 2.0 * gpq;
-          const double tt = (d >= 0.0 ? b2 : -b2) / (fabs(d) + sqrt(fma(d, d, b2 * b2)));
-          c = rsqrt(fma(tt, tt, 1.0));
-          s = tt * c;
-        }
-        s_c[tid] = c;
-        s_s[tid] = s;
-      }
-      __syncthreads();
-      {   // G <- J^T G J on this thread's 2 x 2 block
-        const double cc = s_c[tid % NPAIR], sc = s_s[tid % NPAIR];
-        const double cr = s_c[tid / NPAIR], sr = s_s[tid / NPAIR];
-        if (sc != 0.0 || sr != 0.0) {
-          const double a = sG[pr * GS + pc], b = sG[pr * GS + qc];
-          const double c = sG[qr * GS + pc], d = sG[qr * GS + qc];
-          const double a1 = cc * a - sc * b, b1 = sc * a + cc * b;
-          const double c1 = cc * c - sc * d, d1 = sc * c + cc * d;
-          sG[pr * GS + pc] = cr * a1 - sr * c1;
-          sG[qr * GS + pc] = sr * a1 + cr * c1;
-          sG[pr * GS + qc] = cr * b1 - sr * d1;
-          sG[qr * GS + qc] = sr * b1 + cr * d1;
-        }
-        // R <- R J  (item = (row, pair tid % 16))
-        if (sc != 0.0) {
-#pragma unroll
-          for (int h = 0; h < PW * NPAIR / 256; ++h) {
-            const int r = (tid + 256 * h) / NPAIR;
-            const double u = sR[r * RS + pc], v = sR[r * RS + qc];
-            sR[r * RS + pc] = cc * u - sc * v;
-            sR[r * RS + qc] = sc * u + cc * v;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  if (first) return;   // the panel is orthogonal already
+  if (!jac_inner<BW, false>(sG, sR, s_c, s_s, tol, floor2, inner_sweeps)) return;   // orthogonal already
+  if (tid == 0) *flag = 1;
   // ---- phase 3: P <- P R for the panels of A and of V
   for (int which = 0; which < 2; ++which) {
     double* X = which == 0 ? A : V;
@@ -272,6 +295,148 @@ __global__ void k_colnorm2_max(const double* A, int64_t lda, int M, int N, doubl
   if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(out), (unsigned long long)__double_as_longlong(acc));
 }
 __global__ void k_floor2(double* v, double f) { v[0] *= f; }
+
+// ---- two-sided block Jacobi for a symmetric matrix (dense_syev): the
+// rotations diagonalise A itself, A <- R^T A R.  One-sided Jacobi on A works
+// on A^T A = A^2 and needs ~2x the sweeps on the graded, numerically rank-
+// deficient matrices of the finalisation (L^T L of the pivoted Cholesky
+// factor: 23 sweeps against 8).  A round = disjoint block pairs:
+//   k_jac2_pivot   32 x 32 pivot block of every pair -> R (shared-memory Jacobi)
+//   k_jac2_cols    A[:, IJ] <- A[:, IJ] R, V[:, IJ] <- V[:, IJ] R   (Y = A Rtot)
+//   k_jac2_transp  Y^T
+//   k_jac2_cols    Y^T[:, IJ] <- Y^T[:, IJ] R = (Rtot^T A Rtot)[:, IJ]
+template <int BW>
+__global__ void __launch_bounds__(256) k_jac2_pivot(const double* __restrict__ A, int64_t lda,
+                                                    int N, int NB, int round, double tol,
+                                                    const double* __restrict__ floorp, int inner,
+                                                    double* __restrict__ Rbuf,
+                                                    int* __restrict__ active,
+                                                    int* __restrict__ flag) {
+  pdl_sync();
+  constexpr int PW = 2 * BW, GS = PW + 1, RS = PW + 8, NPAIR = PW / 2;
+  __shared__ double sG[PW * GS];
+  __shared__ double sR[PW * RS];
+  __shared__ double s_c[NPAIR], s_s[NPAIR];
+  const int tid = threadIdx.x;
+  int bi, bj;
+  tournament_pair(NB, round, blockIdx.x, &bi, &bj);
+  if (bi > bj) { const int x = bi; bi = bj; bj = x; }
+  if ((int64_t)bi * BW >= N) {
+    if (tid == 0) active[blockIdx.x] = 0;
+    return;
+  }
+  auto gcol = [&](int c) -> int { return (c < BW) ? bi * BW + c : bj * BW + (c - BW); };
+  for (int e = tid; e < PW * PW; e += 256) {
+    const int i = e / PW, j = e % PW;
+    const int gi = gcol(i), gj = gcol(j);
+    double v = 0.0;
+    if (gi < N && gj < N)
+      v = 0.5 * (A[(int64_t)gj * lda + gi] + A[(int64_t)gi * lda + gj]);
+    sG[i * GS + j] = v;
+  }
+  __syncthreads();
+  const bool rot = jac_inner<BW, true>(sG, sR, s_c, s_s, tol, *floorp, inner);
+  if (tid == 0) {
+    active[blockIdx.x] = rot ? 1 : 0;
+    if (rot) *flag = 1;
+  }
+  if (!rot) return;
+  double* R = Rbuf + (int64_t)blockIdx.x * PW * PW;
+  for (int e = tid; e < PW * PW; e += 256) R[e] = sR[(e / PW) * RS + (e % PW)];
+}
+
+// X[:, IJ] <- X[:, IJ] R for every active pair (blockIdx.y selects X0 / X1)
+template <int BW>
+__global__ void __launch_bounds__(256) k_jac2_cols(double* __restrict__ X0, int64_t ld0, int rows0,
+                                                   double* __restrict__ X1, int64_t ld1, int rows1,
+                                                   int N, int NB, int round,
+                                                   const double* __restrict__ Rbuf,
+                                                   const int* __restrict__ active) {
+  pdl_sync();
+  constexpr int PW = 2 * BW, RS = PW + 8, PER = PW * JCH / 256;
+  __shared__ double sP[PW * JPS];
+  __shared__ double sR[PW * RS];
+  if (!active[blockIdx.x]) return;
+  double* X = blockIdx.y == 0 ? X0 : X1;
+  if (!X) return;
+  const int64_t ldx = blockIdx.y == 0 ? ld0 : ld1;
+  const int rows = blockIdx.y == 0 ? rows0 : rows1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  int bi, bj;
+  tournament_pair(NB, round, blockIdx.x, &bi, &bj);
+  if (bi > bj) { const int x = bi; bi = bj; bj = x; }
+  auto gcol = [&](int c) -> int { return (c < BW) ? bi * BW + c : bj * BW + (c - BW); };
+  const double* R = Rbuf + (int64_t)blockIdx.x * PW * PW;
+  for (int e = tid; e < PW * PW; e += 256) sR[(e / PW) * RS + (e % PW)] = R[e];
+  const int er = tid & (JCH - 1), ec0 = tid >> 6;
+  double pre[PER];
+  auto gload = [&](int row0) {
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int gc = gcol(ec0 + 4 * q), r = row0 + er;
+      pre[q] = (gc < N && r < rows) ? X[(int64_t)gc * ldx + r] : 0.0;
+    }
+  };
+  const int nch = (rows + JCH - 1) / JCH;
+  gload(0);
+  for (int ch = 0; ch < nch; ++ch) {
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < PER; ++q) sP[(ec0 + 4 * q) * JPS + er] = pre[q];
+    __syncthreads();
+    if (ch + 1 < nch) gload((ch + 1) * JCH);
+    double acc[PW / 8][2];
+#pragma unroll
+    for (int nt = 0; nt < PW / 8; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+    const int r0 = warp * 8;
+#pragma unroll
+    for (int ks = 0; ks < PW / 4; ++ks) {
+      const double a = sP[(ks * 4 + t) * JPS + r0 + g];
+#pragma unroll
+      for (int nt = 0; nt < PW / 8; ++nt) jdmma(acc[nt][0], acc[nt][1], a, sR[(ks * 4 + t) * RS + nt * 8 + g]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int nt = 0; nt < PW / 8; ++nt) {
+      sP[(nt * 8 + 2 * t) * JPS + r0 + g] = acc[nt][0];
+      sP[(nt * 8 + 2 * t + 1) * JPS + r0 + g] = acc[nt][1];
+    }
+    __syncthreads();
+    const int row0 = ch * JCH;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int c = ec0 + 4 * q, gc = gcol(c), r = row0 + er;
+      if (gc < N && r < rows) X[(int64_t)gc * ldx + r] = sP[c * JPS + er];
+    }
+  }
+}
+
+__global__ void k_jac2_transp(const double* __restrict__ A, int64_t lda, int n,
+                              double* __restrict__ At, int64_t ldt) {
+  pdl_sync();
+  __shared__ double tile[32][33];
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int r = bx + threadIdx.x, c = by + j;
+    tile[j][threadIdx.x] = (r < n && c < n) ? A[(int64_t)c * lda + r] : 0.0;
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    const int r = by + threadIdx.x, c = bx + j;
+    if (r < n && c < n) At[(int64_t)c * ldt + r] = tile[threadIdx.x][j];
+  }
+}
+
+// out[0] = max_i |a_ii|
+__global__ void k_diag_absmax(const double* A, int64_t lda, int n, double* out) {
+  double m = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, fabs(A[(int64_t)i * lda + i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(out), (unsigned long long)__double_as_longlong(m));
+}
 
 __global__ void k_set_identity(double* V, int64_t ldv, int n) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)n * n;
@@ -409,6 +574,66 @@ int jacobi_sweeps(cudaStream_t st, double* A, int64_t lda, int M, int N, double*
     if (!h) break;
   }
   dfree(flag);
+  if (rc != KRY_OK) return rc;
+  if (sweep >= max_sweeps)
+    return fail(KRY_ERR_FACTORIZATION, "dense Jacobi iteration did not converge");
+  if (sweeps_out) *sweeps_out = sweep + 1;
+  return KRY_OK;
+}
+
+
+// two-sided sweeps on the symmetric A (N x N, lda), V accumulated; At = N x N scratch.
+// On return *final = the buffer (A or At) holding the rotated matrix.
+int jacobi2_sweeps(cudaStream_t st, double* A, int64_t lda, int N, double* V, int64_t ldv,
+                   double* At, int* sweeps_out) {
+  constexpr int BW = 16, PW = 32;
+  int NB = (N + BW - 1) / BW;
+  if (NB < 2) NB = 2;
+  if (NB & 1) ++NB;
+  const double tol = 4.0 * DEPS;
+  int* flag = nullptr;
+  double* Rbuf = nullptr;
+  int rc;
+  if ((rc = dalloc(&flag, 64 + NB)) || (rc = dalloc(&Rbuf, (size_t)(NB / 2) * PW * PW))) {
+    dfree(flag); dfree(Rbuf);
+    return rc;
+  }
+  int* active = flag + 16;
+  double* floorp = reinterpret_cast<double*>(flag + 2);
+  cudaMemsetAsync(flag, 0, (64 + NB) * sizeof(int), st);
+  k_diag_absmax<<<1, 256, 0, st>>>(A, lda, N, floorp);
+  k_floor2<<<1, 1, 0, st>>>(floorp, 1e-3 * DEPS);   // absolute floor: 1e-3 eps max |a_ii|
+  count_launch(2);
+  int inner = 1;
+  if (const char* e = getenv("KRY_JACOBI_INNER")) inner = std::max(1, atoi(e));
+  const int max_sweeps = 60;
+  int sweep = 0;
+  double* cur = A;
+  double* oth = At;
+  dim3 tg((N + 31) / 32, (N + 31) / 32), tb(32, 8);
+  for (; sweep < max_sweeps; ++sweep) {
+    cudaMemsetAsync(flag, 0, sizeof(int), st);
+    for (int r = 0; r < NB - 1; ++r) {
+      pdl_launch(k_jac2_pivot<BW>, dim3(NB / 2), dim3(256), 0, st, (const double*)cur, lda, N, NB, r,
+                 tol, (const double*)floorp, inner, Rbuf, active, flag);
+      pdl_launch(k_jac2_cols<BW>, dim3(NB / 2, 2), dim3(256), 0, st, cur, lda, N, V, ldv, N, N, NB, r,
+                 (const double*)Rbuf, (const int*)active);
+      pdl_launch(k_jac2_transp, tg, tb, 0, st, (const double*)cur, lda, N, oth, lda);
+      pdl_launch(k_jac2_cols<BW>, dim3(NB / 2, 1), dim3(256), 0, st, oth, lda, N, (double*)nullptr,
+                 (int64_t)0, 0, N, NB, r, (const double*)Rbuf, (const int*)active);
+      std::swap(cur, oth);
+    }
+    count_launch(4 * (NB - 1));
+    int h = 0;
+    cudaError_t e = cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      rc = fail(KRY_ERR_CUDA, std::string("Jacobi sweep failed: ") + cudaGetErrorString(e));
+      break;
+    }
+    if (!h) break;
+  }
+  dfree(flag); dfree(Rbuf);
   if (rc != KRY_OK) return rc;
   if (sweep >= max_sweeps)
     return fail(KRY_ERR_FACTORIZATION, "dense Jacobi iteration did not converge");
@@ -1012,10 +1237,21 @@ int dense_syev(cudaStream_t st, double* A, int k, double* w, int* sweeps, bool s
   cudaMemcpyAsync(A0, A, (size_t)k * k * sizeof(double), cudaMemcpyDeviceToDevice, st);
   cudaMemsetAsync(gb, 0, 4 * sizeof(double), st);
   k_gershgorin<<<(k * 32 + 255) / 256, 256, 0, st>>>(A, k, gb);
-  if (!semidefinite) k_apply_shift<<<std::min(148, (k + 255) / 256), 256, 0, st>>>(A, k, gb, gb + 2);
+  const bool two_sided = getenv("KRY_SYEV_ONESIDED") == nullptr;
+  if (!semidefinite && !two_sided)
+    k_apply_shift<<<std::min(148, (k + 255) / 256), 256, 0, st>>>(A, k, gb, gb + 2);
   k_set_identity<<<grid1((int64_t)k * k), 256, 0, st>>>(V, k, k);
   count_launch(3);
-  rc = jacobi_sweeps(st, A, k, k, k, V, k, sweeps);
+  if (two_sided) {
+    // (A0 is still intact: the rotated matrix may end in A or in the scratch;
+    // only V is used below)
+    double* At = nullptr;
+    rc = dalloc(&At, (size_t)k * k);
+    if (rc == KRY_OK) rc = jacobi2_sweeps(st, A, k, k, V, k, At, sweeps);
+    dfree(At);
+  } else {
+    rc = jacobi_sweeps(st, A, k, k, k, V, k, sweeps);
+  }
   // Rayleigh quotients with the ORIGINAL matrix: the rotated columns carry
   // the rounding of every sweep (~ sqrt(#rotations) eps ||A||), A0 v_i does
   // not.  Column i of (A0 V) = row i of V^T A0 (A0 symmetric).
