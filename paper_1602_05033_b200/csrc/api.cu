@@ -2249,8 +2249,21 @@ int kry_finalize_sylv(kry_ctx* a, kry_ctx* bb, double eps, int* rank, double* di
   KRY_CUDA(cudaStreamSynchronize(bb->stream));
   FinalBufs fa, fb;
   int kA = 0, kB = 0;
+  // the two eigendecompositions are independent: the B side runs on its own
+  // stream from a second host thread
+  int rcB = KRY_OK;
+  std::string errB;
+  std::thread tb([&]() {
+    cudaSetDevice(bb->dev);
+    rcB = final_eig(bb, fb, &kB);
+    if (rcB != KRY_OK) errB = g_last_error;
+  });
   int rc = final_eig(a, fa, &kA);
-  if (rc == KRY_OK) rc = final_eig(bb, fb, &kB);
+  tb.join();
+  if (rc == KRY_OK && rcB != KRY_OK) {
+    g_last_error = errB;
+    rc = rcB;
+  }
   KRY_CUDA(cudaStreamSynchronize(bb->stream));
   double *Y = nullptr, *sig = nullptr, *U = nullptr, *VT = nullptr, *mind = nullptr,
          *work = nullptr, *outd = nullptr, *f1 = nullptr, *f2 = nullptr, *gw = nullptr;
