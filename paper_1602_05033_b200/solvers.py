@@ -17,6 +17,7 @@ mode (``basis.py:63-71``).
 """
 
 import ctypes
+from concurrent.futures import ThreadPoolExecutor
 import time
 from dataclasses import dataclass, field
 
@@ -289,8 +290,13 @@ def solve_sylvester_two_sided(op_a, op_b, c1, c2, options=None):
         rank, disc = ctypes.c_int(0), ctypes.c_double(0.0)
         _lib.check(lib.kry_finalize_sylv(pa.ctx.ptr, pb.ctx.ptr, float(opts.trunc_eps),
                                          ctypes.byref(rank), ctypes.byref(disc)))
-        z1 = pa.recover(rank.value)
-        z2 = pb.recover(rank.value)
+        # the two second passes are independent (own contexts and streams):
+        # two host threads (the C-ABI calls release the GIL), so the latency-
+        # bound steps of the two sides interleave on the GPU
+        with ThreadPoolExecutor(max_workers=2) as pool:
+            f2 = pool.submit(pb.recover, rank.value)
+            z1 = pa.recover(rank.value)
+            z2 = f2.result()
         t_rec = time.perf_counter() - tic
         ma, exa = pa.info()
         mb, exb = pb.info()
