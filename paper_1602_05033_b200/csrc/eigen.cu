@@ -29,6 +29,7 @@
 #include "eigen.cuh"
 #include "dense.cuh"
 #include <cstring>
+#include <mutex>
 #include <cmath>
 #include <vector>
 #include <algorithm>
@@ -1716,13 +1717,14 @@ int dc_band_eigh(cudaStream_t st, const double* dsym, const double* sub, int s, 
   // workspace
   double *X[2] = {nullptr, nullptr}, *lam[2] = {nullptr, nullptr}, *Wt = nullptr, *dws = nullptr,
          *giv_c = nullptr;
-  int *iws = nullptr, *giv_i = nullptr, *pos_d = nullptr;
+  int *iws = nullptr, *giv_i = nullptr, *pos_d = nullptr, *node_counts = nullptr;
+  double* node_scal = nullptr;
   DcLeaf* leaves_d = nullptr;
   const size_t nk = (size_t)k + 16;
   auto cleanup = [&]() {
-    for (double* q : {X[0], X[1], lam[0], lam[1], Wt, dws, giv_c})
+    for (double* q : {X[0], X[1], lam[0], lam[1], Wt, dws, giv_c, node_scal})
       if (q) dfree(q);
-    for (int* q : {iws, giv_i, pos_d})
+    for (int* q : {iws, giv_i, pos_d, node_counts})
       if (q) dfree(q);
     if (leaves_d) dfree(leaves_d);
   };
@@ -1731,7 +1733,9 @@ int dc_band_eigh(cudaStream_t st, const double* dsym, const double* sub, int s, 
       (rc = dalloc(&lam[0], nk)) || (rc = dalloc(&lam[1], nk)) ||
       (rc = dalloc(&Wt, (size_t)(k + 1) * ldw)) || (rc = dalloc(&dws, 9 * nk + 64)) ||
       (rc = dalloc(&giv_c, 2 * nk)) || (rc = dalloc(&iws, 7 * nk + 16)) ||
-      (rc = dalloc(&giv_i, 2 * nk)) || (rc = dalloc(&pos_d, nk))) {
+      (rc = dalloc(&giv_i, 2 * nk)) || (rc = dalloc(&pos_d, nk)) ||
+      (rc = dalloc(&node_counts, 16 * nodes.size() + 16)) ||
+      (rc = dalloc(&node_scal, 16 * nodes.size() + 16))) {
     cleanup();
     return rc;
   }
@@ -1781,10 +1785,61 @@ int dc_band_eigh(cudaStream_t st, const double* dsym, const double* sub, int s, 
     else k_dc_leaf<96><<<nl, 1024, lsm, st>>>(leaves_d, s, dsym, sub, lam[0], X[0], ldx);
     count_launch();
   }
-  // internal nodes in post-order (dc_build pushes children first)
+  // Internal nodes in post-order (dc_build pushes children first).  Sibling
+  // subtrees are independent and, below the root, latency-bound (few CTAs per
+  // kernel): nodes are spread over NS streams, a parent waits for the events
+  // of its two children.  Every per-node work array is the shared array
+  // offset by the node's position range [off, off + n) (disjoint between
+  // nodes that can run at the same time: neither is an ancestor of the other).
+  constexpr int NS = 4;
+  static cudaStream_t xs[64][NS] = {{nullptr}};
+  cudaStream_t streams[NS];
+  streams[0] = st;
+  {
+    static std::mutex xs_mu;
+    std::lock_guard<std::mutex> lock(xs_mu);
+    for (int q = 1; q < NS; ++q) {
+      if (!xs[dev & 63][q]) cudaStreamCreateWithFlags(&xs[dev & 63][q], cudaStreamNonBlocking);
+      streams[q] = xs[dev & 63][q];
+    }
+  }
+  const bool multi = getenv("KRY_DC_SERIAL") == nullptr;
+  std::vector<cudaEvent_t> ev(nodes.size(), nullptr);
+  std::vector<int> nstream(nodes.size(), 0);
+  cudaEvent_t ev_leaves = nullptr;
+  cudaEventCreateWithFlags(&ev_leaves, cudaEventDisableTiming);
+  cudaEventRecord(ev_leaves, st);
+  auto destroy_events = [&]() {
+    for (cudaStream_t q : streams) cudaStreamSynchronize(q);
+    for (cudaEvent_t e2 : ev)
+      if (e2) cudaEventDestroy(e2);
+    cudaEventDestroy(ev_leaves);
+  };
+  int next_stream = 0;
   for (size_t ni = 0; ni < nodes.size(); ++ni) {
     DcNode& nd = nodes[ni];
     if (nd.bm < 0) continue;
+    // the root (and every node on the caller's critical path) may use any
+    // stream; the last node must end on `st`
+    const int sid = ((int)ni == root || !multi) ? 0 : (next_stream++ % NS);
+    nstream[ni] = sid;
+    cudaStream_t ns = streams[sid];
+    cudaStreamWaitEvent(ns, ev_leaves, 0);
+    for (int ch : {nd.left, nd.right})
+      if (ch >= 0 && ev[ch]) cudaStreamWaitEvent(ns, ev[ch], 0);
+    // per-node views of the work arrays
+    EigView vn = v;
+    const int off = nd.off;
+    vn.poles += off; vn.zz += off; vn.zhat += off; vn.def_lam += off; vn.mu += off;
+    vn.org += off; vn.tau += off; vn.z += off;
+    vn.pmap += off; vn.def_idx += off; vn.cand += off; vn.dflag += off; vn.pflag += off;
+    vn.counts = node_counts + 16 * (int64_t)ni;
+    vn.scal = node_scal + 16 * (int64_t)ni;
+    int* n_crow = crow + off;
+    int* n_brow = brow + off;
+    int* n_giv_i = giv_i + 2 * (int64_t)off;
+    double* n_giv_c = giv_c + 2 * (int64_t)off;
+    double* n_Wt = Wt + (int64_t)off * ldw;
     const int K0 = nd.nl + nd.nr;
     // both halves in one buffer
     int src = 0;
@@ -1792,13 +1847,13 @@ int dc_band_eigh(cudaStream_t st, const double* dsym, const double* sub, int s, 
     else if (nd.right >= 0) src = nodes[nd.right].buf;
     for (int ch : {nd.left, nd.right}) {
       if (ch < 0 || nodes[ch].buf == src) continue;
-      k_dc_copy<<<nodes[ch].n, 128, 0, st>>>(nodes[ch].off, nodes[ch].n, lam[1 - src], lam[src],
+      k_dc_copy<<<nodes[ch].n, 128, 0, ns>>>(nodes[ch].off, nodes[ch].n, lam[1 - src], lam[src],
                                              X[1 - src], X[src], ldx);
       count_launch();
     }
     int cur = 1 - src;
     if (K0 > 0) {
-      k_dc_merge<<<K0, 128, 0, st>>>(nd.off, nd.nl, nd.nr, lam[src], lam[cur], X[src], X[cur], ldx);
+      k_dc_merge<<<K0, 128, 0, ns>>>(nd.off, nd.nl, nd.nr, lam[src], lam[cur], X[src], X[cur], ldx);
       count_launch();
     }
     for (int a = 0; a < s; ++a) {
@@ -1811,43 +1866,47 @@ int dc_band_eigh(cudaStream_t st, const double* dsym, const double* sub, int s, 
       }
       const size_t dsm = (size_t)K * (sizeof(double) + 3 * sizeof(int)) + 16;
       if (dsm <= 200 * 1024 && !getenv("KRY_DC_NOSMEM"))   // (the variable forces the large-order path: tests)
-        pdl_launch(k_dc_deflate<true>, dim3(1), dim3(1024), dsm, st, v, g, dsym, sub, lam[cur], (const double*)X[cur], ldx, giv_i, giv_c);
+        pdl_launch(k_dc_deflate<true>, dim3(1), dim3(1024), dsm, ns, vn, g, dsym, sub, lam[cur], (const double*)X[cur], ldx, n_giv_i, n_giv_c);
       else
-        pdl_launch(k_dc_deflate<false>, dim3(1), dim3(1024), 0, st, v, g, dsym, sub, lam[cur], (const double*)X[cur], ldx, giv_i, giv_c);
-      if (K > 0) pdl_launch(k_dc_givens, dim3((K + 127) / 128), dim3(128), 0, st, (const int*)v.counts, (const int*)giv_i, (const double*)giv_c, X[cur], ldx, nd.off, K);
+        pdl_launch(k_dc_deflate<false>, dim3(1), dim3(1024), 0, ns, vn, g, dsym, sub, lam[cur], (const double*)X[cur], ldx, n_giv_i, n_giv_c);
+      if (K > 0) pdl_launch(k_dc_givens, dim3((K + 127) / 128), dim3(128), 0, ns, (const int*)vn.counts, (const int*)n_giv_i, (const double*)n_giv_c, X[cur], ldx, nd.off, K);
       if (K >= 1024) {
-        if (K <= 128 * 16) pdl_launch(k_eig_secular<4, 16>, dim3(K + 1), dim3(128), 0, st, v);
-        else pdl_launch(k_eig_secular<4, 0>, dim3(K + 1), dim3(128), 0, st, v);
+        if (K <= 128 * 16) pdl_launch(k_eig_secular<4, 16>, dim3(K + 1), dim3(128), 0, ns, vn);
+        else pdl_launch(k_eig_secular<4, 0>, dim3(K + 1), dim3(128), 0, ns, vn);
       } else if (K >= 256) {
-        pdl_launch(k_eig_secular<2, 16>, dim3(K + 1), dim3(64), 0, st, v);
+        pdl_launch(k_eig_secular<2, 16>, dim3(K + 1), dim3(64), 0, ns, vn);
       } else if (K >= 64) {
-        pdl_launch(k_eig_secular<1, 8>, dim3(K + 1), dim3(32), 0, st, v);
+        pdl_launch(k_eig_secular<1, 8>, dim3(K + 1), dim3(32), 0, ns, vn);
       } else {
-        pdl_launch(k_eig_secular<1, 2>, dim3(K + 1), dim3(32), 0, st, v);
+        pdl_launch(k_eig_secular<1, 2>, dim3(K + 1), dim3(32), 0, ns, vn);
       }
       if (K > 0) {
-        if (K >= 1024) pdl_launch(k_eig_zhat<4>, dim3(K), dim3(128), 0, st, v);
-        else if (K >= 256) pdl_launch(k_eig_zhat<2>, dim3(K), dim3(64), 0, st, v);
-        else pdl_launch(k_eig_zhat<1>, dim3(K), dim3(32), 0, st, v);
+        if (K >= 1024) pdl_launch(k_eig_zhat<4>, dim3(K), dim3(128), 0, ns, vn);
+        else if (K >= 256) pdl_launch(k_eig_zhat<2>, dim3(K), dim3(64), 0, ns, vn);
+        else pdl_launch(k_eig_zhat<1>, dim3(K), dim3(32), 0, ns, vn);
       }
-      pdl_launch(k_dc_wbuild, dim3(2 * K + 1), dim3(128), 0, st, v, nd.off, K, Wt, ldw, crow, brow,
+      pdl_launch(k_dc_wbuild, dim3(2 * K + 1), dim3(128), 0, ns, vn, nd.off, K, n_Wt, ldw, n_crow, n_brow,
                  (const double*)nullptr, lam[1 - cur], (const double*)X[cur], X[1 - cur], ldx);
       count_launch(5);
       if (K > 0) {
-        rc = dense_gemm(st, K + 1, K, K, Wt, ldw, 0, X[cur] + nd.off, ldx, brow,
-                        X[1 - cur] + nd.off, ldx, crow, v.counts);
-        if (rc != KRY_OK) { cleanup(); return rc; }
+        rc = dense_gemm(ns, K + 1, K, K, n_Wt, ldw, 0, X[cur] + nd.off, ldx, n_brow,
+                        X[1 - cur] + nd.off, ldx, n_crow, vn.counts);
+        if (rc != KRY_OK) { destroy_events(); cleanup(); return rc; }
       }
       cur = 1 - cur;
     }
     nd.buf = cur;
+    cudaEventCreateWithFlags(&ev[ni], cudaEventDisableTiming);
+    cudaEventRecord(ev[ni], ns);
   }
+  // (the root ran on `st`, which waited for its children)
   const int rb = nodes[root].buf;
   k_dc_output<<<(int)std::min<int64_t>(((int64_t)k * k + 255) / 256, 148 * 16), 256, 0, st>>>(
       X[rb], ldx, pos_d, k, Q);
   count_launch();
   cudaMemcpyAsync(lam_out, lam[rb], (size_t)k * sizeof(double), cudaMemcpyDeviceToDevice, st);
   cudaError_t e = cudaStreamSynchronize(st);
+  destroy_events();
   cleanup();
   if (e != cudaSuccess) return fail(KRY_ERR_CUDA, std::string("dc_band_eigh: ") + cudaGetErrorString(e));
   return KRY_OK;
