@@ -5,23 +5,34 @@
 // truncated_svd_factor (kernels.py:337) and the eigh of the dense side B of
 // the one-sided Sylvester solver (solvers.py:420).
 //
-// B200 design: a one-sided BLOCK JACOBI method (Hestenes) on DMMA.  The
-// matrix A (M x N, column-major) is orthogonalised from the right,
-// A V = U Sigma, by sweeps over all pairs of column blocks (width 16; round-
-// robin tournament, N/32 independent pairs per round = one CTA each).  A CTA
+// Contents (no library call anywhere):
+//   * k_dgemm            C = A B on DMMA (row maps, device-side sizes)
+//   * k_pchol            pivoted Cholesky of the Cauchy-like PSD reduced
+//                        Lyapunov solution, evaluated from (u, lambda)
+//   * k_gecp             cross factorisation (complete pivoting) of the
+//                        reduced Sylvester solution + SVD of the thin product
+//   * dense_syev         TWO-SIDED block Jacobi for symmetric matrices
+//   * dense_gesvd        ONE-SIDED block Jacobi (Hestenes) SVD
+//
+// Block Jacobi on DMMA.  One-sided (SVD): the matrix A (M x N, column-major)
+// is orthogonalised from the right, A V = U Sigma, by sweeps over all pairs
+// of column blocks (width 16; round-robin tournament, N/32 independent pairs
+// per round = one CTA each).  A CTA
 //   1. streams its M x 32 panel once and forms the 32 x 32 Gram matrix
 //      G = P^T P on the fp64 tensor cores (m8n8k4 DMMA),
 //   2. diagonalises G in shared memory by a parallel cyclic two-sided Jacobi
-//      iteration (16 disjoint rotations per step), accumulating R,
+//      iteration (16 disjoint rotations per barrier), accumulating R,
 //   3. streams the panel again, P <- P R (and the matching panel of V),
 //      again on DMMA.
 // The Gram entries carry a relative error of eps ||a_i|| ||a_j||, so the
 // stopping rule |a_i . a_j| <= tol ||a_i|| ||a_j|| for EVERY pair gives the
 // singular values (column norms) to high relative accuracy, and V is a
-// product of plane rotations (orthogonal to roundoff).  For a symmetric A
-// the columns of V are its eigenvectors and lambda_i = v_i . (A v_i) comes
-// with its sign from the final columns.  Everything runs on one stream; the
-// host reads one convergence word per sweep.
+// product of plane rotations (orthogonal to roundoff).  Two-sided
+// (symmetric eigenproblem): the pivot blocks of A itself are diagonalised
+// and A <- R^T A R is applied as two column-panel updates around a
+// transpose; eigenvalues are Rayleigh quotients with the original matrix.
+// Everything runs on one stream; the host reads one convergence word per
+// sweep.
 #include "dense.cuh"
 #include <algorithm>
 #include <cmath>
