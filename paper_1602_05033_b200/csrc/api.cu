@@ -298,6 +298,7 @@ struct kry_ctx {
   int prof_comb_n = 0;
   cudaEvent_t t_ev[2] = {nullptr, nullptr};
   cudaStream_t estream = nullptr;          // eigen / residual-check stream
+  bool saw_fallback = false;               // a pass-1 step took the explicit path
   cudaEvent_t ev_t = nullptr, ev_res[2] = {nullptr, nullptr};
   // pass-2 chunk buffers, kept across solves (large allocations are slow)
   double* p2buf[2] = {nullptr, nullptr};
@@ -778,6 +779,7 @@ int fused_step(kry_ctx* c, int j, const double* vold, const double* vcur, double
       KRY_CHECK(sync_status(c));
       KRY_CHECK(map_status(c, ("Lanczos step " + std::to_string(j)).c_str()));
       if (c->st_h->flags & KRY_FLAG_FALLBACK) {
+        c->saw_fallback = true;
         if (c->prof) { cudaEventDestroy(evs[0]); cudaEventDestroy(evs[1]); }
         KRY_CHECK(explicit_step(c, j, vold, vcur, vnew, ld, finalize_on_zero, exhausted));
         if (!*exhausted && cc.vn2)
@@ -790,6 +792,7 @@ int fused_step(kry_ctx* c, int j, const double* vold, const double* vcur, double
     KRY_CHECK(sync_status(c));
     KRY_CHECK(map_status(c, ("Lanczos step " + std::to_string(j)).c_str()));
     if (c->st_h->flags & KRY_FLAG_FALLBACK) {
+      c->saw_fallback = true;
       return explicit_step(c, j, vold, vcur, vnew, ld, finalize_on_zero, exhausted);
     }
   }
@@ -860,6 +863,7 @@ int step_core(kry_ctx* c, int finalize_on_zero, int* exhausted) {
     KRY_CHECK(sync_status(c));
     KRY_CHECK(map_status(c, ("Lanczos step " + std::to_string(j)).c_str()));
     if (c->st_h->flags & KRY_FLAG_FALLBACK) {
+      c->saw_fallback = true;
       KRY_CHECK(explicit_step(c, j, j > 1 ? slotp(c, c->i_old) : nullptr, slotp(c, c->i_cur),
                               slotp(c, c->i_new), c->ld, finalize_on_zero, &ex));
       int64_t ld2 = 0;
@@ -1514,6 +1518,7 @@ static int init_basis_common(kry_ctx* c, double* gamma, double* beta2) {
   c->coef_ready = false;
   c->pending_launch = false;
   c->exhausted = false;
+  c->saw_fallback = false;
   c->initialized = false;
   c->eig.reset();
   c->i_old = -1; c->i_cur = 0; c->i_new = 1;
@@ -2672,8 +2677,14 @@ int kry_recover(kry_ctx* c, double* zhost) {
     return KRY_OK;
   };
   // regenerate V_1 (replay mode: coupling blocks compared with pass 1)
-  rc = do_init(c, blk(1), ld, 1);
   const bool speculate = !step_on(c) && !dist(c);
+  // No step of pass 1 left the fused path (the usual case): the replay is
+  // deterministic, so the steps are queued without a host check each (the
+  // regenerated coupling blocks are still compared on the device, and a
+  // fallback raised in this mode poisons the comparison: replay = 2).  The
+  // host round trip per step was most of the second pass of the small configs.
+  const bool async_ok = speculate && !c->saw_fallback && !getenv("KRY_P2_SYNC");
+  rc = do_init(c, blk(1), ld, async_ok ? 2 : 1);
   for (int j = 1; rc == KRY_OK && j < m; ++j) {
     // coefficient solve j on V_j (replay) -- already done by the previous
     // fused launch when coef_ready
@@ -2709,10 +2720,12 @@ int kry_recover(kry_ctx* c, double* zhost) {
       CombineCall cc{vold, ld, blk(j), ld, blk(j + 1), ld, n, j > 1 ? 1 : 0, 1, 1, 1};
       cc.win = wbuf_of(c);
       rc = run_combine(c, cc, nullptr, nullptr);
-      if (rc == KRY_OK) rc = sync_status(c);
-      if (rc == KRY_OK) rc = map_status(c, ("second pass step " + std::to_string(j)).c_str());
-      if (rc == KRY_OK && (c->st_h->flags & KRY_FLAG_FALLBACK))
-        rc = explicit_step(c, j, vold, blk(j), blk(j + 1), ld, 1, &ex);
+      if (!async_ok) {
+        if (rc == KRY_OK) rc = sync_status(c);
+        if (rc == KRY_OK) rc = map_status(c, ("second pass step " + std::to_string(j)).c_str());
+        if (rc == KRY_OK && (c->st_h->flags & KRY_FLAG_FALLBACK))
+          rc = explicit_step(c, j, vold, blk(j), blk(j + 1), ld, 1, &ex);
+      }
     } else if (!fused && (c->st_h->flags & KRY_FLAG_FALLBACK)) {
       rc = explicit_step(c, j, vold, blk(j), blk(j + 1), ld, 1, &ex);
     } else if (step_on(c)) {
@@ -2742,6 +2755,7 @@ int kry_recover(kry_ctx* c, double* zhost) {
   if (rc == KRY_OK) {
     cudaStreamSynchronize(c->estream);
     rc = sync_status(c);
+    if (rc == KRY_OK && async_ok) rc = map_status(c, "second pass");
   }
   if (rc == KRY_OK && c->st_h->replay_err > 1e-8) {
     rc = fail(KRY_ERR_RECURRENCE,

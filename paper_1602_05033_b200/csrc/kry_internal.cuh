@@ -186,7 +186,8 @@ struct DevState {
   int status;
   int flags;                 // KRY_FLAG_*
   int step;                  // completed coefficient solves
-  int replay;                // pass-2 regeneration: compare coupling blocks
+  int replay;                // pass-2 regeneration: compare coupling blocks (2: queued without
+                             // per-step host checks; a fallback poisons replay_err)
   int finalize_on_zero;
   int s;
   int has_old;

@@ -514,7 +514,7 @@ __device__ __noinline__ void coef_solve_w(const double* total, DevState* st, con
     const int bad = w_chol_inv(Gcc, X, Sc, s, &mr, U);
     if (bad) {  // the stored block is not numerically full rank
       if (deferred) {
-        if (lane == 0) st->flags |= KRY_FLAG_FALLBACK;
+        if (lane == 0) { st->flags |= KRY_FLAG_FALLBACK; if (st->replay == 2) st->replay_err = 1e300; }
       } else {
         if (lane == 0 && st->status == KRY_OK) st->status = KRY_ERR_DEFLATION;
       }
@@ -622,7 +622,7 @@ __device__ __noinline__ void coef_solve_w(const double* total, DevState* st, con
   }
   // 6. zero / near-zero residual block: decided by the explicit path
   if (!(w2 > 1e-10 * scale2)) {
-    if (lane == 0) st->flags |= KRY_FLAG_FALLBACK;
+    if (lane == 0) { st->flags |= KRY_FLAG_FALLBACK; if (st->replay == 2) st->replay_err = 1e300; }
     return;
   }
   // 7. Cholesky QR of the residual block
@@ -631,7 +631,7 @@ __device__ __noinline__ void coef_solve_w(const double* total, DevState* st, con
     const int bad = w_chol_inv(U, X, Y, s, &mr, Z);
     const int fail = bad || mr < 1e-5;
     if (fail) {
-      if (lane == 0) st->flags |= KRY_FLAG_FALLBACK;
+      if (lane == 0) { st->flags |= KRY_FLAG_FALLBACK; if (st->replay == 2) st->replay_err = 1e300; }
       return;
     }
     for (int e = lane; e < 64; e += 32) {
