@@ -509,7 +509,7 @@ def main():
         for _ in range(2):
             api_solve()
         e2e_runs = []
-        for _ in range(max(1, min(args.steps, 2))):
+        for _ in range(max(1, min(args.steps, 3))):
             _t.cuda.synchronize()
             t0 = time.perf_counter()
             it_, rk_, tb_, tr_ = api_solve()   # the result is released before the next solve
