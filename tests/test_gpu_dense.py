@@ -202,3 +202,14 @@ def test_band_eigh_large_order_deflation_path(monkeypatch):
                      for _ in range(m)])
     sub = np.array([np.triu(rng.standard_normal((s, s))) for _ in range(m - 1)])
     _check_band(diag, sub)
+
+
+def test_svd_wide_matrix_has_zero_trailing_singular_values():
+    rng = np.random.default_rng(12)
+    a = rng.standard_normal((40, 70))
+    u, sig, vt, _ = _svd(a)
+    ref = np.linalg.svd(a, compute_uv=False)
+    assert np.max(np.abs(sig[:40] - ref)) <= 1e-13 * ref[0]
+    assert np.all(np.abs(sig[40:]) <= 1e-12 * ref[0])
+    assert np.linalg.norm((u * sig) @ vt - a) <= 1e-12 * ref[0] * np.sqrt(70)
+    assert np.linalg.norm(vt @ vt.T - np.eye(70)) <= 1e-12 * np.sqrt(70)
